@@ -1,0 +1,414 @@
+#!/usr/bin/env python
+"""Benchmark of the gate-application hot path (BASELINE.json metric:
+amplitude-updates/s and HBM GB/s (% roofline) per gate pass, n=30 complex128).
+
+Workload (BASELINE config 2): the n=30 gate-throughput sweep —
+one Haar-random U on every qubit q = 0..29, then CX on every ordered pair with
+|c - t| in {1, 15, 29} (120 gate passes). One "step" = one full sweep over the
+device-resident 16 GiB state, one HBM pass per gate (fusion off: the metric is
+per gate pass). amp-updates per pass = 2^n (the reference's one traversal per
+gate, reference kernel.hpp:58-62), so value = 120 * 2^30 / t_step.
+With N > 1 (torchrun), the state is sharded with 2^30 amplitudes per GPU
+(n = 30 + log2 N, weak scaling) and the sweep runs at width n; gates on the
+top log2 N qubits trigger NVLink half-shard exchanges.
+
+  --impl ours (default)  libqvg.so kernels
+  --impl reference       the reference's own CPU engine (oracle/_ref, compiled
+                         from /root/reference by oracle/Makefile) on the host
+                         cores, on a bounded sample of the same sweep.
+
+Inputs are synthetic and seeded (no dataset exists for this path); the state
+(16 GiB) is larger than L2 (126 MB), so no flush is needed between passes.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_QUBITS = 30
+SEED = 2508
+WORKLOAD = "config2: n=30 c128 sweep, Haar U on q=0..29 + CX for |c-t| in {1,15,29} (120 gate passes)"
+METRIC = "amplitude-updates/s per gate pass (n=30 c128 gate sweep)"
+UNIT = "amp-updates/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """NVML sampling of SM clocks and throttle reasons during the timed region
+    (the profiling recipe's clocks line)."""
+
+    NAMES = {
+        0x0000000000000004: "sw_power_cap",
+        0x0000000000000008: "hw_slowdown",
+        0x0000000000000020: "sw_thermal_slowdown",
+        0x0000000000000040: "hw_thermal_slowdown",
+        0x0000000000000080: "hw_power_brake_slowdown",
+    }
+
+    def __init__(self, device=0, period=0.1):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.period, self.stop_evt = period, threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+
+    def _run(self):
+        while not self.stop_evt.is_set():
+            try:
+                self.samples.append(self.nvml.nvmlDeviceGetClockInfo(self.h, self.nvml.NVML_CLOCK_SM))
+                mask = self.nvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.NAMES.items():
+                    if mask & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.ok:
+            self.stop_evt.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons)}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def gate_records(circuit):
+    raw = np.frombuffer(circuit.gates().tobytes(), dtype=np.uint8)
+    return raw.reshape(len(circuit), 80)
+
+
+def algorithmic_bytes(n, rec, S=16):
+    """Bytes one pass must move: dense 1q 2*2^n*S; controlled
+    non-diagonal 2*2^(n-1)*S (sector-rounded when the control is bit 0)."""
+    kind = int(np.frombuffer(rec[:4].tobytes(), np.uint32)[0])
+    if kind == 0:
+        return 2 * (1 << n) * S
+    control = int(np.frombuffer(rec[8:12].tobytes(), np.int32)[0])
+    run = (1 << control) * S
+    b = 2 * (1 << (n - 1)) * S
+    return min(b * max(1, 32 // run) if run < 32 else b, 2 * (1 << n) * S)
+
+
+def kernel_of(n, rec):
+    kind = int(np.frombuffer(rec[:4].tobytes(), np.uint32)[0])
+    target = int(np.frombuffer(rec[4:8].tobytes(), np.uint32)[0])
+    name = "k_low" if target < 5 else "k_pairs"
+    return f"{name}<double,4>" + ("/ctrl" if kind == 1 else "")
+
+
+def run_ours(args, rank, world, dist):
+    import torch
+
+    import paper_2508_15545_b200 as qv
+
+    g = int(math.log2(world))
+    n = N_QUBITS + g
+    torch.cuda.set_device(0 if world == 1 else int(os.environ.get("LOCAL_RANK", rank)))
+    dev = torch.cuda.current_device()
+    circ = qv.haar_sweep_circuit(n, SEED)
+    recs = gate_records(circ)
+    nops = len(recs)
+    if world == 1:
+        st = qv.StateVector.create(n, 128, dev)
+    else:
+        nid = qv.nccl_unique_id() if rank == 0 else None
+        box = [nid]
+        dist.broadcast_object_list(box, src=0)
+        st = qv.StateVector.create_sharded(n, 128, dev, rank, world, box[0])
+    st.set_option(qv.OPT_FUSE, 0)
+    stream = torch.cuda.ExternalStream(st.stream(), device=dev)
+    L = n - g
+    # uniform start state with |a|^2 = 2^-n so no pass sees denormals/zeros
+    st.apply_gates(qv.make_benchmark_circuit(n).gates())
+
+    def one_step(events=None):
+        for i in range(nops):
+            st.apply_gates(recs[i], sync=False)
+            if events is not None:
+                events[i + 1].record(stream)
+
+    for _ in range(args.warmup):
+        one_step()
+    st.sync()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    st.reset_stats()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nops + 1)] for _ in range(args.steps)]
+    sampler = ClockSampler(dev)
+    with sampler:
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for k in range(args.steps):
+            evs[k][0].record(stream)
+            one_step(evs[k])
+        t_end.record(stream)
+        st.sync()
+        torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    total_ms = t_start.elapsed_time(t_end)
+    stats = st.stats()
+    # per-launch durations from the interleaved events (same stream)
+    per_op = np.zeros((args.steps, nops))
+    for k in range(args.steps):
+        for i in range(nops):
+            per_op[k, i] = evs[k][i].elapsed_time(evs[k][i + 1])
+    if dist is not None:
+        t = torch.tensor([total_ms], device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_step = total_ms / args.steps
+    amps_per_gpu = 1 << L
+    value = nops * (1 << n) / (ms_step / 1e3)
+    # roofline of the dominant kernel (largest share of the step's device time)
+    local_bytes = [algorithmic_bytes(L, recs[i]) for i in range(nops)]
+    kernels = [kernel_of(L, recs[i]) for i in range(nops)]
+    mean_op = per_op.mean(axis=0)
+    share = {}
+    for i in range(nops):
+        share.setdefault(kernels[i], [0.0, 0, 0])
+        share[kernels[i]][0] += mean_op[i]
+        share[kernels[i]][1] += local_bytes[i]
+        share[kernels[i]][2] += 1
+    dom = max(share, key=lambda k: share[k][0])
+    dom_ms, dom_bytes, dom_n = share[dom]
+    hbm_peak, peak_kind = peaks()
+    achieved = (dom_bytes / dom_n) / ((dom_ms / dom_n) / 1e3) / 1e9
+    all_gbs = sum(local_bytes) / (mean_op.sum() / 1e3) / 1e9
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "c128 (f64)",
+        "data": "synthetic (seeded Haar-random unitaries, mt19937_64 seed 2508)",
+        "config": {"workload": WORKLOAD, "n_qubits": n, "local_qubits": L, "precision": "complex128",
+                   "gate_passes_per_step": nops, "fusion": "off (one HBM pass per gate)",
+                   "l2": "state 16 GiB/GPU >> 126 MB L2; no flush needed", "parallelism": f"shard{world}"},
+        "hbm_gbs_step": all_gbs,
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm_peak,
+                     "traffic": None, "algorithmic_bytes_per_launch": dom_bytes / dom_n,
+                     "launch_ms": dom_ms / dom_n, "share_of_step": dom_ms / mean_op.sum()},
+        "per_kernel": {k: {"launches_per_step": v[2], "ms_per_launch": v[0] / v[2],
+                           "gbs": (v[1] / v[2]) / ((v[0] / v[2]) / 1e3) / 1e9} for k, v in share.items()},
+        "gpu_launches": int(stats["kernel_launches"]),
+        "exchanges_per_step": stats["exchanges"] / args.steps,
+        "clocks": sampler.summary(),
+    }
+    return st, circ, recs, line, n
+
+
+def fused_leg(qv, st, circ, line, args):
+    """The same sweep through the fused planner (not the headline: the metric
+    is per gate pass)."""
+    import torch
+
+    st.set_option(qv.OPT_FUSE, 1)
+    stream = torch.cuda.ExternalStream(st.stream())
+    st.apply_gates(circ.gates())
+    st.sync()
+    st.reset_stats()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    reps = max(1, args.steps)
+    for _ in range(reps):
+        st.apply_gates(circ.gates(), sync=False)
+    b.record(stream)
+    st.sync()
+    ms = a.elapsed_time(b) / reps
+    s = st.stats()
+    line["fused"] = {"ms_per_step": ms, "value": len(circ) * (1 << circ.n_qubits) / (ms / 1e3),
+                     "passes_per_step": s["passes"] / reps, "fused_passes_per_step": s["fused_passes"] / reps,
+                     "hbm_gbs": s["bytes_moved"] / reps / (ms / 1e3) / 1e9}
+    st.set_option(qv.OPT_FUSE, 0)
+
+
+def e2e_leg(qv, st, circ, recs, line, args):
+    """The same metric through the public API with HOST buffers: every step
+    copies the 16 GiB state from pinned host memory (qvg_load), runs the sweep
+    and reads the state back (qvg_read) inside the timed region."""
+    import torch
+
+    n = circ.n_qubits
+    count = 1 << n
+    host = torch.empty(count * 2, dtype=torch.float64, pin_memory=True)
+    host_np = host.numpy().view(np.complex128)
+    host_np[:] = 1.0 / math.sqrt(count)
+    steps = max(1, min(args.steps, 3))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        st.load_state(host_np)
+        st.apply_gates(circ.gates(), sync=False)
+        st.read_into(host_np)
+    t1 = time.perf_counter()
+    ms = (t1 - t0) * 1e3 / steps
+    line["e2e"] = {"value": len(circ) * count / (ms / 1e3), "unit": UNIT, "ms_per_step": ms,
+                   "h2d_bytes_per_step": count * 16, "d2h_bytes_per_step": count * 16,
+                   "path": "StateVector.load_state -> apply_gates (C-ABI qvg_apply) -> read_state, pinned host"}
+
+
+def cpu_baseline(args, nops_hint=120):
+    """The reference engine (oracle/_ref) on the host cores: a bounded sample of
+    the same n=30 sweep (2 gate passes: a Haar U on q=0 and a CX), strategy
+    paired-cached-parallel, workers = host cores, block 65536, cache
+    workers x 64 MiB, store on /dev/shm (reference's RAM-disk setup)."""
+    from oracle.oracle import GATE_DTYPE, RefEngine, default_scratch
+
+    import paper_2508_15545_b200 as qv
+
+    if not RefEngine.available():
+        return None
+    eng = RefEngine()
+    n = N_QUBITS
+    cores = os.cpu_count() or 1
+    scratch = default_scratch()
+    try:
+        st_ = os.statvfs(scratch)
+        if st_.f_bavail * st_.f_frsize < (16 << 30) * 1.1:
+            return {"value": None, "unit": UNIT, "cores": cores, "kind": "reference",
+                    "sample": f"skipped: {scratch} has < 17.6 GB free for the n=30 store"}
+    except OSError:
+        pass
+    circ = qv.haar_sweep_circuit(n, SEED)
+    ops = np.frombuffer(circ.gates().tobytes(), dtype=GATE_DTYPE)
+    sample = np.concatenate([ops[0:1], ops[30:31]])
+    best = float("inf")
+    with eng.store(n, 65536, 0, scratch) as store:
+        store.apply(sample[:1], "paired-cached-parallel", cores, cores * (64 << 20))  # touch every page
+        for _ in range(2):
+            wall = store.apply(sample, "paired-cached-parallel", cores, cores * (64 << 20))
+            best = min(best, wall)
+    return {"value": len(sample) * (1 << n) / (best / 1e3), "unit": UNIT, "cores": cores, "kind": "reference",
+            "ms_per_gate": best / len(sample),
+            "sample": "2 gate passes of the n=30 sweep (Haar U q=0, CX 0->1), paired-cached-parallel, "
+                      f"workers={cores}, block_amps=65536, store on {scratch}, min of 2"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU path on the host cores."""
+    from oracle.oracle import GATE_DTYPE, RefEngine, default_scratch
+
+    import paper_2508_15545_b200 as qv
+
+    if rank != 0:
+        return None
+    if not RefEngine.available():
+        return {"impl": "reference", "unavailable": "oracle/_ref/libqvsim_ref.so not built (needs /root/reference)"}
+    eng = RefEngine()
+    n = N_QUBITS
+    cores = os.cpu_count() or 1
+    scratch = default_scratch()
+    circ = qv.haar_sweep_circuit(n, SEED)
+    ops = np.frombuffer(circ.gates().tobytes(), dtype=GATE_DTYPE)
+    walls = []
+    with eng.store(n, 65536, 0, scratch) as store:
+        for k in range(args.warmup + args.steps):
+            op = ops[(k * 7) % len(ops):(k * 7) % len(ops) + 1]  # one sweep gate per step, rotating
+            w = store.apply(op, "paired-cached-parallel", cores, cores * (64 << 20))
+            if k >= args.warmup:
+                walls.append(w)
+    ms = sum(walls) / len(walls)
+    value = (1 << n) / (ms / 1e3)
+    return {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "n_qubits": n, "precision": "complex128"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                             "sample": f"1 gate pass of the n=30 sweep per step (rotating), reference "
+                                       f"paired-cached-parallel, workers={cores}, store on {scratch}"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    dist = None
+    if args.impl == "reference":
+        line = run_reference(args, rank, world)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
+        tdist.init_process_group("nccl")
+        dist = tdist
+    import paper_2508_15545_b200 as qv
+
+    st, circ, recs, line, n = run_ours(args, rank, world, dist)
+    if world == 1:
+        fused_leg(qv, st, circ, line, args)
+        if not args.no_e2e:
+            e2e_leg(qv, st, circ, recs, line, args)
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                line["cpu_baseline"] = cpu_baseline(args)
+            except Exception as exc:  # keep the GPU line even if the host run fails
+                line["cpu_baseline"] = {"value": None, "error": str(exc)[:200]}
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

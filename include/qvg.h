@@ -1,0 +1,179 @@
+/*
+ * qvg.h — C-ABI of the B200-native gate-application engine (libqvg.so).
+ *
+ * This is the drop-in boundary for the QVecOpt reference's hot path
+ * (arXiv 2508.15545, /root/reference/proj). The reference has no FFI; its
+ * boundary is the C++ API listed beside each entry point below. The C++ host
+ * layer (paper_2508_15545_b200/csrc/host/) adds `Strategy::gpu` to the
+ * reference's `apply_circuit` dispatch and calls these functions; the pybind11
+ * module exposes the same names the reference's `qvsim._core` does.
+ *
+ * Conventions
+ *   - Plain C types only: pointers, sizes, status codes. No torch, no C++.
+ *   - Qubit 0 is the least-significant bit of the amplitude index
+ *     (reference SPEC.md:96, types.hpp:19-26).
+ *   - Amplitudes are interleaved (re, im) pairs, little-endian, in the state's
+ *     precision: complex128 = 2 x double (16 B, reference types.hpp:13-16),
+ *     complex64 = 2 x float (8 B, not in the reference; added for config 2).
+ *   - Every call returns QVG_OK or a status that maps 1:1 onto the reference's
+ *     error tree (reference include/qvsim/error.hpp:10-50); the message is in
+ *     qvg_last_error() (thread-local).
+ *   - One qvg_state is owned by one host thread (the reference's CacheWindow
+ *     single-owner rule, cache.hpp:44-47). Work is stream-ordered on the
+ *     state's CUDA stream; qvg_sync() waits for it.
+ */
+#ifndef QVG_H
+#define QVG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QVG_ABI_VERSION 1
+
+/* Status codes -> reference exception types (error.hpp:10-50). */
+enum qvg_status {
+    QVG_OK = 0,
+    QVG_ERR_VALIDATION = 1, /* qvsim::ValidationError: bad qubit, size, op */
+    QVG_ERR_CAPACITY = 2,   /* qvsim::CapacityError: device memory too small */
+    QVG_ERR_IO = 3,         /* qvsim::IoError: CUDA / NCCL runtime failure */
+    QVG_ERR_FORMAT = 4,     /* qvsim::FormatError: bad state-file header */
+    QVG_ERR_NO_DEVICE = 5   /* qvsim::IoError: no CUDA device / bad build */
+};
+
+/* Op kinds (reference types.hpp:41 OpKind). */
+enum qvg_op_kind { QVG_OP_SINGLE = 0, QVG_OP_CONTROLLED = 1 };
+
+/* Flattened qvsim::GateOp (reference types.hpp:43-52). The name/params text
+ * form stays on the host; the device only needs the matrix and the qubits.
+ * u[] is the row-major 2x2 matrix as 8 reals in the reference's "u" order
+ * (gates.hpp:26-29): re00 im00 re01 im01 re10 im10 re11 im11. */
+typedef struct qvg_gate {
+    uint32_t kind;    /* qvg_op_kind */
+    uint32_t target;  /* GateOp::target */
+    int32_t control;  /* GateOp::control, -1 when absent */
+    uint32_t flags;   /* reserved, must be 0 */
+    double u[8];
+} qvg_gate;
+
+/* Precision tags for qvg_create. */
+enum qvg_precision { QVG_C64 = 64, QVG_C128 = 128 };
+
+/* Option keys for qvg_set_option. */
+enum qvg_option {
+    QVG_OPT_FUSE = 1,        /* 1: fused low/strided tile passes (default), 0: one pass per gate */
+    QVG_OPT_TILE_QUBITS = 2, /* qubits per fused tile (default 12 for c128, 13 for c64) */
+    QVG_OPT_CARRIERS = 3,    /* lowest qubits every tile keeps contiguous (default 3) */
+    QVG_OPT_LOW_KERNEL = 4   /* 1: warp-shuffle kernel for targets < 5 (default), 0: generic */
+};
+
+/* Counters (the reference's Metrics, metrics.hpp:14-30, plus the GPU pass
+ * accounting of SURVEY §5). Cumulative over the state's lifetime. */
+typedef struct qvg_stats {
+    uint64_t gates_applied;  /* Metrics::gates_applied */
+    uint64_t passes;         /* HBM passes launched (Metrics::traversals analog) */
+    uint64_t fused_passes;   /* of which fused tile passes */
+    uint64_t kernel_launches;
+    uint64_t bytes_moved;    /* algorithmic HBM bytes, read + write */
+    uint64_t exchange_bytes; /* bytes sent over NVLink (sharded states) */
+    uint64_t exchanges;      /* pairwise half-shard exchanges */
+    double kernel_ms;        /* device time of gate kernels (timed states only) */
+    double exchange_ms;
+} qvg_stats;
+
+typedef struct qvg_state qvg_state;
+
+/* ---- lifecycle ------------------------------------------------------------
+ * Replaces BlockStore::create (reference store.hpp:55-57, store.cpp:181-214):
+ * allocates 2^n amplitudes in HBM and initialises |0...0> (amp[0] = 1). */
+int qvg_create(uint32_t n_qubits, uint32_t precision, int device, qvg_state **out);
+
+/* Sharded state over `world` ranks, one process per GPU. Rank r
+ * owns global indices [r*2^L, (r+1)*2^L), L = n - log2(world) (reference
+ * parallel.cpp:13-37, Eq. 9). nccl_id is the 128-byte ncclUniqueId made by
+ * qvg_nccl_unique_id on rank 0 and broadcast by the caller. */
+int qvg_create_sharded(uint32_t n_qubits, uint32_t precision, int device,
+                       uint32_t rank, uint32_t world, const void *nccl_id,
+                       qvg_state **out);
+int qvg_nccl_unique_id(void *out128);
+int qvg_destroy(qvg_state *s);
+
+/* Shape queries. */
+int qvg_info(const qvg_state *s, uint32_t *n_qubits, uint32_t *precision,
+             uint32_t *rank, uint32_t *world);
+
+/* Options (qvg_option). */
+int qvg_set_option(qvg_state *s, int key, int64_t value);
+
+/* ---- state init / transfer -------------------------------------------------
+ * |index> basis state (BlockStore::create gives index 0). Global index. */
+int qvg_init_basis(qvg_state *s, uint64_t index);
+/* Host -> device copy of amplitudes [offset, offset+count) in the state's
+ * precision (write_full_state, reference engine.cpp:496-509). For sharded
+ * states the range is global; each rank copies the part it owns. */
+int qvg_load(qvg_state *s, const void *host, uint64_t offset, uint64_t count);
+/* Device -> host (read_full_state, reference engine.cpp:483-494). */
+int qvg_read(qvg_state *s, void *host, uint64_t offset, uint64_t count);
+
+/* ---- the hot path ------------------------------------------------------------
+ * Apply `count` ops in order (reference apply_circuit for a whole circuit,
+ * engine.cpp:86-157; apply_gate_streamed for count == 1, kernel.cpp:132-146).
+ * Validates every op first (reference kernel.cpp:134-140, circuit.cpp:31-52)
+ * and enqueues nothing on error. Stream-ordered: returns once the work is
+ * enqueued; qvg_sync() waits. */
+int qvg_apply(qvg_state *s, const qvg_gate *ops, uint64_t count);
+int qvg_sync(qvg_state *s);
+
+/* ---- readout ------------------------------------------------------------------
+ * |a_i|^2 = re*re + im*im (std::norm, reference engine.cpp:518) for
+ * i in [offset, offset+count), written as doubles. Synchronous. */
+int qvg_probabilities(qvg_state *s, double *out, uint64_t offset, uint64_t count);
+/* sqrt(sum |a_i|^2) (BlockStore::norm, reference store.cpp:301-316). */
+int qvg_norm(qvg_state *s, double *out);
+/* The k largest |a_i|^2, descending, ties by ascending index
+ * (top_amplitudes, reference engine.cpp:511-544). amps_out gets 2*k reals. */
+int qvg_top_amplitudes(qvg_state *s, uint32_t k, uint64_t *index_out,
+                       double *amps_out);
+
+/* ---- instrumentation --------------------------------------------------------- */
+int qvg_stats_get(const qvg_state *s, qvg_stats *out);
+int qvg_stats_reset(qvg_state *s);
+/* The cudaStream_t the state's work runs on (for CUDA-event timing). */
+int qvg_stream(const qvg_state *s, void **stream_out);
+/* Device pointer and byte size of this rank's amplitude shard. */
+int qvg_device_buffer(const qvg_state *s, void **ptr_out, uint64_t *bytes_out);
+/* Number of gate passes qvg_apply would launch for these ops (planner only,
+ * no device work; usable without a GPU). */
+int qvg_plan_passes(uint32_t n_qubits, uint32_t precision, int fuse,
+                    uint32_t tile_qubits, uint32_t carriers, const qvg_gate *ops,
+                    uint64_t count, uint64_t *passes_out, uint64_t *fused_out,
+                    uint64_t *bytes_out);
+/* Schedule of a state sharded over `world` = 2^g ranks, as run
+ * by qvg_apply on a sharded state; host-only, usable without a GPU. */
+enum qvg_step_type { QVG_STEP_LOCAL = 0, QVG_STEP_EXCHANGE = 1, QVG_STEP_LOCAL_SWAP = 2 };
+typedef struct qvg_shard_step {
+    uint32_t type;       /* qvg_step_type */
+    uint32_t rank_mask;  /* LOCAL: runs on ranks with (rank & rank_mask) == rank_value */
+    uint32_t rank_value;
+    uint32_t gpos;       /* EXCHANGE: global physical qubit (>= L) */
+    uint32_t lpos;       /* EXCHANGE: local qubit swapped with gpos; LOCAL_SWAP: first local qubit */
+    uint32_t lpos2;      /* LOCAL_SWAP: second local qubit */
+    qvg_gate op;         /* LOCAL: op on physical local qubits */
+} qvg_shard_step;
+/* Steps for ops[0..count) from the identity qubit map; with canonicalize != 0
+ * the steps that restore the canonical order follow. Writes at most `cap`
+ * steps and the total count to *nsteps (call with cap = 0 to size). */
+int qvg_shard_schedule(uint32_t n_qubits, uint32_t world, const qvg_gate *ops, uint64_t count,
+                       int canonicalize, qvg_shard_step *steps, uint64_t cap, uint64_t *nsteps);
+/* Thread-local message of the last failing call ("" when none). */
+const char *qvg_last_error(void);
+int qvg_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QVG_H */

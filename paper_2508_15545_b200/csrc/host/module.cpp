@@ -1,0 +1,269 @@
+// module.cpp — pybind11 module `_core`: the Python face of the host layer,
+// mirroring the reference's binding (reference proj/bindings/module.cpp:40-188)
+// with StateVector (device-resident) in place of StateStore and
+// strategy="gpu". Unlike the reference, the GIL is released while the device
+// works.
+#include <pybind11/complex.h>
+#include <pybind11/numpy.h>
+#include <pybind11/pybind11.h>
+#include <pybind11/stl.h>
+
+#include <cstring>
+
+#include "qvsim_gpu.hpp"
+
+namespace py = pybind11;
+using namespace qvsim;
+
+namespace {
+
+py::array_t<std::uint8_t> gates_bytes(const std::vector<qvg_gate> &g) {
+    py::array_t<std::uint8_t> out(g.size() * sizeof(qvg_gate));
+    if (!g.empty()) std::memcpy(out.mutable_data(), g.data(), g.size() * sizeof(qvg_gate));
+    return out;
+}
+
+const qvg_gate *gate_ptr(const py::buffer_info &b, std::size_t &count) {
+    const std::size_t bytes = (std::size_t)(b.size * b.itemsize);
+    if (bytes % sizeof(qvg_gate)) throw ValidationError("gate buffer is not a whole number of 80-byte qvg_gate records");
+    count = bytes / sizeof(qvg_gate);
+    return static_cast<const qvg_gate *>(b.ptr);
+}
+
+py::dict metrics_dict(const Metrics &m, std::uint32_t n) {
+    py::dict d;
+    d["n_qubits"] = n;
+    d["strategy"] = m.strategy;
+    d["workers"] = m.workers;
+    d["gates_applied"] = m.gates_applied;
+    d["traversals"] = m.traversals;
+    d["fused_passes"] = m.fused_passes;
+    d["bytes_moved"] = m.bytes_moved;
+    d["exchange_bytes"] = m.exchange_bytes;
+    d["exchanges"] = m.exchanges;
+    d["wall_ms"] = m.wall_ms;
+    return d;
+}
+
+py::dict stats_dict(const qvg_stats &s) {
+    py::dict d;
+    d["gates_applied"] = s.gates_applied;
+    d["passes"] = s.passes;
+    d["fused_passes"] = s.fused_passes;
+    d["kernel_launches"] = s.kernel_launches;
+    d["bytes_moved"] = s.bytes_moved;
+    d["exchange_bytes"] = s.exchange_bytes;
+    d["exchanges"] = s.exchanges;
+    return d;
+}
+
+}  // namespace
+
+PYBIND11_MODULE(_core, m) {
+    m.doc() = "B200-native gate application for the QVecOpt state-vector simulator";
+
+    auto base = py::register_exception<Error>(m, "QvsimError");
+    py::register_exception<ValidationError>(m, "ValidationError", base.ptr());
+    py::register_exception<CapacityError>(m, "CapacityError", base.ptr());
+    py::register_exception<IoError>(m, "IoError", base.ptr());
+    py::register_exception<FormatError>(m, "FormatError", base.ptr());
+    py::register_exception<ParseError>(m, "ParseError", base.ptr());
+
+    py::class_<Circuit>(m, "Circuit", "Ordered gate list on n qubits")
+        .def_property_readonly("n_qubits", [](const Circuit &c) { return c.n_qubits; })
+        .def("__len__", [](const Circuit &c) { return c.ops.size(); })
+        .def("to_text", &serialize_circuit, "Circuit text that parse_circuit round-trips exactly")
+        .def("gates", [](const Circuit &c) { return gates_bytes(to_gates(c)); },
+             "The ops as packed qvg_gate records (80 bytes each, include/qvg.h)")
+        .def("names", [](const Circuit &c) {
+            std::vector<std::string> out;
+            for (const auto &op : c.ops) out.push_back(op.name);
+            return out;
+        })
+        .def("__repr__", [](const Circuit &c) {
+            return "<Circuit n_qubits=" + std::to_string(c.n_qubits) + " ops=" + std::to_string(c.ops.size()) + ">";
+        });
+
+    m.def("circuit_from_gates", [](std::uint32_t n, py::buffer buf) {
+        const py::buffer_info b = buf.request();
+        std::size_t count = 0;
+        const qvg_gate *g = gate_ptr(b, count);
+        return from_gates(n, g, count);
+    }, py::arg("n_qubits"), py::arg("gates"));
+
+    m.def("parse_circuit",
+          [](const std::string &text, std::optional<std::uint32_t> qubits, bool strict) {
+              return parse_circuit(text, qubits, strict);
+          },
+          py::arg("text"), py::arg("qubits") = std::nullopt, py::arg("strict") = false);
+    m.def("serialize_circuit", &serialize_circuit, py::arg("circuit"));
+    m.def("random_circuit",
+          [](std::uint32_t n, std::uint32_t depth, std::uint64_t seed) { return random_circuit(n, depth, seed); },
+          py::arg("n_qubits"), py::arg("depth"), py::arg("seed"));
+    m.def("make_benchmark_circuit", &make_benchmark_circuit, py::arg("n_qubits"));
+    m.def("u3_ladder_circuit", &u3_ladder_circuit, py::arg("n_qubits"), py::arg("layers") = 20, py::arg("seed") = 1);
+    m.def("qft_circuit", [](std::uint32_t n, std::uint64_t seed) {
+        std::uint64_t b = 0;
+        Circuit c = qft_circuit(n, seed, &b);
+        return py::make_tuple(c, b);
+    }, py::arg("n_qubits"), py::arg("seed") = 1, "(circuit, basis index b)");
+    m.def("haar_sweep_circuit", &haar_sweep_circuit, py::arg("n_qubits"), py::arg("seed") = 1);
+    m.def("grid_circuit", &grid_circuit, py::arg("rows") = 5, py::arg("cols") = 6, py::arg("cycles") = 24,
+          py::arg("seed") = 1);
+    m.def("make_gate", [](const std::string &name, const std::vector<double> &p, bool strict) {
+        const GateMatrix g = make_gate(name, p, strict);
+        return std::vector<amp_t>{g.u00, g.u01, g.u10, g.u11};
+    }, py::arg("name"), py::arg("params") = std::vector<double>{}, py::arg("strict") = false);
+    m.def("strategy_tags", &strategy_tags);
+
+    py::class_<StateVector>(m, "StateVector", "Device-resident state vector (HBM), the GPU analog of StateStore")
+        .def_static("create", &StateVector::create, py::arg("n_qubits"), py::arg("precision") = 128,
+                    py::arg("device") = 0, "New state holding |0...0>")
+        .def_static("create_sharded",
+                    [](std::uint32_t n, std::uint32_t precision, int device, std::uint32_t rank, std::uint32_t world,
+                       std::optional<py::bytes> nccl_id) {
+                        if (!nccl_id)
+                            return StateVector::create_sharded(n, precision, device, rank, world, nullptr);
+                        const std::string id = *nccl_id;
+                        if (id.size() != 128) throw ValidationError("nccl_id must be 128 bytes");
+                        py::gil_scoped_release nogil;
+                        return StateVector::create_sharded(n, precision, device, rank, world, id.data());
+                    },
+                    py::arg("n_qubits"), py::arg("precision"), py::arg("device"), py::arg("rank"), py::arg("world"),
+                    py::arg("nccl_id") = std::nullopt,
+                    "Sharded state; nccl_id=None keeps all shards on this device (virtual shards)")
+        .def_property_readonly("n_qubits", &StateVector::n_qubits)
+        .def_property_readonly("n_amps", &StateVector::n_amps)
+        .def_property_readonly("precision", &StateVector::precision)
+        .def_property_readonly("rank", &StateVector::rank)
+        .def_property_readonly("world", &StateVector::world)
+        .def("init_basis", &StateVector::init_basis, py::arg("index"))
+        .def("norm", [](const StateVector &s) {
+            py::gil_scoped_release nogil;
+            return s.norm();
+        })
+        .def("amplitude", &StateVector::amplitude, py::arg("index"))
+        .def("read_state", [](const StateVector &s, std::uint64_t offset, std::optional<std::uint64_t> count) {
+            const std::uint64_t c = count ? *count : s.n_amps() - std::min(offset, s.n_amps());
+            py::array_t<std::complex<double>> out(c);
+            {
+                py::gil_scoped_release nogil;
+                s.read(out.mutable_data(), offset, c);
+            }
+            return out;
+        }, py::arg("offset") = 0, py::arg("count") = std::nullopt, "Amplitudes as a complex128 numpy array")
+        .def("read_into", [](const StateVector &s, py::array_t<std::complex<double>, py::array::c_style> out,
+                             std::uint64_t offset) {
+            const std::uint64_t c = (std::uint64_t)out.size();
+            amp_t *p = out.mutable_data();
+            py::gil_scoped_release nogil;
+            s.read(p, offset, c);
+        }, py::arg("out"), py::arg("offset") = 0, "Amplitudes into a caller-owned (e.g. pinned) complex128 array")
+        .def("load_state", [](StateVector &s,py::array_t<std::complex<double>, py::array::c_style | py::array::forcecast> a,
+                              std::uint64_t offset) {
+            const std::uint64_t c = (std::uint64_t)a.size();
+            const amp_t *p = a.data();
+            py::gil_scoped_release nogil;
+            s.load(p, offset, c);
+        }, py::arg("amps"), py::arg("offset") = 0)
+        .def("probabilities", [](const StateVector &s, std::uint64_t offset, std::optional<std::uint64_t> count) {
+            const std::uint64_t c = count ? *count : s.n_amps() - std::min(offset, s.n_amps());
+            py::array_t<double> out(c);
+            {
+                py::gil_scoped_release nogil;
+                s.probabilities(out.mutable_data(), offset, c);
+            }
+            return out;
+        }, py::arg("offset") = 0, py::arg("count") = std::nullopt)
+        .def("top_amplitudes", [](const StateVector &s, std::size_t k) {
+            py::gil_scoped_release nogil;
+            return s.top_amplitudes(k);
+        }, py::arg("k") = 8)
+        .def("set_option", &StateVector::set_option, py::arg("key"), py::arg("value"))
+        .def("stats", [](const StateVector &s) { return stats_dict(s.stats()); })
+        .def("reset_stats", [](StateVector &s) { check_status(qvg_stats_reset(s.handle())); })
+        .def("sync", [](const StateVector &s) {
+            py::gil_scoped_release nogil;
+            s.sync();
+        })
+        .def("stream", [](const StateVector &s) {
+            void *st = nullptr;
+            check_status(qvg_stream(s.handle(), &st));
+            return (std::uintptr_t)st;
+        }, "cudaStream_t of the state's work, as an integer")
+        .def("device_buffer", [](const StateVector &s) {
+            void *p = nullptr;
+            std::uint64_t bytes = 0;
+            check_status(qvg_device_buffer(s.handle(), &p, &bytes));
+            return py::make_tuple((std::uintptr_t)p, bytes);
+        })
+        .def("apply_gates", [](StateVector &s, py::buffer buf, bool sync) {
+            const py::buffer_info b = buf.request();
+            std::size_t count = 0;
+            const qvg_gate *g = gate_ptr(b, count);
+            py::gil_scoped_release nogil;
+            check_status(qvg_apply(s.handle(), g, count));
+            if (sync) s.sync();
+        }, py::arg("gates"), py::arg("sync") = true, "Apply packed qvg_gate records (the C-ABI hot path)");
+
+    m.def("apply_circuit",
+          [](StateVector &state, const Circuit &circuit, const std::string &strategy, bool fuse,
+             std::uint32_t tile_qubits, bool sync) {
+              const auto s = parse_strategy(strategy);
+              if (!s) throw ValidationError("unknown strategy '" + strategy + "'");
+              RunConfig cfg;
+              cfg.strategy = *s;
+              cfg.fuse = fuse;
+              cfg.tile_qubits = tile_qubits;
+              cfg.sync = sync;
+              Metrics metrics;
+              {
+                  py::gil_scoped_release nogil;
+                  apply_circuit(state, circuit, cfg, metrics);
+              }
+              return metrics_dict(metrics, state.n_qubits());
+          },
+          py::arg("state"), py::arg("circuit"), py::arg("strategy") = "gpu", py::arg("fuse") = true,
+          py::arg("tile_qubits") = 0, py::arg("sync") = true,
+          "Apply the circuit in place on the device; returns the run's metrics document");
+
+    m.def("nccl_unique_id", []() {
+        std::string id(128, '\0');
+        check_status(qvg_nccl_unique_id(id.data()));
+        return py::bytes(id);
+    });
+
+    m.def("plan_passes",
+          [](std::uint32_t n, py::buffer buf, std::uint32_t precision, bool fuse, std::uint32_t tile_qubits,
+             std::uint32_t carriers) {
+              const py::buffer_info b = buf.request();
+              std::size_t count = 0;
+              const qvg_gate *g = gate_ptr(b, count);
+              std::uint64_t passes = 0, fused = 0, bytes = 0;
+              check_status(qvg_plan_passes(n, precision, fuse, tile_qubits, carriers, g, count, &passes, &fused, &bytes));
+              return py::make_tuple(passes, fused, bytes);
+          },
+          py::arg("n_qubits"), py::arg("gates"), py::arg("precision") = 128, py::arg("fuse") = true,
+          py::arg("tile_qubits") = 0, py::arg("carriers") = 3, "(passes, fused passes, algorithmic bytes)");
+
+    m.def("shard_schedule",
+          [](std::uint32_t n, std::uint32_t world, py::buffer buf, bool canonicalize) {
+              const py::buffer_info b = buf.request();
+              std::size_t count = 0;
+              const qvg_gate *g = gate_ptr(b, count);
+              std::uint64_t nsteps = 0;
+              check_status(qvg_shard_schedule(n, world, g, count, canonicalize, nullptr, 0, &nsteps));
+              py::array_t<std::uint8_t> out(nsteps * sizeof(qvg_shard_step));
+              check_status(qvg_shard_schedule(n, world, g, count, canonicalize,
+                                              reinterpret_cast<qvg_shard_step *>(out.mutable_data()), nsteps, &nsteps));
+              return out;
+          },
+          py::arg("n_qubits"), py::arg("world"), py::arg("gates"), py::arg("canonicalize") = true,
+          "Packed qvg_shard_step records (104 bytes each)");
+
+    m.attr("QVG_ABI_VERSION") = qvg_abi_version();
+    m.attr("OPT_FUSE") = (int)QVG_OPT_FUSE;
+    m.attr("OPT_TILE_QUBITS") = (int)QVG_OPT_TILE_QUBITS;
+    m.attr("OPT_CARRIERS") = (int)QVG_OPT_CARRIERS;
+    m.attr("OPT_LOW_KERNEL") = (int)QVG_OPT_LOW_KERNEL;
+}

@@ -1,0 +1,585 @@
+// qvg_engine.cu — libqvg.so: the C-ABI (include/qvg.h) over the sm_100a
+// kernels in qvg_kernels.cuh and the pass planner in qvg_plan.hpp.
+//
+// Replaces, for the GPU strategy, the reference's block store + window +
+// paired kernel + thread pool (reference store.cpp, cache.cpp, kernel.cpp,
+// parallel.cpp): the state stays resident in HBM for the whole circuit and
+// each planned pass is one kernel launch on the state's stream.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "qvg.h"
+#include "qvg_kernels.cuh"
+#include "qvg_plan.hpp"
+#include "qvg_shard.hpp"
+
+using namespace qvg;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Status {
+    int code;
+    std::string msg;
+};
+
+struct CudaFail : std::runtime_error {
+    int code;
+    CudaFail(int c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+
+void cuda_check(cudaError_t e, const char *what) {
+    if (e == cudaSuccess) return;
+    const int code = (e == cudaErrorMemoryAllocation) ? QVG_ERR_CAPACITY
+                     : (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver ||
+                        e == cudaErrorNoKernelImageForDevice)
+                         ? QVG_ERR_NO_DEVICE
+                         : QVG_ERR_IO;
+    throw CudaFail(code, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class F> int guarded(F &&f) {
+    try {
+        f();
+        g_last_error.clear();
+        return QVG_OK;
+    } catch (const CudaFail &e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const Validation &e) {
+        g_last_error = e.what();
+        return QVG_ERR_VALIDATION;
+    } catch (const std::bad_alloc &) {
+        g_last_error = "host allocation failed";
+        return QVG_ERR_CAPACITY;
+    } catch (const std::exception &e) {
+        g_last_error = e.what();
+        return QVG_ERR_IO;
+    }
+}
+
+}  // namespace
+
+// One rank's share of the state (or one virtual shard when several shards of
+// a sharded state live on this device, see qvg_shard.hpp).
+struct qvg_state {
+    int device = 0;
+    uint32_t n = 0;          // global qubits
+    uint32_t L = 0;          // local qubits per shard
+    uint32_t precision = 128;
+    uint32_t S = 16;         // bytes per amplitude
+    uint32_t rank = 0, world = 1;
+    ShardSet shards;         // device buffers, transport, qubit map
+    cudaStream_t stream = nullptr;
+    int sm_count = 148;
+    // options
+    bool fuse = true;
+    uint32_t tile_qubits = 12;
+    uint32_t carriers = 3;
+    bool low_kernel = true;
+    // device scratch
+    TileOp *d_ops = nullptr;
+    size_t d_ops_cap = 0;
+    double *d_partials = nullptr;
+    double *d_probs = nullptr;
+    qvg_stats stats{};
+};
+
+namespace {
+
+constexpr int kNormBlocks = 1184;  // 8 x 148 SMs; fixed => deterministic norm
+constexpr uint64_t kProbChunk = 1ull << 24;
+
+// ------------------------------------------------------------------------
+// Launchers. All grids are exact power-of-two covers of the enumeration, so
+// the kernels carry no bounds checks.
+template <class R>
+void launch_pairs(const qvg_state &s, void *psi, uint32_t L, const qvg_gate &g, const OpInfo &o) {
+    using T = typename Cplx<R>::T;
+    Mat<R> m;
+    for (int i = 0; i < 8; ++i) m.u[i] = (R)g.u[i];
+    int lo = o.target, hi = -1;
+    uint64_t setm = 0;
+    if (o.control >= 0) {
+        lo = std::min(o.target, o.control);
+        hi = std::max(o.target, o.control);
+        setm = 1ull << o.control;
+    }
+    const uint64_t npairs = 1ull << (L - 1 - (o.control >= 0 ? 1 : 0));
+    T *p = static_cast<T *>(psi);
+    if (npairs >= 1024) {
+        k_pairs<R, 4><<<(unsigned)(npairs / 1024), 256, 0, s.stream>>>(p, o.target, lo, hi, setm, m);
+    } else {
+        const unsigned bs = (unsigned)std::min<uint64_t>(npairs, 256);
+        k_pairs<R, 1><<<(unsigned)(npairs / bs), bs, 0, s.stream>>>(p, o.target, lo, hi, setm, m);
+    }
+}
+
+template <class R>
+void launch_low(const qvg_state &s, void *psi, uint32_t L, const qvg_gate &g, const OpInfo &o) {
+    using T = typename Cplx<R>::T;
+    Mat<R> m;
+    for (int i = 0; i < 8; ++i) m.u[i] = (R)g.u[i];
+    const int c_ins = o.control >= 5 ? o.control : -1;
+    const int c_lane = (o.control >= 0 && o.control < 5) ? o.control : -1;
+    const uint64_t count = 1ull << (L - (c_ins >= 0 ? 1 : 0));
+    T *p = static_cast<T *>(psi);
+    if (count >= 1024) {
+        k_low<R, 4><<<(unsigned)(count / 1024), 256, 0, s.stream>>>(p, o.target, c_ins, c_lane, m);
+    } else {
+        const unsigned bs = (unsigned)std::min<uint64_t>(count, 256);
+        k_low<R, 1><<<(unsigned)(count / bs), bs, 0, s.stream>>>(p, o.target, c_ins, c_lane, m);
+    }
+}
+
+template <class R>
+void launch_phase(const qvg_state &s, void *psi, uint32_t L, const qvg_gate &g, const OpInfo &o) {
+    using T = typename Cplx<R>::T;
+    int lo = o.target, hi = -1;
+    uint64_t setm = 1ull << o.target;
+    if (o.control >= 0) {
+        lo = std::min(o.target, o.control);
+        hi = std::max(o.target, o.control);
+        setm |= 1ull << o.control;
+    }
+    const uint64_t count = 1ull << (L - 1 - (o.control >= 0 ? 1 : 0));
+    T *p = static_cast<T *>(psi);
+    const R dr = (R)g.u[6], di = (R)g.u[7];
+    if (count >= 1024) {
+        k_phase<R, 4><<<(unsigned)(count / 1024), 256, 0, s.stream>>>(p, lo, hi, setm, dr, di);
+    } else {
+        const unsigned bs = (unsigned)std::min<uint64_t>(count, 256);
+        k_phase<R, 1><<<(unsigned)(count / bs), bs, 0, s.stream>>>(p, lo, hi, setm, dr, di);
+    }
+}
+
+template <class R>
+void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *d_ops) {
+    using T = typename Cplx<R>::T;
+    const size_t smem = (sizeof(T) << p.geom.k) + (sizeof(uint64_t) << p.geom.nhi);
+    static bool attr_set[2] = {false, false};
+    const int which = sizeof(R) == 8 ? 1 : 0;
+    if (!attr_set[which]) {
+        cuda_check(cudaFuncSetAttribute(k_tile<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
+                   "cudaFuncSetAttribute(k_tile)");
+        attr_set[which] = true;
+    }
+    int per_sm = 0;
+    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tile<R>, 512, smem),
+               "occupancy(k_tile)");
+    per_sm = std::max(per_sm, 1);
+    const uint64_t grid = std::min<uint64_t>(p.geom.ntiles, (uint64_t)per_sm * s.sm_count);
+    k_tile<R><<<(unsigned)grid, 512, smem, s.stream>>>(static_cast<T *>(psi), p.geom, d_ops + p.op_begin,
+                                                      (int)p.op_count);
+}
+
+PlanOptions plan_options(const qvg_state &s) {
+    PlanOptions po;
+    po.n = s.L;
+    po.amp_bytes = s.S;
+    po.fuse = s.fuse;
+    po.tile_qubits = s.tile_qubits;
+    po.carriers = s.carriers;
+    po.low_kernel = s.low_kernel;
+    return po;
+}
+
+// Run a batch of local ops (physical local qubit indices) on one shard buffer.
+void run_local(qvg_state &s, void *psi, const qvg_gate *ops, uint64_t count) {
+    if (count == 0) return;
+    const Plan plan = make_plan(ops, count, plan_options(s));
+    if (!plan.tile_ops.empty()) {
+        if (plan.tile_ops.size() > s.d_ops_cap) {
+            if (s.d_ops) {
+                cuda_check(cudaStreamSynchronize(s.stream), "sync before op-buffer growth");
+                cudaFree(s.d_ops);
+                s.d_ops = nullptr;
+            }
+            const size_t cap = std::max<size_t>(plan.tile_ops.size(), 1024);
+            cuda_check(cudaMalloc(&s.d_ops, cap * sizeof(TileOp)), "cudaMalloc(tile ops)");
+            s.d_ops_cap = cap;
+        }
+        // The previous batch's tile kernels may still read d_ops: the copy is
+        // stream-ordered after them. A pageable source is consumed before
+        // cudaMemcpyAsync returns, so the host vector may go out of scope.
+        cuda_check(cudaMemcpyAsync(s.d_ops, plan.tile_ops.data(), plan.tile_ops.size() * sizeof(TileOp),
+                                   cudaMemcpyHostToDevice, s.stream),
+                   "upload tile ops");
+    }
+    const bool dbl = s.precision == QVG_C128;
+    for (const Pass &p : plan.passes) {
+        switch (p.kind) {
+        case PASS_PAIRS:
+            dbl ? launch_pairs<double>(s, psi, s.L, p.op, p.info) : launch_pairs<float>(s, psi, s.L, p.op, p.info);
+            break;
+        case PASS_LOW:
+            dbl ? launch_low<double>(s, psi, s.L, p.op, p.info) : launch_low<float>(s, psi, s.L, p.op, p.info);
+            break;
+        case PASS_PHASE:
+            dbl ? launch_phase<double>(s, psi, s.L, p.op, p.info) : launch_phase<float>(s, psi, s.L, p.op, p.info);
+            break;
+        case PASS_TILE:
+            dbl ? launch_tile<double>(s, psi, p, s.d_ops) : launch_tile<float>(s, psi, p, s.d_ops);
+            s.stats.fused_passes += 1;
+            break;
+        }
+        s.stats.passes += 1;
+        s.stats.kernel_launches += 1;
+        s.stats.bytes_moved += p.bytes;
+    }
+    cuda_check(cudaGetLastError(), "kernel launch");
+}
+
+void set_device(const qvg_state *s) { cuda_check(cudaSetDevice(s->device), "cudaSetDevice"); }
+
+void check_state(const qvg_state *s) {
+    if (!s) throw Validation("null state");
+}
+
+void check_range(const qvg_state *s, uint64_t offset, uint64_t count) {
+    const uint64_t dim = 1ull << s->n;
+    if (offset > dim || count > dim - offset)
+        throw Validation("amplitude range [" + std::to_string(offset) + ", " + std::to_string(offset + count) +
+                         ") out of range for " + std::to_string(dim) + " amplitudes");
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Shard executor hooks used by qvg_shard.hpp.
+namespace qvg {
+void cuda_throw(cudaError_t e, const char *what) { cuda_check(e, what); }
+void shard_run_local(qvg_state &s, void *psi, const qvg_gate *ops, uint64_t count) { run_local(s, psi, ops, count); }
+cudaStream_t shard_stream(qvg_state &s) { return s.stream; }
+uint32_t shard_amp_bytes(const qvg_state &s) { return s.S; }
+qvg_stats &shard_stats(qvg_state &s) { return s.stats; }
+}  // namespace qvg
+
+extern "C" {
+
+int qvg_abi_version(void) { return QVG_ABI_VERSION; }
+
+const char *qvg_last_error(void) { return g_last_error.c_str(); }
+
+static int create_impl(uint32_t n, uint32_t precision, int device, uint32_t rank, uint32_t world,
+                       const void *nccl_id, bool virtual_shards, qvg_state **out) {
+    return guarded([&] {
+        if (!out) throw Validation("null output pointer");
+        *out = nullptr;
+        if (precision != QVG_C64 && precision != QVG_C128)
+            throw Validation("precision must be 64 (complex64) or 128 (complex128)");
+        if (world == 0 || (world & (world - 1)) != 0) throw Validation("world size must be a power of two");
+        if (rank >= world) throw Validation("rank out of range");
+        uint32_t g = 0;
+        while ((1u << g) < world) ++g;
+        if (n < 1 || n > 40) throw Validation("n_qubits must be in [1, 40]");
+        if (n < g + 2 && world > 1) throw Validation("too few qubits for this many shards");
+        int ndev = 0;
+        cuda_check(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+        if (device < 0 || device >= ndev) throw CudaFail(QVG_ERR_NO_DEVICE, "no CUDA device " + std::to_string(device));
+        auto *s = new qvg_state();
+        s->device = device;
+        s->n = n;
+        s->L = n - g;
+        s->precision = precision;
+        s->S = precision == QVG_C128 ? 16 : 8;
+        s->rank = rank;
+        s->world = world;
+        s->tile_qubits = precision == QVG_C128 ? 12 : 13;
+        s->carriers = precision == QVG_C128 ? 3 : 4;
+        try {
+            set_device(s);
+            cuda_check(cudaDeviceGetAttribute(&s->sm_count, cudaDevAttrMultiProcessorCount, device), "sm count");
+            cuda_check(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+            cuda_check(cudaMalloc(&s->d_partials, kNormBlocks * sizeof(double)), "cudaMalloc(partials)");
+            s->shards.init(*s, n, s->L, rank, world, nccl_id, virtual_shards);
+            shard_init_basis(*s, s->shards, 0);
+            cuda_check(cudaStreamSynchronize(s->stream), "init sync");
+        } catch (...) {
+            s->shards.release();
+            if (s->d_partials) cudaFree(s->d_partials);
+            if (s->stream) cudaStreamDestroy(s->stream);
+            delete s;
+            throw;
+        }
+        *out = s;
+    });
+}
+
+int qvg_create(uint32_t n_qubits, uint32_t precision, int device, qvg_state **out) {
+    return create_impl(n_qubits, precision, device, 0, 1, nullptr, false, out);
+}
+
+int qvg_create_sharded(uint32_t n_qubits, uint32_t precision, int device, uint32_t rank, uint32_t world,
+                       const void *nccl_id, qvg_state **out) {
+    // nccl_id == NULL: all `world` shards live on this device in one process
+    // (virtual shards; exchanges are device copies). Used to test the sharded
+    // path bit-for-bit on one GPU.
+    return create_impl(n_qubits, precision, device, nccl_id ? rank : 0, world, nccl_id, nccl_id == nullptr, out);
+}
+
+int qvg_nccl_unique_id(void *out128) {
+    return guarded([&] {
+        if (!out128) throw Validation("null output pointer");
+        shard_nccl_unique_id(out128);
+    });
+}
+
+int qvg_destroy(qvg_state *s) {
+    return guarded([&] {
+        if (!s) return;
+        cudaSetDevice(s->device);
+        if (s->stream) cudaStreamSynchronize(s->stream);
+        s->shards.release();
+        if (s->d_ops) cudaFree(s->d_ops);
+        if (s->d_partials) cudaFree(s->d_partials);
+        if (s->d_probs) cudaFree(s->d_probs);
+        if (s->stream) cudaStreamDestroy(s->stream);
+        delete s;
+    });
+}
+
+int qvg_info(const qvg_state *s, uint32_t *n, uint32_t *precision, uint32_t *rank, uint32_t *world) {
+    return guarded([&] {
+        check_state(s);
+        if (n) *n = s->n;
+        if (precision) *precision = s->precision;
+        if (rank) *rank = s->rank;
+        if (world) *world = s->world;
+    });
+}
+
+int qvg_set_option(qvg_state *s, int key, int64_t value) {
+    return guarded([&] {
+        check_state(s);
+        switch (key) {
+        case QVG_OPT_FUSE: s->fuse = value != 0; break;
+        case QVG_OPT_TILE_QUBITS: {
+            const int64_t maxk = s->precision == QVG_C128 ? 13 : 14;
+            if (value < 2 || value > maxk) throw Validation("tile_qubits out of range");
+            s->tile_qubits = (uint32_t)value;
+            break;
+        }
+        case QVG_OPT_CARRIERS:
+            if (value < 0 || value > 10) throw Validation("carriers out of range");
+            s->carriers = (uint32_t)value;
+            break;
+        case QVG_OPT_LOW_KERNEL: s->low_kernel = value != 0; break;
+        default: throw Validation("unknown option " + std::to_string(key));
+        }
+    });
+}
+
+int qvg_init_basis(qvg_state *s, uint64_t index) {
+    return guarded([&] {
+        check_state(s);
+        if (index >= (1ull << s->n)) throw Validation("basis index out of range");
+        set_device(s);
+        shard_init_basis(*s, s->shards, index);
+        cuda_check(cudaStreamSynchronize(s->stream), "init_basis");
+    });
+}
+
+int qvg_load(qvg_state *s, const void *host, uint64_t offset, uint64_t count) {
+    return guarded([&] {
+        check_state(s);
+        check_range(s, offset, count);
+        if (count && !host) throw Validation("null host buffer");
+        set_device(s);
+        shard_transfer(*s, s->shards, const_cast<void *>(host), offset, count, true);
+    });
+}
+
+int qvg_read(qvg_state *s, void *host, uint64_t offset, uint64_t count) {
+    return guarded([&] {
+        check_state(s);
+        check_range(s, offset, count);
+        if (count && !host) throw Validation("null host buffer");
+        set_device(s);
+        shard_transfer(*s, s->shards, host, offset, count, false);
+    });
+}
+
+int qvg_apply(qvg_state *s, const qvg_gate *ops, uint64_t count) {
+    return guarded([&] {
+        check_state(s);
+        if (count && !ops) throw Validation("null op array");
+        for (uint64_t i = 0; i < count; ++i) validate_op(ops[i], s->n, i);
+        set_device(s);
+        shard_apply(*s, s->shards, ops, count);
+        s->stats.gates_applied += count;
+    });
+}
+
+int qvg_sync(qvg_state *s) {
+    return guarded([&] {
+        check_state(s);
+        set_device(s);
+        cuda_check(cudaStreamSynchronize(s->stream), "cudaStreamSynchronize");
+    });
+}
+
+int qvg_norm(qvg_state *s, double *out) {
+    return guarded([&] {
+        check_state(s);
+        if (!out) throw Validation("null output pointer");
+        set_device(s);
+        std::vector<double> partial(kNormBlocks);
+        double sum = 0.0, carry = 0.0;
+        auto kahan = [&](double term) {
+            const double t = term - carry;
+            const double next = sum + t;
+            carry = (next - sum) - t;
+            sum = next;
+        };
+        const uint64_t local = 1ull << s->L;
+        for (void *psi : s->shards.local_buffers()) {
+            if (s->precision == QVG_C128)
+                k_norm_partials<double><<<kNormBlocks, 256, 0, s->stream>>>(static_cast<const double2 *>(psi), local,
+                                                                            s->d_partials);
+            else
+                k_norm_partials<float><<<kNormBlocks, 256, 0, s->stream>>>(static_cast<const float2 *>(psi), local,
+                                                                           s->d_partials);
+            cuda_check(cudaGetLastError(), "norm launch");
+            cuda_check(cudaMemcpyAsync(partial.data(), s->d_partials, kNormBlocks * sizeof(double),
+                                       cudaMemcpyDeviceToHost, s->stream),
+                       "norm D2H");
+            cuda_check(cudaStreamSynchronize(s->stream), "norm sync");
+            for (double v : partial) kahan(v);
+        }
+        sum = shard_allreduce_sum(*s, s->shards, sum);
+        *out = std::sqrt(sum);
+    });
+}
+
+int qvg_probabilities(qvg_state *s, double *out, uint64_t offset, uint64_t count) {
+    return guarded([&] {
+        check_state(s);
+        check_range(s, offset, count);
+        if (count && !out) throw Validation("null output pointer");
+        set_device(s);
+        shard_canonicalize(*s, s->shards);
+        if (!s->d_probs) cuda_check(cudaMalloc(&s->d_probs, kProbChunk * sizeof(double)), "cudaMalloc(probs)");
+        // Each rank fills the part of [offset, offset+count) it owns; the
+        // rest of `out` is left untouched (gather is the caller's job).
+        const uint64_t local = 1ull << s->L;
+        const std::vector<void *> bufs = s->shards.local_buffers();
+        const std::vector<uint32_t> ranks = s->shards.local_ranks();
+        for (size_t b = 0; b < bufs.size(); ++b) {
+            const uint64_t lo = (uint64_t)ranks[b] * local, hi = lo + local;
+            const uint64_t a = std::max(lo, offset), e = std::min(hi, offset + count);
+            for (uint64_t x = a; x < e; x += kProbChunk) {
+                const uint64_t c = std::min(kProbChunk, e - x);
+                const unsigned grid = (unsigned)std::min<uint64_t>((c + 255) / 256, 4096);
+                if (s->precision == QVG_C128)
+                    k_probs<double><<<grid, 256, 0, s->stream>>>(static_cast<const double2 *>(bufs[b]) + (x - lo), c,
+                                                                 s->d_probs);
+                else
+                    k_probs<float><<<grid, 256, 0, s->stream>>>(static_cast<const float2 *>(bufs[b]) + (x - lo), c,
+                                                                s->d_probs);
+                cuda_check(cudaGetLastError(), "probs launch");
+                cuda_check(cudaMemcpyAsync(out + (x - offset), s->d_probs, c * sizeof(double), cudaMemcpyDeviceToHost,
+                                           s->stream),
+                           "probs D2H");
+            }
+        }
+        cuda_check(cudaStreamSynchronize(s->stream), "probs sync");
+    });
+}
+
+int qvg_top_amplitudes(qvg_state *s, uint32_t k, uint64_t *index_out, double *amps_out) {
+    return guarded([&] {
+        check_state(s);
+        if (k && (!index_out || !amps_out)) throw Validation("null output pointer");
+        set_device(s);
+        shard_top_amplitudes(*s, s->shards, k, index_out, amps_out);
+    });
+}
+
+int qvg_stats_get(const qvg_state *s, qvg_stats *out) {
+    return guarded([&] {
+        check_state(s);
+        if (!out) throw Validation("null output pointer");
+        *out = s->stats;
+    });
+}
+
+int qvg_stats_reset(qvg_state *s) {
+    return guarded([&] {
+        check_state(s);
+        s->stats = qvg_stats{};
+    });
+}
+
+int qvg_stream(const qvg_state *s, void **stream_out) {
+    return guarded([&] {
+        check_state(s);
+        if (!stream_out) throw Validation("null output pointer");
+        *stream_out = (void *)s->stream;
+    });
+}
+
+int qvg_device_buffer(const qvg_state *s, void **ptr_out, uint64_t *bytes_out) {
+    return guarded([&] {
+        check_state(s);
+        const std::vector<void *> bufs = const_cast<qvg_state *>(s)->shards.local_buffers();
+        if (ptr_out) *ptr_out = bufs.empty() ? nullptr : bufs[0];
+        if (bytes_out) *bytes_out = (uint64_t)s->S << s->L;
+    });
+}
+
+int qvg_plan_passes(uint32_t n_qubits, uint32_t precision, int fuse, uint32_t tile_qubits, uint32_t carriers,
+                    const qvg_gate *ops, uint64_t count, uint64_t *passes_out, uint64_t *fused_out,
+                    uint64_t *bytes_out) {
+    return guarded([&] {
+        if (precision != QVG_C64 && precision != QVG_C128) throw Validation("precision must be 64 or 128");
+        if (n_qubits < 1 || n_qubits > 40) throw Validation("n_qubits must be in [1, 40]");
+        if (count && !ops) throw Validation("null op array");
+        for (uint64_t i = 0; i < count; ++i) validate_op(ops[i], n_qubits, i);
+        PlanOptions po;
+        po.n = n_qubits;
+        po.amp_bytes = precision == QVG_C128 ? 16 : 8;
+        po.fuse = fuse != 0;
+        po.tile_qubits = tile_qubits ? tile_qubits : (precision == QVG_C128 ? 12 : 13);
+        po.carriers = carriers;
+        const Plan plan = make_plan(ops, count, po);
+        uint64_t fused = 0, bytes = 0;
+        for (const Pass &p : plan.passes) {
+            fused += p.kind == PASS_TILE;
+            bytes += p.bytes;
+        }
+        if (passes_out) *passes_out = plan.passes.size();
+        if (fused_out) *fused_out = fused;
+        if (bytes_out) *bytes_out = bytes;
+    });
+}
+
+int qvg_shard_schedule(uint32_t n_qubits, uint32_t world, const qvg_gate *ops, uint64_t count, int canonicalize,
+                       qvg_shard_step *steps, uint64_t cap, uint64_t *nsteps) {
+    return guarded([&] {
+        if (world == 0 || (world & (world - 1)) != 0) throw Validation("world size must be a power of two");
+        uint32_t g = 0;
+        while ((1u << g) < world) ++g;
+        if (n_qubits < g + 2 || n_qubits > 40) throw Validation("too few qubits for this many shards");
+        if (count && !ops) throw Validation("null op array");
+        for (uint64_t i = 0; i < count; ++i) validate_op(ops[i], n_qubits, i);
+        const uint32_t L = n_qubits - g;
+        QubitMap map;
+        map.reset(n_qubits);
+        std::vector<ShardStep> out;
+        schedule_ops(n_qubits, L, ops, count, map, out);
+        if (canonicalize) schedule_canonicalize(n_qubits, L, map, out);
+        if (nsteps) *nsteps = out.size();
+        if (steps) std::memcpy(steps, out.data(), std::min<uint64_t>(cap, out.size()) * sizeof(ShardStep));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,356 @@
+// qvg_kernels.cuh — sm_100a gate-application kernels.
+//
+// Every kernel is an HBM-bound streaming read-modify-write over the amplitude
+// array (0.44 flop/B for complex128), so the design targets bytes:
+// 16-B vector accesses, enumeration of only the amplitudes a gate changes,
+// and a fused tile pass that applies a run of gates per HBM round trip.
+//
+// Arithmetic parity (reference proj/src/kernel.cpp:14-19): the reference's
+// apply_pair is `lo = u00*a + u01*b; hi = u10*a + u11*b` on std::complex<double>
+// built at -O2 without -march, i.e. (ac-bd, ad+bc) per product and a plain add,
+// no FMA. The complex128 kernels use __dmul_rn/__dsub_rn/__dadd_rn so nvcc
+// cannot contract them, which makes the c128 results bit-identical to the
+// reference. Complex64 (not in the reference) lets the compiler use FFMA.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace qvg {
+
+template <class R> struct Cplx;
+template <> struct Cplx<double> { using T = double2; };
+template <> struct Cplx<float> { using T = float2; };
+
+// Row-major 2x2 matrix as 8 reals: re00 im00 re01 im01 re10 im10 re11 im11.
+template <class R> struct Mat { R u[8]; };
+
+// (m0 * a) + (m1 * b), complex128, reference operation order, no contraction.
+__device__ __forceinline__ double2 madd2(double m0r, double m0i, double2 a, double m1r,
+                                         double m1i, double2 b) {
+    const double re = __dadd_rn(__dsub_rn(__dmul_rn(m0r, a.x), __dmul_rn(m0i, a.y)),
+                                __dsub_rn(__dmul_rn(m1r, b.x), __dmul_rn(m1i, b.y)));
+    const double im = __dadd_rn(__dadd_rn(__dmul_rn(m0r, a.y), __dmul_rn(m0i, a.x)),
+                                __dadd_rn(__dmul_rn(m1r, b.y), __dmul_rn(m1i, b.x)));
+    return make_double2(re, im);
+}
+__device__ __forceinline__ float2 madd2(float m0r, float m0i, float2 a, float m1r, float m1i,
+                                        float2 b) {
+    return make_float2(m0r * a.x - m0i * a.y + (m1r * b.x - m1i * b.y),
+                       m0r * a.y + m0i * a.x + (m1r * b.y + m1i * b.x));
+}
+// d * a. For a diagonal gate the reference computes (0*a) + (d*b); adding the
+// +-0 product leaves d*b unchanged (up to the sign of an exact zero), so this
+// is value-identical to the reference.
+__device__ __forceinline__ double2 cmul(double dr, double di, double2 a) {
+    return make_double2(__dsub_rn(__dmul_rn(dr, a.x), __dmul_rn(di, a.y)),
+                        __dadd_rn(__dmul_rn(dr, a.y), __dmul_rn(di, a.x)));
+}
+__device__ __forceinline__ float2 cmul(float dr, float di, float2 a) {
+    return make_float2(dr * a.x - di * a.y, dr * a.y + di * a.x);
+}
+
+// Streaming loads/stores: every amplitude is touched once per pass, so mark
+// the lines evict-first in L2 (ld.global.cs / st.global.cs).
+__device__ __forceinline__ double2 ld_amp(const double2 *p) { return __ldcs(p); }
+__device__ __forceinline__ float2 ld_amp(const float2 *p) { return __ldcs(p); }
+__device__ __forceinline__ void st_amp(double2 *p, double2 v) { __stcs(p, v); }
+__device__ __forceinline__ void st_amp(float2 *p, float2 v) { __stcs(p, v); }
+
+__device__ __forceinline__ double shfl_x(double v, int m) { return __shfl_xor_sync(0xffffffffu, v, m); }
+__device__ __forceinline__ float shfl_x(float v, int m) { return __shfl_xor_sync(0xffffffffu, v, m); }
+
+// Insert a 0 bit at position b (b < 64): the pair-base enumeration of
+// reference kernel.cpp:72-73 without the nested loop.
+__device__ __forceinline__ uint64_t ins0(uint64_t x, int b) {
+    const uint64_t low = (1ull << b) - 1ull;
+    return ((x & ~low) << 1) | (x & low);
+}
+
+// ---------------------------------------------------------------------------
+// K1: pairs kernel, any target. Enumerates pair bases with a 0 inserted at the
+// target bit and, for a controlled op, the control bit inserted as 1 — so a
+// controlled gate touches only the 2^(n-1) amplitudes whose control bit is 1
+// (the reference streams all of them, kernel.cpp:74-76). ins_lo < ins_hi are
+// the inserted positions (ins_hi = -1 when only the target is inserted); setm
+// is the mask of inserted bits that are 1 (the control).
+// Each thread owns PPT pairs, strided by blockDim so every load instruction of
+// a warp covers consecutive bases.
+template <class R, int PPT>
+__global__ void __launch_bounds__(256)
+k_pairs(typename Cplx<R>::T *__restrict__ psi, int q, int ins_lo, int ins_hi, uint64_t setm, Mat<R> m) {
+    using T = typename Cplx<R>::T;
+    const uint64_t qb = 1ull << q;
+    const uint64_t first = (uint64_t)blockIdx.x * (blockDim.x * PPT) + threadIdx.x;
+    uint64_t lo[PPT];
+    T a[PPT], b[PPT];
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+        uint64_t x = ins0(first + (uint64_t)k * blockDim.x, ins_lo);
+        if (ins_hi >= 0) x = ins0(x, ins_hi);
+        lo[k] = x | setm;
+        a[k] = ld_amp(psi + lo[k]);
+        b[k] = ld_amp(psi + (lo[k] | qb));
+    }
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+        st_amp(psi + lo[k], madd2(m.u[0], m.u[1], a[k], m.u[2], m.u[3], b[k]));
+        st_amp(psi + (lo[k] | qb), madd2(m.u[4], m.u[5], a[k], m.u[6], m.u[7], b[k]));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K2: low-target kernel (target < 5). A warp loads 32 consecutive amplitudes
+// (512 B c128, fully coalesced, one 16-B access per lane) and finds each
+// partner with __shfl_xor(lane ^ 2^q). Each lane writes its own amplitude with
+// the reference expression for its role (lo or hi). A control bit >= 5 is
+// inserted into the enumeration (only control=1 runs are read); a control
+// bit < 5 is a per-lane predicate.
+template <class R, int APT>
+__global__ void __launch_bounds__(256)
+k_low(typename Cplx<R>::T *__restrict__ psi, int q, int c_ins, int c_lane, Mat<R> m) {
+    using T = typename Cplx<R>::T;
+    const uint64_t first = (uint64_t)blockIdx.x * (blockDim.x * APT) + threadIdx.x;
+    const int qm = 1 << q;
+    uint64_t j[APT];
+    T v[APT];
+#pragma unroll
+    for (int k = 0; k < APT; ++k) {
+        uint64_t x = first + (uint64_t)k * blockDim.x;
+        if (c_ins >= 0) x = ins0(x, c_ins) | (1ull << c_ins);
+        j[k] = x;
+        // Control below bit 5 is a lane predicate; the partner shares it, so
+        // control=0 lanes neither load nor store (their sectors stay cold).
+        if (c_lane < 0 || ((x >> c_lane) & 1ull)) v[k] = ld_amp(psi + x);
+        else v[k] = T{};
+    }
+#pragma unroll
+    for (int k = 0; k < APT; ++k) {
+        T p;
+        p.x = shfl_x(v[k].x, qm);
+        p.y = shfl_x(v[k].y, qm);
+        const bool hi = (j[k] >> q) & 1ull;
+        const T out = hi ? madd2(m.u[4], m.u[5], p, m.u[6], m.u[7], v[k])
+                         : madd2(m.u[0], m.u[1], v[k], m.u[2], m.u[3], p);
+        if (c_lane < 0 || ((j[k] >> c_lane) & 1ull)) st_amp(psi + j[k], out);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K3: phase kernel for gates diag(1, d) with optional control (Z, S, T, CZ,
+// CP/R_k): only amplitudes whose target (and control) bits are all 1 change,
+// a quarter of the state for CZ/CP and half for Z/S/T. ins_lo < ins_hi are the
+// forced-1 bit positions (ins_hi = -1 for an uncontrolled phase).
+template <class R, int APT>
+__global__ void __launch_bounds__(256)
+k_phase(typename Cplx<R>::T *__restrict__ psi, int ins_lo, int ins_hi, uint64_t setm, R dr, R di) {
+    const uint64_t first = (uint64_t)blockIdx.x * (blockDim.x * APT) + threadIdx.x;
+    uint64_t j[APT];
+    typename Cplx<R>::T v[APT];
+#pragma unroll
+    for (int k = 0; k < APT; ++k) {
+        uint64_t x = ins0(first + (uint64_t)k * blockDim.x, ins_lo);
+        if (ins_hi >= 0) x = ins0(x, ins_hi);
+        j[k] = x | setm;
+        v[k] = ld_amp(psi + j[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < APT; ++k) st_amp(psi + j[k], cmul(dr, di, v[k]));
+}
+
+// ---------------------------------------------------------------------------
+// K4: fused tile pass — the B200 replacement for the reference's block store +
+// sliding window (store.cpp, cache.cpp, kernel.cpp:113-146). A CTA stages a
+// tile of 2^k amplitudes in shared memory, applies a run of gates in circuit
+// order, and writes the tile back: one HBM round trip for the whole run. The
+// tile is the set of amplitudes that agree on every qubit outside the tile
+// qubit set Q (|Q| = k): its lowest `lowc` qubits are 0..lowc-1 (contiguous
+// 2^lowc-amp segments in HBM); the other k-lowc are arbitrary high qubits, so
+// gates on any qubit can be fused. A control outside Q is constant per tile,
+// and a diagonal gate needs no pairing, so its qubits may lie anywhere.
+enum TileOpKind : int32_t { TILE_PAIR = 0, TILE_DIAG = 1 };
+
+struct TileOp {
+    int32_t kind;      // TileOpKind
+    int32_t tbit;      // tile-local target bit, -1 if the target is outside Q (diag only)
+    int32_t cbit;      // tile-local control bit, -1 if none or outside Q
+    int32_t d0_is_one; // diag: d0 == 1 exactly, so bit-0 amplitudes are untouched
+    uint64_t greq;     // global bits that must be 1 in the tile base (controls outside Q)
+    uint64_t gtgt;     // diag with target outside Q: that global bit
+    double u[8];       // matrix (diag uses u00 = u[0..1], u11 = u[6..7])
+};
+
+struct TileGeom {
+    int n, k, lowc;       // qubits, tile qubits, contiguous low qubits
+    int nhi;              // k - lowc
+    int hiq[24];          // tile qubits >= lowc, ascending (tile-local bits lowc..k-1)
+    uint64_t outmask;     // qubits not in Q
+    uint64_t ntiles;      // 2^(n-k)
+};
+
+__device__ __forceinline__ uint64_t pdep_mask(uint64_t v, uint64_t mask) {
+    uint64_t r = 0;
+    while (mask) {
+        const uint64_t bit = mask & (~mask + 1ull);
+        if (v & 1ull) r |= bit;
+        v >>= 1;
+        mask ^= bit;
+    }
+    return r;
+}
+
+template <class R>
+__device__ __forceinline__ void tile_apply_op(typename Cplx<R>::T *sm, int k, const TileOp &op,
+                                              uint64_t base) {
+    using T = typename Cplx<R>::T;
+    const uint32_t namps = 1u << k;
+    if ((base & op.greq) != op.greq) return;  // control outside the tile is 0
+    if (op.kind == TILE_PAIR) {
+        const R u0 = (R)op.u[0], u1 = (R)op.u[1], u2 = (R)op.u[2], u3 = (R)op.u[3];
+        const R u4 = (R)op.u[4], u5 = (R)op.u[5], u6 = (R)op.u[6], u7 = (R)op.u[7];
+        const uint32_t tb = 1u << op.tbit;
+        const uint32_t low = tb - 1u;
+        for (uint32_t p = threadIdx.x; p < (namps >> 1); p += blockDim.x) {
+            const uint32_t lo = ((p & ~low) << 1) | (p & low);
+            if (op.cbit >= 0 && !((lo >> op.cbit) & 1u)) continue;
+            const T a = sm[lo], b = sm[lo | tb];
+            sm[lo] = madd2(u0, u1, a, u2, u3, b);
+            sm[lo | tb] = madd2(u4, u5, a, u6, u7, b);
+        }
+    } else {
+        const R d0r = (R)op.u[0], d0i = (R)op.u[1], d1r = (R)op.u[6], d1i = (R)op.u[7];
+        if (op.tbit < 0) {
+            const bool one = (base & op.gtgt) != 0;
+            if (!one && op.d0_is_one) return;
+            const R dr = one ? d1r : d0r, di = one ? d1i : d0i;
+            for (uint32_t l = threadIdx.x; l < namps; l += blockDim.x) {
+                if (op.cbit >= 0 && !((l >> op.cbit) & 1u)) continue;
+                sm[l] = cmul(dr, di, sm[l]);
+            }
+        } else {
+            for (uint32_t l = threadIdx.x; l < namps; l += blockDim.x) {
+                if (op.cbit >= 0 && !((l >> op.cbit) & 1u)) continue;
+                const bool one = (l >> op.tbit) & 1u;
+                if (!one && op.d0_is_one) continue;
+                sm[l] = one ? cmul(d1r, d1i, sm[l]) : cmul(d0r, d0i, sm[l]);
+            }
+        }
+    }
+}
+
+template <class R>
+__global__ void __launch_bounds__(512)
+k_tile(typename Cplx<R>::T *__restrict__ psi, TileGeom g, const TileOp *__restrict__ ops, int nops) {
+    using T = typename Cplx<R>::T;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T *sm = reinterpret_cast<T *>(smem_raw);
+    uint64_t *offhi = reinterpret_cast<uint64_t *>(smem_raw + (sizeof(T) << g.k));
+    const uint32_t namps = 1u << g.k;
+    const uint32_t nhi = 1u << g.nhi;
+    const uint32_t lowm = (1u << g.lowc) - 1u;
+    for (uint32_t h = threadIdx.x; h < nhi; h += blockDim.x) {
+        uint64_t off = 0;
+        for (int i = 0; i < g.nhi; ++i)
+            if ((h >> i) & 1u) off |= 1ull << g.hiq[i];
+        offhi[h] = off;
+    }
+    __syncthreads();
+    for (uint64_t tile = blockIdx.x; tile < g.ntiles; tile += gridDim.x) {
+        const uint64_t base = pdep_mask(tile, g.outmask);
+        for (uint32_t l = threadIdx.x; l < namps; l += blockDim.x)
+            sm[l] = ld_amp(psi + (base | offhi[l >> g.lowc] | (l & lowm)));
+        __syncthreads();
+        for (int i = 0; i < nops; ++i) {
+            const TileOp op = ops[i];
+            tile_apply_op<R>(sm, g.k, op, base);
+            __syncthreads();
+        }
+        for (uint32_t l = threadIdx.x; l < namps; l += blockDim.x)
+            st_amp(psi + (base | offhi[l >> g.lowc] | (l & lowm)), sm[l]);
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K5: swap two local qubits a < b in place (pure permutation: amplitudes with
+// bits (a,b) = (1,0) trade places with (0,1)). Used to restore the canonical
+// qubit order of a sharded state and to move a qubit onto the exchange bit.
+template <class R, int APT>
+__global__ void __launch_bounds__(256)
+k_swap_bits(typename Cplx<R>::T *__restrict__ psi, int a, int b) {
+    using T = typename Cplx<R>::T;
+    const uint64_t first = (uint64_t)blockIdx.x * (blockDim.x * APT) + threadIdx.x;
+    uint64_t i0[APT];
+    T x[APT], y[APT];
+#pragma unroll
+    for (int k = 0; k < APT; ++k) {
+        const uint64_t base = ins0(ins0(first + (uint64_t)k * blockDim.x, a), b);
+        i0[k] = base;
+        x[k] = ld_amp(psi + (base | (1ull << a)));
+        y[k] = ld_amp(psi + (base | (1ull << b)));
+    }
+#pragma unroll
+    for (int k = 0; k < APT; ++k) {
+        st_amp(psi + (i0[k] | (1ull << a)), y[k]);
+        st_amp(psi + (i0[k] | (1ull << b)), x[k]);
+    }
+}
+
+// K6: exchange two equal-length ranges (virtual-shard half exchange: both
+// shards live on this device). 16-B accesses, APT per thread.
+template <class R, int APT>
+__global__ void __launch_bounds__(256)
+k_swap_ranges(typename Cplx<R>::T *__restrict__ p, typename Cplx<R>::T *__restrict__ q) {
+    using T = typename Cplx<R>::T;
+    const uint64_t first = (uint64_t)blockIdx.x * (blockDim.x * APT) + threadIdx.x;
+    T x[APT], y[APT];
+#pragma unroll
+    for (int k = 0; k < APT; ++k) {
+        x[k] = ld_amp(p + first + (uint64_t)k * blockDim.x);
+        y[k] = ld_amp(q + first + (uint64_t)k * blockDim.x);
+    }
+#pragma unroll
+    for (int k = 0; k < APT; ++k) {
+        st_amp(p + first + (uint64_t)k * blockDim.x, y[k]);
+        st_amp(q + first + (uint64_t)k * blockDim.x, x[k]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Readout.
+// Per-block partial sums of |a|^2 with a fixed grid, so the result is
+// deterministic run to run (the host sums the partials with Kahan, like
+// BlockStore::norm, reference store.cpp:301-316).
+template <class R>
+__global__ void __launch_bounds__(256)
+k_norm_partials(const typename Cplx<R>::T *__restrict__ psi, uint64_t count, double *__restrict__ partial) {
+    __shared__ double red[256];
+    double acc = 0.0;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const typename Cplx<R>::T v = psi[i];
+        const double x = (double)v.x, y = (double)v.y;
+        acc += __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y));
+    }
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+}
+
+// |a_i|^2 = re*re + im*im (std::norm, reference engine.cpp:518).
+template <class R>
+__global__ void __launch_bounds__(256)
+k_probs(const typename Cplx<R>::T *__restrict__ psi, uint64_t count, double *__restrict__ out) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const typename Cplx<R>::T v = psi[i];
+        const double x = (double)v.x, y = (double)v.y;
+        out[i] = __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y));
+    }
+}
+
+}  // namespace qvg

@@ -1,0 +1,234 @@
+// qvg_plan.hpp — host-side pass planner (no CUDA calls; unit-testable on CPU
+// through qvg_plan_passes).
+//
+// The reference makes exactly one streaming traversal per gate
+// (reference kernel.cpp:132-146: no fusion). The planner maps a
+// circuit onto HBM passes instead:
+//   * one single-gate pass per op, choosing the kernel that touches the fewest
+//     bytes (controlled ops read only control=1 amplitudes, diag(1,d) ops only
+//     the amplitudes whose bits are all 1, identities nothing), or
+//   * one fused tile pass for a maximal run of consecutive ops whose
+//     non-diagonal targets fit in one tile qubit set, when that run would cost
+//     more than one full read+write as single passes.
+// Ops are never reordered, so every amplitude sees the same operations in the
+// same order as in the reference: complex128 results stay bit-identical.
+#pragma once
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "qvg.h"
+#include "qvg_kernels.cuh"
+
+namespace qvg {
+
+struct Validation : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+enum PassKind { PASS_PAIRS = 0, PASS_LOW = 1, PASS_PHASE = 2, PASS_TILE = 3 };
+
+struct OpInfo {
+    bool diag = false;      // u01 == u10 == 0
+    bool phase = false;     // diag and u00 == 1 + 0i
+    bool identity = false;  // phase and u11 == 1 + 0i
+    int target = 0;
+    int control = -1;
+};
+
+inline OpInfo classify(const qvg_gate &g) {
+    OpInfo o;
+    const double *u = g.u;
+    o.diag = u[2] == 0.0 && u[3] == 0.0 && u[4] == 0.0 && u[5] == 0.0;
+    o.phase = o.diag && u[0] == 1.0 && u[1] == 0.0;
+    o.identity = o.phase && u[6] == 1.0 && u[7] == 0.0;
+    o.target = (int)g.target;
+    o.control = g.kind == QVG_OP_CONTROLLED ? g.control : -1;
+    return o;
+}
+
+// Reference validate_circuit (circuit.cpp:31-52) + apply_gate_streamed's
+// check (kernel.cpp:134-140).
+inline void validate_op(const qvg_gate &g, uint32_t n, uint64_t idx) {
+    const std::string at = "op " + std::to_string(idx) + ": ";
+    if (g.kind != QVG_OP_SINGLE && g.kind != QVG_OP_CONTROLLED)
+        throw Validation(at + "unknown op kind " + std::to_string(g.kind));
+    if (g.flags != 0) throw Validation(at + "reserved flags must be 0");
+    if (g.target >= n)
+        throw Validation(at + "target " + std::to_string(g.target) + " >= n_qubits " + std::to_string(n));
+    if (g.kind == QVG_OP_CONTROLLED) {
+        if (g.control < 0 || (uint32_t)g.control >= n)
+            throw Validation(at + "control " + std::to_string(g.control) + " >= n_qubits " + std::to_string(n));
+        if ((uint32_t)g.control == g.target)
+            throw Validation(at + "control equals target (" + std::to_string(g.target) + ")");
+    }
+    for (int i = 0; i < 8; ++i)
+        if (!(g.u[i] - g.u[i] == 0.0)) throw Validation(at + "matrix entry is not finite");
+}
+
+struct Pass {
+    PassKind kind = PASS_PAIRS;
+    qvg_gate op{};          // single-gate passes
+    OpInfo info{};
+    TileGeom geom{};        // tile passes
+    uint32_t op_begin = 0;  // into Plan::tile_ops
+    uint32_t op_count = 0;
+    uint64_t bytes = 0;     // algorithmic HBM bytes (read + write, sector-rounded)
+    uint64_t gates = 0;     // circuit ops covered
+};
+
+struct Plan {
+    std::vector<Pass> passes;
+    std::vector<TileOp> tile_ops;
+    uint64_t gates = 0;
+};
+
+struct PlanOptions {
+    uint32_t n = 0;          // qubits addressed by the kernels (local qubits when sharded)
+    uint32_t amp_bytes = 16; // 16 complex128, 8 complex64
+    bool fuse = true;
+    uint32_t tile_qubits = 12;
+    uint32_t carriers = 3;
+    bool low_kernel = true;
+};
+
+// 2 * touched * S, rounded up to whole 32-B sectors when the touched runs are
+// shorter than a sector.
+inline uint64_t sector_bytes(uint32_t n, int forced_bits, int lowest_forced, uint32_t S) {
+    const uint64_t touched = 1ull << (n - forced_bits);
+    uint64_t bytes = 2ull * touched * S;
+    if (forced_bits > 0) {
+        const uint64_t run = (1ull << lowest_forced) * S;
+        if (run < 32) bytes *= 32 / run;
+    }
+    return std::min<uint64_t>(bytes, 2ull * (1ull << n) * S);
+}
+
+inline Pass single_pass(const qvg_gate &g, const OpInfo &o, const PlanOptions &po) {
+    Pass p;
+    p.op = g;
+    p.info = o;
+    p.gates = 1;
+    const uint32_t n = po.n, S = po.amp_bytes;
+    if (o.phase) {
+        p.kind = PASS_PHASE;
+        const int lowest = o.control >= 0 ? std::min(o.target, o.control) : o.target;
+        p.bytes = sector_bytes(n, o.control >= 0 ? 2 : 1, lowest, S);
+        return p;
+    }
+    // Low-target kernel needs 32 consecutive enumerated amplitudes per warp.
+    const bool ctl_ins = o.control >= 5;
+    const uint32_t enum_bits = n - (ctl_ins ? 1 : 0);
+    if (po.low_kernel && o.target < 5 && enum_bits >= 5 && n >= 6) {
+        p.kind = PASS_LOW;
+    } else {
+        p.kind = PASS_PAIRS;
+    }
+    p.bytes = o.control >= 0 ? sector_bytes(n, 1, o.control, S) : 2ull * (1ull << n) * S;
+    return p;
+}
+
+inline int local_bit(int q, const TileGeom &g) {
+    if (q < g.lowc) return q;
+    for (int i = 0; i < g.nhi; ++i)
+        if (g.hiq[i] == q) return g.lowc + i;
+    return -1;
+}
+
+inline Plan make_plan(const qvg_gate *ops, uint64_t count, const PlanOptions &po) {
+    Plan plan;
+    const uint32_t n = po.n;
+    const uint64_t full = 2ull * (1ull << n) * po.amp_bytes;
+    const uint32_t k = std::min<uint32_t>(po.tile_qubits, n);
+    const uint32_t lowmin = std::min<uint32_t>(po.carriers, k);
+    std::vector<OpInfo> info(count);
+    for (uint64_t i = 0; i < count; ++i) info[i] = classify(ops[i]);
+    plan.gates = count;
+
+    uint64_t i = 0;
+    while (i < count) {
+        if (!po.fuse) {
+            if (!info[i].identity) plan.passes.push_back(single_pass(ops[i], info[i], po));
+            ++i;
+            continue;
+        }
+        // Greedy maximal run whose non-diagonal targets fit in one tile.
+        std::vector<int> high;  // tile qubits >= lowmin required by the run
+        uint64_t j = i, cost = 0, live = 0;
+        while (j < count) {
+            const OpInfo &o = info[j];
+            if (!o.identity) {
+                if (!o.diag && (uint32_t)o.target >= lowmin &&
+                    std::find(high.begin(), high.end(), o.target) == high.end()) {
+                    if (high.size() == k - lowmin) break;
+                    high.push_back(o.target);
+                }
+                cost += single_pass(ops[j], o, po).bytes;
+                ++live;
+            }
+            ++j;
+        }
+        if (j == i) {  // degenerate tile geometry: nothing fits, fall back
+            plan.passes.push_back(single_pass(ops[i], info[i], po));
+            ++i;
+            continue;
+        }
+        if (live >= 2 && cost > full) {
+            // Tile qubit set Q: carriers 0..lowmin-1, the run's high targets,
+            // then the lowest free qubits until |Q| = k.
+            std::vector<char> inq(n, 0);
+            for (uint32_t q = 0; q < lowmin; ++q) inq[q] = 1;
+            for (int q : high) inq[q] = 1;
+            uint32_t size = lowmin + (uint32_t)high.size();
+            for (uint32_t q = 0; q < n && size < k; ++q)
+                if (!inq[q]) { inq[q] = 1; ++size; }
+            TileGeom g{};
+            g.n = (int)n;
+            g.k = (int)k;
+            g.lowc = 0;
+            while (g.lowc < (int)n && inq[g.lowc]) ++g.lowc;
+            g.nhi = 0;
+            g.outmask = 0;
+            for (uint32_t q = 0; q < n; ++q) {
+                if (!inq[q]) g.outmask |= 1ull << q;
+                else if ((int)q >= g.lowc) g.hiq[g.nhi++] = (int)q;
+            }
+            g.ntiles = 1ull << (n - k);
+            Pass p;
+            p.kind = PASS_TILE;
+            p.geom = g;
+            p.op_begin = (uint32_t)plan.tile_ops.size();
+            for (uint64_t x = i; x < j; ++x) {
+                const OpInfo &o = info[x];
+                if (o.identity) continue;
+                TileOp t{};
+                std::memcpy(t.u, ops[x].u, sizeof(t.u));
+                t.kind = o.diag ? TILE_DIAG : TILE_PAIR;
+                t.tbit = local_bit(o.target, g);
+                if (t.tbit < 0) t.gtgt = 1ull << o.target;
+                t.cbit = -1;
+                if (o.control >= 0) {
+                    t.cbit = local_bit(o.control, g);
+                    if (t.cbit < 0) t.greq = 1ull << o.control;
+                }
+                t.d0_is_one = (ops[x].u[0] == 1.0 && ops[x].u[1] == 0.0) ? 1 : 0;
+                plan.tile_ops.push_back(t);
+            }
+            p.op_count = (uint32_t)(plan.tile_ops.size() - p.op_begin);
+            p.bytes = full;
+            p.gates = j - i;
+            plan.passes.push_back(p);
+        } else {
+            for (uint64_t x = i; x < j; ++x)
+                if (!info[x].identity) plan.passes.push_back(single_pass(ops[x], info[x], po));
+        }
+        i = j;
+    }
+    return plan;
+}
+
+}  // namespace qvg

@@ -1,0 +1,169 @@
+// qvg_schedule.hpp — host-only schedule for a state sharded over G = 2^g
+// ranks. No CUDA; exported through qvg_shard_schedule so the
+// logic is testable on CPU (tests/test_shard_gloo.py runs it over gloo).
+//
+// Layout: rank r owns physical indices [r*2^L, (r+1)*2^L), L = n - g — the
+// reference's contiguous Eq. 9 partition (reference parallel.cpp:13-37,
+// PAPER.md:146). A logical->physical qubit map lets an exchange leave the
+// state permuted instead of swapping back.
+//
+// Per logical op (target t, control c; physical pt, pc):
+//   * local target, local/no control       -> local op
+//   * local target, global control         -> local op on ranks whose control bit is 1
+//   * diagonal op, global target           -> rank-dependent phase, no communication
+//   * non-diagonal op, global target       -> pairwise half-shard exchange that
+//     swaps physical qubit pt with local qubit L-1 (the paper's cross-node pair,
+//     PAPER.md:156-160), then a local op on L-1.
+// Exchanges and local ops only move or combine amplitudes with the reference
+// pair formula, so the final state is bit-identical for every G.
+#pragma once
+
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "qvg.h"
+
+namespace qvg {
+
+enum ShardStepType : uint32_t { STEP_LOCAL = 0, STEP_EXCHANGE = 1, STEP_LOCAL_SWAP = 2 };
+
+// One schedule step; the C layout is qvg_shard_step (include/qvg.h).
+// STEP_LOCAL runs `op` (physical local qubits) on ranks with
+// (rank & rank_mask) == rank_value; STEP_EXCHANGE swaps global physical qubit
+// gpos with local qubit lpos (= L-1); STEP_LOCAL_SWAP swaps local lpos, lpos2.
+using ShardStep = qvg_shard_step;
+
+struct QubitMap {
+    std::vector<uint32_t> perm;  // logical -> physical
+    std::vector<uint32_t> inv;   // physical -> logical
+    void reset(uint32_t n) {
+        perm.resize(n);
+        inv.resize(n);
+        for (uint32_t q = 0; q < n; ++q) perm[q] = inv[q] = q;
+    }
+    void swap_phys(uint32_t a, uint32_t b) {
+        const uint32_t la = inv[a], lb = inv[b];
+        inv[a] = lb;
+        inv[b] = la;
+        perm[la] = b;
+        perm[lb] = a;
+    }
+    bool identity() const {
+        for (uint32_t q = 0; q < perm.size(); ++q)
+            if (perm[q] != q) return false;
+        return true;
+    }
+};
+
+inline bool op_is_diag(const qvg_gate &g) {
+    return g.u[2] == 0.0 && g.u[3] == 0.0 && g.u[4] == 0.0 && g.u[5] == 0.0;
+}
+
+inline qvg_gate diag_gate(uint32_t target, double d0r, double d0i, double d1r, double d1i) {
+    qvg_gate g{};
+    g.kind = QVG_OP_SINGLE;
+    g.target = target;
+    g.control = -1;
+    g.u[0] = d0r; g.u[1] = d0i;
+    g.u[6] = d1r; g.u[7] = d1i;
+    return g;
+}
+
+// Append the steps for logical ops[0..count) to `out`, updating `map`.
+inline void schedule_ops(uint32_t n, uint32_t L, const qvg_gate *ops, uint64_t count, QubitMap &map,
+                         std::vector<ShardStep> &out) {
+    for (uint64_t k = 0; k < count; ++k) {
+        const qvg_gate &g = ops[k];
+        const bool ctl = g.kind == QVG_OP_CONTROLLED;
+        uint32_t pt = map.perm[g.target];
+        const bool diag = op_is_diag(g);
+        if (pt >= L && !diag) {
+            ShardStep ex{};
+            ex.type = STEP_EXCHANGE;
+            ex.gpos = pt;
+            ex.lpos = L - 1;
+            out.push_back(ex);
+            map.swap_phys(pt, L - 1);
+            pt = L - 1;
+        }
+        const int32_t pc = ctl ? (int32_t)map.perm[(uint32_t)g.control] : -1;
+        ShardStep st{};
+        st.type = STEP_LOCAL;
+        st.op = g;
+        if (pc >= (int32_t)L) {  // control on a global qubit: rank predicate
+            st.rank_mask |= 1u << (pc - L);
+            st.rank_value |= 1u << (pc - L);
+            st.op.kind = QVG_OP_SINGLE;
+            st.op.control = -1;
+        } else if (ctl) {
+            st.op.control = pc;
+        }
+        if (pt < L) {
+            st.op.target = pt;
+            out.push_back(st);
+            continue;
+        }
+        // Diagonal op on a global target: amplitude x gets d_b, b = its
+        // global target bit (constant per rank). Reference pair formula with
+        // u01 = u10 = 0 reduces to d_b * x (plus an exact zero).
+        const uint32_t bit = 1u << (pt - L);
+        for (uint32_t b = 0; b < 2; ++b) {
+            const double dr = b ? g.u[6] : g.u[0], di = b ? g.u[7] : g.u[1];
+            if (dr == 1.0 && di == 0.0) continue;
+            ShardStep s2 = st;
+            s2.rank_mask |= bit;
+            s2.rank_value |= b ? bit : 0u;
+            if (s2.op.kind == QVG_OP_CONTROLLED) {
+                // phase d_b on the amplitudes whose (local) control bit is 1
+                s2.op = diag_gate((uint32_t)s2.op.control, 1.0, 0.0, dr, di);
+            } else {
+                s2.op = diag_gate(0, dr, di, dr, di);  // every local amplitude
+            }
+            out.push_back(s2);
+        }
+    }
+}
+
+// Steps that bring the map back to the identity (canonical index order).
+inline void schedule_canonicalize(uint32_t n, uint32_t L, QubitMap &map, std::vector<ShardStep> &out) {
+    auto exchange = [&](uint32_t gpos, uint32_t lpos) {
+        if (lpos != L - 1) {
+            ShardStep sw{};
+            sw.type = STEP_LOCAL_SWAP;
+            sw.lpos = lpos;
+            sw.lpos2 = L - 1;
+            out.push_back(sw);
+            map.swap_phys(lpos, L - 1);
+        }
+        ShardStep ex{};
+        ex.type = STEP_EXCHANGE;
+        ex.gpos = gpos;
+        ex.lpos = L - 1;
+        out.push_back(ex);
+        map.swap_phys(gpos, L - 1);
+    };
+    for (uint32_t p = L; p < n; ++p) {
+        if (map.inv[p] == p) continue;
+        uint32_t cur = map.perm[p];
+        if (cur >= L) {  // logical p sits on another global qubit: route via L-1
+            exchange(cur, L - 1);
+            cur = L - 1;
+        }
+        exchange(p, cur);
+    }
+    for (uint32_t l = 0; l < L; ++l) {
+        if (map.inv[l] == l) continue;
+        const uint32_t cur = map.perm[l];
+        ShardStep sw{};
+        sw.type = STEP_LOCAL_SWAP;
+        sw.lpos = l;
+        sw.lpos2 = cur;
+        out.push_back(sw);
+        map.swap_phys(l, cur);
+    }
+}
+
+}  // namespace qvg

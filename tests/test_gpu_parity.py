@@ -1,0 +1,148 @@
+"""CUDA path vs the oracle (the reference's algorithm, oracle/qv_oracle.c) on
+seeded inputs. complex128 must be BIT-IDENTICAL (np.array_equal; the
+reference's own engines compare with `== 0.0`, reference
+tests/test_kernel.cpp:223-251); complex64 within 1e-5 of the complex128
+oracle (north_star tolerance). Every call goes through the C-ABI (libqvg.so)
+via the host module."""
+import numpy as np
+import pytest
+
+from conftest import gate_array
+
+pytestmark = pytest.mark.gpu
+
+
+def run_gpu(qv, circuit, precision=128, fuse=True, tile_qubits=0, init=None, world=1):
+    if world == 1:
+        st = qv.StateVector.create(circuit.n_qubits, precision, 0)
+    else:
+        st = qv.StateVector.create_sharded(circuit.n_qubits, precision, 0, 0, world, None)
+    if init is not None:
+        st.load_state(init)
+    qv.apply_circuit(st, circuit, strategy="gpu", fuse=fuse, tile_qubits=tile_qubits)
+    return st, st.read_state()
+
+
+# --- reference verify-style trials (reference engine.cpp:253-340) -----------------
+@pytest.mark.parametrize("fuse", [True, False])
+def test_random_circuits_bit_exact(qv, oracle, fuse):
+    rng = np.random.default_rng(1)
+    for trial in range(60):
+        n = int(rng.integers(1, 13))
+        depth = int(rng.integers(1, 60))
+        c = qv.random_circuit(n, depth, 1000 + trial)
+        want = oracle.simulate(n, gate_array(c))
+        _, got = run_gpu(qv, c, fuse=fuse)
+        assert np.array_equal(got, want), (trial, n, depth, np.abs(got - want).max())
+
+
+# --- every op flavour on every qubit (reference test_kernel.cpp:223-251) ------------
+@pytest.mark.parametrize("n", [6, 9, 14])
+def test_each_gate_kind_every_qubit(qv, oracle, n):
+    start_c = qv.random_circuit(n, 40, 21)
+    start = oracle.simulate(n, gate_array(start_c))
+    lines = [f"qubits {n}"]
+    for k in range(n):
+        lines += [f"h {k}", f"rz {k} 0.7", f"cx {(k + 3) % n} {k}", f"cz {(k + 1) % n} {k}",
+                  f"cp {(k + 2) % n} {k} 0.3", f"t {k}", f"x {k}", f"cx {(k + n - 1) % n} {k}"]
+    for line in lines[1:]:
+        c = qv.parse_circuit(f"qubits {n}\n{line}\n")
+        want = oracle.apply(n, start.copy(), gate_array(c))
+        for fuse in (False,):
+            _, got = run_gpu(qv, c, fuse=fuse, init=start)
+            assert np.array_equal(got, want), (line, np.abs(got - want).max())
+    # the whole list fused
+    c = qv.parse_circuit("\n".join(lines) + "\n")
+    want = oracle.apply(n, start.copy(), gate_array(c))
+    for tq in (0, 4, 7):
+        _, got = run_gpu(qv, c, fuse=True, tile_qubits=tq, init=start)
+        assert np.array_equal(got, want), (tq, np.abs(got - want).max())
+
+
+def test_x_permutation_pattern(qv):
+    # reference test_kernel.cpp:125-140: X on qubit 1 swaps at stride 2.
+    st = qv.StateVector.create(3, 128, 0)
+    st.load_state(np.arange(1, 9, dtype=np.complex128))
+    qv.apply_circuit(st, qv.parse_circuit("qubits 3\nx 1\n"))
+    assert np.array_equal(st.read_state().real, [3, 4, 1, 2, 7, 8, 5, 6])
+
+
+def test_control_is_global_index(qv):
+    # reference test_kernel.cpp:142-166: control evaluated on the global index.
+    st = qv.StateVector.create(4, 128, 0)
+    st.load_state(np.arange(16, dtype=np.complex128))
+    qv.apply_circuit(st, qv.parse_circuit("qubits 4\ncx 3 0\n"), fuse=False)
+    got = st.read_state().real
+    want = np.arange(16.0)
+    want[8:] = [9, 8, 11, 10, 13, 12, 15, 14]
+    assert np.array_equal(got, want)
+
+
+# --- BASELINE config 0 (n=20, U3 layers + CX ladder, 780 ops) ------------------------
+@pytest.mark.parametrize("fuse", [True, False])
+def test_config0_bit_exact(qv, oracle, fuse):
+    c = qv.u3_ladder_circuit(20, 20, 1)
+    assert len(c) == 780
+    want = oracle.simulate(20, gate_array(c))
+    st, got = run_gpu(qv, c, fuse=fuse)
+    assert np.array_equal(got, want)
+    assert np.array_equal(st.probabilities(), oracle.probabilities(want))
+    assert abs(st.norm() - oracle.norm(want)) <= 1e-12
+
+
+def test_complex64_within_1e5(qv, oracle):
+    for n, c in [(20, qv.u3_ladder_circuit(20, 20, 1)), (16, qv.haar_sweep_circuit(16, 3)),
+                 (12, qv.random_circuit(12, 200, 5))]:
+        want = oracle.simulate(n, gate_array(c))
+        for fuse in (True, False):
+            _, got = run_gpu(qv, c, precision=64, fuse=fuse)
+            assert np.abs(got - want).max() <= 1e-5, (n, fuse)
+
+
+# --- sharded path on one device (virtual shards) must be bit-identical ----------------
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_virtual_shards_bit_identical(qv, oracle, world):
+    for c in [qv.u3_ladder_circuit(14, 6, 3), qv.random_circuit(12, 300, 9), qv.haar_sweep_circuit(16, 2)]:
+        n = c.n_qubits
+        want = oracle.simulate(n, gate_array(c))
+        for fuse in (True, False):
+            st, got = run_gpu(qv, c, fuse=fuse, world=world)
+            assert np.array_equal(got, want), (world, n, fuse)
+            assert st.stats()["exchanges"] > 0 or world == 1
+
+
+# --- readout ---------------------------------------------------------------------------
+def test_readout(qv, oracle):
+    c = qv.random_circuit(10, 80, 3)
+    want = oracle.simulate(10, gate_array(c))
+    st, _ = run_gpu(qv, c)
+    p = oracle.probabilities(want)
+    assert np.array_equal(st.probabilities(), p)
+    assert np.array_equal(st.probabilities(offset=100, count=50), p[100:150])
+    top = st.top_amplitudes(5)
+    order = sorted(range(len(p)), key=lambda i: (-p[i], i))[:5]
+    assert [i for i, _ in top] == order
+    assert abs(st.norm() - oracle.norm(want)) <= 1e-13
+    assert st.amplitude(7) == want[7]
+
+
+def test_ghz_bell(qv):
+    st = qv.StateVector.create(3, 128, 0)
+    m = qv.apply_circuit(st, qv.parse_circuit("qubits 3\nh 0\ncx 0 1\ncx 1 2\n"), fuse=False)
+    assert m["gates_applied"] == 3 and m["traversals"] == 3 and m["strategy"] == "gpu"
+    s = st.read_state()
+    r = 1 / np.sqrt(2)
+    assert abs(s[0] - r) < 1e-15 and abs(s[7] - r) < 1e-15
+    assert sorted(i for i, _ in st.top_amplitudes(2)) == [0, 7]
+
+
+def test_errors_are_typed(qv):
+    st = qv.StateVector.create(3, 128, 0)
+    with pytest.raises(qv.ValidationError):
+        st.apply_gates(qv.parse_circuit("qubits 5\nh 4\n").gates())
+    with pytest.raises(qv.ValidationError):
+        qv.apply_circuit(st, qv.parse_circuit("qubits 4\nh 0\n"))
+    with pytest.raises(qv.ValidationError):
+        qv.apply_circuit(st, qv.parse_circuit("qubits 3\nh 0\n"), strategy="paired-cached")
+    with pytest.raises(qv.QvsimError):
+        qv.StateVector.create(3, 96, 0)
