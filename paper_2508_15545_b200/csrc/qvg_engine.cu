@@ -106,20 +106,22 @@ void launch_pairs(const qvg_state &s, void *psi, uint32_t L, const qvg_gate &g, 
     using T = typename Cplx<R>::T;
     Mat<R> m;
     for (int i = 0; i < 8; ++i) m.u[i] = (R)g.u[i];
-    int lo = o.target, hi = -1;
+    int lo = o.target, hi = -1, c_lane = -1;
     uint64_t setm = 0;
-    if (o.control >= 0) {
+    if (o.control >= 5 || (o.control >= 0 && L < 7)) {  // insert the control bit: read only control=1
         lo = std::min(o.target, o.control);
         hi = std::max(o.target, o.control);
         setm = 1ull << o.control;
+    } else if (o.control >= 0) {
+        c_lane = o.control;  // low control: per-pair predicate
     }
-    const uint64_t npairs = 1ull << (L - 1 - (o.control >= 0 ? 1 : 0));
+    const uint64_t npairs = 1ull << (L - 1 - (hi >= 0 ? 1 : 0));
     T *p = static_cast<T *>(psi);
     if (npairs >= 1024) {
-        k_pairs<R, 4><<<(unsigned)(npairs / 1024), 256, 0, s.stream>>>(p, o.target, lo, hi, setm, m);
+        k_pairs<R, 4><<<(unsigned)(npairs / 1024), 256, 0, s.stream>>>(p, o.target, lo, hi, setm, c_lane, m);
     } else {
         const unsigned bs = (unsigned)std::min<uint64_t>(npairs, 256);
-        k_pairs<R, 1><<<(unsigned)(npairs / bs), bs, 0, s.stream>>>(p, o.target, lo, hi, setm, m);
+        k_pairs<R, 1><<<(unsigned)(npairs / bs), bs, 0, s.stream>>>(p, o.target, lo, hi, setm, c_lane, m);
     }
 }
 
@@ -164,7 +166,8 @@ void launch_phase(const qvg_state &s, void *psi, uint32_t L, const qvg_gate &g, 
 template <class R>
 void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *d_ops) {
     using T = typename Cplx<R>::T;
-    const size_t smem = (sizeof(T) << p.geom.k) + (sizeof(uint64_t) << p.geom.nhi);
+    const unsigned threads = 1u << (p.geom.k - 3);  // one 8-amplitude subcube per thread
+    const size_t smem = (sizeof(uint64_t) << p.geom.nhi) + (p.geom.ngroups > 1 ? (sizeof(T) << p.geom.k) : 0);
     static bool attr_set[2] = {false, false};
     const int which = sizeof(R) == 8 ? 1 : 0;
     if (!attr_set[which]) {
@@ -173,12 +176,11 @@ void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *d_ops) {
         attr_set[which] = true;
     }
     int per_sm = 0;
-    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tile<R>, 512, smem),
+    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tile<R>, (int)threads, smem),
                "occupancy(k_tile)");
     per_sm = std::max(per_sm, 1);
     const uint64_t grid = std::min<uint64_t>(p.geom.ntiles, (uint64_t)per_sm * s.sm_count);
-    k_tile<R><<<(unsigned)grid, 512, smem, s.stream>>>(static_cast<T *>(psi), p.geom, d_ops + p.op_begin,
-                                                      (int)p.op_count);
+    k_tile<R><<<(unsigned)grid, threads, smem, s.stream>>>(static_cast<T *>(psi), p.geom, d_ops + p.op_begin);
 }
 
 PlanOptions plan_options(const qvg_state &s) {

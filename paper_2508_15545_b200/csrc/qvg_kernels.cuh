@@ -78,7 +78,8 @@ __device__ __forceinline__ uint64_t ins0(uint64_t x, int b) {
 // a warp covers consecutive bases.
 template <class R, int PPT>
 __global__ void __launch_bounds__(256)
-k_pairs(typename Cplx<R>::T *__restrict__ psi, int q, int ins_lo, int ins_hi, uint64_t setm, Mat<R> m) {
+k_pairs(typename Cplx<R>::T *__restrict__ psi, int q, int ins_lo, int ins_hi, uint64_t setm, int c_lane,
+        Mat<R> m) {
     using T = typename Cplx<R>::T;
     const uint64_t qb = 1ull << q;
     const uint64_t first = (uint64_t)blockIdx.x * (blockDim.x * PPT) + threadIdx.x;
@@ -89,11 +90,17 @@ k_pairs(typename Cplx<R>::T *__restrict__ psi, int q, int ins_lo, int ins_hi, ui
         uint64_t x = ins0(first + (uint64_t)k * blockDim.x, ins_lo);
         if (ins_hi >= 0) x = ins0(x, ins_hi);
         lo[k] = x | setm;
-        a[k] = ld_amp(psi + lo[k]);
-        b[k] = ld_amp(psi + (lo[k] | qb));
+        // A control below bit 5 is a per-pair predicate instead of an inserted
+        // bit: warps keep 32 consecutive bases, so the skipped halves do not
+        // turn the accesses into strided partial-sector traffic.
+        if (c_lane < 0 || ((lo[k] >> c_lane) & 1ull)) {
+            a[k] = ld_amp(psi + lo[k]);
+            b[k] = ld_amp(psi + (lo[k] | qb));
+        }
     }
 #pragma unroll
     for (int k = 0; k < PPT; ++k) {
+        if (c_lane >= 0 && !((lo[k] >> c_lane) & 1ull)) continue;
         st_amp(psi + lo[k], madd2(m.u[0], m.u[1], a[k], m.u[2], m.u[3], b[k]));
         st_amp(psi + (lo[k] | qb), madd2(m.u[4], m.u[5], a[k], m.u[6], m.u[7], b[k]));
     }
@@ -160,22 +167,29 @@ k_phase(typename Cplx<R>::T *__restrict__ psi, int ins_lo, int ins_hi, uint64_t 
 
 // ---------------------------------------------------------------------------
 // K4: fused tile pass — the B200 replacement for the reference's block store +
-// sliding window (store.cpp, cache.cpp, kernel.cpp:113-146). A CTA stages a
-// tile of 2^k amplitudes in shared memory, applies a run of gates in circuit
-// order, and writes the tile back: one HBM round trip for the whole run. The
-// tile is the set of amplitudes that agree on every qubit outside the tile
-// qubit set Q (|Q| = k): its lowest `lowc` qubits are 0..lowc-1 (contiguous
-// 2^lowc-amp segments in HBM); the other k-lowc are arbitrary high qubits, so
-// gates on any qubit can be fused. A control outside Q is constant per tile,
-// and a diagonal gate needs no pairing, so its qubits may lie anywhere.
-enum TileOpKind : int32_t { TILE_PAIR = 0, TILE_DIAG = 1 };
+// sliding window (store.cpp, cache.cpp, kernel.cpp:113-146). A CTA owns a tile
+// of 2^k amplitudes and applies a run of gates to it in circuit order, so the
+// whole run costs one HBM round trip. The tile is the set of amplitudes that
+// agree on every qubit outside the tile qubit set Q (|Q| = k): its lowest
+// `lowc` qubits are 0..lowc-1 (contiguous 2^lowc-amp segments in HBM), the
+// other k-lowc are arbitrary high qubits, so gates on any qubit can be fused.
+// A control outside Q is constant per tile, and a diagonal gate needs no
+// pairing, so its qubits may lie anywhere.
+//
+// Inside the tile the run is cut into groups whose pair ops touch at most 3
+// tile bits. For a group, each of the 2^(k-3) threads holds the 8 amplitudes
+// of one 3-bit subcube in registers and applies all the group's ops there;
+// shared memory is only the transpose buffer between groups. The first group
+// reads HBM directly and the last one writes HBM directly, so a run that fits
+// one group never touches shared memory.
+enum TileOpKind : int32_t { TILE_PAIR = 0, TILE_DIAG = 1, TILE_GROUP = 2 };
 
 struct TileOp {
     int32_t kind;      // TileOpKind
-    int32_t tbit;      // tile-local target bit, -1 if the target is outside Q (diag only)
-    int32_t cbit;      // tile-local control bit, -1 if none or outside Q
-    int32_t d0_is_one; // diag: d0 == 1 exactly, so bit-0 amplitudes are untouched
-    uint64_t greq;     // global bits that must be 1 in the tile base (controls outside Q)
+    int32_t tbit;      // pair/diag: tile-local target bit, -1 if outside Q (diag only); group: b0
+    int32_t cbit;      // tile-local control bit, -1 if none or outside Q; group: b1
+    int32_t d0_is_one; // diag: d0 == 1 exactly (bit-0 amplitudes untouched); group: b2
+    uint64_t greq;     // global bits that must be 1 in the tile base (controls outside Q); group: op count
     uint64_t gtgt;     // diag with target outside Q: that global bit
     double u[8];       // matrix (diag uses u00 = u[0..1], u11 = u[6..7])
 };
@@ -183,6 +197,7 @@ struct TileOp {
 struct TileGeom {
     int n, k, lowc;       // qubits, tile qubits, contiguous low qubits
     int nhi;              // k - lowc
+    int ngroups;          // register groups in this pass
     int hiq[24];          // tile qubits >= lowc, ascending (tile-local bits lowc..k-1)
     uint64_t outmask;     // qubits not in Q
     uint64_t ntiles;      // 2^(n-k)
@@ -199,75 +214,105 @@ __device__ __forceinline__ uint64_t pdep_mask(uint64_t v, uint64_t mask) {
     return r;
 }
 
-template <class R>
-__device__ __forceinline__ void tile_apply_op(typename Cplx<R>::T *sm, int k, const TileOp &op,
-                                              uint64_t base) {
-    using T = typename Cplx<R>::T;
-    const uint32_t namps = 1u << k;
-    if ((base & op.greq) != op.greq) return;  // control outside the tile is 0
-    if (op.kind == TILE_PAIR) {
-        const R u0 = (R)op.u[0], u1 = (R)op.u[1], u2 = (R)op.u[2], u3 = (R)op.u[3];
-        const R u4 = (R)op.u[4], u5 = (R)op.u[5], u6 = (R)op.u[6], u7 = (R)op.u[7];
-        const uint32_t tb = 1u << op.tbit;
-        const uint32_t low = tb - 1u;
-        for (uint32_t p = threadIdx.x; p < (namps >> 1); p += blockDim.x) {
-            const uint32_t lo = ((p & ~low) << 1) | (p & low);
-            if (op.cbit >= 0 && !((lo >> op.cbit) & 1u)) continue;
-            const T a = sm[lo], b = sm[lo | tb];
-            sm[lo] = madd2(u0, u1, a, u2, u3, b);
-            sm[lo | tb] = madd2(u4, u5, a, u6, u7, b);
-        }
-    } else {
-        const R d0r = (R)op.u[0], d0i = (R)op.u[1], d1r = (R)op.u[6], d1i = (R)op.u[7];
-        if (op.tbit < 0) {
-            const bool one = (base & op.gtgt) != 0;
-            if (!one && op.d0_is_one) return;
-            const R dr = one ? d1r : d0r, di = one ? d1i : d0i;
-            for (uint32_t l = threadIdx.x; l < namps; l += blockDim.x) {
-                if (op.cbit >= 0 && !((l >> op.cbit) & 1u)) continue;
-                sm[l] = cmul(dr, di, sm[l]);
-            }
-        } else {
-            for (uint32_t l = threadIdx.x; l < namps; l += blockDim.x) {
-                if (op.cbit >= 0 && !((l >> op.cbit) & 1u)) continue;
-                const bool one = (l >> op.tbit) & 1u;
-                if (!one && op.d0_is_one) continue;
-                sm[l] = one ? cmul(d1r, d1i, sm[l]) : cmul(d0r, d0i, sm[l]);
-            }
-        }
+// Pair op on group bit J: register pairs (r, r | 2^J) for the 4 r with bit J = 0.
+// cmask: bit r set when element r's control is 1 (all set when uncontrolled).
+template <class R, int J>
+__device__ __forceinline__ void group_pair(typename Cplx<R>::T (&v)[8], uint32_t cmask, const R *u) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        if ((r >> J) & 1) continue;
+        if (!((cmask >> r) & 1u)) continue;
+        const typename Cplx<R>::T a = v[r], b = v[r | (1 << J)];
+        v[r] = madd2(u[0], u[1], a, u[2], u[3], b);
+        v[r | (1 << J)] = madd2(u[4], u[5], a, u[6], u[7], b);
     }
 }
 
 template <class R>
-__global__ void __launch_bounds__(512)
-k_tile(typename Cplx<R>::T *__restrict__ psi, TileGeom g, const TileOp *__restrict__ ops, int nops) {
+__global__ void __launch_bounds__(512, 2)
+k_tile(typename Cplx<R>::T *__restrict__ psi, TileGeom g, const TileOp *__restrict__ ops) {
     using T = typename Cplx<R>::T;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    T *sm = reinterpret_cast<T *>(smem_raw);
-    uint64_t *offhi = reinterpret_cast<uint64_t *>(smem_raw + (sizeof(T) << g.k));
-    const uint32_t namps = 1u << g.k;
+    uint64_t *offhi = reinterpret_cast<uint64_t *>(smem_raw);
+    T *sm = reinterpret_cast<T *>(smem_raw + (sizeof(uint64_t) << g.nhi));
     const uint32_t nhi = 1u << g.nhi;
     const uint32_t lowm = (1u << g.lowc) - 1u;
     for (uint32_t h = threadIdx.x; h < nhi; h += blockDim.x) {
         uint64_t off = 0;
-        for (int i = 0; i < g.nhi; ++i)
-            if ((h >> i) & 1u) off |= 1ull << g.hiq[i];
+#pragma unroll
+        for (int i = 0; i < 24; ++i)
+            if (i < g.nhi && ((h >> i) & 1u)) off |= 1ull << g.hiq[i];
         offhi[h] = off;
     }
     __syncthreads();
     for (uint64_t tile = blockIdx.x; tile < g.ntiles; tile += gridDim.x) {
         const uint64_t base = pdep_mask(tile, g.outmask);
-        for (uint32_t l = threadIdx.x; l < namps; l += blockDim.x)
-            sm[l] = ld_amp(psi + (base | offhi[l >> g.lowc] | (l & lowm)));
-        __syncthreads();
-        for (int i = 0; i < nops; ++i) {
-            const TileOp op = ops[i];
-            tile_apply_op<R>(sm, g.k, op, base);
-            __syncthreads();
+        int rec = 0;
+        for (int gi = 0; gi < g.ngroups; ++gi) {
+            const TileOp hdr = ops[rec++];
+            const int b0 = hdr.tbit, b1 = hdr.cbit, b2 = hdr.d0_is_one;
+            const int nops = (int)hdr.greq;
+            // this thread's subcube: local indices l0 | {0, 2^b0} | {0, 2^b1} | {0, 2^b2}
+            const uint32_t l0 = (uint32_t)ins0(ins0(ins0(threadIdx.x, b0), b1), b2);
+            auto lidx = [&](int r) {
+                return l0 | ((r & 1) ? 1u << b0 : 0u) | ((r & 2) ? 1u << b1 : 0u) | ((r & 4) ? 1u << b2 : 0u);
+            };
+            // 8-bit mask over the subcube: element r has tile-local bit `bit` set
+            auto rmask = [&](int bit) -> uint32_t {
+                if (bit < 0) return 0xFFu;
+                if (bit == b0) return 0xAAu;
+                if (bit == b1) return 0xCCu;
+                if (bit == b2) return 0xF0u;
+                return ((l0 >> bit) & 1u) ? 0xFFu : 0u;
+            };
+            T v[8];
+            if (gi == 0) {
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    const uint32_t lr = lidx(r);
+                    v[r] = ld_amp(psi + (base | offhi[lr >> g.lowc] | (lr & lowm)));
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < 8; ++r) v[r] = sm[lidx(r)];
+            }
+            for (int i = 0; i < nops; ++i) {
+                const TileOp &op = ops[rec + i];
+                if ((base & op.greq) != op.greq) continue;  // control outside the tile is 0
+                R u[8];
+#pragma unroll
+                for (int x = 0; x < 8; ++x) u[x] = (R)op.u[x];
+                if (op.kind == TILE_PAIR) {
+                    const uint32_t cm = rmask(op.cbit);
+                    if (op.tbit == b0) group_pair<R, 0>(v, cm, u);
+                    else if (op.tbit == b1) group_pair<R, 1>(v, cm, u);
+                    else group_pair<R, 2>(v, cm, u);
+                } else {
+                    const uint32_t cm = rmask(op.cbit);
+                    const uint32_t tm = op.tbit >= 0 ? rmask(op.tbit) : ((base & op.gtgt) ? 0xFFu : 0u);
+#pragma unroll
+                    for (int r = 0; r < 8; ++r) {
+                        if (!((cm >> r) & 1u)) continue;
+                        const bool one = (tm >> r) & 1u;
+                        if (!one && op.d0_is_one) continue;
+                        v[r] = one ? cmul(u[6], u[7], v[r]) : cmul(u[0], u[1], v[r]);
+                    }
+                }
+            }
+            rec += nops;
+            if (gi == g.ngroups - 1) {
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    const uint32_t lr = lidx(r);
+                    st_amp(psi + (base | offhi[lr >> g.lowc] | (lr & lowm)), v[r]);
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < 8; ++r) sm[lidx(r)] = v[r];
+                __syncthreads();
+            }
         }
-        for (uint32_t l = threadIdx.x; l < namps; l += blockDim.x)
-            st_amp(psi + (base | offhi[l >> g.lowc] | (l & lowm)), sm[l]);
-        __syncthreads();
+        if (g.ngroups > 1) __syncthreads();  // last group read sm; the next tile's groups write it
     }
 }
 

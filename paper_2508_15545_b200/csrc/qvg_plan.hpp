@@ -144,6 +144,7 @@ inline Plan make_plan(const qvg_gate *ops, uint64_t count, const PlanOptions &po
     const uint32_t n = po.n;
     const uint64_t full = 2ull * (1ull << n) * po.amp_bytes;
     const uint32_t k = std::min<uint32_t>(po.tile_qubits, n);
+    const bool fuse = po.fuse && k >= 5;  // a tile needs >= 4 threads of 8-amplitude subcubes
     const uint32_t lowmin = std::min<uint32_t>(po.carriers, k);
     std::vector<OpInfo> info(count);
     for (uint64_t i = 0; i < count; ++i) info[i] = classify(ops[i]);
@@ -151,7 +152,7 @@ inline Plan make_plan(const qvg_gate *ops, uint64_t count, const PlanOptions &po
 
     uint64_t i = 0;
     while (i < count) {
-        if (!po.fuse) {
+        if (!fuse) {
             if (!info[i].identity) plan.passes.push_back(single_pass(ops[i], info[i], po));
             ++i;
             continue;
@@ -202,6 +203,32 @@ inline Plan make_plan(const qvg_gate *ops, uint64_t count, const PlanOptions &po
             p.kind = PASS_TILE;
             p.geom = g;
             p.op_begin = (uint32_t)plan.tile_ops.size();
+            // Records: [group header, its ops]... Each group's pair ops touch
+            // at most 3 tile bits (the thread's register subcube).
+            std::vector<TileOp> group;
+            int gbits[3];
+            int nb = 0;
+            auto close_group = [&] {
+                if (group.empty()) return;
+                for (int b = 0; nb < 3 && b < g.k; ++b) {  // pad with the lowest unused bits
+                    bool used = false;
+                    for (int x = 0; x < nb; ++x) used |= gbits[x] == b;
+                    if (!used) gbits[nb++] = b;
+                }
+                std::sort(gbits, gbits + 3);
+                TileOp h{};
+                h.kind = TILE_GROUP;
+                h.tbit = gbits[0];
+                h.cbit = gbits[1];
+                h.d0_is_one = gbits[2];
+                h.greq = group.size();
+                plan.tile_ops.push_back(h);
+                plan.tile_ops.insert(plan.tile_ops.end(), group.begin(), group.end());
+                group.clear();
+                nb = 0;
+                g.ngroups += 1;
+            };
+            g.ngroups = 0;
             for (uint64_t x = i; x < j; ++x) {
                 const OpInfo &o = info[x];
                 if (o.identity) continue;
@@ -216,8 +243,18 @@ inline Plan make_plan(const qvg_gate *ops, uint64_t count, const PlanOptions &po
                     if (t.cbit < 0) t.greq = 1ull << o.control;
                 }
                 t.d0_is_one = (ops[x].u[0] == 1.0 && ops[x].u[1] == 0.0) ? 1 : 0;
-                plan.tile_ops.push_back(t);
+                if (t.kind == TILE_PAIR) {
+                    bool have = false;
+                    for (int b = 0; b < nb; ++b) have |= gbits[b] == t.tbit;
+                    if (!have) {
+                        if (nb == 3) close_group();
+                        gbits[nb++] = t.tbit;
+                    }
+                }
+                group.push_back(t);
             }
+            close_group();
+            p.geom = g;
             p.op_count = (uint32_t)(plan.tile_ops.size() - p.op_begin);
             p.bytes = full;
             p.gates = j - i;

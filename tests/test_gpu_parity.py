@@ -54,7 +54,7 @@ def test_each_gate_kind_every_qubit(qv, oracle, n):
     # the whole list fused
     c = qv.parse_circuit("\n".join(lines) + "\n")
     want = oracle.apply(n, start.copy(), gate_array(c))
-    for tq in (0, 4, 7):
+    for tq in (0, 5, 7):
         _, got = run_gpu(qv, c, fuse=True, tile_qubits=tq, init=start)
         assert np.array_equal(got, want), (tq, np.abs(got - want).max())
 
