@@ -167,7 +167,8 @@ template <class R>
 void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *d_ops) {
     using T = typename Cplx<R>::T;
     const unsigned threads = 1u << (p.geom.k - 3);  // one 8-amplitude subcube per thread
-    const size_t smem = (sizeof(uint64_t) << p.geom.nhi) + (p.geom.ngroups > 1 ? (sizeof(T) << p.geom.k) : 0);
+    const size_t smem = (((sizeof(uint64_t) << p.geom.nhi) + 15) & ~size_t(15)) +
+                        (p.geom.ngroups > 1 ? (sizeof(T) << p.geom.k) : 0);
     static bool attr_set[2] = {false, false};
     const int which = sizeof(R) == 8 ? 1 : 0;
     if (!attr_set[which]) {

@@ -234,7 +234,8 @@ k_tile(typename Cplx<R>::T *__restrict__ psi, TileGeom g, const TileOp *__restri
     using T = typename Cplx<R>::T;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint64_t *offhi = reinterpret_cast<uint64_t *>(smem_raw);
-    T *sm = reinterpret_cast<T *>(smem_raw + (sizeof(uint64_t) << g.nhi));
+    // offset table first, padded to 16 B so the double2 tile stays aligned
+    T *sm = reinterpret_cast<T *>(smem_raw + (((sizeof(uint64_t) << g.nhi) + 15) & ~size_t(15)));
     const uint32_t nhi = 1u << g.nhi;
     const uint32_t lowm = (1u << g.lowc) - 1u;
     for (uint32_t h = threadIdx.x; h < nhi; h += blockDim.x) {
