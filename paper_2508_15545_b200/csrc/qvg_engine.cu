@@ -296,7 +296,7 @@ static int create_impl(uint32_t n, uint32_t precision, int device, uint32_t rank
         s->S = precision == QVG_C128 ? 16 : 8;
         s->rank = rank;
         s->world = world;
-        s->tile_qubits = precision == QVG_C128 ? 12 : 13;
+        s->tile_qubits = 12;  // 2^12 amplitudes: 512 threads x one 8-amplitude subcube
         s->carriers = precision == QVG_C128 ? 3 : 4;
         try {
             set_device(s);
@@ -366,7 +366,7 @@ int qvg_set_option(qvg_state *s, int key, int64_t value) {
         switch (key) {
         case QVG_OPT_FUSE: s->fuse = value != 0; break;
         case QVG_OPT_TILE_QUBITS: {
-            const int64_t maxk = s->precision == QVG_C128 ? 13 : 14;
+            const int64_t maxk = 12;  // k_tile runs 2^(k-3) <= 512 threads
             if (value < 2 || value > maxk) throw Validation("tile_qubits out of range");
             s->tile_qubits = (uint32_t)value;
             break;
@@ -551,7 +551,7 @@ int qvg_plan_passes(uint32_t n_qubits, uint32_t precision, int fuse, uint32_t ti
         po.n = n_qubits;
         po.amp_bytes = precision == QVG_C128 ? 16 : 8;
         po.fuse = fuse != 0;
-        po.tile_qubits = tile_qubits ? tile_qubits : (precision == QVG_C128 ? 12 : 13);
+        po.tile_qubits = tile_qubits ? std::min<uint32_t>(tile_qubits, 12) : 12;
         po.carriers = carriers;
         const Plan plan = make_plan(ops, count, po);
         uint64_t fused = 0, bytes = 0;
