@@ -1,0 +1,178 @@
+"""Host-side logic on CPU: the C++ host mirror of the reference API (circuit
+text, seeded generator, config builders), the pass planner, and the C-ABI
+library's exports. No device work."""
+import ctypes
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, gate_array
+from oracle.oracle import GATE_DTYPE
+
+GOLD = os.path.join(ROOT, "tests", "golden")
+
+
+def cuda_present():
+    try:
+        import torch
+
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+# --- reference API parity ---------------------------------------------------------
+def test_random_circuit_matches_reference(qv):
+    gold = np.load(os.path.join(GOLD, "ref_random.npz"))
+    for key in sorted({k.rsplit("_", 1)[0] for k in gold.files}):
+        n, d, s = (int(x[1:]) for x in key.split("_"))
+        c = qv.random_circuit(n, d, s)
+        assert c.gates().tobytes() == gold[f"{key}_ops"].tobytes(), key
+        assert c.to_text() == gold[f"{key}_text"].tobytes().decode(), key
+
+
+def test_text_round_trip_and_determinism(qv):
+    # reference tests/python/test_smoke.py:28-44
+    c = qv.random_circuit(5, 25, 42)
+    text = c.to_text()
+    back = qv.parse_circuit(text)
+    assert back.n_qubits == 5 and len(back) == 25
+    assert back.to_text() == text == qv.serialize_circuit(back)
+    assert qv.random_circuit(4, 30, 7).to_text() == qv.random_circuit(4, 30, 7).to_text()
+    assert qv.random_circuit(4, 30, 7).to_text() != qv.random_circuit(4, 30, 8).to_text()
+
+
+def test_extended_grammar_round_trips(qv):
+    text = "qubits 4\ncp 0 3 0.39269908169872414\ncu 1 2 0 0 1 0 1 0 0 0\np 2 1.5\nu3 1 0.5 0.25 0.125\nsx 0\nsy 1\nsw 2\ncx 3 0\ncz 1 0\n"
+    c = qv.parse_circuit(text)
+    assert c.to_text() == text
+    assert qv.parse_circuit(c.to_text()).gates().tobytes() == c.gates().tobytes()
+
+
+def test_errors_are_typed_with_lines(qv):
+    # reference tests/python/test_smoke.py:110-123
+    with pytest.raises(qv.QvsimError, match="line 2"):
+        qv.parse_circuit("qubits 2\nh 7\n")
+    with pytest.raises(qv.ParseError):
+        qv.parse_circuit("h 0\n")
+    with pytest.raises(qv.ParseError, match="unknown instruction"):
+        qv.parse_circuit("qubits 2\nfoo 0\n")
+    with pytest.raises(qv.ParseError, match="control equals target"):
+        qv.parse_circuit("qubits 2\ncx 1 1\n")
+    with pytest.raises(qv.ParseError, match="not unitary"):
+        qv.parse_circuit("qubits 1\nu 0 1 0 1 0 0 0 1 0\n")
+
+
+def test_gate_library(qv):
+    r = 1 / math.sqrt(2)
+    assert np.allclose(qv.make_gate("h"), [r, r, r, -r])
+    sx = np.array(qv.make_gate("sx")).reshape(2, 2)
+    assert np.allclose(sx @ sx, [[0, 1], [1, 0]], atol=1e-15)
+    sy = np.array(qv.make_gate("sy")).reshape(2, 2)
+    assert np.allclose(sy @ sy, [[0, -1j], [1j, 0]], atol=1e-15)
+    sw = np.array(qv.make_gate("sw")).reshape(2, 2)
+    w = np.array([[0, (1 - 1j) * r], [(1 + 1j) * r, 0]])
+    assert np.allclose(sw @ sw, w, atol=1e-15)
+    th, ph, la = 0.3, 1.1, 2.5
+    u3 = np.array(qv.make_gate("u3", [th, ph, la])).reshape(2, 2)
+    want = np.array([[math.cos(th / 2), -np.exp(1j * la) * math.sin(th / 2)],
+                     [np.exp(1j * ph) * math.sin(th / 2), np.exp(1j * (ph + la)) * math.cos(th / 2)]])
+    assert np.allclose(u3, want, atol=1e-15)
+
+
+# --- BASELINE config builders -------------------------------------------
+def test_config_builders_shapes(qv):
+    c0 = qv.u3_ladder_circuit(20, 20, 1)
+    assert len(c0) == 20 * (20 + 19)
+    c1, b = qv.qft_circuit(26, 1)
+    names = c1.names()
+    assert names.count("cp") == 325 and names.count("h") == 52 and names.count("cx") == 39
+    assert names.count("x") == bin(b).count("1") and 0 <= b < 2 ** 26
+    c2 = qv.haar_sweep_circuit(30, 2508)
+    assert c2.names().count("u") == 30 and c2.names().count("cx") == 90
+    c3 = qv.grid_circuit(5, 6, 24, 1)
+    nm = c3.names()
+    assert sum(nm.count(g) for g in ("sx", "sy", "sw")) == 720 and nm.count("cz") == 294
+    # never the same 1q gate twice in a row on a qubit
+    ops = gate_array(c3)
+    last = {}
+    for name, op in zip(nm, ops):
+        if name in ("sx", "sy", "sw"):
+            assert last.get(int(op["target"])) != name
+            last[int(op["target"])] = name
+
+
+def test_haar_unitaries(qv):
+    ops = gate_array(qv.haar_sweep_circuit(30, 2508))[:30]
+    for op in ops:
+        u = op["u"].view(np.complex128).reshape(2, 2)
+        assert np.abs(u.conj().T @ u - np.eye(2)).max() < 1e-14
+
+
+# --- planner -------------------------------------------------------------------------
+def test_planner_bytes_and_fusion(qv):
+    n, S = 20, 16
+    full = 2 * (1 << n) * S
+    one = lambda text: qv.plan_passes(n, qv.parse_circuit(f"qubits {n}\n{text}\n").gates(), fuse=False)
+    assert one("h 7") == (1, 0, full)
+    assert one("cx 3 9") == (1, 0, full // 2)       # only control=1 amplitudes
+    assert one("cx 0 9") == (1, 0, full)           # control bit 0: sector-rounded
+    assert one("cz 4 9") == (1, 0, full // 4)       # diag(1,-1) with control: |11> quarter
+    assert one("t 9") == (1, 0, full // 2)
+    assert one("cp 2 9 0") == (0, 0, 0)            # identity: no pass
+    # 12 Hadamards on 0..11 fuse into one tile pass
+    text = "\n".join(f"h {q}" for q in range(12))
+    assert qv.plan_passes(n, qv.parse_circuit(f"qubits {n}\n{text}\n").gates()) == (1, 1, full)
+    # config 3 (n=30): fused passes are far fewer than ops
+    c3 = qv.grid_circuit(5, 6, 24, 1)
+    p, f, b = qv.plan_passes(30, c3.gates())
+    assert f == p and p < len(c3) / 8
+
+
+def test_planner_rejects_bad_ops(qv):
+    with pytest.raises(qv.ValidationError):
+        qv.plan_passes(3, qv.parse_circuit("qubits 4\nh 3\n").gates())
+
+
+# --- the C-ABI boundary --------------------------------------------------------------
+def header_functions():
+    with open(os.path.join(ROOT, "include", "qvg.h")) as f:
+        src = f.read()
+    return sorted(set(re.findall(r"^\s*(?:int|const char \*)\s*(qvg_\w+)\s*\(", src, re.M)))
+
+
+def test_capi_exports_every_declared_symbol(qv):
+    lib = ctypes.CDLL(qv.LIBQVG)
+    names = header_functions()
+    assert len(names) >= 20
+    for name in names:
+        assert hasattr(lib, name), name
+    lib.qvg_abi_version.restype = ctypes.c_int
+    assert lib.qvg_abi_version() == qv.QVG_ABI_VERSION == 1
+
+
+@pytest.mark.skipif(cuda_present(), reason="checks the no-device error path")
+def test_no_device_fails_loudly(qv):
+    lib = ctypes.CDLL(qv.LIBQVG)
+    lib.qvg_last_error.restype = ctypes.c_char_p
+    st = ctypes.c_void_p()
+    rc = lib.qvg_create(4, 128, 0, ctypes.byref(st))
+    assert rc in (3, 5) and not st.value and lib.qvg_last_error()
+    with pytest.raises(qv.IoError):
+        qv.StateVector.create(4)
+
+
+def test_capi_validation_codes(qv):
+    lib = ctypes.CDLL(qv.LIBQVG)
+    lib.qvg_last_error.restype = ctypes.c_char_p
+    out = ctypes.c_uint64()
+    g = np.zeros(1, GATE_DTYPE)
+    g[0]["target"] = 5
+    g[0]["control"] = -1
+    rc = lib.qvg_plan_passes(4, 128, 1, 0, 3, g.ctypes.data_as(ctypes.c_void_p), 1, ctypes.byref(out), None, None)
+    assert rc == 1 and b"target 5" in lib.qvg_last_error()
+    rc = lib.qvg_create(4, 96, 0, ctypes.byref(ctypes.c_void_p()))
+    assert rc == 1

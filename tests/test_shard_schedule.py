@@ -1,0 +1,179 @@
+"""The sharded (multi-GPU) path's host logic on CPU.
+
+libqvg plans a sharded circuit as a list of steps (qvg_shard_schedule): local
+ops with rank predicates, pairwise half-shard exchanges, local qubit swaps.
+Here the same steps are executed on CPU shards — local ops through the oracle
+(test infrastructure), exchanges as numpy copies in one process, and over
+torch.distributed `gloo` with world_size 2 and 4 in separate processes — and
+the gathered state must equal the unsharded oracle bit for bit (the
+reference's worker-count invariance, reference tests/acceptance.cpp:196-242)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from conftest import gate_array
+from oracle.oracle import GATE_DTYPE
+
+STEP_DTYPE = np.dtype([("type", "<u4"), ("rank_mask", "<u4"), ("rank_value", "<u4"), ("gpos", "<u4"),
+                       ("lpos", "<u4"), ("lpos2", "<u4"), ("op", GATE_DTYPE)])
+assert STEP_DTYPE.itemsize == 104
+
+
+def schedule(qv, circuit, world, canonicalize=True):
+    raw = qv.shard_schedule(circuit.n_qubits, world, circuit.gates(), canonicalize)
+    return np.frombuffer(raw.tobytes(), STEP_DTYPE)
+
+
+def swap_local_bits(shard, a, b):
+    L = int(np.log2(shard.size))
+    idx = np.arange(shard.size)
+    ba, bb = (idx >> a) & 1, (idx >> b) & 1
+    src = idx ^ ((ba ^ bb) << a) ^ ((ba ^ bb) << b)
+    return shard[src]
+
+
+def run_local_steps(oracle, L, shard, rank, steps):
+    for st in steps:
+        if st["type"] == 0 and (rank & st["rank_mask"]) == st["rank_value"]:
+            oracle.apply(L, shard, st["op"].reshape(1))
+        elif st["type"] == 2:
+            shard[:] = swap_local_bits(shard, int(st["lpos"]), int(st["lpos2"]))
+
+
+def emulate(oracle, n, world, steps):
+    """All shards in one process; exchange = swap of half-shards."""
+    g = int(np.log2(world))
+    L = n - g
+    shards = [np.zeros(1 << L, np.complex128) for _ in range(world)]
+    shards[0][0] = 1.0
+    half = 1 << (L - 1)
+    for st in steps:
+        if st["type"] == 1:
+            bit = 1 << (int(st["gpos"]) - L)
+            assert st["lpos"] == L - 1
+            for r in range(world):
+                if r & bit:
+                    continue
+                p = r | bit
+                mine, theirs = shards[r][half:].copy(), shards[p][:half].copy()
+                shards[r][half:], shards[p][:half] = theirs, mine
+        else:
+            for r in range(world):
+                run_local_steps(oracle, L, shards[r], r, [st])
+    return np.concatenate(shards)
+
+
+CIRCUITS = [
+    ("u3_ladder_circuit", (10, 4, 3)),
+    ("random_circuit", (9, 200, 9)),
+    ("haar_sweep_circuit", (12, 2)),
+    ("grid_circuit", (3, 4, 6, 1)),
+    ("qft_circuit", (10, 4)),
+]
+
+
+def build(qv, fn, args):
+    out = getattr(qv, fn)(*args)
+    return out[0] if isinstance(out, tuple) else out
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("fn,args", CIRCUITS)
+def test_schedule_emulated_bit_identical(qv, oracle, world, fn, args):
+    c = build(qv, fn, args)
+    steps = schedule(qv, c, world)
+    want = oracle.simulate(c.n_qubits, gate_array(c))
+    got = emulate(oracle, c.n_qubits, world, steps)
+    assert np.array_equal(got, want)
+
+
+def test_schedule_shape(qv):
+    # local-only circuit: no exchange; a global target: one exchange; a global
+    # control: a rank-predicated local op; a diagonal global gate: no exchange.
+    n = 6
+    sch = lambda text: schedule(qv, qv.parse_circuit(f"qubits {n}\n{text}\n"), 2, canonicalize=False)
+    s = sch("h 0\ncx 1 2")
+    assert list(s["type"]) == [0, 0]
+    s = sch("h 5")
+    assert list(s["type"]) == [1, 0] and s[0]["gpos"] == 5 and s[0]["lpos"] == 4
+    s = sch("cx 5 0")
+    assert list(s["type"]) == [0] and s[0]["rank_mask"] == 1 and s[0]["rank_value"] == 1
+    s = sch("cz 0 5\nrz 5 0.3\nt 5")
+    assert 1 not in list(s["type"])
+    full = schedule(qv, qv.parse_circuit(f"qubits {n}\nh 5\n"), 2, canonicalize=True)
+    assert list(full["type"]).count(1) == 2  # the exchange and its undo
+
+
+# --- multi-process: gloo, world_size 2 and 4 -----------------------------------------------
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, fn, args, q):
+    import sys
+
+    import torch
+    import torch.distributed as dist
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    sys.path.insert(0, os.path.join(root, "tests"))
+    import paper_2508_15545_b200 as qv
+    from oracle.oracle import Oracle
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        oracle = Oracle()
+        c = build(qv, fn, args)
+        n = c.n_qubits
+        L = n - int(np.log2(world))
+        steps = schedule(qv, c, world)
+        shard = np.zeros(1 << L, np.complex128)
+        if rank == 0:
+            shard[0] = 1.0
+        half = 1 << (L - 1)
+        for st in steps:
+            if st["type"] == 1:  # pairwise half-shard exchange with the partner rank
+                bit = 1 << (int(st["gpos"]) - L)
+                partner = rank ^ bit
+                mine = shard[half:] if not (rank & bit) else shard[:half]
+                send = torch.from_numpy(mine.copy().view(np.float64))
+                recv = torch.empty_like(send)
+                reqs = [dist.isend(send, partner), dist.irecv(recv, partner)]
+                for r in reqs:
+                    r.wait()
+                mine[:] = recv.numpy().view(np.complex128)
+            else:
+                run_local_steps(oracle, L, shard, rank, [st])
+        parts = [torch.empty(2 << L, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(parts, torch.from_numpy(shard.view(np.float64).copy()))
+        if rank == 0:
+            got = np.concatenate([p.numpy().view(np.complex128) for p in parts])
+            want = oracle.simulate(n, gate_array(c))
+            q.put(bool(np.array_equal(got, want)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_gloo_multiprocess_bit_identical(world):
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    for fn, args in [("u3_ladder_circuit", (10, 3, 5)), ("random_circuit", (8, 120, 4))]:
+        port = _free_port()
+        procs = [ctx.Process(target=_worker, args=(r, world, port, fn, args, q)) for r in range(world)]
+        for p in procs:
+            p.start()
+        for p in procs:
+            p.join(120)
+            assert p.exitcode == 0
+        assert q.get(timeout=10) is True
