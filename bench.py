@@ -108,6 +108,24 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+def measured_traffic(kernel_class):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of this kernel
+    class, from the newest ncu launch-list summary committed under profiles/
+    (tools/ncu_summary.py). None when no capture exists."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_bench_launches.json")))
+    for path in reversed(files):
+        try:
+            with open(path) as f:
+                c = json.load(f)["classes"].get(kernel_class)
+            if c:
+                return c["dram_bytes_per_launch"], os.path.relpath(path, ROOT)
+        except Exception:
+            continue
+    return None, None
+
+
 def gate_records(circuit):
     raw = np.frombuffer(circuit.gates().tobytes(), dtype=np.uint8)
     return raw.reshape(len(circuit), 80)
@@ -212,6 +230,10 @@ def run_ours(args, rank, world, dist):
     dom_ms, dom_bytes, dom_n = share[dom]
     hbm_peak, peak_kind = peaks()
     achieved = (dom_bytes / dom_n) / ((dom_ms / dom_n) / 1e3) / 1e9
+    traffic, traffic_src = measured_traffic(dom)
+    for i in range(nops):  # per-op diagnostics (stderr): ms and algorithmic GB/s
+        print(f"op {i:3d} {kernels[i]:24s} {mean_op[i]:8.3f} ms {local_bytes[i] / (mean_op[i] / 1e3) / 1e9:8.1f} GB/s",
+              file=sys.stderr)
     all_gbs = sum(local_bytes) / (mean_op.sum() / 1e3) / 1e9
     line = {
         "metric": METRIC,
@@ -232,7 +254,8 @@ def run_ours(args, rank, world, dist):
         "hbm_gbs_step": all_gbs,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm_peak,
-                     "traffic": None, "algorithmic_bytes_per_launch": dom_bytes / dom_n,
+                     "traffic": traffic, "traffic_source": traffic_src,
+                     "algorithmic_bytes_per_launch": dom_bytes / dom_n,
                      "launch_ms": dom_ms / dom_n, "share_of_step": dom_ms / mean_op.sum()},
         "per_kernel": {k: {"launches_per_step": v[2], "ms_per_launch": v[0] / v[2],
                            "gbs": (v[1] / v[2]) / ((v[0] / v[2]) / 1e3) / 1e9} for k, v in share.items()},
@@ -271,7 +294,8 @@ def fused_leg(qv, st, circ, line, args):
 def e2e_leg(qv, st, circ, recs, line, args):
     """The same metric through the public API with HOST buffers: every step
     copies the 16 GiB state from pinned host memory (qvg_load), runs the sweep
-    and reads the state back (qvg_read) inside the timed region."""
+    with the API's defaults (`apply_circuit(state, circuit)`: strategy gpu,
+    fusion on) and reads the state back (qvg_read) inside the timed region."""
     import torch
 
     n = circ.n_qubits
@@ -282,15 +306,19 @@ def e2e_leg(qv, st, circ, recs, line, args):
     steps = max(1, min(args.steps, 3))
     torch.cuda.synchronize()
     t0 = time.perf_counter()
+    passes = 0
     for _ in range(steps):
         st.load_state(host_np)
-        st.apply_gates(circ.gates(), sync=False)
+        m = qv.apply_circuit(st, circ)
+        passes += m["traversals"]
         st.read_into(host_np)
     t1 = time.perf_counter()
     ms = (t1 - t0) * 1e3 / steps
     line["e2e"] = {"value": len(circ) * count / (ms / 1e3), "unit": UNIT, "ms_per_step": ms,
                    "h2d_bytes_per_step": count * 16, "d2h_bytes_per_step": count * 16,
-                   "path": "StateVector.load_state -> apply_gates (C-ABI qvg_apply) -> read_state, pinned host"}
+                   "hbm_passes_per_step": passes / steps,
+                   "path": "StateVector.load_state -> apply_circuit(state, circuit) [API defaults: gpu, fused] "
+                           "-> read_into, pinned host buffers, host wall clock"}
 
 
 def cpu_baseline(args, nops_hint=120):
