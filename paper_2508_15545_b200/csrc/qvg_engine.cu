@@ -106,22 +106,23 @@ void launch_pairs(const qvg_state &s, void *psi, uint32_t L, const qvg_gate &g, 
     using T = typename Cplx<R>::T;
     Mat<R> m;
     for (int i = 0; i < 8; ++i) m.u[i] = (R)g.u[i];
-    int lo = o.target, hi = -1, c_lane = -1;
+    int lo = o.target, hi = -1, c_pred = -1;
     uint64_t setm = 0;
-    if (o.control >= 5 || (o.control >= 0 && L < 7)) {  // insert the control bit: read only control=1
+    if (o.control >= 0 && (sizeof(typename Cplx<R>::T) << o.control) >= 32) {
+        // control-1 runs fill whole sectors: insert the bit, read only control=1
         lo = std::min(o.target, o.control);
         hi = std::max(o.target, o.control);
         setm = 1ull << o.control;
     } else if (o.control >= 0) {
-        c_lane = o.control;  // low control: per-pair predicate
+        c_pred = o.control;  // sub-sector runs: read everything, store control=1
     }
     const uint64_t npairs = 1ull << (L - 1 - (hi >= 0 ? 1 : 0));
     T *p = static_cast<T *>(psi);
     if (npairs >= 1024) {
-        k_pairs<R, 4><<<(unsigned)(npairs / 1024), 256, 0, s.stream>>>(p, o.target, lo, hi, setm, c_lane, m);
+        k_pairs<R, 4><<<(unsigned)(npairs / 1024), 256, 0, s.stream>>>(p, o.target, lo, hi, setm, c_pred, m);
     } else {
         const unsigned bs = (unsigned)std::min<uint64_t>(npairs, 256);
-        k_pairs<R, 1><<<(unsigned)(npairs / bs), bs, 0, s.stream>>>(p, o.target, lo, hi, setm, c_lane, m);
+        k_pairs<R, 1><<<(unsigned)(npairs / bs), bs, 0, s.stream>>>(p, o.target, lo, hi, setm, c_pred, m);
     }
 }
 
@@ -130,15 +131,19 @@ void launch_low(const qvg_state &s, void *psi, uint32_t L, const qvg_gate &g, co
     using T = typename Cplx<R>::T;
     Mat<R> m;
     for (int i = 0; i < 8; ++i) m.u[i] = (R)g.u[i];
-    const int c_ins = o.control >= 5 ? o.control : -1;
-    const int c_lane = (o.control >= 0 && o.control < 5) ? o.control : -1;
+    // Insert the control when its control-1 runs fill whole 32-B sectors;
+    // otherwise (bit 0 in c128, bits 0-1 in c64) read all, store control=1.
+    const bool ins = o.control >= 0 && (sizeof(T) << o.control) >= 32;
+    const int c_ins = ins ? o.control : -1;
+    const int c_pred = (o.control >= 0 && !ins) ? o.control : -1;
+    const int qm = 1 << ((c_ins >= 0 && c_ins < o.target) ? o.target - 1 : o.target);
     const uint64_t count = 1ull << (L - (c_ins >= 0 ? 1 : 0));
     T *p = static_cast<T *>(psi);
     if (count >= 1024) {
-        k_low<R, 4><<<(unsigned)(count / 1024), 256, 0, s.stream>>>(p, o.target, c_ins, c_lane, m);
+        k_low<R, 4><<<(unsigned)(count / 1024), 256, 0, s.stream>>>(p, o.target, qm, c_ins, c_pred, m);
     } else {
         const unsigned bs = (unsigned)std::min<uint64_t>(count, 256);
-        k_low<R, 1><<<(unsigned)(count / bs), bs, 0, s.stream>>>(p, o.target, c_ins, c_lane, m);
+        k_low<R, 1><<<(unsigned)(count / bs), bs, 0, s.stream>>>(p, o.target, qm, c_ins, c_pred, m);
     }
 }
 

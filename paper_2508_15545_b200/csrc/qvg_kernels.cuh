@@ -74,11 +74,15 @@ __device__ __forceinline__ uint64_t ins0(uint64_t x, int b) {
 // (the reference streams all of them, kernel.cpp:74-76). ins_lo < ins_hi are
 // the inserted positions (ins_hi = -1 when only the target is inserted); setm
 // is the mask of inserted bits that are 1 (the control).
+// When the control-1 runs would be shorter than a 32-B sector (control bit 0
+// in c128) inserting it saves no DRAM sectors but halves the lanes' access
+// efficiency, so that control is instead a store predicate (c_pred): every
+// pair is read, only control=1 pairs are written.
 // Each thread owns PPT pairs, strided by blockDim so every load instruction of
 // a warp covers consecutive bases.
 template <class R, int PPT>
 __global__ void __launch_bounds__(256)
-k_pairs(typename Cplx<R>::T *__restrict__ psi, int q, int ins_lo, int ins_hi, uint64_t setm, int c_lane,
+k_pairs(typename Cplx<R>::T *__restrict__ psi, int q, int ins_lo, int ins_hi, uint64_t setm, int c_pred,
         Mat<R> m) {
     using T = typename Cplx<R>::T;
     const uint64_t qb = 1ull << q;
@@ -90,35 +94,32 @@ k_pairs(typename Cplx<R>::T *__restrict__ psi, int q, int ins_lo, int ins_hi, ui
         uint64_t x = ins0(first + (uint64_t)k * blockDim.x, ins_lo);
         if (ins_hi >= 0) x = ins0(x, ins_hi);
         lo[k] = x | setm;
-        // A control below bit 5 is a per-pair predicate instead of an inserted
-        // bit: warps keep 32 consecutive bases, so the skipped halves do not
-        // turn the accesses into strided partial-sector traffic.
-        if (c_lane < 0 || ((lo[k] >> c_lane) & 1ull)) {
-            a[k] = ld_amp(psi + lo[k]);
-            b[k] = ld_amp(psi + (lo[k] | qb));
-        }
+        a[k] = ld_amp(psi + lo[k]);
+        b[k] = ld_amp(psi + (lo[k] | qb));
     }
 #pragma unroll
     for (int k = 0; k < PPT; ++k) {
-        if (c_lane >= 0 && !((lo[k] >> c_lane) & 1ull)) continue;
+        if (c_pred >= 0 && !((lo[k] >> c_pred) & 1ull)) continue;
         st_amp(psi + lo[k], madd2(m.u[0], m.u[1], a[k], m.u[2], m.u[3], b[k]));
         st_amp(psi + (lo[k] | qb), madd2(m.u[4], m.u[5], a[k], m.u[6], m.u[7], b[k]));
     }
 }
 
 // ---------------------------------------------------------------------------
-// K2: low-target kernel (target < 5). A warp loads 32 consecutive amplitudes
-// (512 B c128, fully coalesced, one 16-B access per lane) and finds each
-// partner with __shfl_xor(lane ^ 2^q). Each lane writes its own amplitude with
-// the reference expression for its role (lo or hi). A control bit >= 5 is
-// inserted into the enumeration (only control=1 runs are read); a control
-// bit < 5 is a per-lane predicate.
+// K2: low-target kernel (target < 5). A warp loads 32 consecutive enumerated
+// amplitudes (512 B c128 when uncontrolled, one 16-B access per lane) and
+// finds each partner with __shfl_xor(lane ^ qm). Each lane writes its own
+// amplitude with the reference expression for its role (lo or hi).
+// A control is inserted into the enumeration as a 1 bit (c_ins, any position
+// whose control-1 runs fill whole sectors), so every lane is active and only
+// control=1 amplitudes are read; qm is the partner's lane distance in the
+// enumeration (2^q, or 2^(q-1) when c_ins < q). A control whose runs are
+// shorter than a sector is a store predicate instead (c_pred).
 template <class R, int APT>
 __global__ void __launch_bounds__(256)
-k_low(typename Cplx<R>::T *__restrict__ psi, int q, int c_ins, int c_lane, Mat<R> m) {
+k_low(typename Cplx<R>::T *__restrict__ psi, int q, int qm, int c_ins, int c_pred, Mat<R> m) {
     using T = typename Cplx<R>::T;
     const uint64_t first = (uint64_t)blockIdx.x * (blockDim.x * APT) + threadIdx.x;
-    const int qm = 1 << q;
     uint64_t j[APT];
     T v[APT];
 #pragma unroll
@@ -126,10 +127,7 @@ k_low(typename Cplx<R>::T *__restrict__ psi, int q, int c_ins, int c_lane, Mat<R
         uint64_t x = first + (uint64_t)k * blockDim.x;
         if (c_ins >= 0) x = ins0(x, c_ins) | (1ull << c_ins);
         j[k] = x;
-        // Control below bit 5 is a lane predicate; the partner shares it, so
-        // control=0 lanes neither load nor store (their sectors stay cold).
-        if (c_lane < 0 || ((x >> c_lane) & 1ull)) v[k] = ld_amp(psi + x);
-        else v[k] = T{};
+        v[k] = ld_amp(psi + x);
     }
 #pragma unroll
     for (int k = 0; k < APT; ++k) {
@@ -139,7 +137,7 @@ k_low(typename Cplx<R>::T *__restrict__ psi, int q, int c_ins, int c_lane, Mat<R
         const bool hi = (j[k] >> q) & 1ull;
         const T out = hi ? madd2(m.u[4], m.u[5], p, m.u[6], m.u[7], v[k])
                          : madd2(m.u[0], m.u[1], v[k], m.u[2], m.u[3], p);
-        if (c_lane < 0 || ((j[k] >> c_lane) & 1ull)) st_amp(psi + j[k], out);
+        if (c_pred < 0 || ((j[k] >> c_pred) & 1ull)) st_amp(psi + j[k], out);
     }
 }
 

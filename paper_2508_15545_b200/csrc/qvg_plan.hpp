@@ -121,7 +121,7 @@ inline Pass single_pass(const qvg_gate &g, const OpInfo &o, const PlanOptions &p
         return p;
     }
     // Low-target kernel needs 32 consecutive enumerated amplitudes per warp.
-    const bool ctl_ins = o.control >= 5;
+    const bool ctl_ins = o.control >= 0 && ((uint64_t)S << o.control) >= 32;
     const uint32_t enum_bits = n - (ctl_ins ? 1 : 0);
     if (po.low_kernel && o.target < 5 && enum_bits >= 5 && n >= 6) {
         p.kind = PASS_LOW;
