@@ -114,7 +114,7 @@ void launch_pairs(const qvg_state &s, void *psi, uint32_t L, const qvg_gate &g, 
         hi = std::max(o.target, o.control);
         setm = 1ull << o.control;
     } else if (o.control >= 0) {
-        c_pred = o.control;  // sub-sector runs: read everything, store control=1
+        c_pred = o.control;  // sub-sector runs: dense pass, control=0 pairs written unchanged
     }
     const uint64_t npairs = 1ull << (L - 1 - (hi >= 0 ? 1 : 0));
     T *p = static_cast<T *>(psi);

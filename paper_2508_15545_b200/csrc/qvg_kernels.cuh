@@ -76,8 +76,9 @@ __device__ __forceinline__ uint64_t ins0(uint64_t x, int b) {
 // is the mask of inserted bits that are 1 (the control).
 // When the control-1 runs would be shorter than a 32-B sector (control bit 0
 // in c128) inserting it saves no DRAM sectors but halves the lanes' access
-// efficiency, so that control is instead a store predicate (c_pred): every
-// pair is read, only control=1 pairs are written.
+// efficiency, so that control is instead a select (c_pred): every pair is
+// read and written, control=0 pairs unchanged (the dense pass's bytes, which
+// the sector-rounded algorithmic count charges anyway).
 // Each thread owns PPT pairs, strided by blockDim so every load instruction of
 // a warp covers consecutive bases.
 template <class R, int PPT>
@@ -99,9 +100,11 @@ k_pairs(typename Cplx<R>::T *__restrict__ psi, int q, int ins_lo, int ins_hi, ui
     }
 #pragma unroll
     for (int k = 0; k < PPT; ++k) {
-        if (c_pred >= 0 && !((lo[k] >> c_pred) & 1ull)) continue;
-        st_amp(psi + lo[k], madd2(m.u[0], m.u[1], a[k], m.u[2], m.u[3], b[k]));
-        st_amp(psi + (lo[k] | qb), madd2(m.u[4], m.u[5], a[k], m.u[6], m.u[7], b[k]));
+        const bool on = c_pred < 0 || ((lo[k] >> c_pred) & 1ull);
+        // control=0 pairs are written back unchanged: whole-sector stores
+        // measured faster than 16-B masked ones (profiles/r01_*).
+        st_amp(psi + lo[k], on ? madd2(m.u[0], m.u[1], a[k], m.u[2], m.u[3], b[k]) : a[k]);
+        st_amp(psi + (lo[k] | qb), on ? madd2(m.u[4], m.u[5], a[k], m.u[6], m.u[7], b[k]) : b[k]);
     }
 }
 
@@ -114,7 +117,8 @@ k_pairs(typename Cplx<R>::T *__restrict__ psi, int q, int ins_lo, int ins_hi, ui
 // whose control-1 runs fill whole sectors), so every lane is active and only
 // control=1 amplitudes are read; qm is the partner's lane distance in the
 // enumeration (2^q, or 2^(q-1) when c_ins < q). A control whose runs are
-// shorter than a sector is a store predicate instead (c_pred).
+// shorter than a sector is a select instead (c_pred; control=0 amplitudes
+// are written back unchanged).
 template <class R, int APT>
 __global__ void __launch_bounds__(256)
 k_low(typename Cplx<R>::T *__restrict__ psi, int q, int qm, int c_ins, int c_pred, Mat<R> m) {
@@ -137,7 +141,7 @@ k_low(typename Cplx<R>::T *__restrict__ psi, int q, int qm, int c_ins, int c_pre
         const bool hi = (j[k] >> q) & 1ull;
         const T out = hi ? madd2(m.u[4], m.u[5], p, m.u[6], m.u[7], v[k])
                          : madd2(m.u[0], m.u[1], v[k], m.u[2], m.u[3], p);
-        if (c_pred < 0 || ((j[k] >> c_pred) & 1ull)) st_amp(psi + j[k], out);
+        st_amp(psi + j[k], (c_pred < 0 || ((j[k] >> c_pred) & 1ull)) ? out : v[k]);
     }
 }
 
