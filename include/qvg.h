@@ -67,7 +67,10 @@ enum qvg_option {
     QVG_OPT_FUSE = 1,        /* 1: fused low/strided tile passes (default), 0: one pass per gate */
     QVG_OPT_TILE_QUBITS = 2, /* qubits per fused tile, 5..12 (default 12) */
     QVG_OPT_CARRIERS = 3,    /* lowest qubits every tile keeps contiguous (default 3) */
-    QVG_OPT_LOW_KERNEL = 4   /* 1: warp-shuffle kernel for targets < 5 (default), 0: generic */
+    QVG_OPT_LOW_KERNEL = 4,  /* 1: warp-shuffle kernel for targets < 5, 0: k_pairs (default, measured faster) */
+    QVG_OPT_MIN_RUN = 5,     /* bytes: a control/phase bit whose 1-runs are shorter is selected
+                                inside a dense pass instead of enumerated (default 32) */
+    QVG_OPT_PRED_STORE = 6   /* 1: skip stores of unselected amplitudes; 0: write them back (default) */
 };
 
 /* Counters (the reference's Metrics, metrics.hpp:14-30, plus the GPU pass

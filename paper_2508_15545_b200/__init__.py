@@ -30,6 +30,8 @@ from ._core import (  # noqa: E402
     OPT_CARRIERS,
     OPT_FUSE,
     OPT_LOW_KERNEL,
+    OPT_MIN_RUN,
+    OPT_PRED_STORE,
     OPT_TILE_QUBITS,
     QVG_ABI_VERSION,
     CapacityError,

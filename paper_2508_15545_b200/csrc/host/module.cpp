@@ -266,4 +266,6 @@ PYBIND11_MODULE(_core, m) {
     m.attr("OPT_TILE_QUBITS") = (int)QVG_OPT_TILE_QUBITS;
     m.attr("OPT_CARRIERS") = (int)QVG_OPT_CARRIERS;
     m.attr("OPT_LOW_KERNEL") = (int)QVG_OPT_LOW_KERNEL;
+    m.attr("OPT_MIN_RUN") = (int)QVG_OPT_MIN_RUN;
+    m.attr("OPT_PRED_STORE") = (int)QVG_OPT_PRED_STORE;
 }

@@ -84,7 +84,9 @@ struct qvg_state {
     bool fuse = true;
     uint32_t tile_qubits = 12;
     uint32_t carriers = 3;
-    bool low_kernel = true;
+    bool low_kernel = false;   // k_pairs measured faster for targets < 5 (profiles/r01_kernel_ab.json)
+    uint32_t min_run = 32;     // bytes: shortest 1-run of a forced bit that is inserted
+    bool pred_store = false;   // select-and-store-all for non-inserted forced bits
     // device scratch
     TileOp *d_ops = nullptr;
     size_t d_ops_cap = 0;
@@ -101,6 +103,15 @@ constexpr uint64_t kProbChunk = 1ull << 24;
 // ------------------------------------------------------------------------
 // Launchers. All grids are exact power-of-two covers of the enumeration, so
 // the kernels carry no bounds checks.
+// Forced bits (controls, phase targets) whose 1-runs are at least
+// s.min_run bytes are inserted into the enumeration (only those amplitudes
+// move); shorter runs would turn into scattered sub-granule DRAM accesses, so
+// they are selected per amplitude inside a dense pass instead.
+template <class R>
+bool inserted(const qvg_state &s, int bit) {
+    return bit >= 0 && ((uint64_t)sizeof(typename Cplx<R>::T) << bit) >= s.min_run;
+}
+
 template <class R>
 void launch_pairs(const qvg_state &s, void *psi, uint32_t L, const qvg_gate &g, const OpInfo &o) {
     using T = typename Cplx<R>::T;
@@ -108,21 +119,21 @@ void launch_pairs(const qvg_state &s, void *psi, uint32_t L, const qvg_gate &g, 
     for (int i = 0; i < 8; ++i) m.u[i] = (R)g.u[i];
     int lo = o.target, hi = -1, c_pred = -1;
     uint64_t setm = 0;
-    if (o.control >= 0 && (sizeof(typename Cplx<R>::T) << o.control) >= 32) {
-        // control-1 runs fill whole sectors: insert the bit, read only control=1
+    if (inserted<R>(s, o.control)) {
         lo = std::min(o.target, o.control);
         hi = std::max(o.target, o.control);
         setm = 1ull << o.control;
     } else if (o.control >= 0) {
-        c_pred = o.control;  // sub-sector runs: dense pass, control=0 pairs written unchanged
+        c_pred = o.control;
     }
     const uint64_t npairs = 1ull << (L - 1 - (hi >= 0 ? 1 : 0));
     T *p = static_cast<T *>(psi);
+    const int ps = s.pred_store ? 1 : 0;
     if (npairs >= 1024) {
-        k_pairs<R, 4><<<(unsigned)(npairs / 1024), 256, 0, s.stream>>>(p, o.target, lo, hi, setm, c_pred, m);
+        k_pairs<R, 4><<<(unsigned)(npairs / 1024), 256, 0, s.stream>>>(p, o.target, lo, hi, setm, c_pred, ps, m);
     } else {
         const unsigned bs = (unsigned)std::min<uint64_t>(npairs, 256);
-        k_pairs<R, 1><<<(unsigned)(npairs / bs), bs, 0, s.stream>>>(p, o.target, lo, hi, setm, c_pred, m);
+        k_pairs<R, 1><<<(unsigned)(npairs / bs), bs, 0, s.stream>>>(p, o.target, lo, hi, setm, c_pred, ps, m);
     }
 }
 
@@ -131,9 +142,7 @@ void launch_low(const qvg_state &s, void *psi, uint32_t L, const qvg_gate &g, co
     using T = typename Cplx<R>::T;
     Mat<R> m;
     for (int i = 0; i < 8; ++i) m.u[i] = (R)g.u[i];
-    // Insert the control when its control-1 runs fill whole 32-B sectors;
-    // otherwise (bit 0 in c128, bits 0-1 in c64) read all, store control=1.
-    const bool ins = o.control >= 0 && (sizeof(T) << o.control) >= 32;
+    const bool ins = inserted<R>(s, o.control);
     const int c_ins = ins ? o.control : -1;
     const int c_pred = (o.control >= 0 && !ins) ? o.control : -1;
     const int qm = 1 << ((c_ins >= 0 && c_ins < o.target) ? o.target - 1 : o.target);
@@ -150,21 +159,28 @@ void launch_low(const qvg_state &s, void *psi, uint32_t L, const qvg_gate &g, co
 template <class R>
 void launch_phase(const qvg_state &s, void *psi, uint32_t L, const qvg_gate &g, const OpInfo &o) {
     using T = typename Cplx<R>::T;
-    int lo = o.target, hi = -1;
-    uint64_t setm = 1ull << o.target;
-    if (o.control >= 0) {
-        lo = std::min(o.target, o.control);
-        hi = std::max(o.target, o.control);
-        setm |= 1ull << o.control;
+    int bits[2] = {o.target, o.control};
+    int ins[2] = {-1, -1}, nins = 0;
+    uint64_t setm = 0, selm = 0;
+    for (int b : bits) {
+        if (b < 0) continue;
+        if (inserted<R>(s, b)) {
+            ins[nins++] = b;
+            setm |= 1ull << b;
+        } else {
+            selm |= 1ull << b;
+        }
     }
-    const uint64_t count = 1ull << (L - 1 - (o.control >= 0 ? 1 : 0));
+    if (nins == 2 && ins[0] > ins[1]) std::swap(ins[0], ins[1]);
+    const uint64_t count = 1ull << (L - nins);
     T *p = static_cast<T *>(psi);
     const R dr = (R)g.u[6], di = (R)g.u[7];
+    const int ps = s.pred_store ? 1 : 0;
     if (count >= 1024) {
-        k_phase<R, 4><<<(unsigned)(count / 1024), 256, 0, s.stream>>>(p, lo, hi, setm, dr, di);
+        k_phase<R, 4><<<(unsigned)(count / 1024), 256, 0, s.stream>>>(p, ins[0], ins[1], setm, selm, ps, dr, di);
     } else {
         const unsigned bs = (unsigned)std::min<uint64_t>(count, 256);
-        k_phase<R, 1><<<(unsigned)(count / bs), bs, 0, s.stream>>>(p, lo, hi, setm, dr, di);
+        k_phase<R, 1><<<(unsigned)(count / bs), bs, 0, s.stream>>>(p, ins[0], ins[1], setm, selm, ps, dr, di);
     }
 }
 
@@ -197,6 +213,7 @@ PlanOptions plan_options(const qvg_state &s) {
     po.tile_qubits = s.tile_qubits;
     po.carriers = s.carriers;
     po.low_kernel = s.low_kernel;
+    po.min_run = s.min_run;
     return po;
 }
 
@@ -381,6 +398,11 @@ int qvg_set_option(qvg_state *s, int key, int64_t value) {
             s->carriers = (uint32_t)value;
             break;
         case QVG_OPT_LOW_KERNEL: s->low_kernel = value != 0; break;
+        case QVG_OPT_MIN_RUN:
+            if (value < 8 || value > (1 << 20) || (value & (value - 1))) throw Validation("min_run must be a power of two >= 8");
+            s->min_run = (uint32_t)value;
+            break;
+        case QVG_OPT_PRED_STORE: s->pred_store = value != 0; break;
         default: throw Validation("unknown option " + std::to_string(key));
         }
     });

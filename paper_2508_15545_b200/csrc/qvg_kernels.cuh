@@ -84,7 +84,7 @@ __device__ __forceinline__ uint64_t ins0(uint64_t x, int b) {
 template <class R, int PPT>
 __global__ void __launch_bounds__(256)
 k_pairs(typename Cplx<R>::T *__restrict__ psi, int q, int ins_lo, int ins_hi, uint64_t setm, int c_pred,
-        Mat<R> m) {
+        int pred_store, Mat<R> m) {
     using T = typename Cplx<R>::T;
     const uint64_t qb = 1ull << q;
     const uint64_t first = (uint64_t)blockIdx.x * (blockDim.x * PPT) + threadIdx.x;
@@ -101,8 +101,10 @@ k_pairs(typename Cplx<R>::T *__restrict__ psi, int q, int ins_lo, int ins_hi, ui
 #pragma unroll
     for (int k = 0; k < PPT; ++k) {
         const bool on = c_pred < 0 || ((lo[k] >> c_pred) & 1ull);
-        // control=0 pairs are written back unchanged: whole-sector stores
-        // measured faster than 16-B masked ones (profiles/r01_*).
+        // control=0 pairs are written back unchanged (whole-sector stores
+        // measured faster than 16-B masked ones, profiles/r01_*) unless
+        // pred_store asks to skip them.
+        if (!on && pred_store) continue;
         st_amp(psi + lo[k], on ? madd2(m.u[0], m.u[1], a[k], m.u[2], m.u[3], b[k]) : a[k]);
         st_amp(psi + (lo[k] | qb), on ? madd2(m.u[4], m.u[5], a[k], m.u[6], m.u[7], b[k]) : b[k]);
     }
@@ -148,23 +150,32 @@ k_low(typename Cplx<R>::T *__restrict__ psi, int q, int qm, int c_ins, int c_pre
 // ---------------------------------------------------------------------------
 // K3: phase kernel for gates diag(1, d) with optional control (Z, S, T, CZ,
 // CP/R_k): only amplitudes whose target (and control) bits are all 1 change,
-// a quarter of the state for CZ/CP and half for Z/S/T. ins_lo < ins_hi are the
-// forced-1 bit positions (ins_hi = -1 for an uncontrolled phase).
+// a quarter of the state for CZ/CP and half for Z/S/T. Forced-1 bits whose
+// runs fill whole DRAM granules are inserted into the enumeration (ins_lo <
+// ins_hi, -1 = unused; setm = their mask); the others (selm) select per
+// amplitude, with unselected amplitudes written back unchanged (or not
+// stored when pred_store).
 template <class R, int APT>
 __global__ void __launch_bounds__(256)
-k_phase(typename Cplx<R>::T *__restrict__ psi, int ins_lo, int ins_hi, uint64_t setm, R dr, R di) {
+k_phase(typename Cplx<R>::T *__restrict__ psi, int ins_lo, int ins_hi, uint64_t setm, uint64_t selm,
+        int pred_store, R dr, R di) {
     const uint64_t first = (uint64_t)blockIdx.x * (blockDim.x * APT) + threadIdx.x;
     uint64_t j[APT];
     typename Cplx<R>::T v[APT];
 #pragma unroll
     for (int k = 0; k < APT; ++k) {
-        uint64_t x = ins0(first + (uint64_t)k * blockDim.x, ins_lo);
+        uint64_t x = first + (uint64_t)k * blockDim.x;
+        if (ins_lo >= 0) x = ins0(x, ins_lo);
         if (ins_hi >= 0) x = ins0(x, ins_hi);
         j[k] = x | setm;
         v[k] = ld_amp(psi + j[k]);
     }
 #pragma unroll
-    for (int k = 0; k < APT; ++k) st_amp(psi + j[k], cmul(dr, di, v[k]));
+    for (int k = 0; k < APT; ++k) {
+        const bool on = (j[k] & selm) == selm;
+        if (on) st_amp(psi + j[k], cmul(dr, di, v[k]));
+        else if (!pred_store) st_amp(psi + j[k], v[k]);
+    }
 }
 
 // ---------------------------------------------------------------------------

@@ -93,7 +93,8 @@ struct PlanOptions {
     bool fuse = true;
     uint32_t tile_qubits = 12;
     uint32_t carriers = 3;
-    bool low_kernel = true;
+    bool low_kernel = false;
+    uint32_t min_run = 32;   // see qvg_state::min_run
 };
 
 // 2 * touched * S, rounded up to whole 32-B sectors when the touched runs are
@@ -121,7 +122,7 @@ inline Pass single_pass(const qvg_gate &g, const OpInfo &o, const PlanOptions &p
         return p;
     }
     // Low-target kernel needs 32 consecutive enumerated amplitudes per warp.
-    const bool ctl_ins = o.control >= 0 && ((uint64_t)S << o.control) >= 32;
+    const bool ctl_ins = o.control >= 0 && ((uint64_t)S << o.control) >= po.min_run;
     const uint32_t enum_bits = n - (ctl_ins ? 1 : 0);
     if (po.low_kernel && o.target < 5 && enum_bits >= 5 && n >= 6) {
         p.kind = PASS_LOW;

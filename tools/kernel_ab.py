@@ -21,6 +21,11 @@ import torch  # noqa: E402
 import paper_2508_15545_b200 as qv  # noqa: E402
 
 
+# (name, low-target shuffle kernel, min_run bytes, predicated stores)
+VARIANTS = [("pairs_run32", 0, 32, 0), ("pairs_run64", 0, 64, 0), ("pairs_run128", 0, 128, 0),
+            ("pairs_run128_pred", 0, 128, 1), ("pairs_run32_pred", 0, 32, 1), ("low_run32", 1, 32, 0)]
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=30)
@@ -46,8 +51,10 @@ def main():
         gates = qv.parse_circuit(f"qubits {n}\n{text}\n").gates()
         _, _, nbytes = qv.plan_passes(n, gates, a.precision, False)
         res = {}
-        for low in (1, 0):
+        for vname, low, min_run, pred in VARIANTS:
             st.set_option(qv.OPT_LOW_KERNEL, low)
+            st.set_option(qv.OPT_MIN_RUN, min_run)
+            st.set_option(qv.OPT_PRED_STORE, pred)
             ts = []
             for _ in range(a.reps):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -57,11 +64,9 @@ def main():
                 st.sync()
                 ts.append(e0.elapsed_time(e1))
             ms = statistics.median(ts)
-            res["low_kernel" if low else "pairs_kernel"] = {"ms": ms, "gbs": nbytes / (ms / 1e3) / 1e9}
+            res[vname] = {"ms": ms, "gbs": nbytes / (ms / 1e3) / 1e9}
         rows.append({"op": name, "alg_bytes": nbytes, **res})
-        print(f"{name:12s} " + " ".join(f"{k}={v['ms']:.3f}ms/{v['gbs']:.0f}GB/s" for k, v in res.items()
-                                         if isinstance(v, dict)), file=sys.stderr)
-    st.set_option(qv.OPT_LOW_KERNEL, 1)
+        print(f"{name:10s} " + " ".join(f"{k}={v['ms']:.2f}" for k, v in res.items()), file=sys.stderr)
     print(json.dumps({"n": n, "precision": a.precision, "reps": a.reps, "rows": rows}, indent=1))
 
 
