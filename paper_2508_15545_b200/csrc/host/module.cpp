@@ -102,11 +102,11 @@ PYBIND11_MODULE(_core, m) {
           py::arg("n_qubits"), py::arg("depth"), py::arg("seed"));
     m.def("make_benchmark_circuit", &make_benchmark_circuit, py::arg("n_qubits"));
     m.def("u3_ladder_circuit", &u3_ladder_circuit, py::arg("n_qubits"), py::arg("layers") = 20, py::arg("seed") = 1);
-    m.def("qft_circuit", [](std::uint32_t n, std::uint64_t seed) {
+    m.def("qft_circuit", [](std::uint32_t n, std::uint64_t seed, bool h_layer) {
         std::uint64_t b = 0;
-        Circuit c = qft_circuit(n, seed, &b);
+        Circuit c = qft_circuit(n, seed, &b, h_layer);
         return py::make_tuple(c, b);
-    }, py::arg("n_qubits"), py::arg("seed") = 1, "(circuit, basis index b)");
+    }, py::arg("n_qubits"), py::arg("seed") = 1, py::arg("h_layer") = true, "(circuit, basis index b)");
     m.def("haar_sweep_circuit", &haar_sweep_circuit, py::arg("n_qubits"), py::arg("seed") = 1);
     m.def("grid_circuit", &grid_circuit, py::arg("rows") = 5, py::arg("cols") = 6, py::arg("cycles") = 24,
           py::arg("seed") = 1);

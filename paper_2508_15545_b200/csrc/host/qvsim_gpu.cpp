@@ -405,7 +405,7 @@ Circuit u3_ladder_circuit(std::uint32_t n, std::uint32_t layers, std::uint64_t s
     return c;
 }
 
-Circuit qft_circuit(std::uint32_t n, std::uint64_t seed, std::uint64_t *basis_index) {
+Circuit qft_circuit(std::uint32_t n, std::uint64_t seed, std::uint64_t *basis_index, bool h_layer) {
     if (n < 1 || n > 63) throw ValidationError("qft needs 1..63 qubits");
     std::mt19937_64 rng(seed);
     const std::uint64_t b = uniform_below(rng, std::uint64_t{1} << n);
@@ -414,7 +414,8 @@ Circuit qft_circuit(std::uint32_t n, std::uint64_t seed, std::uint64_t *basis_in
     c.n_qubits = n;
     for (std::uint32_t q = 0; q < n; ++q)
         if ((b >> q) & 1u) c.ops.push_back(single_op("x", q));
-    for (std::uint32_t q = 0; q < n; ++q) c.ops.push_back(single_op("h", q));
+    if (h_layer)
+        for (std::uint32_t q = 0; q < n; ++q) c.ops.push_back(single_op("h", q));
     for (std::int64_t t = n - 1; t >= 0; --t) {
         c.ops.push_back(single_op("h", (std::uint32_t)t));
         for (std::int64_t ctl = t - 1; ctl >= 0; --ctl) {

@@ -116,7 +116,10 @@ Circuit make_benchmark_circuit(std::uint32_t n_qubits);
 Circuit u3_ladder_circuit(std::uint32_t n_qubits, std::uint32_t layers, std::uint64_t seed);
 // C1: X on the bits of a seeded basis index b, H on all qubits, QFT
 // (H + controlled-phase R_k, 2pi/2^k), bit-reversal SWAPs as 3 CX each.
-Circuit qft_circuit(std::uint32_t n_qubits, std::uint64_t seed, std::uint64_t *basis_index = nullptr);
+// h_layer = false drops the H layer: the output is then the plain QFT of |b>,
+// amplitude 2^(-n/2) e^(2 pi i b y / 2^n) at y (an analytic check at any n).
+Circuit qft_circuit(std::uint32_t n_qubits, std::uint64_t seed, std::uint64_t *basis_index = nullptr,
+                    bool h_layer = true);
 // C2: one Haar-random U per qubit q = 0..n-1, then CX(c, t) for every ordered
 // pair with |c - t| in {1, 15, 29}.
 Circuit haar_sweep_circuit(std::uint32_t n_qubits, std::uint64_t seed);
