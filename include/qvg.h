@@ -70,7 +70,8 @@ enum qvg_option {
     QVG_OPT_LOW_KERNEL = 4,  /* 1: warp-shuffle kernel for targets < 5, 0: k_pairs (default, measured faster) */
     QVG_OPT_MIN_RUN = 5,     /* bytes: a control/phase bit whose 1-runs are shorter is selected
                                 inside a dense pass instead of enumerated (default 32) */
-    QVG_OPT_PRED_STORE = 6   /* 1: skip stores of unselected amplitudes; 0: write them back (default) */
+    QVG_OPT_PRED_STORE = 6,  /* 1: skip stores of unselected amplitudes; 0: write them back (default) */
+    QVG_OPT_SUB_BITS = 7     /* fused tile: 2^b register amplitudes per thread, b = 3 or 4 (default 4) */
 };
 
 /* Counters (the reference's Metrics, metrics.hpp:14-30, plus the GPU pass

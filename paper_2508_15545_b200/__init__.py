@@ -32,6 +32,7 @@ from ._core import (  # noqa: E402
     OPT_LOW_KERNEL,
     OPT_MIN_RUN,
     OPT_PRED_STORE,
+    OPT_SUB_BITS,
     OPT_TILE_QUBITS,
     QVG_ABI_VERSION,
     CapacityError,

@@ -87,6 +87,7 @@ struct qvg_state {
     bool low_kernel = false;   // k_pairs measured faster for targets < 5 (profiles/r01_kernel_ab.json)
     uint32_t min_run = 32;     // bytes: shortest 1-run of a forced bit that is inserted
     bool pred_store = false;   // select-and-store-all for non-inserted forced bits
+    uint32_t sub_bits = 4;     // fused tile: 2^sub register amplitudes per thread
     // device scratch
     TileOp *d_ops = nullptr;
     size_t d_ops_cap = 0;
@@ -187,22 +188,23 @@ void launch_phase(const qvg_state &s, void *psi, uint32_t L, const qvg_gate &g, 
 template <class R>
 void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *d_ops) {
     using T = typename Cplx<R>::T;
-    const unsigned threads = 1u << (p.geom.k - 3);  // one 8-amplitude subcube per thread
-    const size_t smem = (((sizeof(uint64_t) << p.geom.nhi) + 15) & ~size_t(15)) +
-                        (p.geom.ngroups > 1 ? (sizeof(T) << p.geom.k) : 0);
-    static bool attr_set[2] = {false, false};
-    const int which = sizeof(R) == 8 ? 1 : 0;
-    if (!attr_set[which]) {
-        cuda_check(cudaFuncSetAttribute(k_tile<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
+    const TileGeom &g = p.geom;
+    const unsigned threads = 1u << (g.k - g.sub);  // one 2^sub-amplitude subcube per thread
+    const size_t smem = sizeof(TileOp) * g.nrec + (((sizeof(uint64_t) << g.nhi) + 15) & ~size_t(15)) +
+                        (g.ngroups > 1 ? (sizeof(T) << g.k) : 0);
+    auto kern = g.sub == 4 ? k_tile<R, 4> : k_tile<R, 3>;
+    static bool attr_set[2][2] = {{false, false}, {false, false}};
+    bool &set = attr_set[sizeof(R) == 8][g.sub == 4];
+    if (!set) {
+        cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
                    "cudaFuncSetAttribute(k_tile)");
-        attr_set[which] = true;
+        set = true;
     }
     int per_sm = 0;
-    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tile<R>, (int)threads, smem),
-               "occupancy(k_tile)");
+    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (int)threads, smem), "occupancy(k_tile)");
     per_sm = std::max(per_sm, 1);
-    const uint64_t grid = std::min<uint64_t>(p.geom.ntiles, (uint64_t)per_sm * s.sm_count);
-    k_tile<R><<<(unsigned)grid, threads, smem, s.stream>>>(static_cast<T *>(psi), p.geom, d_ops + p.op_begin);
+    const uint64_t grid = std::min<uint64_t>(g.ntiles, (uint64_t)per_sm * s.sm_count);
+    kern<<<(unsigned)grid, threads, smem, s.stream>>>(static_cast<T *>(psi), g, d_ops + p.op_begin);
 }
 
 PlanOptions plan_options(const qvg_state &s) {
@@ -214,6 +216,7 @@ PlanOptions plan_options(const qvg_state &s) {
     po.carriers = s.carriers;
     po.low_kernel = s.low_kernel;
     po.min_run = s.min_run;
+    po.sub_bits = s.sub_bits;
     return po;
 }
 
@@ -403,6 +406,10 @@ int qvg_set_option(qvg_state *s, int key, int64_t value) {
             s->min_run = (uint32_t)value;
             break;
         case QVG_OPT_PRED_STORE: s->pred_store = value != 0; break;
+        case QVG_OPT_SUB_BITS:
+            if (value != 3 && value != 4) throw Validation("sub_bits must be 3 or 4");
+            s->sub_bits = (uint32_t)value;
+            break;
         default: throw Validation("unknown option " + std::to_string(key));
         }
     });

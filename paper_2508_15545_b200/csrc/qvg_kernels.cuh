@@ -177,159 +177,6 @@ k_phase(typename Cplx<R>::T *__restrict__ psi, int ins_lo, int ins_hi, uint64_t 
         else if (!pred_store) st_amp(psi + j[k], v[k]);
     }
 }
-
-// ---------------------------------------------------------------------------
-// K4: fused tile pass — the B200 replacement for the reference's block store +
-// sliding window (store.cpp, cache.cpp, kernel.cpp:113-146). A CTA owns a tile
-// of 2^k amplitudes and applies a run of gates to it in circuit order, so the
-// whole run costs one HBM round trip. The tile is the set of amplitudes that
-// agree on every qubit outside the tile qubit set Q (|Q| = k): its lowest
-// `lowc` qubits are 0..lowc-1 (contiguous 2^lowc-amp segments in HBM), the
-// other k-lowc are arbitrary high qubits, so gates on any qubit can be fused.
-// A control outside Q is constant per tile, and a diagonal gate needs no
-// pairing, so its qubits may lie anywhere.
-//
-// Inside the tile the run is cut into groups whose pair ops touch at most 3
-// tile bits. For a group, each of the 2^(k-3) threads holds the 8 amplitudes
-// of one 3-bit subcube in registers and applies all the group's ops there;
-// shared memory is only the transpose buffer between groups. The first group
-// reads HBM directly and the last one writes HBM directly, so a run that fits
-// one group never touches shared memory.
-enum TileOpKind : int32_t { TILE_PAIR = 0, TILE_DIAG = 1, TILE_GROUP = 2 };
-
-struct TileOp {
-    int32_t kind;      // TileOpKind
-    int32_t tbit;      // pair/diag: tile-local target bit, -1 if outside Q (diag only); group: b0
-    int32_t cbit;      // tile-local control bit, -1 if none or outside Q; group: b1
-    int32_t d0_is_one; // diag: d0 == 1 exactly (bit-0 amplitudes untouched); group: b2
-    uint64_t greq;     // global bits that must be 1 in the tile base (controls outside Q); group: op count
-    uint64_t gtgt;     // diag with target outside Q: that global bit
-    double u[8];       // matrix (diag uses u00 = u[0..1], u11 = u[6..7])
-};
-
-struct TileGeom {
-    int n, k, lowc;       // qubits, tile qubits, contiguous low qubits
-    int nhi;              // k - lowc
-    int ngroups;          // register groups in this pass
-    int hiq[24];          // tile qubits >= lowc, ascending (tile-local bits lowc..k-1)
-    uint64_t outmask;     // qubits not in Q
-    uint64_t ntiles;      // 2^(n-k)
-};
-
-__device__ __forceinline__ uint64_t pdep_mask(uint64_t v, uint64_t mask) {
-    uint64_t r = 0;
-    while (mask) {
-        const uint64_t bit = mask & (~mask + 1ull);
-        if (v & 1ull) r |= bit;
-        v >>= 1;
-        mask ^= bit;
-    }
-    return r;
-}
-
-// Pair op on group bit J: register pairs (r, r | 2^J) for the 4 r with bit J = 0.
-// cmask: bit r set when element r's control is 1 (all set when uncontrolled).
-template <class R, int J>
-__device__ __forceinline__ void group_pair(typename Cplx<R>::T (&v)[8], uint32_t cmask, const R *u) {
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-        if ((r >> J) & 1) continue;
-        if (!((cmask >> r) & 1u)) continue;
-        const typename Cplx<R>::T a = v[r], b = v[r | (1 << J)];
-        v[r] = madd2(u[0], u[1], a, u[2], u[3], b);
-        v[r | (1 << J)] = madd2(u[4], u[5], a, u[6], u[7], b);
-    }
-}
-
-template <class R>
-__global__ void __launch_bounds__(512, 2)
-k_tile(typename Cplx<R>::T *__restrict__ psi, TileGeom g, const TileOp *__restrict__ ops) {
-    using T = typename Cplx<R>::T;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    uint64_t *offhi = reinterpret_cast<uint64_t *>(smem_raw);
-    // offset table first, padded to 16 B so the double2 tile stays aligned
-    T *sm = reinterpret_cast<T *>(smem_raw + (((sizeof(uint64_t) << g.nhi) + 15) & ~size_t(15)));
-    const uint32_t nhi = 1u << g.nhi;
-    const uint32_t lowm = (1u << g.lowc) - 1u;
-    for (uint32_t h = threadIdx.x; h < nhi; h += blockDim.x) {
-        uint64_t off = 0;
-#pragma unroll
-        for (int i = 0; i < 24; ++i)
-            if (i < g.nhi && ((h >> i) & 1u)) off |= 1ull << g.hiq[i];
-        offhi[h] = off;
-    }
-    __syncthreads();
-    for (uint64_t tile = blockIdx.x; tile < g.ntiles; tile += gridDim.x) {
-        const uint64_t base = pdep_mask(tile, g.outmask);
-        int rec = 0;
-        for (int gi = 0; gi < g.ngroups; ++gi) {
-            const TileOp hdr = ops[rec++];
-            const int b0 = hdr.tbit, b1 = hdr.cbit, b2 = hdr.d0_is_one;
-            const int nops = (int)hdr.greq;
-            // this thread's subcube: local indices l0 | {0, 2^b0} | {0, 2^b1} | {0, 2^b2}
-            const uint32_t l0 = (uint32_t)ins0(ins0(ins0(threadIdx.x, b0), b1), b2);
-            auto lidx = [&](int r) {
-                return l0 | ((r & 1) ? 1u << b0 : 0u) | ((r & 2) ? 1u << b1 : 0u) | ((r & 4) ? 1u << b2 : 0u);
-            };
-            // 8-bit mask over the subcube: element r has tile-local bit `bit` set
-            auto rmask = [&](int bit) -> uint32_t {
-                if (bit < 0) return 0xFFu;
-                if (bit == b0) return 0xAAu;
-                if (bit == b1) return 0xCCu;
-                if (bit == b2) return 0xF0u;
-                return ((l0 >> bit) & 1u) ? 0xFFu : 0u;
-            };
-            T v[8];
-            if (gi == 0) {
-#pragma unroll
-                for (int r = 0; r < 8; ++r) {
-                    const uint32_t lr = lidx(r);
-                    v[r] = ld_amp(psi + (base | offhi[lr >> g.lowc] | (lr & lowm)));
-                }
-            } else {
-#pragma unroll
-                for (int r = 0; r < 8; ++r) v[r] = sm[lidx(r)];
-            }
-            for (int i = 0; i < nops; ++i) {
-                const TileOp &op = ops[rec + i];
-                if ((base & op.greq) != op.greq) continue;  // control outside the tile is 0
-                R u[8];
-#pragma unroll
-                for (int x = 0; x < 8; ++x) u[x] = (R)op.u[x];
-                if (op.kind == TILE_PAIR) {
-                    const uint32_t cm = rmask(op.cbit);
-                    if (op.tbit == b0) group_pair<R, 0>(v, cm, u);
-                    else if (op.tbit == b1) group_pair<R, 1>(v, cm, u);
-                    else group_pair<R, 2>(v, cm, u);
-                } else {
-                    const uint32_t cm = rmask(op.cbit);
-                    const uint32_t tm = op.tbit >= 0 ? rmask(op.tbit) : ((base & op.gtgt) ? 0xFFu : 0u);
-#pragma unroll
-                    for (int r = 0; r < 8; ++r) {
-                        if (!((cm >> r) & 1u)) continue;
-                        const bool one = (tm >> r) & 1u;
-                        if (!one && op.d0_is_one) continue;
-                        v[r] = one ? cmul(u[6], u[7], v[r]) : cmul(u[0], u[1], v[r]);
-                    }
-                }
-            }
-            rec += nops;
-            if (gi == g.ngroups - 1) {
-#pragma unroll
-                for (int r = 0; r < 8; ++r) {
-                    const uint32_t lr = lidx(r);
-                    st_amp(psi + (base | offhi[lr >> g.lowc] | (lr & lowm)), v[r]);
-                }
-            } else {
-#pragma unroll
-                for (int r = 0; r < 8; ++r) sm[lidx(r)] = v[r];
-                __syncthreads();
-            }
-        }
-        if (g.ngroups > 1) __syncthreads();  // last group read sm; the next tile's groups write it
-    }
-}
-
 // ---------------------------------------------------------------------------
 // K5: swap two local qubits a < b in place (pure permutation: amplitudes with
 // bits (a,b) = (1,0) trade places with (0,1)). Used to restore the canonical

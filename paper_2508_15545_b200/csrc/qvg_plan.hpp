@@ -23,6 +23,7 @@
 
 #include "qvg.h"
 #include "qvg_kernels.cuh"
+#include "qvg_tile.cuh"
 
 namespace qvg {
 
@@ -95,7 +96,11 @@ struct PlanOptions {
     uint32_t carriers = 3;
     bool low_kernel = false;
     uint32_t min_run = 32;   // see qvg_state::min_run
+    uint32_t sub_bits = 4;   // tile register subcube: 2^sub amplitudes per thread (3 or 4)
 };
+
+// Ops per fused pass: the records are staged in shared memory (96 B each).
+constexpr uint64_t kMaxRunOps = 192;
 
 // 2 * touched * S, rounded up to whole 32-B sectors when the touched runs are
 // shorter than a sector.
@@ -147,6 +152,7 @@ inline Plan make_plan(const qvg_gate *ops, uint64_t count, const PlanOptions &po
     const uint32_t k = std::min<uint32_t>(po.tile_qubits, n);
     const bool fuse = po.fuse && k >= 5;  // a tile needs >= 4 threads of 8-amplitude subcubes
     const uint32_t lowmin = std::min<uint32_t>(po.carriers, k);
+    const uint32_t sub = po.sub_bits;
     std::vector<OpInfo> info(count);
     for (uint64_t i = 0; i < count; ++i) info[i] = classify(ops[i]);
     plan.gates = count;
@@ -161,7 +167,7 @@ inline Plan make_plan(const qvg_gate *ops, uint64_t count, const PlanOptions &po
         // Greedy maximal run whose non-diagonal targets fit in one tile.
         std::vector<int> high;  // tile qubits >= lowmin required by the run
         uint64_t j = i, cost = 0, live = 0;
-        while (j < count) {
+        while (j < count && live < kMaxRunOps) {
             const OpInfo &o = info[j];
             if (!o.identity) {
                 if (!o.diag && (uint32_t)o.target >= lowmin &&
@@ -194,35 +200,34 @@ inline Plan make_plan(const qvg_gate *ops, uint64_t count, const PlanOptions &po
             g.lowc = 0;
             while (g.lowc < (int)n && inq[g.lowc]) ++g.lowc;
             g.nhi = 0;
-            g.outmask = 0;
-            for (uint32_t q = 0; q < n; ++q) {
-                if (!inq[q]) g.outmask |= 1ull << q;
-                else if ((int)q >= g.lowc) g.hiq[g.nhi++] = (int)q;
-            }
+            for (uint32_t q = (uint32_t)g.lowc; q < n; ++q)
+                if (inq[q]) g.hiq[g.nhi++] = (int)q;
             g.ntiles = 1ull << (n - k);
+            g.sub = (int)std::min<uint32_t>(sub, k - 2);
             Pass p;
             p.kind = PASS_TILE;
-            p.geom = g;
             p.op_begin = (uint32_t)plan.tile_ops.size();
             // Records: [group header, its ops]... Each group's pair ops touch
-            // at most 3 tile bits (the thread's register subcube).
+            // at most `sub` tile bits (the thread's register subcube).
             std::vector<TileOp> group;
-            int gbits[3];
+            int gbits[4];
             int nb = 0;
             auto close_group = [&] {
                 if (group.empty()) return;
-                for (int b = 0; nb < 3 && b < g.k; ++b) {  // pad with the lowest unused bits
+                for (int b = 0; nb < g.sub && b < g.k; ++b) {  // pad with the lowest unused bits
                     bool used = false;
                     for (int x = 0; x < nb; ++x) used |= gbits[x] == b;
                     if (!used) gbits[nb++] = b;
                 }
-                std::sort(gbits, gbits + 3);
+                std::sort(gbits, gbits + g.sub);
+                for (TileOp &t : group)  // target slot within the sorted group bits
+                    if (t.kind == TILE_PAIR)
+                        for (int s = 0; s < g.sub; ++s)
+                            if (gbits[s] == t.tbit) t.slot = s;
                 TileOp h{};
                 h.kind = TILE_GROUP;
-                h.tbit = gbits[0];
-                h.cbit = gbits[1];
-                h.d0_is_one = gbits[2];
-                h.greq = group.size();
+                h.tbit = (int32_t)group.size();
+                for (int s = 0; s < g.sub; ++s) h.gtgt |= (uint64_t)gbits[s] << (8 * s);
                 plan.tile_ops.push_back(h);
                 plan.tile_ops.insert(plan.tile_ops.end(), group.begin(), group.end());
                 group.clear();
@@ -243,18 +248,19 @@ inline Plan make_plan(const qvg_gate *ops, uint64_t count, const PlanOptions &po
                     t.cbit = local_bit(o.control, g);
                     if (t.cbit < 0) t.greq = 1ull << o.control;
                 }
-                t.d0_is_one = (ops[x].u[0] == 1.0 && ops[x].u[1] == 0.0) ? 1 : 0;
+                if (t.kind == TILE_DIAG) t.slot = (ops[x].u[0] == 1.0 && ops[x].u[1] == 0.0) ? 1 : 0;
                 if (t.kind == TILE_PAIR) {
                     bool have = false;
                     for (int b = 0; b < nb; ++b) have |= gbits[b] == t.tbit;
                     if (!have) {
-                        if (nb == 3) close_group();
+                        if (nb == g.sub) close_group();
                         gbits[nb++] = t.tbit;
                     }
                 }
                 group.push_back(t);
             }
             close_group();
+            g.nrec = (int)(plan.tile_ops.size() - p.op_begin);
             p.geom = g;
             p.op_count = (uint32_t)(plan.tile_ops.size() - p.op_begin);
             p.bytes = full;

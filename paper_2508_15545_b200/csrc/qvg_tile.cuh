@@ -1,0 +1,192 @@
+// qvg_tile.cuh — K4, the fused tile pass: the B200 replacement for the
+// reference's block store + sliding window (reference store.cpp, cache.cpp,
+// kernel.cpp:113-146).
+//
+// A CTA owns a tile of 2^k amplitudes and applies a run of gates to it in
+// circuit order, so the whole run costs one HBM round trip instead of one per
+// gate. The tile is the set of amplitudes that agree on every qubit outside
+// the tile qubit set Q (|Q| = k): its lowest `lowc` qubits are 0..lowc-1
+// (contiguous 2^lowc-amplitude segments in HBM, >= 128 B), the other k-lowc
+// are arbitrary high qubits, so gates on any qubit can be fused. A control
+// outside Q is constant per tile, and a diagonal gate needs no pairing, so its
+// qubits may lie anywhere.
+//
+// Inside the tile the run is cut into groups whose pair ops touch at most SUB
+// tile bits. For a group, each of the 2^(k-SUB) threads holds the 2^SUB
+// amplitudes of one SUB-bit subcube in registers and applies all the group's
+// ops there; shared memory is only the transpose buffer between groups. The
+// first group reads HBM directly and the last one writes HBM directly, so a
+// run that fits one group never touches the shared tile. The op records are
+// staged in shared memory once per CTA (they are the same for every tile).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "qvg_kernels.cuh"
+
+namespace qvg {
+
+enum TileOpKind : int32_t { TILE_PAIR = 0, TILE_DIAG = 1, TILE_GROUP = 2 };
+
+// One record of a tile pass: a group header followed by its ops.
+struct __align__(16) TileOp {
+    int32_t kind;      // TileOpKind
+    int32_t tbit;      // pair/diag: tile-local target bit (-1: diag target outside Q); group: op count
+    int32_t cbit;      // tile-local control bit, -1 if none or outside Q
+    int32_t slot;      // pair: index of the target among the group's bits; diag: d0 == 1 exactly
+    uint64_t greq;     // global bits that must be 1 in the tile base (controls outside Q)
+    uint64_t gtgt;     // diag: global target bit outside Q; group: packed bits b0 | b1<<8 | b2<<16 | b3<<24
+    double u[8];       // matrix (diag uses u00 = u[0..1], u11 = u[6..7])
+};
+static_assert(sizeof(TileOp) == 96, "TileOp layout");
+
+struct TileGeom {
+    int n, k, lowc;       // qubits, tile qubits, contiguous low qubits
+    int nhi;              // k - lowc
+    int ngroups;          // register groups in this pass
+    int nrec;             // records (headers + ops)
+    int sub;              // subcube bits per thread (3 or 4)
+    int pad;
+    int hiq[24];          // tile qubits >= lowc, ascending (tile-local bits lowc..k-1)
+    uint64_t ntiles;      // 2^(n-k)
+};
+
+// Pair op on group bit J over the 2^SUB register amplitudes.
+// cmask: bit r set when element r's control is 1 (all set when uncontrolled).
+template <class R, int SUB, int J>
+__device__ __forceinline__ void group_pair(typename Cplx<R>::T (&v)[1 << SUB], uint32_t cmask, const R *u) {
+#pragma unroll
+    for (int r = 0; r < (1 << SUB); ++r) {
+        if ((r >> J) & 1) continue;
+        if (!((cmask >> r) & 1u)) continue;
+        const typename Cplx<R>::T a = v[r], b = v[r | (1 << J)];
+        v[r] = madd2(u[0], u[1], a, u[2], u[3], b);
+        v[r | (1 << J)] = madd2(u[4], u[5], a, u[6], u[7], b);
+    }
+}
+
+// Mask over the subcube: bit r set when element r has tile-local bit `bit`.
+template <int SUB>
+__device__ __forceinline__ uint32_t sub_mask(int bit, const int (&b)[SUB], uint32_t l0) {
+    constexpr uint32_t full = (1u << (1 << SUB)) - 1u;
+    if (bit < 0) return full;
+    uint32_t m = ((l0 >> bit) & 1u) ? full : 0u;
+#pragma unroll
+    for (int j = 0; j < SUB; ++j) {
+        if (bit == b[j]) {
+            uint32_t mj = 0;
+#pragma unroll
+            for (int r = 0; r < (1 << SUB); ++r) mj |= ((r >> j) & 1) ? (1u << r) : 0u;
+            m = mj;
+        }
+    }
+    return m;
+}
+
+template <class R, int SUB>
+__global__ void __launch_bounds__(1 << (12 - SUB), 2)
+k_tile(typename Cplx<R>::T *__restrict__ psi, const TileGeom g, const TileOp *__restrict__ ops_g) {
+    using T = typename Cplx<R>::T;
+    constexpr int E = 1 << SUB;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    TileOp *ops = reinterpret_cast<TileOp *>(smem_raw);
+    uint64_t *offhi = reinterpret_cast<uint64_t *>(smem_raw + sizeof(TileOp) * g.nrec);
+    T *sm = reinterpret_cast<T *>(smem_raw + sizeof(TileOp) * g.nrec + (((sizeof(uint64_t) << g.nhi) + 15) & ~15ull));
+    const uint32_t nhi = 1u << g.nhi;
+    const uint32_t lowm = (1u << g.lowc) - 1u;
+    {  // stage the op records (16-B vectors) and the high-qubit offset table
+        const int4 *src = reinterpret_cast<const int4 *>(ops_g);
+        int4 *dst = reinterpret_cast<int4 *>(ops);
+        for (int i = threadIdx.x; i < g.nrec * 6; i += blockDim.x) dst[i] = src[i];
+        for (uint32_t h = threadIdx.x; h < nhi; h += blockDim.x) {
+            uint64_t off = 0;
+#pragma unroll
+            for (int i = 0; i < 24; ++i)
+                if (i < g.nhi && ((h >> i) & 1u)) off |= 1ull << g.hiq[i];
+            offhi[h] = off;
+        }
+    }
+    __syncthreads();
+    for (uint64_t tile = blockIdx.x; tile < g.ntiles; tile += gridDim.x) {
+        // base index: the tile number spread over the qubits outside Q
+        uint64_t base = tile << g.lowc;
+#pragma unroll
+        for (int i = 0; i < 24; ++i)
+            if (i < g.nhi) base = ins0(base, g.hiq[i]);
+        int rec = 0;
+        for (int gi = 0; gi < g.ngroups; ++gi) {
+            const int nops = ops[rec].tbit;
+            const uint64_t packed = ops[rec].gtgt;
+            ++rec;
+            int b[SUB];
+#pragma unroll
+            for (int j = 0; j < SUB; ++j) b[j] = (int)((packed >> (8 * j)) & 0xff);
+            // this thread's subcube: local indices l0 | sum_j {0, 2^b_j}
+            uint32_t l0 = threadIdx.x;
+#pragma unroll
+            for (int j = 0; j < SUB; ++j) l0 = (uint32_t)ins0(l0, b[j]);
+            auto lidx = [&](int r) {
+                uint32_t l = l0;
+#pragma unroll
+                for (int j = 0; j < SUB; ++j) l |= ((r >> j) & 1) ? (1u << b[j]) : 0u;
+                return l;
+            };
+            T v[E];
+            if (gi == 0) {
+#pragma unroll
+                for (int r = 0; r < E; ++r) {
+                    const uint32_t lr = lidx(r);
+                    v[r] = ld_amp(psi + (base | offhi[lr >> g.lowc] | (lr & lowm)));
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < E; ++r) v[r] = sm[lidx(r)];
+            }
+            for (int i = 0; i < nops; ++i) {
+                const TileOp &op = ops[rec + i];
+                if ((base & op.greq) != op.greq) continue;  // control outside the tile is 0
+                R u[8];
+#pragma unroll
+                for (int x = 0; x < 8; ++x) u[x] = (R)op.u[x];
+                const uint32_t cm = sub_mask<SUB>(op.cbit, b, l0);
+                if (op.kind == TILE_PAIR) {
+                    switch (op.slot) {
+                    case 0: group_pair<R, SUB, 0>(v, cm, u); break;
+                    case 1: group_pair<R, SUB, 1>(v, cm, u); break;
+                    case 2: group_pair<R, SUB, 2>(v, cm, u); break;
+                    default:
+                        if constexpr (SUB > 3) group_pair<R, SUB, SUB - 1>(v, cm, u);
+                        break;
+                    }
+                } else {
+                    const uint32_t tm = op.tbit >= 0 ? sub_mask<SUB>(op.tbit, b, l0)
+                                                     : ((base & op.gtgt) ? 0xFFFFu : 0u);
+                    const bool d0_one = op.slot != 0;
+#pragma unroll
+                    for (int r = 0; r < E; ++r) {
+                        if (!((cm >> r) & 1u)) continue;
+                        const bool one = (tm >> r) & 1u;
+                        if (!one && d0_one) continue;
+                        v[r] = one ? cmul(u[6], u[7], v[r]) : cmul(u[0], u[1], v[r]);
+                    }
+                }
+            }
+            rec += nops;
+            if (gi == g.ngroups - 1) {
+#pragma unroll
+                for (int r = 0; r < E; ++r) {
+                    const uint32_t lr = lidx(r);
+                    st_amp(psi + (base | offhi[lr >> g.lowc] | (lr & lowm)), v[r]);
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < E; ++r) sm[lidx(r)] = v[r];
+                __syncthreads();
+            }
+        }
+        if (g.ngroups > 1) __syncthreads();  // last group read sm; the next tile's groups write it
+    }
+}
+
+}  // namespace qvg

@@ -1,0 +1,74 @@
+"""Fused-pass timing on the BASELINE circuits (n=30 by default): device time
+per circuit (CUDA events on the state's stream, median of reps), HBM passes,
+and effective amp-updates/s, for each fused-tile variant and per-gate.
+
+    python tools/fused_ab.py [--n 30] [--reps 3] > profiles/rNN_fused_ab.json
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_2508_15545_b200 as qv  # noqa: E402
+
+# (name, fuse, sub_bits)
+VARIANTS = [("fused_sub4", 1, 4), ("fused_sub3", 1, 3), ("per_gate", 0, 4)]
+
+
+def circuits(n):
+    return [
+        ("config2_haar_sweep", qv.haar_sweep_circuit(n, 2508)),
+        ("config3_grid_5x6_c24", qv.grid_circuit(5, 6, 24, 1) if n == 30 else None),
+        ("config1_qft", qv.qft_circuit(n, 1)[0]),
+        ("config0_u3_ladder_l4", qv.u3_ladder_circuit(n, 4, 1)),
+    ]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=30)
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--precision", type=int, default=128)
+    a = ap.parse_args()
+    st = qv.StateVector.create(a.n, a.precision, 0)
+    stream = torch.cuda.ExternalStream(st.stream())
+    out = []
+    for name, c in circuits(a.n):
+        if c is None:
+            continue
+        g = c.gates()
+        row = {"circuit": name, "ops": len(c)}
+        for vname, fuse, sub in VARIANTS:
+            st.set_option(qv.OPT_FUSE, fuse)
+            st.set_option(qv.OPT_SUB_BITS, sub)
+            st.apply_gates(g)  # warm-up (and plan)
+            st.reset_stats()
+            ts = []
+            for _ in range(a.reps):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                st.apply_gates(g, sync=False)
+                e1.record(stream)
+                st.sync()
+                ts.append(e0.elapsed_time(e1))
+            ms = statistics.median(ts)
+            s = st.stats()
+            row[vname] = {"ms": ms, "passes": s["passes"] / a.reps,
+                          "amp_updates_per_s": len(c) * (1 << a.n) / (ms / 1e3),
+                          "hbm_gbs": s["bytes_moved"] / a.reps / (ms / 1e3) / 1e9}
+        out.append(row)
+        print(name, " ".join(f"{k}={v['ms']:.1f}ms/{v['passes']:.0f}p" for k, v in row.items() if isinstance(v, dict)),
+              file=sys.stderr)
+    st.set_option(qv.OPT_SUB_BITS, 4)
+    st.set_option(qv.OPT_FUSE, 1)
+    print(json.dumps({"n": a.n, "precision": a.precision, "reps": a.reps, "rows": out}, indent=1))
+
+
+if __name__ == "__main__":
+    main()
