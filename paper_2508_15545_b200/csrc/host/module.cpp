@@ -269,4 +269,5 @@ PYBIND11_MODULE(_core, m) {
     m.attr("OPT_MIN_RUN") = (int)QVG_OPT_MIN_RUN;
     m.attr("OPT_PRED_STORE") = (int)QVG_OPT_PRED_STORE;
     m.attr("OPT_SUB_BITS") = (int)QVG_OPT_SUB_BITS;
+    m.attr("OPT_FMA") = (int)QVG_OPT_FMA;
 }

@@ -87,7 +87,8 @@ struct qvg_state {
     bool low_kernel = false;   // k_pairs measured faster for targets < 5 (profiles/r01_kernel_ab.json)
     uint32_t min_run = 32;     // bytes: shortest 1-run of a forced bit that is inserted
     bool pred_store = false;   // select-and-store-all for non-inserted forced bits
-    uint32_t sub_bits = 4;     // fused tile: 2^sub register amplitudes per thread
+    uint32_t sub_bits = 3;     // fused tile: 2^sub register amplitudes per thread (3 measured faster)
+    bool fma = false;          // fused tile c128: DFMA arithmetic (not bit-identical to the reference)
     // device scratch
     TileOp *d_ops = nullptr;
     size_t d_ops_cap = 0;
@@ -192,9 +193,11 @@ void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *d_ops) {
     const unsigned threads = 1u << (g.k - g.sub);  // one 2^sub-amplitude subcube per thread
     const size_t smem = sizeof(TileOp) * g.nrec + (((sizeof(uint64_t) << g.nhi) + 15) & ~size_t(15)) +
                         (g.ngroups > 1 ? (sizeof(T) << g.k) : 0);
-    auto kern = g.sub == 4 ? k_tile<R, 4> : k_tile<R, 3>;
-    static bool attr_set[2][2] = {{false, false}, {false, false}};
-    bool &set = attr_set[sizeof(R) == 8][g.sub == 4];
+    const bool fma = s.fma && sizeof(R) == 8;  // complex64 always contracts
+    auto kern = g.sub == 4 ? (fma ? k_tile<R, 4, true> : k_tile<R, 4, false>)
+                           : (fma ? k_tile<R, 3, true> : k_tile<R, 3, false>);
+    static bool attr_set[2][2][2] = {};
+    bool &set = attr_set[sizeof(R) == 8][g.sub == 4][fma];
     if (!set) {
         cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
                    "cudaFuncSetAttribute(k_tile)");
@@ -410,6 +413,7 @@ int qvg_set_option(qvg_state *s, int key, int64_t value) {
             if (value != 3 && value != 4) throw Validation("sub_bits must be 3 or 4");
             s->sub_bits = (uint32_t)value;
             break;
+        case QVG_OPT_FMA: s->fma = value != 0; break;
         default: throw Validation("unknown option " + std::to_string(key));
         }
     });

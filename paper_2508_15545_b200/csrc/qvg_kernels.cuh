@@ -50,6 +50,31 @@ __device__ __forceinline__ float2 cmul(float dr, float di, float2 a) {
     return make_float2(dr * a.x - di * a.y, dr * a.y + di * a.x);
 }
 
+// Opt-in fast variants for complex128 (QVG_OPT_FMA): DFMA-contracted, 8
+// instead of 14 FP64 instructions per output, within ~1e-16 relative of the
+// exact forms but no longer bit-identical to the reference. complex64 always
+// contracts, so both variants are the same there.
+template <bool FMA>
+__device__ __forceinline__ double2 madd2x(double m0r, double m0i, double2 a, double m1r, double m1i, double2 b) {
+    if constexpr (!FMA) return madd2(m0r, m0i, a, m1r, m1i, b);
+    const double re = fma(m0r, a.x, fma(-m0i, a.y, fma(m1r, b.x, -(m1i * b.y))));
+    const double im = fma(m0r, a.y, fma(m0i, a.x, fma(m1r, b.y, m1i * b.x)));
+    return make_double2(re, im);
+}
+template <bool FMA>
+__device__ __forceinline__ float2 madd2x(float m0r, float m0i, float2 a, float m1r, float m1i, float2 b) {
+    return madd2(m0r, m0i, a, m1r, m1i, b);
+}
+template <bool FMA>
+__device__ __forceinline__ double2 cmulx(double dr, double di, double2 a) {
+    if constexpr (!FMA) return cmul(dr, di, a);
+    return make_double2(fma(dr, a.x, -(di * a.y)), fma(dr, a.y, di * a.x));
+}
+template <bool FMA>
+__device__ __forceinline__ float2 cmulx(float dr, float di, float2 a) {
+    return cmul(dr, di, a);
+}
+
 // Streaming loads/stores: every amplitude is touched once per pass, so mark
 // the lines evict-first in L2 (ld.global.cs / st.global.cs).
 __device__ __forceinline__ double2 ld_amp(const double2 *p) { return __ldcs(p); }

@@ -96,7 +96,7 @@ struct PlanOptions {
     uint32_t carriers = 3;
     bool low_kernel = false;
     uint32_t min_run = 32;   // see qvg_state::min_run
-    uint32_t sub_bits = 4;   // tile register subcube: 2^sub amplitudes per thread (3 or 4)
+    uint32_t sub_bits = 3;   // tile register subcube: 2^sub amplitudes per thread (3 or 4)
 };
 
 // Ops per fused pass: the records are staged in shared memory (96 B each).
@@ -250,11 +250,26 @@ inline Plan make_plan(const qvg_gate *ops, uint64_t count, const PlanOptions &po
                 }
                 if (t.kind == TILE_DIAG) t.slot = (ops[x].u[0] == 1.0 && ops[x].u[1] == 0.0) ? 1 : 0;
                 if (t.kind == TILE_PAIR) {
-                    bool have = false;
-                    for (int b = 0; b < nb; ++b) have |= gbits[b] == t.tbit;
-                    if (!have) {
-                        if (nb == g.sub) close_group();
-                        gbits[nb++] = t.tbit;
+                    // The target must be a register bit. An in-tile control is
+                    // made one too: the control test is then the same for every
+                    // thread (no lane divergence) and skips half the pairs.
+                    int need[2] = {t.tbit, t.cbit};
+                    auto missing = [&] {
+                        int m = 0;
+                        for (int x : need) {
+                            if (x < 0) continue;
+                            bool have = false;
+                            for (int b = 0; b < nb; ++b) have |= gbits[b] == x;
+                            m += have ? 0 : 1;
+                        }
+                        return m;
+                    };
+                    if (nb + missing() > g.sub) close_group();
+                    for (int x : need) {
+                        if (x < 0) continue;
+                        bool have = false;
+                        for (int b = 0; b < nb; ++b) have |= gbits[b] == x;
+                        if (!have) gbits[nb++] = x;
                     }
                 }
                 group.push_back(t);

@@ -54,15 +54,15 @@ struct TileGeom {
 
 // Pair op on group bit J over the 2^SUB register amplitudes.
 // cmask: bit r set when element r's control is 1 (all set when uncontrolled).
-template <class R, int SUB, int J>
+template <class R, int SUB, int J, bool FMA>
 __device__ __forceinline__ void group_pair(typename Cplx<R>::T (&v)[1 << SUB], uint32_t cmask, const R *u) {
 #pragma unroll
     for (int r = 0; r < (1 << SUB); ++r) {
         if ((r >> J) & 1) continue;
         if (!((cmask >> r) & 1u)) continue;
         const typename Cplx<R>::T a = v[r], b = v[r | (1 << J)];
-        v[r] = madd2(u[0], u[1], a, u[2], u[3], b);
-        v[r | (1 << J)] = madd2(u[4], u[5], a, u[6], u[7], b);
+        v[r] = madd2x<FMA>(u[0], u[1], a, u[2], u[3], b);
+        v[r | (1 << J)] = madd2x<FMA>(u[4], u[5], a, u[6], u[7], b);
     }
 }
 
@@ -84,7 +84,7 @@ __device__ __forceinline__ uint32_t sub_mask(int bit, const int (&b)[SUB], uint3
     return m;
 }
 
-template <class R, int SUB>
+template <class R, int SUB, bool FMA>
 __global__ void __launch_bounds__(1 << (12 - SUB), 2)
 k_tile(typename Cplx<R>::T *__restrict__ psi, const TileGeom g, const TileOp *__restrict__ ops_g) {
     using T = typename Cplx<R>::T;
@@ -152,11 +152,11 @@ k_tile(typename Cplx<R>::T *__restrict__ psi, const TileGeom g, const TileOp *__
                 const uint32_t cm = sub_mask<SUB>(op.cbit, b, l0);
                 if (op.kind == TILE_PAIR) {
                     switch (op.slot) {
-                    case 0: group_pair<R, SUB, 0>(v, cm, u); break;
-                    case 1: group_pair<R, SUB, 1>(v, cm, u); break;
-                    case 2: group_pair<R, SUB, 2>(v, cm, u); break;
+                    case 0: group_pair<R, SUB, 0, FMA>(v, cm, u); break;
+                    case 1: group_pair<R, SUB, 1, FMA>(v, cm, u); break;
+                    case 2: group_pair<R, SUB, 2, FMA>(v, cm, u); break;
                     default:
-                        if constexpr (SUB > 3) group_pair<R, SUB, SUB - 1>(v, cm, u);
+                        if constexpr (SUB > 3) group_pair<R, SUB, SUB - 1, FMA>(v, cm, u);
                         break;
                     }
                 } else {
@@ -168,7 +168,7 @@ k_tile(typename Cplx<R>::T *__restrict__ psi, const TileGeom g, const TileOp *__
                         if (!((cm >> r) & 1u)) continue;
                         const bool one = (tm >> r) & 1u;
                         if (!one && d0_one) continue;
-                        v[r] = one ? cmul(u[6], u[7], v[r]) : cmul(u[0], u[1], v[r]);
+                        v[r] = one ? cmulx<FMA>(u[6], u[7], v[r]) : cmulx<FMA>(u[0], u[1], v[r]);
                     }
                 }
             }

@@ -146,3 +146,28 @@ def test_errors_are_typed(qv):
         qv.apply_circuit(st, qv.parse_circuit("qubits 3\nh 0\n"), strategy="paired-cached")
     with pytest.raises(qv.QvsimError):
         qv.StateVector.create(3, 96, 0)
+
+
+def test_fma_mode_within_tolerance(qv, oracle):
+    """QVG_OPT_FMA (opt-in DFMA tile arithmetic) is not bit-exact but stays
+    within the north_star 1e-12 of the reference algorithm."""
+    for c in [qv.u3_ladder_circuit(20, 20, 1), qv.grid_circuit(4, 5, 12, 3), qv.random_circuit(12, 300, 7)]:
+        n = c.n_qubits
+        want = oracle.simulate(n, gate_array(c))
+        st = qv.StateVector.create(n, 128, 0)
+        st.set_option(qv.OPT_FMA, 1)
+        qv.apply_circuit(st, c)
+        got = st.read_state()
+        assert np.abs(got - want).max() <= 1e-12
+
+
+@pytest.mark.parametrize("sub", [3, 4])
+def test_tile_subcube_variants_bit_exact(qv, oracle, sub):
+    for c in [qv.u3_ladder_circuit(16, 6, 2), qv.grid_circuit(3, 5, 10, 4), qv.qft_circuit(14, 3)[0]]:
+        n = c.n_qubits
+        want = oracle.simulate(n, gate_array(c))
+        st = qv.StateVector.create(n, 128, 0)
+        st.set_option(qv.OPT_SUB_BITS, sub)
+        m = qv.apply_circuit(st, c)
+        assert m["fused_passes"] > 0
+        assert np.array_equal(st.read_state(), want)

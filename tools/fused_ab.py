@@ -17,8 +17,9 @@ import torch  # noqa: E402
 
 import paper_2508_15545_b200 as qv  # noqa: E402
 
-# (name, fuse, sub_bits)
-VARIANTS = [("fused_sub4", 1, 4), ("fused_sub3", 1, 3), ("per_gate", 0, 4)]
+# (name, fuse, sub_bits, fma)
+VARIANTS = [("fused_sub3", 1, 3, 0), ("fused_sub4", 1, 4, 0), ("fused_sub3_fma", 1, 3, 1),
+            ("fused_sub4_fma", 1, 4, 1), ("per_gate", 0, 3, 0)]
 
 
 def circuits(n):
@@ -44,9 +45,10 @@ def main():
             continue
         g = c.gates()
         row = {"circuit": name, "ops": len(c)}
-        for vname, fuse, sub in VARIANTS:
+        for vname, fuse, sub, fma in VARIANTS:
             st.set_option(qv.OPT_FUSE, fuse)
             st.set_option(qv.OPT_SUB_BITS, sub)
+            st.set_option(qv.OPT_FMA, fma)
             st.apply_gates(g)  # warm-up (and plan)
             st.reset_stats()
             ts = []
@@ -65,7 +67,8 @@ def main():
         out.append(row)
         print(name, " ".join(f"{k}={v['ms']:.1f}ms/{v['passes']:.0f}p" for k, v in row.items() if isinstance(v, dict)),
               file=sys.stderr)
-    st.set_option(qv.OPT_SUB_BITS, 4)
+    st.set_option(qv.OPT_SUB_BITS, 3)
+    st.set_option(qv.OPT_FMA, 0)
     st.set_option(qv.OPT_FUSE, 1)
     print(json.dumps({"n": a.n, "precision": a.precision, "reps": a.reps, "rows": out}, indent=1))
 
