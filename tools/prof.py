@@ -18,11 +18,15 @@ def main():
     ap.add_argument("--n", type=int, default=28)
     ap.add_argument("--precision", type=int, default=128)
     ap.add_argument("--fused", action="store_true", help="only the fused sweep")
+    ap.add_argument("--circuit", default="sweep", choices=["sweep", "grid", "ladder", "qft"])
     a = ap.parse_args()
     n = a.n
     st = qv.StateVector.create(n, a.precision, 0)
     st.apply_gates(qv.make_benchmark_circuit(n).gates())  # H on all: k_low x5 + k_pairs x(n-5)
-    sweep = qv.haar_sweep_circuit(n, 2508)
+    sweep = {"sweep": lambda: qv.haar_sweep_circuit(n, 2508),
+             "grid": lambda: qv.grid_circuit(4, n // 4, 6, 1),
+             "ladder": lambda: qv.u3_ladder_circuit(n, 2, 1),
+             "qft": lambda: qv.qft_circuit(n, 1)[0]}[a.circuit]()
     if a.fused:
         st.set_option(qv.OPT_FUSE, 1)
         st.apply_gates(sweep.gates())
