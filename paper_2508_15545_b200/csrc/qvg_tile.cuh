@@ -143,8 +143,12 @@ k_tile(typename Cplx<R>::T *__restrict__ psi, const TileGeom g, const TileOp *__
 #pragma unroll
                 for (int r = 0; r < E; ++r) v[r] = sm[lidx(r)];
             }
+            // The next op's record is fetched from shared memory while the
+            // current one computes (its load latency was the top stall).
+            TileOp nxt = ops[rec];
             for (int i = 0; i < nops; ++i) {
-                const TileOp &op = ops[rec + i];
+                const TileOp op = nxt;
+                if (i + 1 < nops) nxt = ops[rec + i + 1];
                 if ((base & op.greq) != op.greq) continue;  // control outside the tile is 0
                 R u[8];
 #pragma unroll

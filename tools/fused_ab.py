@@ -17,9 +17,9 @@ import torch  # noqa: E402
 
 import paper_2508_15545_b200 as qv  # noqa: E402
 
-# (name, fuse, sub_bits, fma)
-VARIANTS = [("fused_sub3", 1, 3, 0), ("fused_sub4", 1, 4, 0), ("fused_sub3_fma", 1, 3, 1),
-            ("fused_sub4_fma", 1, 4, 1), ("per_gate", 0, 3, 0)]
+# (name, fuse, sub_bits, fma, tile qubits)
+VARIANTS = [("fused_sub3", 1, 3, 0, 12), ("fused_sub4", 1, 4, 0, 12), ("fused_sub3_k11", 1, 3, 0, 11),
+            ("fused_sub3_k10", 1, 3, 0, 10), ("fused_sub3_fma", 1, 3, 1, 12), ("per_gate", 0, 3, 0, 12)]
 
 
 def circuits(n):
@@ -45,7 +45,8 @@ def main():
             continue
         g = c.gates()
         row = {"circuit": name, "ops": len(c)}
-        for vname, fuse, sub, fma in VARIANTS:
+        for vname, fuse, sub, fma, k in VARIANTS:
+            st.set_option(qv.OPT_TILE_QUBITS, k)
             st.set_option(qv.OPT_FUSE, fuse)
             st.set_option(qv.OPT_SUB_BITS, sub)
             st.set_option(qv.OPT_FMA, fma)
@@ -70,6 +71,7 @@ def main():
     st.set_option(qv.OPT_SUB_BITS, 3)
     st.set_option(qv.OPT_FMA, 0)
     st.set_option(qv.OPT_FUSE, 1)
+    st.set_option(qv.OPT_TILE_QUBITS, 12)
     print(json.dumps({"n": a.n, "precision": a.precision, "reps": a.reps, "rows": out}, indent=1))
 
 
