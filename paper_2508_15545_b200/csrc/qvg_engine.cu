@@ -187,11 +187,15 @@ void launch_phase(const qvg_state &s, void *psi, uint32_t L, const qvg_gate &g, 
 }
 
 template <class R>
-void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *d_ops) {
+void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *recs) {
     using T = typename Cplx<R>::T;
     const TileGeom &g = p.geom;
+    if (g.nrec > kMaxTileRecs) throw std::runtime_error("internal: tile pass exceeds the record limit");
+    static TileParams prm;  // 25 KB; launch copies it into the parameter block
+    prm.g = g;
+    std::memcpy(prm.ops, recs + p.op_begin, sizeof(TileOp) * g.nrec);
     const unsigned threads = 1u << (g.k - g.sub);  // one 2^sub-amplitude subcube per thread
-    const size_t smem = sizeof(TileOp) * g.nrec + (((sizeof(uint64_t) << g.nhi) + 15) & ~size_t(15)) +
+    const size_t smem = (((sizeof(uint64_t) << g.nhi) + 15) & ~size_t(15)) +
                         (g.ngroups > 1 ? (sizeof(T) << g.k) : 0);
     const bool fma = s.fma && sizeof(R) == 8;  // complex64 always contracts
     auto kern = g.sub == 4 ? (fma ? k_tile<R, 4, true> : k_tile<R, 4, false>)
@@ -207,7 +211,7 @@ void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *d_ops) {
     cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (int)threads, smem), "occupancy(k_tile)");
     per_sm = std::max(per_sm, 1);
     const uint64_t grid = std::min<uint64_t>(g.ntiles, (uint64_t)per_sm * s.sm_count);
-    kern<<<(unsigned)grid, threads, smem, s.stream>>>(static_cast<T *>(psi), g, d_ops + p.op_begin);
+    kern<<<(unsigned)grid, threads, smem, s.stream>>>(static_cast<T *>(psi), prm);
 }
 
 PlanOptions plan_options(const qvg_state &s) {
@@ -227,24 +231,6 @@ PlanOptions plan_options(const qvg_state &s) {
 void run_local(qvg_state &s, void *psi, const qvg_gate *ops, uint64_t count) {
     if (count == 0) return;
     const Plan plan = make_plan(ops, count, plan_options(s));
-    if (!plan.tile_ops.empty()) {
-        if (plan.tile_ops.size() > s.d_ops_cap) {
-            if (s.d_ops) {
-                cuda_check(cudaStreamSynchronize(s.stream), "sync before op-buffer growth");
-                cudaFree(s.d_ops);
-                s.d_ops = nullptr;
-            }
-            const size_t cap = std::max<size_t>(plan.tile_ops.size(), 1024);
-            cuda_check(cudaMalloc(&s.d_ops, cap * sizeof(TileOp)), "cudaMalloc(tile ops)");
-            s.d_ops_cap = cap;
-        }
-        // The previous batch's tile kernels may still read d_ops: the copy is
-        // stream-ordered after them. A pageable source is consumed before
-        // cudaMemcpyAsync returns, so the host vector may go out of scope.
-        cuda_check(cudaMemcpyAsync(s.d_ops, plan.tile_ops.data(), plan.tile_ops.size() * sizeof(TileOp),
-                                   cudaMemcpyHostToDevice, s.stream),
-                   "upload tile ops");
-    }
     const bool dbl = s.precision == QVG_C128;
     for (const Pass &p : plan.passes) {
         switch (p.kind) {
@@ -258,7 +244,8 @@ void run_local(qvg_state &s, void *psi, const qvg_gate *ops, uint64_t count) {
             dbl ? launch_phase<double>(s, psi, s.L, p.op, p.info) : launch_phase<float>(s, psi, s.L, p.op, p.info);
             break;
         case PASS_TILE:
-            dbl ? launch_tile<double>(s, psi, p, s.d_ops) : launch_tile<float>(s, psi, p, s.d_ops);
+            dbl ? launch_tile<double>(s, psi, p, plan.tile_ops.data())
+                : launch_tile<float>(s, psi, p, plan.tile_ops.data());
             s.stats.fused_passes += 1;
             break;
         }
@@ -324,7 +311,7 @@ static int create_impl(uint32_t n, uint32_t precision, int device, uint32_t rank
         s->S = precision == QVG_C128 ? 16 : 8;
         s->rank = rank;
         s->world = world;
-        s->tile_qubits = 12;  // 2^12 amplitudes: 512 threads x one 8-amplitude subcube
+        s->tile_qubits = 11;  // 2^11 amplitudes: 256 threads x 8; measured best (profiles/r01_fused_ab.json)
         s->carriers = precision == QVG_C128 ? 3 : 4;
         try {
             set_device(s);
@@ -589,7 +576,7 @@ int qvg_plan_passes(uint32_t n_qubits, uint32_t precision, int fuse, uint32_t ti
         po.n = n_qubits;
         po.amp_bytes = precision == QVG_C128 ? 16 : 8;
         po.fuse = fuse != 0;
-        po.tile_qubits = tile_qubits ? std::min<uint32_t>(tile_qubits, 12) : 12;
+        po.tile_qubits = tile_qubits ? std::min<uint32_t>(tile_qubits, 12) : 11;
         po.carriers = carriers;
         const Plan plan = make_plan(ops, count, po);
         uint64_t fused = 0, bytes = 0;

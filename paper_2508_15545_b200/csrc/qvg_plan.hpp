@@ -99,8 +99,9 @@ struct PlanOptions {
     uint32_t sub_bits = 3;   // tile register subcube: 2^sub amplitudes per thread (3 or 4)
 };
 
-// Ops per fused pass: the records are staged in shared memory (96 B each).
-constexpr uint64_t kMaxRunOps = 192;
+// Ops per fused pass: with at most one group header per op the records fit
+// the kernel parameter block (kMaxTileRecs).
+constexpr uint64_t kMaxRunOps = kMaxTileRecs / 2;
 
 // 2 * touched * S, rounded up to whole 32-B sectors when the touched runs are
 // shorter than a sector.

@@ -52,6 +52,15 @@ struct TileGeom {
     uint64_t ntiles;      // 2^(n-k)
 };
 
+// Records per fused pass; they travel as the kernel's parameter block
+// (CUDA 12.1+ allows 32 KB of parameters).
+constexpr int kMaxTileRecs = 256;
+struct TileParams {
+    TileGeom g;
+    TileOp ops[kMaxTileRecs];
+};
+static_assert(sizeof(TileParams) < 32000, "kernel parameter block limit");
+
 // Pair op on group bit J over the 2^SUB register amplitudes.
 // cmask: bit r set when element r's control is 1 (all set when uncontrolled).
 template <class R, int SUB, int J, bool FMA>
@@ -86,19 +95,20 @@ __device__ __forceinline__ uint32_t sub_mask(int bit, const int (&b)[SUB], uint3
 
 template <class R, int SUB, bool FMA>
 __global__ void __launch_bounds__(1 << (12 - SUB), 2)
-k_tile(typename Cplx<R>::T *__restrict__ psi, const TileGeom g, const TileOp *__restrict__ ops_g) {
+k_tile(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams prm) {
     using T = typename Cplx<R>::T;
     constexpr int E = 1 << SUB;
+    const TileGeom &g = prm.g;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    TileOp *ops = reinterpret_cast<TileOp *>(smem_raw);
-    uint64_t *offhi = reinterpret_cast<uint64_t *>(smem_raw + sizeof(TileOp) * g.nrec);
-    T *sm = reinterpret_cast<T *>(smem_raw + sizeof(TileOp) * g.nrec + (((sizeof(uint64_t) << g.nhi) + 15) & ~15ull));
+    // Op records are read straight from the kernel's parameter (constant)
+    // bank: the index is warp-uniform, so they load through the constant
+    // cache into uniform registers with no shared-memory traffic.
+    const TileOp *ops = prm.ops;
+    uint64_t *offhi = reinterpret_cast<uint64_t *>(smem_raw);
+    T *sm = reinterpret_cast<T *>(smem_raw + (((sizeof(uint64_t) << g.nhi) + 15) & ~15ull));
     const uint32_t nhi = 1u << g.nhi;
     const uint32_t lowm = (1u << g.lowc) - 1u;
-    {  // stage the op records (16-B vectors) and the high-qubit offset table
-        const int4 *src = reinterpret_cast<const int4 *>(ops_g);
-        int4 *dst = reinterpret_cast<int4 *>(ops);
-        for (int i = threadIdx.x; i < g.nrec * 6; i += blockDim.x) dst[i] = src[i];
+    {  // the high-qubit offset table
         for (uint32_t h = threadIdx.x; h < nhi; h += blockDim.x) {
             uint64_t off = 0;
 #pragma unroll

@@ -18,8 +18,8 @@ import torch  # noqa: E402
 import paper_2508_15545_b200 as qv  # noqa: E402
 
 # (name, fuse, sub_bits, fma, tile qubits)
-VARIANTS = [("fused_sub3", 1, 3, 0, 12), ("fused_sub4", 1, 4, 0, 12), ("fused_sub3_k11", 1, 3, 0, 11),
-            ("fused_sub3_k10", 1, 3, 0, 10), ("fused_sub3_fma", 1, 3, 1, 12), ("per_gate", 0, 3, 0, 12)]
+VARIANTS = [("fused_sub3_k11", 1, 3, 0, 11), ("fused_sub3_k12", 1, 3, 0, 12), ("fused_sub4_k12", 1, 4, 0, 12),
+            ("fused_sub3_k10", 1, 3, 0, 10), ("fused_sub3_k11_fma", 1, 3, 1, 11), ("per_gate", 0, 3, 0, 11)]
 
 
 def circuits(n):
@@ -71,7 +71,7 @@ def main():
     st.set_option(qv.OPT_SUB_BITS, 3)
     st.set_option(qv.OPT_FMA, 0)
     st.set_option(qv.OPT_FUSE, 1)
-    st.set_option(qv.OPT_TILE_QUBITS, 12)
+    st.set_option(qv.OPT_TILE_QUBITS, 11)
     print(json.dumps({"n": a.n, "precision": a.precision, "reps": a.reps, "rows": out}, indent=1))
 
 
