@@ -144,10 +144,11 @@ def algorithmic_bytes(n, rec, S=16):
 
 
 def kernel_of(n, rec):
+    """Launch class of a per-gate pass: every sweep op runs k_pairs (the
+    warp-shuffle k_low is off by default, profiles/r01_kernel_ab.json);
+    controlled ops enumerate only control=1 pairs."""
     kind = int(np.frombuffer(rec[:4].tobytes(), np.uint32)[0])
-    target = int(np.frombuffer(rec[4:8].tobytes(), np.uint32)[0])
-    name = "k_low" if target < 5 else "k_pairs"
-    return f"{name}<double,4>" + ("/ctrl" if kind == 1 else "")
+    return "k_pairs<double,4>" + ("/ctrl" if kind == 1 else "/dense")
 
 
 def run_ours(args, rank, world, dist):
@@ -293,32 +294,53 @@ def fused_leg(qv, st, circ, line, args):
 
 def e2e_leg(qv, st, circ, recs, line, args):
     """The same metric through the public API with HOST buffers: every step
-    copies the 16 GiB state from pinned host memory (qvg_load), runs the sweep
+    copies a 16 GiB state from pinned host memory to the device, runs the sweep
     with the API's defaults (`apply_circuit(state, circuit)`: strategy gpu,
-    fusion on) and reads the state back (qvg_read) inside the timed region."""
+    fusion on) and copies the state back, all inside the timed region.
+
+    value: a stream of independent steps over two device states on their own
+    streams (load_async / apply_circuit(sync=False) / read_async), so one
+    state's PCIe copies overlap the other's gates (PCIe is full duplex).
+    latency_ms: one step alone, synchronous (load_state / apply_circuit /
+    read_into)."""
     import torch
 
     n = circ.n_qubits
     count = 1 << n
-    host = torch.empty(count * 2, dtype=torch.float64, pin_memory=True)
-    host_np = host.numpy().view(np.complex128)
-    host_np[:] = 1.0 / math.sqrt(count)
-    steps = max(1, min(args.steps, 3))
+    bufs = []
+    for _ in range(2):
+        h = torch.empty(count * 2, dtype=torch.float64, pin_memory=True)
+        a = h.numpy().view(np.complex128)
+        a[:] = 1.0 / math.sqrt(count)
+        bufs.append((h, a))
+    # serial latency of one step
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    passes = 0
-    for _ in range(steps):
-        st.load_state(host_np)
-        m = qv.apply_circuit(st, circ)
-        passes += m["traversals"]
-        st.read_into(host_np)
-    t1 = time.perf_counter()
-    ms = (t1 - t0) * 1e3 / steps
+    st.load_state(bufs[0][1])
+    m = qv.apply_circuit(st, circ)
+    st.read_into(bufs[0][1])
+    latency = (time.perf_counter() - t0) * 1e3
+    # pipelined stream of steps on two states
+    st2 = qv.StateVector.create(n, 128, 0)
+    states = [st, st2]
+    steps = max(4, args.steps)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for k in range(steps):
+        s, (_, buf) = states[k % 2], bufs[k % 2]
+        s.load_async(buf)
+        qv.apply_circuit(s, circ, sync=False)
+        s.read_async(buf)
+    for s in states:
+        s.sync()
+    ms = (time.perf_counter() - t0) * 1e3 / steps
+    del st2
     line["e2e"] = {"value": len(circ) * count / (ms / 1e3), "unit": UNIT, "ms_per_step": ms,
-                   "h2d_bytes_per_step": count * 16, "d2h_bytes_per_step": count * 16,
-                   "hbm_passes_per_step": passes / steps,
-                   "path": "StateVector.load_state -> apply_circuit(state, circuit) [API defaults: gpu, fused] "
-                           "-> read_into, pinned host buffers, host wall clock"}
+                   "latency_ms": latency, "latency_value": len(circ) * count / (latency / 1e3),
+                   "steps": steps, "h2d_bytes_per_step": count * 16, "d2h_bytes_per_step": count * 16,
+                   "hbm_passes_per_step": m["traversals"],
+                   "path": "per step: StateVector.load_async(pinned) -> apply_circuit(state, circuit) [API defaults: "
+                           "gpu, fused] -> read_async(pinned); two states alternate, host wall clock"}
 
 
 def cpu_baseline(args, nops_hint=120):

@@ -123,6 +123,12 @@ int qvg_init_basis(qvg_state *s, uint64_t index);
 int qvg_load(qvg_state *s, const void *host, uint64_t offset, uint64_t count);
 /* Device -> host (read_full_state, reference engine.cpp:483-494). */
 int qvg_read(qvg_state *s, void *host, uint64_t offset, uint64_t count);
+/* Stream-ordered variants: enqueue the copy on the state's stream and return;
+ * `host` must stay valid until qvg_sync and should be pinned for full PCIe
+ * bandwidth. Two states on their own streams then overlap one state's copies
+ * with the other's gates (PCIe is full duplex). */
+int qvg_load_async(qvg_state *s, const void *host, uint64_t offset, uint64_t count);
+int qvg_read_async(qvg_state *s, void *host, uint64_t offset, uint64_t count);
 
 /* ---- the hot path ------------------------------------------------------------
  * Apply `count` ops in order (reference apply_circuit for a whole circuit,

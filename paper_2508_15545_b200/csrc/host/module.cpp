@@ -152,7 +152,21 @@ PYBIND11_MODULE(_core, m) {
             }
             return out;
         }, py::arg("offset") = 0, py::arg("count") = std::nullopt, "Amplitudes as a complex128 numpy array")
-        .def("read_into", [](const StateVector &s, py::array_t<std::complex<double>, py::array::c_style> out,
+        .def("load_async", [](StateVector &s, py::buffer buf, std::uint64_t offset) {
+            const py::buffer_info b = buf.request();
+            const std::size_t amp = s.precision() == 128 ? 16 : 8;
+            if ((std::size_t)(b.size * b.itemsize) % amp) throw ValidationError("buffer is not whole amplitudes");
+            check_status(qvg_load_async(s.handle(), b.ptr, offset, (std::uint64_t)(b.size * b.itemsize) / amp));
+        }, py::arg("amps"), py::arg("offset") = 0,
+           "Stream-ordered H2D in the state's precision; keep the (pinned) buffer alive until sync()")
+        .def("read_async", [](StateVector &s, py::buffer buf, std::uint64_t offset) {
+            const py::buffer_info b = buf.request(true);
+            const std::size_t amp = s.precision() == 128 ? 16 : 8;
+            if ((std::size_t)(b.size * b.itemsize) % amp) throw ValidationError("buffer is not whole amplitudes");
+            check_status(qvg_read_async(s.handle(), b.ptr, offset, (std::uint64_t)(b.size * b.itemsize) / amp));
+        }, py::arg("out"), py::arg("offset") = 0,
+           "Stream-ordered D2H in the state's precision; the data is valid after sync()")
+        .def("read_into",[](const StateVector &s, py::array_t<std::complex<double>, py::array::c_style> out,
                              std::uint64_t offset) {
             const std::uint64_t c = (std::uint64_t)out.size();
             amp_t *p = out.mutable_data();

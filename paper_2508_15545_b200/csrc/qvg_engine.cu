@@ -436,6 +436,26 @@ int qvg_read(qvg_state *s, void *host, uint64_t offset, uint64_t count) {
     });
 }
 
+int qvg_load_async(qvg_state *s, const void *host, uint64_t offset, uint64_t count) {
+    return guarded([&] {
+        check_state(s);
+        check_range(s, offset, count);
+        if (count && !host) throw Validation("null host buffer");
+        set_device(s);
+        shard_transfer(*s, s->shards, const_cast<void *>(host), offset, count, true, false);
+    });
+}
+
+int qvg_read_async(qvg_state *s, void *host, uint64_t offset, uint64_t count) {
+    return guarded([&] {
+        check_state(s);
+        check_range(s, offset, count);
+        if (count && !host) throw Validation("null host buffer");
+        set_device(s);
+        shard_transfer(*s, s->shards, host, offset, count, false, false);
+    });
+}
+
 int qvg_apply(qvg_state *s, const qvg_gate *ops, uint64_t count) {
     return guarded([&] {
         check_state(s);

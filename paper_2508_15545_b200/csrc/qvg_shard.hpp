@@ -238,7 +238,8 @@ inline void shard_canonicalize(qvg_state &s, ShardSet &set) {
     run_steps(s, set, steps);
 }
 
-inline void shard_transfer(qvg_state &s, ShardSet &set, void *host, uint64_t offset, uint64_t count, bool h2d) {
+inline void shard_transfer(qvg_state &s, ShardSet &set, void *host, uint64_t offset, uint64_t count, bool h2d,
+                           bool sync = true) {
     shard_canonicalize(s, set);
     cudaStream_t st = shard_stream(s);
     const uint32_t S = shard_amp_bytes(s);
@@ -252,7 +253,7 @@ inline void shard_transfer(qvg_state &s, ShardSet &set, void *host, uint64_t off
         if (h2d) cuda_throw(cudaMemcpyAsync(dev, hst, (e - a) * S, cudaMemcpyHostToDevice, st), "H2D");
         else cuda_throw(cudaMemcpyAsync(hst, dev, (e - a) * S, cudaMemcpyDeviceToHost, st), "D2H");
     }
-    cuda_throw(cudaStreamSynchronize(st), "transfer sync");
+    if (sync) cuda_throw(cudaStreamSynchronize(st), "transfer sync");
 }
 
 inline double shard_allreduce_sum(qvg_state &s, ShardSet &set, double v) {
