@@ -123,9 +123,13 @@ def test_planner_bytes_and_fusion(qv):
     assert one("cz 4 9") == (1, 0, full // 4)       # diag(1,-1) with control: |11> quarter
     assert one("t 9") == (1, 0, full // 2)
     assert one("cp 2 9 0") == (0, 0, 0)            # identity: no pass
-    # 12 Hadamards on 0..11 fuse into one tile pass
-    text = "\n".join(f"h {q}" for q in range(12))
+    # 11 Hadamards on 0..10 fuse into one tile pass (default tile: 11 qubits);
+    # a 12th target needs a second pass
+    text = "\n".join(f"h {q}" for q in range(11))
     assert qv.plan_passes(n, qv.parse_circuit(f"qubits {n}\n{text}\n").gates()) == (1, 1, full)
+    text += "\nh 11"
+    assert qv.plan_passes(n, qv.parse_circuit(f"qubits {n}\n{text}\n").gates())[:2] == (2, 1)
+    assert qv.plan_passes(n, qv.parse_circuit(f"qubits {n}\n{text}\n").gates(), tile_qubits=12) == (1, 1, full)
     # config 3 (n=30): fused passes are far fewer than ops
     c3 = qv.grid_circuit(5, 6, 24, 1)
     p, f, b = qv.plan_passes(30, c3.gates())
