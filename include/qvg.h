@@ -130,6 +130,10 @@ int qvg_read(qvg_state *s, void *host, uint64_t offset, uint64_t count);
 int qvg_load_async(qvg_state *s, const void *host, uint64_t offset, uint64_t count);
 int qvg_read_async(qvg_state *s, void *host, uint64_t offset, uint64_t count);
 
+/* Page-locked host memory for the async copies (cudaHostAlloc / cudaFreeHost). */
+int qvg_host_alloc(uint64_t bytes, void **out);
+int qvg_host_free(void *ptr);
+
 /* ---- the hot path ------------------------------------------------------------
  * Apply `count` ops in order (reference apply_circuit for a whole circuit,
  * engine.cpp:86-157; apply_gate_streamed for count == 1, kernel.cpp:132-146).

@@ -117,6 +117,9 @@ class RefEngine:
         lib.qvr_store_norm.argtypes = [_P, ctypes.POINTER(_DBL)]
         lib.qvr_store_sync.argtypes = [_P]
         lib.qvr_store_destroy.argtypes = [_P]
+        lib.qvr_store_open.argtypes = [ctypes.c_char_p]
+        lib.qvr_store_open.restype = _P
+        lib.qvr_store_close.argtypes = [_P]
         self.lib = lib
 
     def _check(self, rc: int):
@@ -137,6 +140,16 @@ class RefEngine:
 
     def store(self, n: int, block_amps: int = 65536, init_index: int = 0, scratch: str | None = None):
         return RefStore(self, n, block_amps, init_index, scratch)
+
+    def open_store(self, path: str, n: int):
+        """An existing QVSV file through the reference's BlockStore::open; closing
+        it keeps the file."""
+        st = RefStore.__new__(RefStore)
+        st.eng, st.n, st.keep = self, n, True
+        st.h = self.lib.qvr_store_open(path.encode())
+        if not st.h:
+            raise RuntimeError(self.lib.qvr_last_error().decode())
+        return st
 
 
 def default_scratch() -> str:
@@ -182,7 +195,10 @@ class RefStore:
 
     def close(self):
         if self.h:
-            self.eng.lib.qvr_store_destroy(self.h)
+            if getattr(self, "keep", False):
+                self.eng.lib.qvr_store_close(self.h)
+            else:
+                self.eng.lib.qvr_store_destroy(self.h)
             self.h = None
 
     def __enter__(self):

@@ -127,9 +127,10 @@ void *qvr_store_create(const char *dir, std::uint32_t n, std::uint64_t block_amp
                        std::uint64_t init_index) {
     void *h = nullptr;
     guarded([&] {
+        static std::uint64_t serial = 0;  // distinct files for concurrent stores
         const std::filesystem::path p =
             std::filesystem::path(dir) / ("qvr-" + std::to_string(::getpid()) + "-" +
-                                          std::to_string(n) + ".qvs");
+                                          std::to_string(n) + "-" + std::to_string(serial++) + ".qvs");
         const std::uint64_t ba = std::min<std::uint64_t>(block_amps, std::uint64_t{1} << n);
         auto handle = std::make_unique<Handle>(Handle{qvsim::BlockStore::create(p, n, ba, true)});
         if (init_index != 0) {
@@ -146,6 +147,17 @@ void *qvr_store_create(const char *dir, std::uint32_t n, std::uint64_t block_amp
     });
     return h;
 }
+
+// An existing QVSV file through the reference's BlockStore::open
+// (reference store.cpp:216-245).
+void *qvr_store_open(const char *path) {
+    void *h = nullptr;
+    guarded([&] { h = new Handle{qvsim::BlockStore::open(path)}; });
+    return h;
+}
+
+// Close without deleting the file.
+void qvr_store_close(void *h) { delete static_cast<Handle *>(h); }
 
 int qvr_store_load(void *h, const double *amps) {
     return guarded([&] {

@@ -42,8 +42,11 @@ from ._core import (  # noqa: E402
     IoError,
     ParseError,
     QvsimError,
+    DEFAULT_BLOCK_AMPS,
+    StateStore,
     StateVector,
     ValidationError,
+    top_amplitudes,
     apply_circuit,
     circuit_from_gates,
     grid_circuit,

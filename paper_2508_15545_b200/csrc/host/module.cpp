@@ -241,6 +241,55 @@ PYBIND11_MODULE(_core, m) {
           py::arg("tile_qubits") = 0, py::arg("sync") = true,
           "Apply the circuit in place on the device; returns the run's metrics document");
 
+    py::class_<StateStore>(m, "StateStore", "QVSV state file, interchangeable with the reference's BlockStore")
+        .def_static("create", [](const std::string &path, std::uint32_t n, std::uint64_t block_amps, bool overwrite) {
+            const std::uint64_t ba = std::min<std::uint64_t>(block_amps, std::uint64_t{1} << std::min(n, 62u));
+            return StateStore::create(path, n, ba, overwrite);
+        }, py::arg("path"), py::arg("n_qubits"), py::arg("block_amps") = kDefaultBlockAmps,
+           py::arg("overwrite") = false, "New store holding |0...0>; block_amps is capped at 2^n")
+        .def_static("open", &StateStore::open, py::arg("path"))
+        .def_property_readonly("n_qubits", &StateStore::n_qubits)
+        .def_property_readonly("n_amps", &StateStore::n_amps)
+        .def_property_readonly("block_amps", &StateStore::block_amps)
+        .def_property_readonly("n_blocks", &StateStore::n_blocks)
+        .def_property_readonly("path", &StateStore::path)
+        .def("norm", &StateStore::norm)
+        .def("amplitude", &StateStore::amplitude, py::arg("index"))
+        .def("read_state", [](const StateStore &s) {
+            py::array_t<std::complex<double>> out(s.n_amps());
+            s.read(out.mutable_data(), 0, s.n_amps());
+            return out;
+        }, "All 2^n amplitudes (numpy complex128)")
+        .def("sync", &StateStore::sync);
+
+    m.def("apply_circuit",
+          [](StateStore &store, const Circuit &circuit, const std::string &strategy, bool fuse, int device) {
+              const auto s = parse_strategy(strategy);
+              if (!s) throw ValidationError("unknown strategy '" + strategy + "'");
+              RunConfig cfg;
+              cfg.strategy = *s;
+              cfg.fuse = fuse;
+              Metrics metrics;
+              {
+                  py::gil_scoped_release nogil;
+                  apply_circuit(store, circuit, cfg, metrics, device);
+              }
+              py::dict d = metrics_dict(metrics, store.n_qubits());
+              d["bytes_read"] = metrics.bytes_read;
+              d["bytes_written"] = metrics.bytes_written;
+              return d;
+          },
+          py::arg("store"), py::arg("circuit"), py::arg("strategy") = "gpu", py::arg("fuse") = true,
+          py::arg("device") = 0, "File-backed apply: store -> HBM -> circuit on the GPU -> store");
+
+    m.def("top_amplitudes", [](const StateStore &store, std::size_t k) { return top_amplitudes(store, k); },
+          py::arg("store"), py::arg("k") = 8, "(index, amplitude) pairs, largest magnitude first");
+    m.def("top_amplitudes", [](const StateVector &state, std::size_t k) {
+        py::gil_scoped_release nogil;
+        return state.top_amplitudes(k);
+    }, py::arg("store"), py::arg("k") = 8);
+    m.attr("DEFAULT_BLOCK_AMPS") = kDefaultBlockAmps;
+
     m.def("nccl_unique_id", []() {
         std::string id(128, '\0');
         check_status(qvg_nccl_unique_id(id.data()));

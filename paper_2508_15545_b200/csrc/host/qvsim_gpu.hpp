@@ -145,6 +145,8 @@ struct RunConfig {
 };
 
 struct Metrics {
+    std::uint64_t bytes_read = 0;     // state-file bytes read (StateStore path)
+    std::uint64_t bytes_written = 0;  // state-file bytes written
     std::uint64_t gates_applied = 0;
     std::uint64_t traversals = 0;  // HBM passes (the reference's one traversal per gate)
     std::uint64_t fused_passes = 0;
@@ -198,5 +200,55 @@ class StateVector {
 // Only Strategy::gpu runs here; the CPU strategies belong to the reference's
 // block-store engine. Metrics accumulate; wall_ms is this call's elapsed time.
 void apply_circuit(StateVector &state, const Circuit &circuit, const RunConfig &config, Metrics &metrics);
+
+// ---- QVSV state file (the reference's on-disk format) ------------------------
+// 32-byte header: "QVSV", u32 version 1, u32 n_qubits, u64 block_amps, 12 zero
+// bytes; then 2^n complex128 little-endian, index-ascending (reference
+// store.hpp:24-29, 47-57). Files are interchangeable with the reference's
+// BlockStore; block_amps is kept for that compatibility (the GPU path moves
+// the state in large pinned chunks, not blocks).
+inline constexpr std::uint64_t kDefaultBlockAmps = 65536;
+inline constexpr std::uint32_t kMaxQubits = 58;
+
+class StateStore {
+  public:
+    // |0...0>: a sparse file with amplitude 0 = 1 (reference store.cpp:181-214).
+    static StateStore create(const std::string &path, std::uint32_t n_qubits,
+                             std::uint64_t block_amps = kDefaultBlockAmps, bool overwrite = false);
+    static StateStore open(const std::string &path);
+    StateStore(StateStore &&o) noexcept;
+    StateStore &operator=(StateStore &&o) noexcept;
+    StateStore(const StateStore &) = delete;
+    StateStore &operator=(const StateStore &) = delete;
+    ~StateStore();
+
+    const std::string &path() const noexcept { return path_; }
+    std::uint32_t n_qubits() const noexcept { return n_; }
+    std::uint64_t n_amps() const noexcept { return std::uint64_t{1} << n_; }
+    std::uint64_t block_amps() const noexcept { return block_amps_; }
+    std::uint64_t n_blocks() const noexcept { return n_amps() / block_amps_; }
+
+    void read(amp_t *out, std::uint64_t offset, std::uint64_t count) const;
+    void write(const amp_t *in, std::uint64_t offset, std::uint64_t count);
+    amp_t amplitude(std::uint64_t index) const;
+    double norm() const;  // Kahan, like BlockStore::norm (store.cpp:301-316)
+    void sync() const;
+
+  private:
+    StateStore(int fd, std::string path, std::uint32_t n, std::uint64_t block_amps);
+    int fd_ = -1;
+    std::string path_;
+    std::uint32_t n_ = 0;
+    std::uint64_t block_amps_ = 0;
+};
+
+// The drop-in for the reference's apply_circuit(BlockStore&, ...) with
+// strategy "gpu": the file streams into HBM through pinned chunks, the circuit
+// runs on the device, and the state streams back.
+void apply_circuit(StateStore &store, const Circuit &circuit, const RunConfig &config, Metrics &metrics,
+                   int device = 0);
+
+// reference top_amplitudes (engine.cpp:511-544): k largest |a|^2, ties by index.
+std::vector<std::pair<std::uint64_t, amp_t>> top_amplitudes(const StateStore &store, std::size_t k);
 
 }  // namespace qvsim

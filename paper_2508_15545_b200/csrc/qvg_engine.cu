@@ -436,6 +436,20 @@ int qvg_read(qvg_state *s, void *host, uint64_t offset, uint64_t count) {
     });
 }
 
+int qvg_host_alloc(uint64_t bytes, void **out) {
+    return guarded([&] {
+        if (!out) throw Validation("null output pointer");
+        *out = nullptr;
+        cuda_check(cudaHostAlloc(out, bytes, cudaHostAllocPortable), "cudaHostAlloc");
+    });
+}
+
+int qvg_host_free(void *ptr) {
+    return guarded([&] {
+        if (ptr) cuda_check(cudaFreeHost(ptr), "cudaFreeHost");
+    });
+}
+
 int qvg_load_async(qvg_state *s, const void *host, uint64_t offset, uint64_t count) {
     return guarded([&] {
         check_state(s);

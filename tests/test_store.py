@@ -1,0 +1,107 @@
+"""QVSV state files: our StateStore and the reference's BlockStore read and
+write the same bytes (reference store.hpp:24-29, store.cpp:181-316), so the
+file-backed `apply_circuit(store, circuit, strategy="gpu")` is a drop-in for
+the reference's strategies on the same file."""
+import os
+import shutil
+
+import numpy as np
+import pytest
+
+from conftest import gate_array
+from oracle.oracle import RefEngine
+
+needs_ref = pytest.mark.skipif(not RefEngine.available(), reason="oracle/_ref not built")
+
+
+def test_create_matches_reference_bytes(qv, tmp_path):
+    # |0...0> stores from both implementations are byte-identical
+    ours = tmp_path / "ours.qvs"
+    s = qv.StateStore.create(str(ours), 6, block_amps=4)
+    assert (s.n_qubits, s.n_amps, s.block_amps, s.n_blocks) == (6, 64, 4, 16)
+    assert s.path == str(ours)
+    del s
+    raw = ours.read_bytes()
+    assert raw[:4] == b"QVSV" and len(raw) == 32 + 64 * 16
+    assert int.from_bytes(raw[4:8], "little") == 1 and int.from_bytes(raw[8:12], "little") == 6
+    assert int.from_bytes(raw[12:20], "little") == 4 and raw[20:32] == bytes(12)
+    amps = np.frombuffer(raw[32:], np.complex128)
+    assert amps[0] == 1 and not amps[1:].any()
+    if RefEngine.available():
+        eng = RefEngine()
+        with eng.store(6, block_amps=4, scratch=str(tmp_path)) as ref:
+            ref.sync()
+            ref_bytes = None
+            for f in tmp_path.iterdir():
+                if f.name.startswith("qvr-"):
+                    ref_bytes = f.read_bytes()
+        assert ref_bytes == raw
+
+
+@needs_ref
+def test_reference_file_readable_and_ours_readable_by_reference(qv, tmp_path):
+    eng = RefEngine()
+    ops, _ = eng.random_circuit(8, 60, 4)
+    path = str(tmp_path / "a.qvs")
+    qv.StateStore.create(path, 8, block_amps=16)
+    ref = eng.open_store(path, 8)
+    ref.apply(ops, "paired-cached", 1, 4 * 16 * 16)
+    want = ref.read()
+    ref_norm = ref.norm()
+    ref.close()
+    s = qv.StateStore.open(path)
+    assert np.array_equal(s.read_state(), want)
+    assert s.norm() == ref_norm  # same Kahan order
+    assert s.amplitude(5) == want[5]
+    p = np.abs(want) ** 2
+    order = sorted(range(len(p)), key=lambda i: (-p[i], i))[:6]
+    assert [i for i, _ in qv.top_amplitudes(s, 6)] == order
+
+
+def test_bad_files(qv, tmp_path):
+    p = tmp_path / "bad.qvs"
+    p.write_bytes(b"QVSX" + bytes(28) + bytes(64))
+    with pytest.raises(qv.FormatError):
+        qv.StateStore.open(str(p))
+    p.write_bytes(b"QV")
+    with pytest.raises(qv.FormatError):
+        qv.StateStore.open(str(p))
+    good = tmp_path / "g.qvs"
+    qv.StateStore.create(str(good), 3)
+    data = good.read_bytes()
+    good.write_bytes(data[:-16])
+    with pytest.raises(qv.FormatError, match="length"):
+        qv.StateStore.open(str(good))
+    with pytest.raises(qv.IoError):
+        qv.StateStore.create(str(good), 3)  # exists, no overwrite
+    with pytest.raises(qv.ValidationError):
+        qv.StateStore.create(str(tmp_path / "x.qvs"), 4, block_amps=3)
+    with pytest.raises(qv.ValidationError):
+        qv.apply_circuit(qv.StateStore.create(str(tmp_path / "y.qvs"), 3), qv.parse_circuit("qubits 3\nh 0\n"),
+                         strategy="paired-cached")
+
+
+@pytest.mark.gpu
+@needs_ref
+@pytest.mark.parametrize("n", [10, 22])
+def test_gpu_strategy_on_store_matches_reference_strategy(qv, tmp_path, n):
+    """Same file, reference `paired-cached-parallel` vs our `gpu`."""
+    eng = RefEngine()
+    c = qv.u3_ladder_circuit(n, 3, 9)
+    a = str(tmp_path / "a.qvs")
+    qv.StateStore.create(a, n, block_amps=1024)
+    b = str(tmp_path / "b.qvs")
+    shutil.copyfile(a, b)
+    ref = eng.open_store(a, n)
+    ref.apply(gate_array(c), "paired-cached-parallel", 4, 4 * (64 << 20))
+    want = ref.read()
+    ref.close()
+    m = qv.apply_circuit(qv.StateStore.open(b), c, strategy="gpu")
+    assert m["strategy"] == "gpu" and m["gates_applied"] == len(c)
+    assert m["bytes_read"] == m["bytes_written"] == 16 << n
+    got = qv.StateStore.open(b).read_state()
+    assert np.array_equal(got, want)
+    # and the reference can continue on our output
+    ref = eng.open_store(b, n)
+    assert np.array_equal(ref.read(), want)
+    ref.close()
