@@ -61,6 +61,11 @@ struct TileParams {
 };
 static_assert(sizeof(TileParams) < 32000, "kernel parameter block limit");
 
+// Shared-tile slot of local index l: the 16-B column within each 128-B row is
+// XORed with the row's low bits, so lanes whose amplitudes are 2^3, 2^4 or
+// 2^5 apart (a group over the carrier bits) hit different banks.
+__device__ __forceinline__ uint32_t swz(uint32_t l) { return l ^ ((l >> 3) & 7u); }
+
 // Pair op on group bit J over the 2^SUB register amplitudes.
 // cmask: bit r set when element r's control is 1 (all set when uncontrolled).
 template <class R, int SUB, int J, bool FMA>
@@ -151,7 +156,7 @@ k_tile(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams
                 }
             } else {
 #pragma unroll
-                for (int r = 0; r < E; ++r) v[r] = sm[lidx(r)];
+                for (int r = 0; r < E; ++r) v[r] = sm[swz(lidx(r))];
             }
             // The next op's record is fetched from shared memory while the
             // current one computes (its load latency was the top stall).
@@ -195,7 +200,7 @@ k_tile(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams
                 }
             } else {
 #pragma unroll
-                for (int r = 0; r < E; ++r) sm[lidx(r)] = v[r];
+                for (int r = 0; r < E; ++r) sm[swz(lidx(r))] = v[r];
                 __syncthreads();
             }
         }
