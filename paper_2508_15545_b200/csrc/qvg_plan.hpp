@@ -221,10 +221,15 @@ inline Plan make_plan(const qvg_gate *ops, uint64_t count, const PlanOptions &po
                     if (!used) gbits[nb++] = b;
                 }
                 std::sort(gbits, gbits + g.sub);
-                for (TileOp &t : group)  // target slot within the sorted group bits
-                    if (t.kind == TILE_PAIR)
-                        for (int s = 0; s < g.sub; ++s)
-                            if (gbits[s] == t.tbit) t.slot = s;
+                for (TileOp &t : group) {  // slot code 8*J + (K+1): target / control register slots
+                    if (t.kind != TILE_PAIR) continue;
+                    int J = -1, K = -1;
+                    for (int s = 0; s < g.sub; ++s) {
+                        if (gbits[s] == t.tbit) J = s;
+                        if (t.cbit >= 0 && gbits[s] == t.cbit) K = s;
+                    }
+                    t.slot = 8 * J + K + 1;
+                }
                 TileOp h{};
                 h.kind = TILE_GROUP;
                 h.tbit = (int32_t)group.size();

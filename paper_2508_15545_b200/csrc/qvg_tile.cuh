@@ -68,16 +68,36 @@ __device__ __forceinline__ uint32_t swz(uint32_t l) { return l ^ ((l >> 3) & 7u)
 
 // Pair op on group bit J over the 2^SUB register amplitudes.
 // cmask: bit r set when element r's control is 1 (all set when uncontrolled).
-template <class R, int SUB, int J, bool FMA>
-__device__ __forceinline__ void group_pair(typename Cplx<R>::T (&v)[1 << SUB], uint32_t cmask, const R *u) {
+// Target on register slot J, control on slot K (-1: none / decided per tile):
+// both are compile-time, so a controlled op costs exactly its pairs and no
+// per-pair tests run (the instruction mix was 60% non-FP64 before this).
+template <class R, int SUB, int J, int K, bool FMA>
+__device__ __forceinline__ void group_pair(typename Cplx<R>::T (&v)[1 << SUB], const R *u) {
+    if constexpr (J < SUB && K < SUB && J != K) {
 #pragma unroll
-    for (int r = 0; r < (1 << SUB); ++r) {
-        if ((r >> J) & 1) continue;
-        if (!((cmask >> r) & 1u)) continue;
-        const typename Cplx<R>::T a = v[r], b = v[r | (1 << J)];
-        v[r] = madd2x<FMA>(u[0], u[1], a, u[2], u[3], b);
-        v[r | (1 << J)] = madd2x<FMA>(u[4], u[5], a, u[6], u[7], b);
+        for (int r = 0; r < (1 << SUB); ++r) {
+            if ((r >> J) & 1) continue;
+            if (K >= 0 && !((r >> K) & 1)) continue;
+            const typename Cplx<R>::T a = v[r], b = v[r | (1 << J)];
+            v[r] = madd2x<FMA>(u[0], u[1], a, u[2], u[3], b);
+            v[r | (1 << J)] = madd2x<FMA>(u[4], u[5], a, u[6], u[7], b);
+        }
     }
+}
+
+// slot code = 8*J + (K+1)
+template <class R, int SUB, bool FMA>
+__device__ __forceinline__ void group_pair_dispatch(int code, typename Cplx<R>::T (&v)[1 << SUB], const R *u) {
+#define QVG_GP(J, K) \
+    case 8 * (J) + (K) + 1: group_pair<R, SUB, J, K, FMA>(v, u); break;
+    switch (code) {
+        QVG_GP(0, -1) QVG_GP(0, 1) QVG_GP(0, 2) QVG_GP(0, 3)
+        QVG_GP(1, -1) QVG_GP(1, 0) QVG_GP(1, 2) QVG_GP(1, 3)
+        QVG_GP(2, -1) QVG_GP(2, 0) QVG_GP(2, 1) QVG_GP(2, 3)
+        QVG_GP(3, -1) QVG_GP(3, 0) QVG_GP(3, 1) QVG_GP(3, 2)
+    default: break;
+    }
+#undef QVG_GP
 }
 
 // Mask over the subcube: bit r set when element r has tile-local bit `bit`.
@@ -168,26 +188,18 @@ k_tile(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams
                 R u[8];
 #pragma unroll
                 for (int x = 0; x < 8; ++x) u[x] = (R)op.u[x];
-                const uint32_t cm = sub_mask<SUB>(op.cbit, b, l0);
                 if (op.kind == TILE_PAIR) {
-                    switch (op.slot) {
-                    case 0: group_pair<R, SUB, 0, FMA>(v, cm, u); break;
-                    case 1: group_pair<R, SUB, 1, FMA>(v, cm, u); break;
-                    case 2: group_pair<R, SUB, 2, FMA>(v, cm, u); break;
-                    default:
-                        if constexpr (SUB > 3) group_pair<R, SUB, SUB - 1, FMA>(v, cm, u);
-                        break;
-                    }
+                    group_pair_dispatch<R, SUB, FMA>(op.slot, v, u);
                 } else {
+                    const uint32_t cm = sub_mask<SUB>(op.cbit, b, l0);
                     const uint32_t tm = op.tbit >= 0 ? sub_mask<SUB>(op.tbit, b, l0)
                                                      : ((base & op.gtgt) ? 0xFFFFu : 0u);
-                    const bool d0_one = op.slot != 0;
+                    // elements that change: control set and (d0 != 1 or target bit set)
+                    const uint32_t sel = cm & (op.slot != 0 ? tm : 0xFFFFu);
 #pragma unroll
                     for (int r = 0; r < E; ++r) {
-                        if (!((cm >> r) & 1u)) continue;
-                        const bool one = (tm >> r) & 1u;
-                        if (!one && d0_one) continue;
-                        v[r] = one ? cmulx<FMA>(u[6], u[7], v[r]) : cmulx<FMA>(u[0], u[1], v[r]);
+                        if (!((sel >> r) & 1u)) continue;
+                        v[r] = ((tm >> r) & 1u) ? cmulx<FMA>(u[6], u[7], v[r]) : cmulx<FMA>(u[0], u[1], v[r]);
                     }
                 }
             }
