@@ -415,6 +415,69 @@ def run_reference(args, rank, world):
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
+def configs_mode(args):
+    """`--configs`: one JSON line per BASELINE config with device
+    time fused (API default) and per-gate, HBM passes, amp-updates/s, and the
+    reference engine (oracle/_ref, all host cores) on the same circuit or a
+    bounded sample of it (stated in each line). Not the driver's headline."""
+    import torch
+
+    from oracle.oracle import GATE_DTYPE, RefEngine, default_scratch
+
+    import paper_2508_15545_b200 as qv
+
+    cores = os.cpu_count() or 1
+    eng = RefEngine() if RefEngine.available() else None
+    specs = [
+        ("config0", "U3 layers + CX ladder, n=20, 20 layers", lambda: qv.u3_ladder_circuit(20, 20, 1), 128, None),
+        ("config1", "H layer + QFT (CP R_k) + bit-reversal SWAPs, n=26, seeded basis input",
+         lambda: qv.qft_circuit(26, 1)[0], 128, 60),
+        ("config2_c128", "Haar U on q=0..29 + 90 CX, n=30", lambda: qv.haar_sweep_circuit(30, SEED), 128, 2),
+        ("config2_c64", "Haar U on q=0..29 + 90 CX, n=30, complex64", lambda: qv.haar_sweep_circuit(30, SEED), 64, 2),
+        ("config3", "5x6 grid, 24 cycles of sqrt-X/Y/W + CZ patterns, n=30", lambda: qv.grid_circuit(5, 6, 24, 1),
+         128, 2),
+        ("config4_g1", "U3 layers + CX ladder, n=32 on 1 GPU (64 GiB), 20 layers",
+         lambda: qv.u3_ladder_circuit(32, 20, 1), 128, 0),
+    ]
+    for name, desc, build, prec, sample in specs:
+        c = build()
+        n = c.n_qubits
+        g = c.gates()
+        st = qv.StateVector.create(n, prec, 0)
+        stream = torch.cuda.ExternalStream(st.stream())
+        res = {}
+        for mode, fuse in (("fused", 1), ("per_gate", 0)):
+            st.set_option(qv.OPT_FUSE, fuse)
+            st.apply_gates(g)  # warm-up
+            st.reset_stats()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            st.apply_gates(g, sync=False)
+            e1.record(stream)
+            st.sync()
+            ms = e0.elapsed_time(e1)
+            s = st.stats()
+            res[mode] = {"ms": ms, "passes": s["passes"], "amp_updates_per_s": len(c) * (1 << n) / (ms / 1e3),
+                         "hbm_gbs": s["bytes_moved"] / (ms / 1e3) / 1e9}
+        del st
+        cpu = None
+        if eng is not None and sample != 0:
+            ops = np.frombuffer(g.tobytes(), dtype=GATE_DTYPE)
+            part = ops if sample is None else ops[:sample]
+            with eng.store(n, 65536, 0, default_scratch()) as rs:
+                wall = rs.apply(part, "paired-cached-parallel", cores, cores * (64 << 20))
+            per_gate = wall / len(part)
+            cpu = {"ms_total" if sample is None else "ms_total_extrapolated": per_gate * len(c),
+                   "ms_per_gate": per_gate, "cores": cores, "kind": "reference",
+                   "sample": "whole circuit" if sample is None else f"first {len(part)} ops"}
+        elif sample == 0:
+            cpu = {"note": "n=32 state is 64 GiB: reference CPU run infeasible here; "
+                           "extrapolate x4 per gate from config2 (SPEC.md:618 growth law)"}
+        print(json.dumps({"config": name, "workload": desc, "n_qubits": n, "precision": prec, "ops": len(c),
+                          "gpu": res, "speedup_fused_vs_per_gate": res["per_gate"]["ms"] / res["fused"]["ms"],
+                          "cpu_reference": cpu}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -423,7 +486,11 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--configs", action="store_true", help="per-config lines (C0..C4) instead of the headline")
     args = ap.parse_args()
+    if args.configs:
+        configs_mode(args)
+        return
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
