@@ -207,11 +207,16 @@ int qvo_apply_gate(uint32_t n, double *amps, const qvo_gate *op) {
     const uint64_t stride = 1ULL << op->target;
     const int has_ctrl = op->kind == 1;
     const uint64_t cmask = has_ctrl ? (1ULL << op->control) : 0;
-    for (uint64_t group = 0; group < dim; group += 2 * stride) {
-        for (uint64_t j = group; j < group + stride; ++j) {
-            if (has_ctrl && !(j & cmask)) continue;
-            pair_update(&amps[2 * j], &amps[2 * (j + stride)], op->u);
-        }
+    /* The reference's (group, j) double loop (kernel.cpp:72-73) visits the
+     * bases j = insert-0-at-target(p), p in [0, dim/2); pairs are disjoint,
+     * so splitting p over OpenMP threads gives the same bits. */
+    const int64_t npairs = (int64_t)(dim >> 1);
+    const unsigned t = op->target;
+#pragma omp parallel for schedule(static) if (npairs >= (1 << 16))
+    for (int64_t p = 0; p < npairs; ++p) {
+        const uint64_t j = (((uint64_t)p >> t) << (t + 1)) | ((uint64_t)p & (stride - 1));
+        if (has_ctrl && !(j & cmask)) continue;
+        pair_update(&amps[2 * j], &amps[2 * (j + stride)], op->u);
     }
     return 0;
 }

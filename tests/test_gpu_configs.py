@@ -127,3 +127,25 @@ def test_config4_shard_invariance_n28(qv, world):
     st, m = run(qv, c, world=world)
     assert m["exchanges"] >= 4
     assert np.array_equal(st.read_state(), want)
+
+
+def test_config1_n26_bit_exact_vs_oracle(qv, oracle):
+    """Config 1 at full size (n=26, H + QFT + SWAPs, 430 ops) against the
+    oracle (OpenMP over disjoint pairs, same bits as the reference's loop)."""
+    c, _ = qv.qft_circuit(26, 1)
+    want = oracle.simulate(26, gate_array(c))
+    for fuse in (True, False):
+        st, _ = run(qv, c, fuse)
+        assert np.array_equal(st.read_state(), want), fuse
+        del st
+
+
+def test_config2_n28_bit_exact_vs_oracle(qv, oracle):
+    """The config-2 sweep shape at n=28 (Haar U on every qubit + CX for
+    |c-t| in {1,15}) against the oracle, fused and per gate."""
+    c = qv.haar_sweep_circuit(28, 2508)
+    want = oracle.simulate(28, gate_array(c))
+    for fuse in (True, False):
+        st, _ = run(qv, c, fuse)
+        assert np.array_equal(st.read_state(), want), fuse
+        del st
