@@ -50,50 +50,6 @@ __device__ __forceinline__ float2 cmul(float dr, float di, float2 a) {
     return make_float2(dr * a.x - di * a.y, dr * a.y + di * a.x);
 }
 
-// Matrix arithmetic classes for the fused tile (complex128), each bit-identical
-// to the reference's (ac-bd)+(...) form but with fewer FP64 instructions:
-//   MC_GEN   general entries: 7 per output component (28 per pair)
-//   MC_REAL  every imaginary part is 0 (H, X, Ry, CX's X): a 0*x product is an
-//            exact +-0 and drops out, so re = ur0*ar + ur1*br (12 per pair)
-//   MC_EXACT every entry has a component that is 0 or a power of two (sqrt X,
-//            sqrt Y, sqrt W, S, T...): that component's products are exact, so
-//            round(p_exact - round(p_other)) == fma(exact, x, -round(p_other))
-//            (20 per pair). Bit e of the 4-bit mask (entry e = u00,u01,u10,u11)
-//            says the exact component is the imaginary one.
-// Exactness needs normal (or zero) products; the host only picks MC_EXACT for
-// coefficients in [2^-64, 2^64], far from the subnormal range for amplitudes.
-enum MatClass : int { MC_GEN = 0, MC_REAL = 1, MC_EXACT = 2 };
-
-template <int IMAG_EXACT>
-__device__ __forceinline__ double2 term_exact(double ur, double ui, double2 x) {
-    if constexpr (!IMAG_EXACT)
-        return make_double2(__fma_rn(ur, x.x, -__dmul_rn(ui, x.y)), __fma_rn(ur, x.y, __dmul_rn(ui, x.x)));
-    else
-        return make_double2(__fma_rn(-ui, x.y, __dmul_rn(ur, x.x)), __fma_rn(ui, x.x, __dmul_rn(ur, x.y)));
-}
-
-// Row ROW (0: lo = u00*a + u01*b, 1: hi = u10*a + u11*b) of the pair update.
-template <int CLS, int ROW>
-__device__ __forceinline__ double2 row_madd(const double *u, double2 a, double2 b) {
-    const double *m = u + 4 * ROW;  // m0r m0i m1r m1i
-    if constexpr (CLS == MC_REAL) {
-        return make_double2(__dadd_rn(__dmul_rn(m[0], a.x), __dmul_rn(m[2], b.x)),
-                            __dadd_rn(__dmul_rn(m[0], a.y), __dmul_rn(m[2], b.y)));
-    } else if constexpr (CLS >= MC_EXACT) {
-        constexpr int mask = CLS - MC_EXACT;
-        const double2 t0 = term_exact<(mask >> (2 * ROW)) & 1>(m[0], m[1], a);
-        const double2 t1 = term_exact<(mask >> (2 * ROW + 1)) & 1>(m[2], m[3], b);
-        return make_double2(__dadd_rn(t0.x, t1.x), __dadd_rn(t0.y, t1.y));
-    } else {
-        return madd2(m[0], m[1], a, m[2], m[3], b);
-    }
-}
-template <int CLS, int ROW>
-__device__ __forceinline__ float2 row_madd(const float *u, float2 a, float2 b) {
-    const float *m = u + 4 * ROW;
-    return madd2(m[0], m[1], a, m[2], m[3], b);
-}
-
 // Opt-in fast variants for complex128 (QVG_OPT_FMA): DFMA-contracted, 8
 // instead of 14 FP64 instructions per output, within ~1e-16 relative of the
 // exact forms but no longer bit-identical to the reference. complex64 always

@@ -15,7 +15,6 @@
 #pragma once
 
 #include <algorithm>
-#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <stdexcept>
@@ -140,26 +139,6 @@ inline Pass single_pass(const qvg_gate &g, const OpInfo &o, const PlanOptions &p
     return p;
 }
 
-// Arithmetic class of a pair op's matrix for the fused tile (MatClass in
-// qvg_kernels.cuh): which FP64 shortcuts stay bit-identical to the reference.
-inline bool exact_coeff(double v) {
-    if (v == 0.0) return true;
-    int e = 0;
-    const double m = std::frexp(std::fabs(v), &e);
-    return m == 0.5 && e > -63 && e < 65;  // +-2^k, far from under/overflow
-}
-
-inline int matrix_class(const double *u) {
-    if (u[1] == 0.0 && u[3] == 0.0 && u[5] == 0.0 && u[7] == 0.0) return MC_REAL;
-    int mask = 0;
-    for (int e = 0; e < 4; ++e) {
-        if (exact_coeff(u[2 * e])) continue;            // real part exact
-        if (exact_coeff(u[2 * e + 1])) mask |= 1 << e;  // imaginary part exact
-        else return MC_GEN;
-    }
-    return MC_EXACT + mask;
-}
-
 inline int local_bit(int q, const TileGeom &g) {
     if (q < g.lowc) return q;
     for (int i = 0; i < g.nhi; ++i)
@@ -249,7 +228,7 @@ inline Plan make_plan(const qvg_gate *ops, uint64_t count, const PlanOptions &po
                         if (gbits[s] == t.tbit) J = s;
                         if (t.cbit >= 0 && gbits[s] == t.cbit) K = s;
                     }
-                    t.slot = (8 * J + K + 1) | (matrix_class(t.u) << 8);
+                    t.slot = 8 * J + K + 1;
                 }
                 TileOp h{};
                 h.kind = TILE_GROUP;

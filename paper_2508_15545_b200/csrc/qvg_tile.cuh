@@ -71,7 +71,7 @@ __device__ __forceinline__ uint32_t swz(uint32_t l) { return l ^ ((l >> 3) & 7u)
 // Target on register slot J, control on slot K (-1: none / decided per tile):
 // both are compile-time, so a controlled op costs exactly its pairs and no
 // per-pair tests run (the instruction mix was 60% non-FP64 before this).
-template <class R, int SUB, int J, int K, bool FMA, int CLS>
+template <class R, int SUB, int J, int K, bool FMA>
 __device__ __forceinline__ void group_pair(typename Cplx<R>::T (&v)[1 << SUB], const R *u) {
     if constexpr (J < SUB && K < SUB && J != K) {
 #pragma unroll
@@ -79,45 +79,18 @@ __device__ __forceinline__ void group_pair(typename Cplx<R>::T (&v)[1 << SUB], c
             if ((r >> J) & 1) continue;
             if (K >= 0 && !((r >> K) & 1)) continue;
             const typename Cplx<R>::T a = v[r], b = v[r | (1 << J)];
-            if constexpr (FMA || CLS == MC_GEN || sizeof(R) == 4) {
-                v[r] = madd2x<FMA>(u[0], u[1], a, u[2], u[3], b);
-                v[r | (1 << J)] = madd2x<FMA>(u[4], u[5], a, u[6], u[7], b);
-            } else {
-                v[r] = row_madd<CLS, 0>(u, a, b);
-                v[r | (1 << J)] = row_madd<CLS, 1>(u, a, b);
-            }
+            v[r] = madd2x<FMA>(u[0], u[1], a, u[2], u[3], b);
+            v[r | (1 << J)] = madd2x<FMA>(u[4], u[5], a, u[6], u[7], b);
         }
     }
 }
 
-// slot code = 8*J + (K+1) in the low byte, arithmetic class (MC_*) above it.
-template <class R, int SUB, bool FMA, int J, int K>
-__device__ __forceinline__ void group_pair_cls(int cls, typename Cplx<R>::T (&v)[1 << SUB], const R *u) {
-    if constexpr (FMA || sizeof(R) == 4) {
-        group_pair<R, SUB, J, K, FMA, MC_GEN>(v, u);
-    } else {
-#define QVG_CLS(C) \
-    case C: group_pair<R, SUB, J, K, FMA, C>(v, u); break;
-        switch (cls) {
-            QVG_CLS(MC_REAL)
-            QVG_CLS(MC_EXACT + 0) QVG_CLS(MC_EXACT + 1) QVG_CLS(MC_EXACT + 2) QVG_CLS(MC_EXACT + 3)
-            QVG_CLS(MC_EXACT + 4) QVG_CLS(MC_EXACT + 5) QVG_CLS(MC_EXACT + 6) QVG_CLS(MC_EXACT + 7)
-            QVG_CLS(MC_EXACT + 8) QVG_CLS(MC_EXACT + 9) QVG_CLS(MC_EXACT + 10) QVG_CLS(MC_EXACT + 11)
-            QVG_CLS(MC_EXACT + 12) QVG_CLS(MC_EXACT + 13) QVG_CLS(MC_EXACT + 14) QVG_CLS(MC_EXACT + 15)
-        default: group_pair<R, SUB, J, K, FMA, MC_GEN>(v, u); break;
-        }
-#undef QVG_CLS
-    }
-}
-
+// slot code = 8*J + (K+1)
 template <class R, int SUB, bool FMA>
 __device__ __forceinline__ void group_pair_dispatch(int code, typename Cplx<R>::T (&v)[1 << SUB], const R *u) {
-    const int cls = code >> 8;
 #define QVG_GP(J, K) \
-    case 8 * (J) + (K) + 1: \
-        if constexpr ((J) < SUB && (K) < SUB) group_pair_cls<R, SUB, FMA, J, K>(cls, v, u); \
-        break;
-    switch (code & 0xff) {
+    case 8 * (J) + (K) + 1: group_pair<R, SUB, J, K, FMA>(v, u); break;
+    switch (code) {
         QVG_GP(0, -1) QVG_GP(0, 1) QVG_GP(0, 2) QVG_GP(0, 3)
         QVG_GP(1, -1) QVG_GP(1, 0) QVG_GP(1, 2) QVG_GP(1, 3)
         QVG_GP(2, -1) QVG_GP(2, 0) QVG_GP(2, 1) QVG_GP(2, 3)
