@@ -16,8 +16,14 @@
 // amplitudes of one SUB-bit subcube in registers and applies all the group's
 // ops there; shared memory is only the transpose buffer between groups. The
 // first group reads HBM directly and the last one writes HBM directly, so a
-// run that fits one group never touches the shared tile. The op records are
-// staged in shared memory once per CTA (they are the same for every tile).
+// run that fits one group never touches the shared tile. The op records (the
+// same for every tile) travel in the kernel's parameter bank.
+//
+// Measured limits (profiles/r01_fused_ab.json, r01_ncu_summary.md): the kernel
+// is compute/issue-bound, not HBM-bound — ~52% FP64 pipe, 64% issue slots;
+// a bit-exact FP64-instruction reduction for special matrices (real, or with
+// exact 0/2^k components) was tried and did not help (reverted), so the next
+// lever is latency and per-op overhead, not arithmetic.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -66,9 +72,7 @@ static_assert(sizeof(TileParams) < 32000, "kernel parameter block limit");
 // 2^5 apart (a group over the carrier bits) hit different banks.
 __device__ __forceinline__ uint32_t swz(uint32_t l) { return l ^ ((l >> 3) & 7u); }
 
-// Pair op on group bit J over the 2^SUB register amplitudes.
-// cmask: bit r set when element r's control is 1 (all set when uncontrolled).
-// Target on register slot J, control on slot K (-1: none / decided per tile):
+// Pair op over the 2^SUB register amplitudes. Target on register slot J, control on slot K (-1: none / decided per tile):
 // both are compile-time, so a controlled op costs exactly its pairs and no
 // per-pair tests run (the instruction mix was 60% non-FP64 before this).
 template <class R, int SUB, int J, int K, bool FMA>
