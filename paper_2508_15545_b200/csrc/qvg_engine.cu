@@ -198,10 +198,12 @@ void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *recs) {
     const size_t smem = (((sizeof(uint64_t) << g.nhi) + 15) & ~size_t(15)) +
                         (g.ngroups > 1 ? (sizeof(T) << g.k) : 0);
     const bool fma = s.fma && sizeof(R) == 8;  // complex64 always contracts
-    auto kern = g.sub == 4 ? (fma ? k_tile<R, 4, true> : k_tile<R, 4, false>)
-                           : (fma ? k_tile<R, 3, true> : k_tile<R, 3, false>);
-    static bool attr_set[2][2][2] = {};
-    bool &set = attr_set[sizeof(R) == 8][g.sub == 4][fma];
+    const bool small = threads <= 256;
+    auto kern = g.sub == 4 ? (fma ? k_tile<R, 4, true, 256> : k_tile<R, 4, false, 256>)
+                : small    ? (fma ? k_tile<R, 3, true, 256> : k_tile<R, 3, false, 256>)
+                           : (fma ? k_tile<R, 3, true, 512> : k_tile<R, 3, false, 512>);
+    static bool attr_set[2][2][2][2] = {};
+    bool &set = attr_set[sizeof(R) == 8][g.sub == 4][fma][small];
     if (!set) {
         cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
                    "cudaFuncSetAttribute(k_tile)");

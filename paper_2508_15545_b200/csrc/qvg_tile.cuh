@@ -122,8 +122,10 @@ __device__ __forceinline__ uint32_t sub_mask(int bit, const int (&b)[SUB], uint3
     return m;
 }
 
-template <class R, int SUB, bool FMA>
-__global__ void __launch_bounds__(1 << (12 - SUB), 2)
+// MAXT: the largest CTA this instantiation serves (2^(k-SUB) threads); the
+// minimum-blocks hint sizes the register budget for 3 CTAs/SM at 256 threads.
+template <class R, int SUB, bool FMA, int MAXT>
+__global__ void __launch_bounds__(MAXT, (MAXT <= 256 && SUB == 3) ? 3 : 2)
 k_tile(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams prm) {
     using T = typename Cplx<R>::T;
     constexpr int E = 1 << SUB;
