@@ -34,6 +34,7 @@ from ._core import (  # noqa: E402
     OPT_PRED_STORE,
     OPT_SUB_BITS,
     OPT_FMA,
+    OPT_TIMING,
     OPT_TILE_QUBITS,
     QVG_ABI_VERSION,
     CapacityError,

@@ -54,6 +54,7 @@ py::dict stats_dict(const qvg_stats &s) {
     d["bytes_moved"] = s.bytes_moved;
     d["exchange_bytes"] = s.exchange_bytes;
     d["exchanges"] = s.exchanges;
+    d["kernel_ms"] = s.kernel_ms;
     return d;
 }
 
@@ -333,4 +334,5 @@ PYBIND11_MODULE(_core, m) {
     m.attr("OPT_PRED_STORE") = (int)QVG_OPT_PRED_STORE;
     m.attr("OPT_SUB_BITS") = (int)QVG_OPT_SUB_BITS;
     m.attr("OPT_FMA") = (int)QVG_OPT_FMA;
+    m.attr("OPT_TIMING") = (int)QVG_OPT_TIMING;
 }

@@ -6,6 +6,7 @@
 // parallel.cpp): the state stays resident in HBM for the whole circuit and
 // each planned pass is one kernel launch on the state's stream.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -89,6 +90,8 @@ struct qvg_state {
     bool pred_store = false;   // select-and-store-all for non-inserted forced bits
     uint32_t sub_bits = 3;     // fused tile: 2^sub register amplitudes per thread (3 measured faster)
     bool fma = false;          // fused tile c128: DFMA arithmetic (not bit-identical to the reference)
+    bool timing = false;       // bracket each qvg_apply with CUDA events -> stats.kernel_ms
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
     // device scratch
     TileOp *d_ops = nullptr;
     size_t d_ops_cap = 0;
@@ -358,6 +361,10 @@ int qvg_destroy(qvg_state *s) {
         if (!s) return;
         cudaSetDevice(s->device);
         if (s->stream) cudaStreamSynchronize(s->stream);
+        for (auto &pr : s->pending) {
+            cudaEventDestroy(pr.first);
+            cudaEventDestroy(pr.second);
+        }
         s->shards.release();
         if (s->d_ops) cudaFree(s->d_ops);
         if (s->d_partials) cudaFree(s->d_partials);
@@ -403,6 +410,7 @@ int qvg_set_option(qvg_state *s, int key, int64_t value) {
             s->sub_bits = (uint32_t)value;
             break;
         case QVG_OPT_FMA: s->fma = value != 0; break;
+        case QVG_OPT_TIMING: s->timing = value != 0; break;
         default: throw Validation("unknown option " + std::to_string(key));
         }
     });
@@ -478,7 +486,18 @@ int qvg_apply(qvg_state *s, const qvg_gate *ops, uint64_t count) {
         if (count && !ops) throw Validation("null op array");
         for (uint64_t i = 0; i < count; ++i) validate_op(ops[i], s->n, i);
         set_device(s);
+        nvtxRangePushA("qvg_apply");
+        cudaEvent_t ev[2] = {nullptr, nullptr};
+        if (s->timing) {
+            for (auto &e : ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+            cuda_check(cudaEventRecord(ev[0], s->stream), "cudaEventRecord");
+        }
         shard_apply(*s, s->shards, ops, count);
+        if (s->timing) {
+            cuda_check(cudaEventRecord(ev[1], s->stream), "cudaEventRecord");
+            s->pending.push_back({ev[0], ev[1]});
+        }
+        nvtxRangePop();
         s->stats.gates_applied += count;
     });
 }
@@ -488,6 +507,7 @@ int qvg_sync(qvg_state *s) {
         check_state(s);
         set_device(s);
         cuda_check(cudaStreamSynchronize(s->stream), "cudaStreamSynchronize");
+        shard_check_async(s->shards);  // NCCL errors surface as IoError
     });
 }
 
@@ -572,6 +592,18 @@ int qvg_stats_get(const qvg_state *s, qvg_stats *out) {
     return guarded([&] {
         check_state(s);
         if (!out) throw Validation("null output pointer");
+        // Fold finished timed applies (QVG_OPT_TIMING) into kernel_ms; this
+        // waits for the work the events bracket.
+        auto *m = const_cast<qvg_state *>(s);
+        for (auto &pr : m->pending) {
+            float ms = 0.f;
+            cuda_check(cudaEventSynchronize(pr.second), "cudaEventSynchronize");
+            cuda_check(cudaEventElapsedTime(&ms, pr.first, pr.second), "cudaEventElapsedTime");
+            m->stats.kernel_ms += ms;
+            cudaEventDestroy(pr.first);
+            cudaEventDestroy(pr.second);
+        }
+        m->pending.clear();
         *out = s->stats;
     });
 }

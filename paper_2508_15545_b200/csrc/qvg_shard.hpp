@@ -256,6 +256,16 @@ inline void shard_transfer(qvg_state &s, ShardSet &set, void *host, uint64_t off
     if (sync) cuda_throw(cudaStreamSynchronize(st), "transfer sync");
 }
 
+// Asynchronous NCCL failures (a peer died, a link error) are reported on the
+// next qvg_sync as IoError; the whole circuit fails (no elastic recovery, like
+// the reference's rethrow-after-join, parallel.cpp:128-132).
+inline void shard_check_async(ShardSet &set) {
+    if (!set.comm) return;
+    ncclResult_t r = ncclSuccess;
+    nccl_check(ncclCommGetAsyncError(set.comm, &r), "ncclCommGetAsyncError");
+    nccl_check(r, "NCCL asynchronous error");
+}
+
 inline double shard_allreduce_sum(qvg_state &s, ShardSet &set, double v) {
     if (!set.comm) return v;
     cudaStream_t st = shard_stream(s);

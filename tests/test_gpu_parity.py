@@ -171,3 +171,18 @@ def test_tile_subcube_variants_bit_exact(qv, oracle, sub):
         m = qv.apply_circuit(st, c)
         assert m["fused_passes"] > 0
         assert np.array_equal(st.read_state(), want)
+
+
+def test_timing_and_async_copies(qv):
+    """QVG_OPT_TIMING fills kernel_ms; load_async/read_async round-trip."""
+    n = 16
+    st = qv.StateVector.create(n, 128, 0)
+    st.set_option(qv.OPT_TIMING, 1)
+    qv.apply_circuit(st, qv.make_benchmark_circuit(n))
+    assert st.stats()["kernel_ms"] > 0.0
+    host = np.random.default_rng(0).standard_normal(2 << n).view(np.complex128)
+    st.load_async(host)
+    out = np.empty_like(host)
+    st.read_async(out)
+    st.sync()
+    assert np.array_equal(out, host)
