@@ -41,6 +41,8 @@ SEED = 2508
 WORKLOAD = "config2: n=30 c128 sweep, Haar U on q=0..29 + CX for |c-t| in {1,15,29} (120 gate passes)"
 METRIC = "amplitude-updates/s per gate pass (n=30 c128 gate sweep)"
 UNIT = "amp-updates/s"
+E2E_STATES = 3
+E2E_CHUNKS = 8
 
 
 def peaks():
@@ -298,9 +300,9 @@ def e2e_leg(qv, st, circ, recs, line, args):
     with the API's defaults (`apply_circuit(state, circuit)`: strategy gpu,
     fusion on) and copies the state back, all inside the timed region.
 
-    value: a stream of independent steps over two device states on their own
-    streams (load_async / apply_circuit(sync=False) / read_async), so one
-    state's PCIe copies overlap the other's gates (PCIe is full duplex).
+    value: a stream of independent steps over E2E_STATES device states on their
+    own streams (load_async / apply_circuit(sync=False) / read_async), so one
+    state's PCIe copies overlap another's gates (PCIe is full duplex).
     latency_ms: one step alone, synchronous (load_state / apply_circuit /
     read_into)."""
     import torch
@@ -308,7 +310,7 @@ def e2e_leg(qv, st, circ, recs, line, args):
     n = circ.n_qubits
     count = 1 << n
     bufs = []
-    for _ in range(2):
+    for _ in range(E2E_STATES):
         h = torch.empty(count * 2, dtype=torch.float64, pin_memory=True)
         a = h.numpy().view(np.complex128)
         a[:] = 1.0 / math.sqrt(count)
@@ -320,27 +322,32 @@ def e2e_leg(qv, st, circ, recs, line, args):
     m = qv.apply_circuit(st, circ)
     st.read_into(bufs[0][1])
     latency = (time.perf_counter() - t0) * 1e3
-    # pipelined stream of steps on two states
-    st2 = qv.StateVector.create(n, 128, 0)
-    states = [st, st2]
-    steps = max(4, args.steps)
+    # pipelined stream of steps over E2E_STATES device states, each copy in
+    # E2E_CHUNKS pieces so the copy engines interleave H2D and D2H
+    # (profiles/r01_e2e_ab.json: 3 states x 8 chunks 416 ms/step, 2 x 1 472)
+    states = [st] + [qv.StateVector.create(n, 128, 0) for _ in range(E2E_STATES - 1)]
+    steps = max(2 * E2E_STATES, args.steps)
+    per = count // E2E_CHUNKS
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for k in range(steps):
-        s, (_, buf) = states[k % 2], bufs[k % 2]
-        s.load_async(buf)
+        s, (_, buf) = states[k % E2E_STATES], bufs[k % E2E_STATES]
+        for c in range(E2E_CHUNKS):
+            s.load_async(buf[c * per:(c + 1) * per], c * per)
         qv.apply_circuit(s, circ, sync=False)
-        s.read_async(buf)
+        for c in range(E2E_CHUNKS):
+            s.read_async(buf[c * per:(c + 1) * per], c * per)
     for s in states:
         s.sync()
     ms = (time.perf_counter() - t0) * 1e3 / steps
-    del st2
+    del states[1:]
     line["e2e"] = {"value": len(circ) * count / (ms / 1e3), "unit": UNIT, "ms_per_step": ms,
                    "latency_ms": latency, "latency_value": len(circ) * count / (latency / 1e3),
                    "steps": steps, "h2d_bytes_per_step": count * 16, "d2h_bytes_per_step": count * 16,
                    "hbm_passes_per_step": m["traversals"],
                    "path": "per step: StateVector.load_async(pinned) -> apply_circuit(state, circuit) [API defaults: "
-                           "gpu, fused] -> read_async(pinned); two states alternate, host wall clock"}
+                           f"gpu, fused] -> read_async(pinned); {E2E_STATES} states rotate, copies in "
+                           f"{E2E_CHUNKS} chunks, host wall clock"}
 
 
 def cpu_baseline(args, nops_hint=120):
