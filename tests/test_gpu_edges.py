@@ -1,0 +1,114 @@
+"""Edge cases on the device path: the smallest and empty inputs, range and
+capacity errors, basis states, precision mixes, repeated apply calls (plan
+buffers reused), and odd tile options (reference tests: test_store.cpp size
+checks, test_kernel.cpp:120-123 out-of-range targets, test_parallel.cpp
+worker-count edges)."""
+import numpy as np
+import pytest
+
+from conftest import gate_array
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5])
+def test_tiny_states_every_kernel(qv, oracle, n):
+    c = qv.random_circuit(n, 80, 100 + n)
+    want = oracle.simulate(n, gate_array(c))
+    for fuse in (True, False):
+        for prec in (128, 64):
+            st = qv.StateVector.create(n, prec, 0)
+            qv.apply_circuit(st, c, fuse=fuse)
+            got = st.read_state()
+            if prec == 128:
+                assert np.array_equal(got, want), (n, fuse)
+            else:
+                assert np.abs(got - want).max() <= 1e-5
+
+
+def test_empty_circuit_and_identity_ops(qv):
+    st = qv.StateVector.create(6, 128, 0)
+    m = qv.apply_circuit(st, qv.parse_circuit("qubits 6\n"))
+    assert m["gates_applied"] == 0 and m["traversals"] == 0
+    m = qv.apply_circuit(st, qv.parse_circuit("qubits 6\ncp 1 2 0\nrz 3 0\n"), fuse=False)
+    # cp(0) is the identity (no pass); rz(0) = diag(1,1) as well
+    assert m["traversals"] == 0
+    s = st.read_state()
+    assert s[0] == 1 and not s[1:].any()
+
+
+def test_basis_init_and_ranges(qv):
+    st = qv.StateVector.create(8, 128, 0)
+    st.init_basis(200)
+    s = st.read_state()
+    assert s[200] == 1 and np.count_nonzero(s) == 1
+    assert st.amplitude(200) == 1
+    with pytest.raises(qv.ValidationError):
+        st.init_basis(256)
+    with pytest.raises(qv.ValidationError):
+        st.read_state(250, 10)
+    with pytest.raises(qv.ValidationError):
+        st.load_state(np.zeros(10, np.complex128), 250)
+    with pytest.raises(qv.ValidationError):
+        st.amplitude(256)
+    assert st.read_state(256, 0).size == 0
+
+
+def test_capacity_error_is_typed(qv):
+    # 2^40 complex128 amplitudes = 16 TiB: the device allocation must fail as CapacityError
+    with pytest.raises(qv.CapacityError):
+        qv.StateVector.create(40, 128, 0)
+    with pytest.raises(qv.ValidationError):
+        qv.StateVector.create(41, 128, 0)
+
+
+def test_shard_limits(qv):
+    with pytest.raises(qv.ValidationError):
+        qv.StateVector.create_sharded(3, 128, 0, 0, 4, None)  # too few qubits for 4 shards
+    with pytest.raises(qv.ValidationError):
+        qv.StateVector.create_sharded(10, 128, 0, 0, 3, None)  # not a power of two
+    st = qv.StateVector.create_sharded(4, 128, 0, 0, 4, None)  # L = 2, the minimum
+    c = qv.random_circuit(4, 60, 9)
+    st2 = qv.StateVector.create(4, 128, 0)
+    qv.apply_circuit(st, c)
+    qv.apply_circuit(st2, c)
+    assert np.array_equal(st.read_state(), st2.read_state())
+
+
+def test_repeated_apply_reuses_plan_buffers(qv, oracle):
+    n = 14
+    st = qv.StateVector.create(n, 128, 0)
+    want = oracle.basis(n)
+    for seed in range(6):
+        c = qv.random_circuit(n, 50 + 37 * seed, seed)
+        qv.apply_circuit(st, c)
+        oracle.apply(n, want, gate_array(c))
+    assert np.array_equal(st.read_state(), want)
+
+
+@pytest.mark.parametrize("opt,val", [("OPT_TILE_QUBITS", 5), ("OPT_TILE_QUBITS", 12), ("OPT_CARRIERS", 0),
+                                     ("OPT_CARRIERS", 6), ("OPT_SUB_BITS", 4), ("OPT_LOW_KERNEL", 1),
+                                     ("OPT_MIN_RUN", 128), ("OPT_PRED_STORE", 1)])
+def test_options_keep_bits(qv, oracle, opt, val):
+    c = qv.random_circuit(13, 400, 77)
+    want = oracle.simulate(13, gate_array(c))
+    st = qv.StateVector.create(13, 128, 0)
+    st.set_option(getattr(qv, opt), val)
+    qv.apply_circuit(st, c, tile_qubits=val if opt == "OPT_TILE_QUBITS" else 0)
+    assert np.array_equal(st.read_state(), want)
+
+
+def test_bad_options(qv):
+    st = qv.StateVector.create(4, 128, 0)
+    for key, val in [(qv.OPT_TILE_QUBITS, 13), (qv.OPT_TILE_QUBITS, 1), (qv.OPT_MIN_RUN, 3),
+                     (qv.OPT_SUB_BITS, 5), (999, 1)]:
+        with pytest.raises(qv.ValidationError):
+            st.set_option(key, val)
+
+
+def test_nonfinite_matrix_rejected(qv):
+    st = qv.StateVector.create(4, 128, 0)
+    g = gate_array(qv.parse_circuit("qubits 4\nh 1\n"))
+    g[0]["u"][0] = np.nan
+    with pytest.raises(qv.ValidationError, match="finite"):
+        st.apply_gates(g.tobytes())
