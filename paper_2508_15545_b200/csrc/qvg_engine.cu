@@ -39,6 +39,9 @@ struct CudaFail : std::runtime_error {
 
 void cuda_check(cudaError_t e, const char *what) {
     if (e == cudaSuccess) return;
+    // A failed call (e.g. an oversized cudaMalloc) also sets the runtime's
+    // last-error slot; clear it so the next launch check does not report it.
+    (void)cudaGetLastError();
     const int code = (e == cudaErrorMemoryAllocation) ? QVG_ERR_CAPACITY
                      : (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver ||
                         e == cudaErrorNoKernelImageForDevice)
