@@ -52,6 +52,9 @@ struct ShardSet {
     ncclComm_t comm = nullptr;
     void *scratch = nullptr;
     uint64_t scratch_bytes = 0;
+    uint64_t chunk_bytes = 0;
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t received[2] = {nullptr, nullptr}, copied[2] = {nullptr, nullptr};
     double *d_scalar = nullptr;
 
     void init(qvg_state &s, uint32_t n_, uint32_t L_, uint32_t rank_, uint32_t world_, const void *nccl_id,
@@ -74,9 +77,15 @@ struct ShardSet {
             ncclUniqueId id;
             std::memcpy(&id, nccl_id, sizeof(id));
             nccl_check(ncclCommInitRank(&comm, (int)world, id, (int)rank), "ncclCommInitRank");
-            scratch_bytes = std::min<uint64_t>(bytes / 2, 512ull << 20);
+            chunk_bytes = std::min<uint64_t>(bytes / 2, 256ull << 20);
+            scratch_bytes = 2 * chunk_bytes;  // double-buffered
             cuda_throw(cudaMalloc(&scratch, scratch_bytes), "cudaMalloc(exchange scratch)");
             cuda_throw(cudaMalloc(&d_scalar, 64), "cudaMalloc(scalar)");
+            cuda_throw(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking), "cudaStreamCreate(copy)");
+            for (int b = 0; b < 2; ++b) {
+                cuda_throw(cudaEventCreateWithFlags(&received[b], cudaEventDisableTiming), "cudaEventCreate");
+                cuda_throw(cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming), "cudaEventCreate");
+            }
         }
     }
 
@@ -86,6 +95,13 @@ struct ShardSet {
         ranks.clear();
         if (scratch) cudaFree(scratch);
         scratch = nullptr;
+        if (copy_stream) cudaStreamDestroy(copy_stream);
+        copy_stream = nullptr;
+        for (int b = 0; b < 2; ++b) {
+            if (received[b]) cudaEventDestroy(received[b]);
+            if (copied[b]) cudaEventDestroy(copied[b]);
+            received[b] = copied[b] = nullptr;
+        }
         if (d_scalar) cudaFree(d_scalar);
         d_scalar = nullptr;
         if (comm) ncclCommDestroy(comm);
@@ -134,14 +150,19 @@ inline void launch_swap_bits(cudaStream_t st, void *psi, uint32_t L, uint32_t a,
     }
 }
 
+// Virtual-shard exchange: p's amplitudes with local bit lpos = 1 trade places
+// with q's amplitudes with local bit lpos = 0.
 template <class R>
-inline void launch_swap_ranges(cudaStream_t st, void *p, void *q, uint64_t count) {
+inline void launch_swap_halves(cudaStream_t st, void *p, void *q, uint32_t L, uint32_t lpos) {
     using T = typename Cplx<R>::T;
+    const uint64_t count = 1ull << (L - 1);
     if (count >= 1024)
-        k_swap_ranges<R, 4><<<(unsigned)(count / 1024), 256, 0, st>>>(static_cast<T *>(p), static_cast<T *>(q));
+        k_swap_halves<R, 4><<<(unsigned)(count / 1024), 256, 0, st>>>(static_cast<T *>(p), static_cast<T *>(q),
+                                                                       (int)lpos);
     else {
         const unsigned bs = (unsigned)std::min<uint64_t>(count, 256);
-        k_swap_ranges<R, 1><<<(unsigned)(count / bs), bs, 0, st>>>(static_cast<T *>(p), static_cast<T *>(q));
+        k_swap_halves<R, 1><<<(unsigned)(count / bs), bs, 0, st>>>(static_cast<T *>(p), static_cast<T *>(q),
+                                                                    (int)lpos);
     }
 }
 
@@ -158,9 +179,15 @@ inline void run_local_swap(qvg_state &s, ShardSet &set, uint32_t a, uint32_t b) 
 }
 
 // Half-shard exchange swapping global physical qubit gpos with local qubit
-// L-1: a rank whose gpos bit is b sends its half with local bit L-1 = 1-b and
-// receives the partner's half into the same place.
-inline void run_exchange(qvg_state &s, ShardSet &set, uint32_t gpos) {
+// lpos: a rank whose gpos bit is b sends the amplitudes whose local bit lpos is
+// 1-b (2^(L-1-lpos) blocks of 2^lpos contiguous amplitudes) and receives the
+// partner's matching half into the same places.
+//
+// NCCL transport: each block goes in chunks through two scratch buffers; the
+// send/recv of chunk i+1 (state stream) overlaps the scratch -> shard copy of
+// chunk i (copy stream), ordered by events. A chunk's copy waits for its own
+// send/recv group, so the bytes it overwrites were already sent.
+inline void run_exchange(qvg_state &s, ShardSet &set, uint32_t gpos, uint32_t lpos) {
     cudaStream_t st = shard_stream(s);
     const uint32_t S = shard_amp_bytes(s);
     const uint64_t half = 1ull << (set.L - 1);
@@ -171,11 +198,9 @@ inline void run_exchange(qvg_state &s, ShardSet &set, uint32_t gpos) {
             const uint32_t r = set.ranks[b];
             if (r & bit) continue;
             const uint32_t partner = r | bit;
-            // r has bit 0: sends its upper half; partner (bit 1) its lower half.
-            char *mine = static_cast<char *>(set.bufs[b]) + half_bytes;
-            char *theirs = static_cast<char *>(set.bufs[partner]);
-            if (S == 16) launch_swap_ranges<double>(st, mine, theirs, half);
-            else launch_swap_ranges<float>(st, mine, theirs, half);
+            // r (bit 0) sends its lpos=1 half; partner (bit 1) its lpos=0 half.
+            if (S == 16) launch_swap_halves<double>(st, set.bufs[b], set.bufs[partner], set.L, lpos);
+            else launch_swap_halves<float>(st, set.bufs[b], set.bufs[partner], set.L, lpos);
         }
         cuda_throw(cudaGetLastError(), "exchange launch");
         shard_stats(s).exchanges += 1;
@@ -183,16 +208,29 @@ inline void run_exchange(qvg_state &s, ShardSet &set, uint32_t gpos) {
         return;
     }
     const int partner = (int)(set.rank ^ bit);
-    const bool myb = (set.rank & bit) != 0;
-    char *mine = static_cast<char *>(set.bufs[0]) + (myb ? 0 : half_bytes);
-    for (uint64_t off = 0; off < half_bytes; off += set.scratch_bytes) {
-        const uint64_t c = std::min<uint64_t>(set.scratch_bytes, half_bytes - off);
-        nccl_check(ncclGroupStart(), "ncclGroupStart");
-        nccl_check(ncclSend(mine + off, c, ncclChar, partner, set.comm, st), "ncclSend");
-        nccl_check(ncclRecv(set.scratch, c, ncclChar, partner, set.comm, st), "ncclRecv");
-        nccl_check(ncclGroupEnd(), "ncclGroupEnd");
-        cuda_throw(cudaMemcpyAsync(mine + off, set.scratch, c, cudaMemcpyDeviceToDevice, st), "exchange copy");
+    const uint64_t sendbit = (set.rank & bit) ? 0 : 1;  // my half: local bit lpos == sendbit
+    const uint64_t block_bytes = (uint64_t)S << lpos;
+    const uint64_t nblocks = 1ull << (set.L - 1 - lpos);
+    char *base = static_cast<char *>(set.bufs[0]);
+    uint64_t i = 0;
+    for (uint64_t k = 0; k < nblocks; ++k) {
+        char *blk = base + (((k << 1) | sendbit) * block_bytes);
+        for (uint64_t off = 0; off < block_bytes; off += set.chunk_bytes, ++i) {
+            const uint64_t c = std::min<uint64_t>(set.chunk_bytes, block_bytes - off);
+            char *scr = static_cast<char *>(set.scratch) + (i & 1) * set.chunk_bytes;
+            if (i >= 2) cuda_throw(cudaStreamWaitEvent(st, set.copied[i & 1], 0), "wait scratch");
+            nccl_check(ncclGroupStart(), "ncclGroupStart");
+            nccl_check(ncclSend(blk + off, c, ncclChar, partner, set.comm, st), "ncclSend");
+            nccl_check(ncclRecv(scr, c, ncclChar, partner, set.comm, st), "ncclRecv");
+            nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+            cuda_throw(cudaEventRecord(set.received[i & 1], st), "record received");
+            cuda_throw(cudaStreamWaitEvent(set.copy_stream, set.received[i & 1], 0), "wait received");
+            cuda_throw(cudaMemcpyAsync(blk + off, scr, c, cudaMemcpyDeviceToDevice, set.copy_stream), "exchange copy");
+            cuda_throw(cudaEventRecord(set.copied[i & 1], set.copy_stream), "record copied");
+        }
     }
+    for (int b = 0; b < 2 && (uint64_t)b < i; ++b)  // later work on the state stream sees every copy
+        cuda_throw(cudaStreamWaitEvent(st, set.copied[b], 0), "wait copies");
     shard_stats(s).exchanges += 1;
     shard_stats(s).exchange_bytes += half_bytes;
 }
@@ -215,7 +253,7 @@ inline void run_steps(qvg_state &s, ShardSet &set, const std::vector<ShardStep> 
             continue;
         }
         flush();
-        if (st.type == STEP_EXCHANGE) run_exchange(s, set, st.gpos);
+        if (st.type == STEP_EXCHANGE) run_exchange(s, set, st.gpos, st.lpos);
         else run_local_swap(s, set, st.lpos, st.lpos2);
     }
     flush();

@@ -26,6 +26,13 @@ def schedule(qv, circuit, world, canonicalize=True):
     return np.frombuffer(raw.tobytes(), STEP_DTYPE)
 
 
+def half_indices(L, lpos):
+    """Local indices with bit lpos = 0, ascending (one side of an exchange)."""
+    p = np.arange(1 << (L - 1), dtype=np.int64)
+    low = (1 << lpos) - 1
+    return ((p & ~low) << 1) | (p & low)
+
+
 def swap_local_bits(shard, a, b):
     L = int(np.log2(shard.size))
     idx = np.arange(shard.size)
@@ -52,13 +59,15 @@ def emulate(oracle, n, world, steps):
     for st in steps:
         if st["type"] == 1:
             bit = 1 << (int(st["gpos"]) - L)
-            assert st["lpos"] == L - 1
+            lpos = int(st["lpos"])
+            base = half_indices(L, lpos)
             for r in range(world):
                 if r & bit:
                     continue
-                p = r | bit
-                mine, theirs = shards[r][half:].copy(), shards[p][:half].copy()
-                shards[r][half:], shards[p][:half] = theirs, mine
+                p = r | bit  # r sends its local-bit-lpos=1 half, p its bit=0 half
+                ri, pi = base | (1 << lpos), base
+                mine, theirs = shards[r][ri].copy(), shards[p][pi].copy()
+                shards[r][ri], shards[p][pi] = theirs, mine
         else:
             for r in range(world):
                 run_local_steps(oracle, L, shards[r], r, [st])
@@ -106,6 +115,18 @@ def test_schedule_shape(qv):
     assert list(full["type"]).count(1) == 2  # the exchange and its undo
 
 
+def test_victim_choice_cuts_exchanges(qv):
+    """Config 4 at full width: the Belady victim choice among the high local
+    qubits needs far fewer half-shard exchanges than always swapping with
+    L-1 (79 / 119 / 159 for 20 layers at 2 / 4 / 8 shards)."""
+    for n, world, limit in [(33, 2, 45), (34, 4, 90), (35, 8, 135)]:
+        s = schedule(qv, qv.u3_ladder_circuit(n, 20, 1), world, canonicalize=False)
+        ex = s[s["type"] == 1]
+        L = n - int(np.log2(world))
+        assert len(ex) <= limit, (n, world, len(ex))
+        assert ex["lpos"].min() >= max(L - 12, L // 2)  # blocks of >= 2^20 amplitudes
+
+
 # --- multi-process: gloo, world_size 2 and 4 -----------------------------------------------
 def _free_port():
     with socket.socket() as s:
@@ -141,14 +162,16 @@ def _worker(rank, world, port, fn, args, q):
         for st in steps:
             if st["type"] == 1:  # pairwise half-shard exchange with the partner rank
                 bit = 1 << (int(st["gpos"]) - L)
+                lpos = int(st["lpos"])
                 partner = rank ^ bit
-                mine = shard[half:] if not (rank & bit) else shard[:half]
-                send = torch.from_numpy(mine.copy().view(np.float64))
+                sendbit = 0 if (rank & bit) else 1
+                idx = half_indices(L, lpos) | (sendbit << lpos)
+                send = torch.from_numpy(shard[idx].view(np.float64).copy())
                 recv = torch.empty_like(send)
                 reqs = [dist.isend(send, partner), dist.irecv(recv, partner)]
                 for r in reqs:
                     r.wait()
-                mine[:] = recv.numpy().view(np.complex128)
+                shard[idx] = recv.numpy().view(np.complex128)
             else:
                 run_local_steps(oracle, L, shard, rank, [st])
         parts = [torch.empty(2 << L, dtype=torch.float64) for _ in range(world)]
