@@ -155,6 +155,12 @@ int qvg_norm(qvg_state *s, double *out);
 int qvg_top_amplitudes(qvg_state *s, uint32_t k, uint64_t *index_out,
                        double *amps_out);
 
+/* <a|b> = sum_i conj(a_i) b_i for two states of the same shape (
+ * fidelity = |<a|b>|^2, the north_star parity measure). */
+int qvg_inner_product(qvg_state *a, qvg_state *b, double *re, double *im);
+/* max_i |a_i - b_i| (max_deviation, reference dense.cpp:174-183). */
+int qvg_max_deviation(qvg_state *a, qvg_state *b, double *out);
+
 /* ---- instrumentation --------------------------------------------------------- */
 int qvg_stats_get(const qvg_state *s, qvg_stats *out);
 int qvg_stats_reset(qvg_state *s);

@@ -194,6 +194,30 @@ PYBIND11_MODULE(_core, m) {
             py::gil_scoped_release nogil;
             return s.top_amplitudes(k);
         }, py::arg("k") = 8)
+        .def("inner", [](StateVector &a, StateVector &b) {
+            double re = 0, im = 0;
+            {
+                py::gil_scoped_release nogil;
+                check_status(qvg_inner_product(a.handle(), b.handle(), &re, &im));
+            }
+            return std::complex<double>(re, im);
+        }, py::arg("other"), "<self|other> = sum conj(a_i) b_i on the device")
+        .def("fidelity", [](StateVector &a, StateVector &b) {
+            double re = 0, im = 0;
+            {
+                py::gil_scoped_release nogil;
+                check_status(qvg_inner_product(a.handle(), b.handle(), &re, &im));
+            }
+            return re * re + im * im;
+        }, py::arg("other"), "|<self|other>|^2")
+        .def("max_deviation", [](StateVector &a, StateVector &b) {
+            double m = 0;
+            {
+                py::gil_scoped_release nogil;
+                check_status(qvg_max_deviation(a.handle(), b.handle(), &m));
+            }
+            return m;
+        }, py::arg("other"), "max_i |a_i - b_i| on the device")
         .def("set_option", &StateVector::set_option, py::arg("key"), py::arg("value"))
         .def("stats", [](const StateVector &s) { return stats_dict(s.stats()); })
         .def("reset_stats", [](StateVector &s) { check_status(qvg_stats_reset(s.handle())); })

@@ -591,6 +591,89 @@ int qvg_top_amplitudes(qvg_state *s, uint32_t k, uint64_t *index_out, double *am
     });
 }
 
+}  // extern "C"
+
+static void check_same_shape(const qvg_state *a, const qvg_state *b) {
+    if (!a || !b) throw Validation("null state");
+    if (a->n != b->n || a->precision != b->precision || a->world != b->world || a->rank != b->rank ||
+        a->device != b->device || a->shards.is_virtual != b->shards.is_virtual)
+        throw Validation("states differ in shape (qubits, precision, sharding or device)");
+}
+
+// Two-state reduction over matching local shard buffers; both states are
+// first brought to canonical order and `b`'s work is ordered before `a`'s
+// stream reads it.
+template <class Launch>
+static void two_state_reduce(qvg_state *a, qvg_state *b, int words, Launch launch, std::vector<double> &partials) {
+    check_same_shape(a, b);
+    set_device(a);
+    shard_canonicalize(*a, a->shards);
+    shard_canonicalize(*b, b->shards);
+    cuda_check(cudaStreamSynchronize(b->stream), "sync second state");
+    const uint64_t local = 1ull << a->L;
+    const std::vector<void *> pa = a->shards.local_buffers(), pb = b->shards.local_buffers();
+    partials.assign((size_t)kNormBlocks * words * pa.size(), 0.0);
+    for (size_t i = 0; i < pa.size(); ++i) {
+        launch(pa[i], pb[i], local);
+        cuda_check(cudaGetLastError(), "reduction launch");
+        cuda_check(cudaMemcpyAsync(partials.data() + (size_t)kNormBlocks * words * i, a->d_partials,
+                                   (size_t)kNormBlocks * words * sizeof(double), cudaMemcpyDeviceToHost, a->stream),
+                   "D2H partials");
+        cuda_check(cudaStreamSynchronize(a->stream), "reduction sync");
+    }
+}
+
+extern "C" {
+
+int qvg_inner_product(qvg_state *a, qvg_state *b, double *re, double *im) {
+    return guarded([&] {
+        if (!re || !im) throw Validation("null output pointer");
+        std::vector<double> part;
+        two_state_reduce(a, b, 2, [&](void *x, void *y, uint64_t local) {
+            if (a->precision == QVG_C128)
+                k_inner_partials<double><<<kNormBlocks, 256, 0, a->stream>>>(static_cast<const double2 *>(x),
+                                                                              static_cast<const double2 *>(y), local,
+                                                                              a->d_partials);
+            else
+                k_inner_partials<float><<<kNormBlocks, 256, 0, a->stream>>>(static_cast<const float2 *>(x),
+                                                                             static_cast<const float2 *>(y), local,
+                                                                             a->d_partials);
+        }, part);
+        double sr = 0.0, cr = 0.0, si = 0.0, ci = 0.0;  // Kahan, fixed order
+        for (size_t i = 0; i < part.size(); i += 2) {
+            const double tr = part[i] - cr, nr = sr + tr;
+            cr = (nr - sr) - tr;
+            sr = nr;
+            const double ti = part[i + 1] - ci, ni = si + ti;
+            ci = (ni - si) - ti;
+            si = ni;
+        }
+        *re = shard_allreduce_sum(*a, a->shards, sr);
+        *im = shard_allreduce_sum(*a, a->shards, si);
+    });
+}
+
+int qvg_max_deviation(qvg_state *a, qvg_state *b, double *out) {
+    return guarded([&] {
+        if (!out) throw Validation("null output pointer");
+        std::vector<double> part;
+        two_state_reduce(a, b, 1, [&](void *x, void *y, uint64_t local) {
+            if (a->precision == QVG_C128)
+                k_maxdiff_partials<double><<<kNormBlocks, 256, 0, a->stream>>>(static_cast<const double2 *>(x),
+                                                                                static_cast<const double2 *>(y),
+                                                                                local, a->d_partials);
+            else
+                k_maxdiff_partials<float><<<kNormBlocks, 256, 0, a->stream>>>(static_cast<const float2 *>(x),
+                                                                               static_cast<const float2 *>(y),
+                                                                               local, a->d_partials);
+        }, part);
+        double m = 0.0;
+        for (double v : part)
+            if (v > m || v != v) m = v;
+        *out = shard_allreduce_max(*a, a->shards, m);
+    });
+}
+
 int qvg_stats_get(const qvg_state *s, qvg_stats *out) {
     return guarded([&] {
         check_state(s);

@@ -26,6 +26,7 @@
 #include "qvg.h"
 #include "qvg_kernels.cuh"
 #include "qvg_plan.hpp"
+#include "qvg_readout.cuh"
 #include "qvg_schedule.hpp"
 
 struct qvg_state;
@@ -304,11 +305,21 @@ inline void shard_check_async(ShardSet &set) {
     nccl_check(r, "NCCL asynchronous error");
 }
 
+inline double shard_allreduce_op(qvg_state &s, ShardSet &set, double v, ncclRedOp_t op);
+
+inline double shard_allreduce_max(qvg_state &s, ShardSet &set, double v) {
+    return shard_allreduce_op(s, set, v, ncclMax);
+}
+
 inline double shard_allreduce_sum(qvg_state &s, ShardSet &set, double v) {
+    return shard_allreduce_op(s, set, v, ncclSum);
+}
+
+inline double shard_allreduce_op(qvg_state &s, ShardSet &set, double v, ncclRedOp_t op) {
     if (!set.comm) return v;
     cudaStream_t st = shard_stream(s);
     cuda_throw(cudaMemcpyAsync(set.d_scalar, &v, sizeof(double), cudaMemcpyHostToDevice, st), "H2D scalar");
-    nccl_check(ncclAllReduce(set.d_scalar, set.d_scalar, 1, ncclDouble, ncclSum, set.comm, st), "ncclAllReduce");
+    nccl_check(ncclAllReduce(set.d_scalar, set.d_scalar, 1, ncclDouble, op, set.comm, st), "ncclAllReduce");
     double out = 0.0;
     cuda_throw(cudaMemcpyAsync(&out, set.d_scalar, sizeof(double), cudaMemcpyDeviceToHost, st), "D2H scalar");
     cuda_throw(cudaStreamSynchronize(st), "allreduce sync");
@@ -316,92 +327,172 @@ inline double shard_allreduce_sum(qvg_state &s, ShardSet &set, double v) {
 }
 
 // top_amplitudes (reference engine.cpp:511-544): the k largest |a|^2,
-// descending, ties by ascending index. Streams the shard through a chunked
-// D2H copy and keeps a k-heap on the host.
+// descending, ties by ascending index — an exact radix select on the device
+// (qvg_readout.cuh): six histogram passes over the IEEE bits of |a|^2 find the
+// k-th largest key tau, one pass collects the keys above it, and ties at tau
+// are taken in index order from the first chunks that hold them. Sharded
+// states reduce the histograms with ncclAllReduce and gather the candidates.
 inline void shard_top_amplitudes(qvg_state &s, ShardSet &set, uint32_t k, uint64_t *index_out, double *amps_out) {
     if (k == 0) return;
     shard_canonicalize(s, set);
     cudaStream_t st = shard_stream(s);
     const uint32_t S = shard_amp_bytes(s);
-    struct Entry {
-        double p;
-        uint64_t i;
-        double re, im;
-    };
-    auto better = [](const Entry &a, const Entry &b) { return a.p != b.p ? a.p > b.p : a.i < b.i; };
-    std::priority_queue<Entry, std::vector<Entry>, decltype(better)> heap(better);
     const uint64_t local = 1ull << set.L;
-    const uint64_t chunk = std::min<uint64_t>(local, 1ull << 22);
-    std::vector<double> host(chunk * 2);
-    std::vector<float> hostf(S == 8 ? chunk * 2 : 0);
-    for (size_t b = 0; b < set.bufs.size(); ++b) {
-        const uint64_t base = (uint64_t)set.ranks[b] * local;
-        for (uint64_t off = 0; off < local; off += chunk) {
-            void *dst = S == 16 ? (void *)host.data() : (void *)hostf.data();
-            cuda_throw(cudaMemcpyAsync(dst, static_cast<char *>(set.bufs[b]) + off * S, chunk * S,
-                                       cudaMemcpyDeviceToHost, st),
-                       "top-k D2H");
-            cuda_throw(cudaStreamSynchronize(st), "top-k sync");
-            for (uint64_t j = 0; j < chunk; ++j) {
-                const double re = S == 16 ? host[2 * j] : (double)hostf[2 * j];
-                const double im = S == 16 ? host[2 * j + 1] : (double)hostf[2 * j + 1];
-                const Entry e{re * re + im * im, base + off + j, re, im};
-                if (heap.size() < k) heap.push(e);
-                else if (better(e, heap.top())) {
-                    heap.pop();
-                    heap.push(e);
+    const uint64_t total = 1ull << set.n;
+    const uint32_t kk = (uint32_t)std::min<uint64_t>(k, total);
+    const bool dbl = S == 16;
+    const unsigned grid = (unsigned)std::min<uint64_t>((local + 255) / 256, 4096);
+    // device scratch: histogram, candidate list, counters
+    unsigned int *d_hist = nullptr, *d_n = nullptr;
+    TopkEntry *d_out = nullptr;
+    cuda_throw(cudaMalloc(&d_hist, kTopkBins * sizeof(unsigned int)), "cudaMalloc(top-k hist)");
+    cuda_throw(cudaMalloc(&d_n, sizeof(unsigned int)), "cudaMalloc(top-k count)");
+    cuda_throw(cudaMalloc(&d_out, (size_t)kk * sizeof(TopkEntry)), "cudaMalloc(top-k out)");
+    struct Free {
+        void *p[3];
+        ~Free() {
+            for (void *q : p) cudaFree(q);
+        }
+    } guard{{d_hist, d_n, d_out}};
+    std::vector<unsigned int> h(kTopkBins);
+    static const int widths[6] = {11, 11, 11, 11, 11, 9};
+    uint64_t prefix = 0, needed = kk, tau = 0;
+    bool all_above = false;  // every key >= the selected bin's low edge is in
+    int shift = 64;
+    for (int level = 0; level < 6; ++level) {
+        const int w = widths[level];
+        shift -= w;
+        cuda_throw(cudaMemsetAsync(d_hist, 0, kTopkBins * sizeof(unsigned int), st), "memset hist");
+        for (void *psi : set.bufs) {
+            if (dbl) k_topk_hist<double><<<grid, 256, 0, st>>>(static_cast<const double2 *>(psi), local, prefix, shift, w, d_hist);
+            else k_topk_hist<float><<<grid, 256, 0, st>>>(static_cast<const float2 *>(psi), local, prefix, shift, w, d_hist);
+        }
+        cuda_throw(cudaGetLastError(), "top-k hist launch");
+        if (set.comm)
+            nccl_check(ncclAllReduce(d_hist, d_hist, kTopkBins, ncclUint32, ncclSum, set.comm, st), "ncclAllReduce(hist)");
+        cuda_throw(cudaMemcpyAsync(h.data(), d_hist, kTopkBins * sizeof(unsigned int), cudaMemcpyDeviceToHost, st),
+                   "D2H hist");
+        cuda_throw(cudaStreamSynchronize(st), "top-k sync");
+        uint64_t cum = 0;
+        int sel = 0;
+        for (int b = (1 << w) - 1; b >= 0; --b) {
+            if (cum + h[b] >= needed) {
+                sel = b;
+                break;
+            }
+            cum += h[b];
+        }
+        needed -= cum;
+        prefix = (prefix << w) | (uint64_t)sel;
+        if (h[sel] == needed) {  // the whole bin is in: no ties to break
+            all_above = true;
+            needed = 0;
+            break;
+        }
+    }
+    // keys strictly above tau are all in; `needed` keys equal to tau follow
+    if (all_above) {
+        const uint64_t low_edge = prefix << shift;
+        tau = low_edge == 0 ? 0 : low_edge - 1;
+        if (low_edge == 0) needed = 0;  // every key qualifies: handled by the tie path below
+    } else {
+        tau = prefix;
+    }
+    const bool take_all_zero = all_above && (prefix << shift) == 0;
+    std::vector<TopkEntry> cand;
+    auto gather_rank_lists = [&](std::vector<TopkEntry> &mine) {
+        if (!set.comm) return mine;
+        // fixed-size allgather of kk entries per rank (index ~0 = empty)
+        const size_t per = (size_t)kk * sizeof(TopkEntry);
+        std::vector<TopkEntry> pad(kk, TopkEntry{~0ull, 0.0, 0.0});
+        std::copy(mine.begin(), mine.begin() + std::min<size_t>(mine.size(), kk), pad.begin());
+        char *d = nullptr;
+        cuda_throw(cudaMalloc(&d, per * (set.world + 1)), "cudaMalloc(top-k gather)");
+        cuda_throw(cudaMemcpyAsync(d, pad.data(), per, cudaMemcpyHostToDevice, st), "H2D");
+        nccl_check(ncclAllGather(d, d + per, per, ncclChar, set.comm, st), "ncclAllGather(top-k)");
+        std::vector<TopkEntry> all((size_t)kk * set.world);
+        cuda_throw(cudaMemcpyAsync(all.data(), d + per, per * set.world, cudaMemcpyDeviceToHost, st), "D2H");
+        cuda_throw(cudaStreamSynchronize(st), "gather sync");
+        cudaFree(d);
+        std::vector<TopkEntry> out;
+        for (const TopkEntry &e : all)
+            if (e.index != ~0ull) out.push_back(e);
+        return out;
+    };
+    if (!take_all_zero) {
+        cuda_throw(cudaMemsetAsync(d_n, 0, sizeof(unsigned int), st), "memset count");
+        for (size_t b = 0; b < set.bufs.size(); ++b) {
+            const uint64_t base = (uint64_t)set.ranks[b] * local;
+            if (dbl) k_topk_collect<double><<<grid, 256, 0, st>>>(static_cast<const double2 *>(set.bufs[b]), local, base, tau, d_out, d_n, kk);
+            else k_topk_collect<float><<<grid, 256, 0, st>>>(static_cast<const float2 *>(set.bufs[b]), local, base, tau, d_out, d_n, kk);
+        }
+        cuda_throw(cudaGetLastError(), "top-k collect launch");
+        unsigned int n_out = 0;
+        cuda_throw(cudaMemcpyAsync(&n_out, d_n, sizeof(n_out), cudaMemcpyDeviceToHost, st), "D2H count");
+        cuda_throw(cudaStreamSynchronize(st), "top-k sync");
+        std::vector<TopkEntry> mine(std::min<unsigned int>(n_out, kk));
+        if (!mine.empty())
+            cuda_throw(cudaMemcpy(mine.data(), d_out, mine.size() * sizeof(TopkEntry), cudaMemcpyDeviceToHost), "D2H");
+        cand = gather_rank_lists(mine);
+    } else {
+        needed = kk;  // all keys are 0: the first kk indices
+        tau = 0;
+    }
+    if (needed > 0) {  // ties at tau, by ascending global index
+        constexpr uint64_t chunk = 1ull << 16;
+        const uint64_t nchunks = (local + chunk - 1) / chunk;
+        unsigned int *d_cnt = nullptr;
+        cuda_throw(cudaMalloc(&d_cnt, nchunks * sizeof(unsigned int)), "cudaMalloc(tie counts)");
+        std::vector<TopkEntry> ties;
+        std::vector<unsigned int> cnt(nchunks);
+        std::vector<char> host((size_t)chunk * S);
+        for (size_t b = 0; b < set.bufs.size() && ties.size() < needed; ++b) {
+            if (dbl) k_topk_tie_counts<double><<<(unsigned)nchunks, 256, 0, st>>>(static_cast<const double2 *>(set.bufs[b]), local, chunk, tau, d_cnt);
+            else k_topk_tie_counts<float><<<(unsigned)nchunks, 256, 0, st>>>(static_cast<const float2 *>(set.bufs[b]), local, chunk, tau, d_cnt);
+            cuda_throw(cudaGetLastError(), "tie count launch");
+            cuda_throw(cudaMemcpyAsync(cnt.data(), d_cnt, nchunks * sizeof(unsigned int), cudaMemcpyDeviceToHost, st), "D2H");
+            cuda_throw(cudaStreamSynchronize(st), "tie sync");
+            const uint64_t base = (uint64_t)set.ranks[b] * local;
+            for (uint64_t c = 0; c < nchunks && ties.size() < needed; ++c) {
+                if (!cnt[c]) continue;
+                const uint64_t len = std::min(chunk, local - c * chunk);
+                cuda_throw(cudaMemcpy(host.data(), static_cast<char *>(set.bufs[b]) + c * chunk * S, len * S,
+                                      cudaMemcpyDeviceToHost), "D2H tie chunk");
+                for (uint64_t j = 0; j < len && ties.size() < needed; ++j) {
+                    double re, im;
+                    if (dbl) {
+                        re = reinterpret_cast<const double *>(host.data())[2 * j];
+                        im = reinterpret_cast<const double *>(host.data())[2 * j + 1];
+                    } else {
+                        re = reinterpret_cast<const float *>(host.data())[2 * j];
+                        im = reinterpret_cast<const float *>(host.data())[2 * j + 1];
+                    }
+                    const double p = re * re + im * im;
+                    uint64_t key;
+                    std::memcpy(&key, &p, sizeof(key));
+                    if (key == tau) ties.push_back(TopkEntry{base + c * chunk + j, re, im});
                 }
             }
         }
+        cudaFree(d_cnt);
+        // sharded: every rank offers its first ties; the lowest indices win below
+        std::vector<TopkEntry> all_ties = gather_rank_lists(ties);
+        cand.insert(cand.end(), all_ties.begin(), all_ties.end());
     }
-    std::vector<Entry> all;
-    while (!heap.empty()) {
-        all.push_back(heap.top());
-        heap.pop();
-    }
-    if (set.comm) {
-        // Gather every rank's k candidates (padded) and re-select.
-        std::vector<double> mine(4 * (size_t)k, 0.0);
-        for (size_t j = 0; j < all.size(); ++j) {
-            mine[4 * j] = all[j].p;
-            std::memcpy(&mine[4 * j + 1], &all[j].i, sizeof(uint64_t));
-            mine[4 * j + 2] = all[j].re;
-            mine[4 * j + 3] = all[j].im;
-        }
-        for (size_t j = all.size(); j < k; ++j) mine[4 * j] = -1.0;
-        double *d = nullptr;
-        const size_t per = 4 * (size_t)k;
-        cuda_throw(cudaMalloc(&d, per * (set.world + 1) * sizeof(double)), "cudaMalloc(top-k gather)");
-        cuda_throw(cudaMemcpyAsync(d, mine.data(), per * sizeof(double), cudaMemcpyHostToDevice, st), "H2D");
-        nccl_check(ncclAllGather(d, d + per, per, ncclDouble, set.comm, st), "ncclAllGather");
-        std::vector<double> gathered(per * set.world);
-        cuda_throw(cudaMemcpyAsync(gathered.data(), d + per, gathered.size() * sizeof(double),
-                                   cudaMemcpyDeviceToHost, st),
-                   "D2H");
-        cuda_throw(cudaStreamSynchronize(st), "top-k gather sync");
-        cudaFree(d);
-        all.clear();
-        for (size_t j = 0; j < (size_t)k * set.world; ++j) {
-            if (gathered[4 * j] < 0) continue;
-            Entry e;
-            e.p = gathered[4 * j];
-            std::memcpy(&e.i, &gathered[4 * j + 1], sizeof(uint64_t));
-            e.re = gathered[4 * j + 2];
-            e.im = gathered[4 * j + 3];
-            all.push_back(e);
-        }
-    }
-    std::sort(all.begin(), all.end(), better);
+    auto prob = [](const TopkEntry &e) { return e.re * e.re + e.im * e.im; };
+    std::sort(cand.begin(), cand.end(), [&](const TopkEntry &a, const TopkEntry &b) {
+        const double pa = prob(a), pb = prob(b);
+        return pa != pb ? pa > pb : a.index < b.index;
+    });
     for (uint32_t j = 0; j < k; ++j) {
-        if (j < all.size()) {
-            index_out[j] = all[j].i;
-            amps_out[2 * j] = all[j].re;
-            amps_out[2 * j + 1] = all[j].im;
+        if (j < cand.size() && j < kk) {
+            index_out[j] = cand[j].index;
+            amps_out[2 * j] = cand[j].re;
+            amps_out[2 * j + 1] = cand[j].im;
         } else {
             index_out[j] = ~0ull;
             amps_out[2 * j] = amps_out[2 * j + 1] = 0.0;
         }
     }
 }
-
 }  // namespace qvg
