@@ -325,7 +325,7 @@ static int create_impl(uint32_t n, uint32_t precision, int device, uint32_t rank
             set_device(s);
             cuda_check(cudaDeviceGetAttribute(&s->sm_count, cudaDevAttrMultiProcessorCount, device), "sm count");
             cuda_check(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking), "cudaStreamCreate");
-            cuda_check(cudaMalloc(&s->d_partials, kNormBlocks * sizeof(double)), "cudaMalloc(partials)");
+            cuda_check(cudaMalloc(&s->d_partials, 2 * kNormBlocks * sizeof(double)), "cudaMalloc(partials)");
             s->shards.init(*s, n, s->L, rank, world, nccl_id, virtual_shards);
             shard_init_basis(*s, s->shards, 0);
             cuda_check(cudaStreamSynchronize(s->stream), "init sync");
