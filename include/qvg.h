@@ -131,6 +131,18 @@ int qvg_read(qvg_state *s, void *host, uint64_t offset, uint64_t count);
 int qvg_load_async(qvg_state *s, const void *host, uint64_t offset, uint64_t count);
 int qvg_read_async(qvg_state *s, void *host, uint64_t offset, uint64_t count);
 
+/* Out-of-core apply (the paper's sliding window over a block
+ * store, lifted to host memory -> HBM): the state is 2^n amplitudes in HOST
+ * memory (page-locked for full PCIe bandwidth), the device holds two windows
+ * of 2^window_qubits amplitudes. Each segment of the circuit whose
+ * non-diagonal targets fit one window streams the whole state host -> HBM ->
+ * host once, chunk by chunk, with the fused planner inside each chunk. Results
+ * are bit-identical to qvg_apply on a device-resident state. stats_out (may
+ * be NULL): passes/bytes of the device work; exchanges = segments,
+ * exchange_bytes = PCIe bytes. */
+int qvg_apply_host(void *host_state, uint32_t n_qubits, uint32_t precision, int device,
+                   uint32_t window_qubits, const qvg_gate *ops, uint64_t count, qvg_stats *stats_out);
+
 /* Page-locked host memory for the async copies (cudaHostAlloc / cudaFreeHost). */
 int qvg_host_alloc(uint64_t bytes, void **out);
 int qvg_host_free(void *ptr);

@@ -49,6 +49,7 @@ from ._core import (  # noqa: E402
     ValidationError,
     top_amplitudes,
     apply_circuit,
+    apply_circuit_host,
     circuit_from_gates,
     grid_circuit,
     haar_sweep_circuit,

@@ -307,6 +307,34 @@ PYBIND11_MODULE(_core, m) {
           py::arg("store"), py::arg("circuit"), py::arg("strategy") = "gpu", py::arg("fuse") = true,
           py::arg("device") = 0, "File-backed apply: store -> HBM -> circuit on the GPU -> store");
 
+    m.def("apply_circuit_host",
+          [](py::buffer amps, const Circuit &circuit, std::uint32_t window_qubits, int device) {
+              const py::buffer_info b = amps.request(true);
+              const std::size_t bytes = (std::size_t)(b.size * b.itemsize);
+              std::uint32_t precision = 0;
+              if (b.format == py::format_descriptor<std::complex<double>>::format()) precision = 128;
+              else if (b.format == py::format_descriptor<std::complex<float>>::format()) precision = 64;
+              else throw ValidationError("amplitudes must be complex128 or complex64");
+              const std::size_t count = bytes / (precision / 8);
+              std::uint32_t n = 0;
+              while ((std::size_t{1} << n) < count) ++n;
+              if ((std::size_t{1} << n) != count) throw ValidationError("amplitude count is not a power of two");
+              if (n != circuit.n_qubits) throw ValidationError("circuit qubit count does not match the state");
+              const std::vector<qvg_gate> gates = to_gates(circuit);
+              qvg_stats st{};
+              {
+                  py::gil_scoped_release nogil;
+                  check_status(qvg_apply_host(b.ptr, n, precision, device, window_qubits, gates.data(), gates.size(),
+                                              &st));
+              }
+              py::dict d = stats_dict(st);
+              d["segments"] = st.exchanges;
+              d["host_bytes"] = st.exchange_bytes;
+              return d;
+          },
+          py::arg("amps"), py::arg("circuit"), py::arg("window_qubits"), py::arg("device") = 0,
+          "Out-of-core apply: host-resident state streamed through a 2^window_qubits HBM window");
+
     m.def("top_amplitudes", [](const StateStore &store, std::size_t k) { return top_amplitudes(store, k); },
           py::arg("store"), py::arg("k") = 8, "(index, amplitude) pairs, largest magnitude first");
     m.def("top_amplitudes", [](const StateVector &state, std::size_t k) {

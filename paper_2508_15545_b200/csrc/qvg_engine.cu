@@ -18,6 +18,7 @@
 
 #include "qvg.h"
 #include "qvg_kernels.cuh"
+#include "qvg_ooc.hpp"
 #include "qvg_plan.hpp"
 #include "qvg_shard.hpp"
 
@@ -716,6 +717,72 @@ int qvg_device_buffer(const qvg_state *s, void **ptr_out, uint64_t *bytes_out) {
         if (ptr_out) *ptr_out = bufs.empty() ? nullptr : bufs[0];
         if (bytes_out) *bytes_out = (uint64_t)s->S << s->L;
     });
+}
+
+int qvg_apply_host(void *host, uint32_t n, uint32_t precision, int device, uint32_t window_qubits,
+                   const qvg_gate *ops, uint64_t count, qvg_stats *stats_out) {
+    qvg_state *win[2] = {nullptr, nullptr};
+    const int rc = guarded([&] {
+        if (!host) throw Validation("null host state");
+        if (precision != QVG_C64 && precision != QVG_C128) throw Validation("precision must be 64 or 128");
+        if (n < 1 || n > 48) throw Validation("n_qubits must be in [1, 48]");
+        if (count && !ops) throw Validation("null op array");
+        for (uint64_t i = 0; i < count; ++i) validate_op(ops[i], n, i);
+        const uint32_t w = std::min(window_qubits, n);
+        if (w < 4) throw Validation("window_qubits must be >= 4");
+        // two windows on their own streams: chunk k+1's H2D and gates overlap chunk k's D2H
+        for (auto &ws : win) {
+            const int r = create_impl(w, precision, device, 0, 1, nullptr, false, &ws);
+            if (r != QVG_OK) throw CudaFail(r, g_last_error);
+        }
+        const uint64_t S = precision == QVG_C128 ? 16 : 8;
+        char *h = static_cast<char *>(host);
+        const std::vector<OocSegment> segs = plan_ooc(n, w, ops, count);
+        std::vector<qvg_gate> local;
+        uint64_t host_bytes = 0;
+        for (const OocSegment &sg : segs) {
+            const uint64_t nchunks = 1ull << (n - w);
+            const uint64_t piece = 1ull << sg.lowc;
+            const uint64_t npieces = 1ull << sg.hiq.size();
+            std::vector<uint64_t> offhi(npieces, 0);
+            for (uint64_t m = 0; m < npieces; ++m)
+                for (size_t b = 0; b < sg.hiq.size(); ++b)
+                    if ((m >> b) & 1) offhi[m] |= 1ull << sg.hiq[b];
+            for (uint64_t c = 0; c < nchunks; ++c) {
+                qvg_state &W = *win[c & 1];
+                char *buf = static_cast<char *>(W.shards.bufs[0]);
+                const uint64_t base_off = pdep_host(c, sg.outmask);
+                for (uint64_t m = 0; m < npieces; ++m)
+                    cuda_check(cudaMemcpyAsync(buf + m * piece * S, h + (base_off + offhi[m]) * S, piece * S,
+                                               cudaMemcpyHostToDevice, W.stream),
+                               "out-of-core H2D");
+                chunk_ops(sg, ops, base_off, local);
+                run_local(W, buf, local.data(), local.size());
+                for (uint64_t m = 0; m < npieces; ++m)
+                    cuda_check(cudaMemcpyAsync(h + (base_off + offhi[m]) * S, buf + m * piece * S, piece * S,
+                                               cudaMemcpyDeviceToHost, W.stream),
+                               "out-of-core D2H");
+                host_bytes += 2 * (piece * npieces) * S;
+            }
+            // the next segment regroups the qubits: every chunk must be home first
+            for (auto *ws : win) cuda_check(cudaStreamSynchronize(ws->stream), "out-of-core sync");
+        }
+        if (stats_out) {
+            *stats_out = qvg_stats{};
+            for (auto *ws : win) {
+                stats_out->passes += ws->stats.passes;
+                stats_out->fused_passes += ws->stats.fused_passes;
+                stats_out->kernel_launches += ws->stats.kernel_launches;
+                stats_out->bytes_moved += ws->stats.bytes_moved;
+            }
+            stats_out->gates_applied = count;
+            stats_out->exchanges = segs.size();      // host round trips of the whole state
+            stats_out->exchange_bytes = host_bytes;  // PCIe bytes, both directions
+        }
+    });
+    for (auto *ws : win)
+        if (ws) qvg_destroy(ws);
+    return rc;
 }
 
 int qvg_plan_passes(uint32_t n_qubits, uint32_t precision, int fuse, uint32_t tile_qubits, uint32_t carriers,

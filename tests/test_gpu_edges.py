@@ -112,3 +112,24 @@ def test_nonfinite_matrix_rejected(qv):
     g[0]["u"][0] = np.nan
     with pytest.raises(qv.ValidationError, match="finite"):
         st.apply_gates(g.tobytes())
+
+
+@pytest.mark.parametrize("prec", [128, 64])
+def test_out_of_core_bit_identical(qv, oracle, prec):
+    """qvg_apply_host: state in host memory, 2^w-amplitude HBM windows; the
+    result equals the device-resident run bit for bit (c128 also equals the
+    oracle), for circuits whose gates hit every qubit."""
+    cdt = np.complex128 if prec == 128 else np.complex64
+    for c, w in [(qv.u3_ladder_circuit(18, 3, 5), 12), (qv.random_circuit(16, 400, 8), 8),
+                 (qv.grid_circuit(4, 5, 6, 2), 14), (qv.qft_circuit(17, 3)[0], 10)]:
+        n = c.n_qubits
+        dev = qv.StateVector.create(n, prec, 0)
+        qv.apply_circuit(dev, c)
+        want = dev.read_state().astype(cdt)
+        host = np.zeros(1 << n, cdt)
+        host[0] = 1
+        st = qv.apply_circuit_host(host, c, w)
+        assert st["segments"] >= 2 and st["host_bytes"] == st["segments"] * 2 * host.nbytes
+        assert np.array_equal(host, want), (n, w)
+        if prec == 128:
+            assert np.array_equal(host, oracle.simulate(n, gate_array(c)))
