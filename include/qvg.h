@@ -143,6 +143,19 @@ int qvg_read_async(qvg_state *s, void *host, uint64_t offset, uint64_t count);
 int qvg_apply_host(void *host_state, uint32_t n_qubits, uint32_t precision, int device,
                    uint32_t window_qubits, const qvg_gate *ops, uint64_t count, qvg_stats *stats_out);
 
+/* Out-of-core apply with caller I/O: the state lives wherever `io` reads and
+ * writes it (e.g. a QVSV file via pread/pwrite, the paper's disk tier).
+ * io(user, offset, count, buf, write) moves `count` amplitudes at amplitude
+ * offset `offset` between the store and `buf` (write = 0: store -> buf) and
+ * returns 0 on success. Same segment planning and results as qvg_apply_host;
+ * two pinned staging buffers of 2^window_qubits amplitudes let the file I/O of
+ * one chunk overlap the device work on another. */
+typedef int (*qvg_io_fn)(void *user, uint64_t offset, uint64_t count, void *buf, int write);
+int qvg_apply_stream(qvg_io_fn io, void *user, uint32_t n_qubits, uint32_t precision, int device,
+                     uint32_t window_qubits, const qvg_gate *ops, uint64_t count, qvg_stats *stats_out);
+/* Free / total device memory (cudaMemGetInfo), to size windows or pick a path. */
+int qvg_device_memory(int device, uint64_t *free_bytes, uint64_t *total_bytes);
+
 /* Page-locked host memory for the async copies (cudaHostAlloc / cudaFreeHost). */
 int qvg_host_alloc(uint64_t bytes, void **out);
 int qvg_host_free(void *ptr);

@@ -288,12 +288,14 @@ PYBIND11_MODULE(_core, m) {
         .def("sync", &StateStore::sync);
 
     m.def("apply_circuit",
-          [](StateStore &store, const Circuit &circuit, const std::string &strategy, bool fuse, int device) {
+          [](StateStore &store, const Circuit &circuit, const std::string &strategy, bool fuse, int device,
+             std::uint32_t window_qubits) {
               const auto s = parse_strategy(strategy);
               if (!s) throw ValidationError("unknown strategy '" + strategy + "'");
               RunConfig cfg;
               cfg.strategy = *s;
               cfg.fuse = fuse;
+              cfg.window_qubits = window_qubits;
               Metrics metrics;
               {
                   py::gil_scoped_release nogil;
@@ -305,7 +307,9 @@ PYBIND11_MODULE(_core, m) {
               return d;
           },
           py::arg("store"), py::arg("circuit"), py::arg("strategy") = "gpu", py::arg("fuse") = true,
-          py::arg("device") = 0, "File-backed apply: store -> HBM -> circuit on the GPU -> store");
+          py::arg("device") = 0, py::arg("window_qubits") = 0,
+          "File-backed apply: store -> HBM -> circuit on the GPU -> store; window_qubits > 0 (or a state larger "
+          "than device memory) streams the file through two HBM windows instead");
 
     m.def("apply_circuit_host",
           [](py::buffer amps, const Circuit &circuit, std::uint32_t window_qubits, int device) {

@@ -142,6 +142,10 @@ struct RunConfig {
     bool fuse = true;               // fused tile passes (QVG_OPT_FUSE)
     std::uint32_t tile_qubits = 0;  // 0: engine default
     bool sync = true;               // wait for the device before returning
+    // StateStore path: 0 = the whole state in HBM when it fits, else stream
+    // the file through two HBM windows (out-of-core); > 0 forces streaming
+    // with windows of 2^window_qubits amplitudes.
+    std::uint32_t window_qubits = 0;
 };
 
 struct Metrics {

@@ -216,6 +216,44 @@ void apply_circuit(StateStore &store, const Circuit &circuit, const RunConfig &c
         throw ValidationError("invalid circuit: op " + std::to_string(v.front().op_index) + ": " + v.front().message);
     const double before = metrics.wall_ms;
     const auto t0 = std::chrono::steady_clock::now();
+    // Out-of-core when asked, or when the state does not fit next to the
+    // workspace: two HBM windows of the largest power of two that fits 40% of
+    // free memory each (the paper's disk tier on the GPU).
+    std::uint32_t w = config.window_qubits;
+    if (w == 0) {
+        std::uint64_t free_b = 0, total_b = 0;
+        check_status(qvg_device_memory(device, &free_b, &total_b));
+        if ((16ull << store.n_qubits()) > free_b * 9 / 10) {
+            w = 4;
+            while ((16ull << (w + 1)) <= free_b * 4 / 10 && w + 1 < store.n_qubits()) ++w;
+        }
+    }
+    if (w > 0) {
+        const std::vector<qvg_gate> gates = to_gates(circuit);
+        auto io = [](void *user, std::uint64_t off, std::uint64_t cnt, void *buf, int write) -> int {
+            auto *st = static_cast<StateStore *>(user);
+            try {
+                if (write) st->write(static_cast<const amp_t *>(buf), off, cnt);
+                else st->read(static_cast<amp_t *>(buf), off, cnt);
+                return 0;
+            } catch (...) {
+                return 1;
+            }
+        };
+        qvg_stats s{};
+        check_status(qvg_apply_stream(io, &store, store.n_qubits(), 128, device, w, gates.data(), gates.size(), &s));
+        metrics.strategy = strategy_tag(config.strategy);
+        metrics.gates_applied += s.gates_applied;
+        metrics.traversals += s.passes;
+        metrics.fused_passes += s.fused_passes;
+        metrics.bytes_moved += s.bytes_moved;
+        metrics.bytes_read += s.exchange_bytes / 2;
+        metrics.bytes_written += s.exchange_bytes / 2;
+        metrics.exchanges += s.exchanges;  // whole-state round trips (segments)
+        metrics.wall_ms =
+            before + std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        return;
+    }
     StateVector sv = StateVector::create(store.n_qubits(), 128, device);
     const std::uint64_t total = store.n_amps();
     const std::uint64_t chunk = std::min<std::uint64_t>(total, kChunkAmps);

@@ -14,6 +14,8 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <functional>
+#include <memory>
 #include <vector>
 
 #include "qvg.h"
@@ -719,70 +721,199 @@ int qvg_device_buffer(const qvg_state *s, void **ptr_out, uint64_t *bytes_out) {
     });
 }
 
-int qvg_apply_host(void *host, uint32_t n, uint32_t precision, int device, uint32_t window_qubits,
-                   const qvg_gate *ops, uint64_t count, qvg_stats *stats_out) {
+}  // extern "C"
+
+namespace {
+
+// Where the out-of-core state lives. A chunk is npieces pieces of `piece`
+// amplitudes at host offsets base_off + offhi[m]; window slot m holds piece m.
+struct OocIo {
+    virtual ~OocIo() = default;
+    // enqueue (or perform) the host -> window copies of chunk c on window w
+    virtual void fetch(qvg_state &W, int w, char *win, uint64_t base_off, const std::vector<uint64_t> &offhi,
+                       uint64_t piece) = 0;
+    // enqueue the window -> host copies
+    virtual void store(qvg_state &W, int w, const char *win, uint64_t base_off, const std::vector<uint64_t> &offhi,
+                       uint64_t piece) = 0;
+    // all chunks of the segment are home (streams synchronized)
+    virtual void drain() {}
+};
+
+// Host memory: copies go straight between the user's buffer and HBM.
+struct HostMemIo : OocIo {
+    char *h;
+    uint64_t S;
+    HostMemIo(void *host, uint64_t s) : h(static_cast<char *>(host)), S(s) {}
+    void fetch(qvg_state &W, int, char *win, uint64_t base_off, const std::vector<uint64_t> &offhi,
+               uint64_t piece) override {
+        for (size_t m = 0; m < offhi.size(); ++m)
+            cuda_check(cudaMemcpyAsync(win + m * piece * S, h + (base_off + offhi[m]) * S, piece * S,
+                                       cudaMemcpyHostToDevice, W.stream),
+                       "out-of-core H2D");
+    }
+    void store(qvg_state &W, int, const char *win, uint64_t base_off, const std::vector<uint64_t> &offhi,
+               uint64_t piece) override {
+        for (size_t m = 0; m < offhi.size(); ++m)
+            cuda_check(cudaMemcpyAsync(h + (base_off + offhi[m]) * S, win + m * piece * S, piece * S,
+                                       cudaMemcpyDeviceToHost, W.stream),
+                       "out-of-core D2H");
+    }
+};
+
+// Caller I/O (e.g. pread/pwrite on a QVSV file): each window has a pinned
+// staging buffer; the host reads the next chunk and writes back the previous
+// one while the device works on the other window.
+struct CallbackIo : OocIo {
+    qvg_io_fn io;
+    void *user;
+    uint64_t S;
+    void *stage[2] = {nullptr, nullptr};
+    struct Pending {
+        bool live = false;
+        uint64_t base_off = 0, piece = 0;
+        std::vector<uint64_t> offhi;
+    } pending[2];
+    qvg_state *wins[2] = {nullptr, nullptr};
+    CallbackIo(qvg_io_fn f, void *u, uint64_t s, uint64_t window_bytes) : io(f), user(u), S(s) {
+        for (auto &p : stage) cuda_check(cudaHostAlloc(&p, window_bytes, cudaHostAllocPortable), "cudaHostAlloc(staging)");
+    }
+    ~CallbackIo() override {
+        for (auto *p : stage)
+            if (p) cudaFreeHost(p);
+    }
+    void call(uint64_t off, uint64_t cnt, void *buf, int write) {
+        if (io(user, off, cnt, buf, write) != 0)
+            throw CudaFail(QVG_ERR_IO, std::string("state I/O callback failed (") + (write ? "write" : "read") + ")");
+    }
+    void flush(int w) {
+        if (!pending[w].live) return;
+        char *st = static_cast<char *>(stage[w]);
+        for (size_t m = 0; m < pending[w].offhi.size(); ++m)
+            call(pending[w].base_off + pending[w].offhi[m], pending[w].piece, st + m * pending[w].piece * S, 1);
+        pending[w].live = false;
+    }
+    void fetch(qvg_state &W, int w, char *win, uint64_t base_off, const std::vector<uint64_t> &offhi,
+               uint64_t piece) override {
+        wins[w] = &W;
+        cuda_check(cudaStreamSynchronize(W.stream), "out-of-core staging sync");  // staging free again
+        flush(w);
+        char *st = static_cast<char *>(stage[w]);
+        for (size_t m = 0; m < offhi.size(); ++m) call(base_off + offhi[m], piece, st + m * piece * S, 0);
+        cuda_check(cudaMemcpyAsync(win, st, offhi.size() * piece * S, cudaMemcpyHostToDevice, W.stream),
+                   "out-of-core H2D");
+    }
+    void store(qvg_state &W, int w, const char *win, uint64_t base_off, const std::vector<uint64_t> &offhi,
+               uint64_t piece) override {
+        cuda_check(cudaMemcpyAsync(stage[w], win, offhi.size() * piece * S, cudaMemcpyDeviceToHost, W.stream),
+                   "out-of-core D2H");
+        pending[w] = Pending{true, base_off, piece, offhi};
+    }
+    void drain() override {
+        for (int w = 0; w < 2; ++w) flush(w);
+    }
+};
+
+// The out-of-core executor shared by qvg_apply_host and qvg_apply_stream.
+void ooc_run(OocIo &io, uint32_t n, uint32_t precision, uint32_t w, const qvg_gate *ops, uint64_t count,
+             qvg_state *const win[2], qvg_stats *stats_out) {
+    const uint64_t S = precision == QVG_C128 ? 16 : 8;
+    const std::vector<OocSegment> segs = plan_ooc(n, w, ops, count);
+    std::vector<qvg_gate> local;
+    uint64_t host_bytes = 0;
+    for (const OocSegment &sg : segs) {
+        const uint64_t nchunks = 1ull << (n - w);
+        const uint64_t piece = 1ull << sg.lowc;
+        const uint64_t npieces = 1ull << sg.hiq.size();
+        std::vector<uint64_t> offhi(npieces, 0);
+        for (uint64_t m = 0; m < npieces; ++m)
+            for (size_t b = 0; b < sg.hiq.size(); ++b)
+                if ((m >> b) & 1) offhi[m] |= 1ull << sg.hiq[b];
+        for (uint64_t c = 0; c < nchunks; ++c) {
+            const int wi = (int)(c & 1);
+            qvg_state &W = *win[wi];
+            char *buf = static_cast<char *>(W.shards.bufs[0]);
+            const uint64_t base_off = pdep_host(c, sg.outmask);
+            io.fetch(W, wi, buf, base_off, offhi, piece);
+            chunk_ops(sg, ops, base_off, local);
+            run_local(W, buf, local.data(), local.size());
+            io.store(W, wi, buf, base_off, offhi, piece);
+            host_bytes += 2 * (piece * npieces) * S;
+        }
+        // the next segment regroups the qubits: every chunk must be home first
+        for (int i = 0; i < 2; ++i) cuda_check(cudaStreamSynchronize(win[i]->stream), "out-of-core sync");
+        io.drain();
+    }
+    if (stats_out) {
+        *stats_out = qvg_stats{};
+        for (int i = 0; i < 2; ++i) {
+            stats_out->passes += win[i]->stats.passes;
+            stats_out->fused_passes += win[i]->stats.fused_passes;
+            stats_out->kernel_launches += win[i]->stats.kernel_launches;
+            stats_out->bytes_moved += win[i]->stats.bytes_moved;
+        }
+        stats_out->gates_applied = count;
+        stats_out->exchanges = segs.size();      // round trips of the whole state through HBM
+        stats_out->exchange_bytes = host_bytes;  // PCIe bytes, both directions
+    }
+}
+
+int ooc_entry(uint32_t n, uint32_t precision, int device, uint32_t window_qubits, const qvg_gate *ops,
+              uint64_t count, qvg_stats *stats_out, const std::function<std::unique_ptr<OocIo>(uint64_t)> &make_io) {
     qvg_state *win[2] = {nullptr, nullptr};
     const int rc = guarded([&] {
-        if (!host) throw Validation("null host state");
         if (precision != QVG_C64 && precision != QVG_C128) throw Validation("precision must be 64 or 128");
         if (n < 1 || n > 48) throw Validation("n_qubits must be in [1, 48]");
         if (count && !ops) throw Validation("null op array");
         for (uint64_t i = 0; i < count; ++i) validate_op(ops[i], n, i);
         const uint32_t w = std::min(window_qubits, n);
         if (w < 4) throw Validation("window_qubits must be >= 4");
-        // two windows on their own streams: chunk k+1's H2D and gates overlap chunk k's D2H
+        // two windows on their own streams: chunk k+1's copies and gates overlap chunk k's
         for (auto &ws : win) {
             const int r = create_impl(w, precision, device, 0, 1, nullptr, false, &ws);
             if (r != QVG_OK) throw CudaFail(r, g_last_error);
         }
-        const uint64_t S = precision == QVG_C128 ? 16 : 8;
-        char *h = static_cast<char *>(host);
-        const std::vector<OocSegment> segs = plan_ooc(n, w, ops, count);
-        std::vector<qvg_gate> local;
-        uint64_t host_bytes = 0;
-        for (const OocSegment &sg : segs) {
-            const uint64_t nchunks = 1ull << (n - w);
-            const uint64_t piece = 1ull << sg.lowc;
-            const uint64_t npieces = 1ull << sg.hiq.size();
-            std::vector<uint64_t> offhi(npieces, 0);
-            for (uint64_t m = 0; m < npieces; ++m)
-                for (size_t b = 0; b < sg.hiq.size(); ++b)
-                    if ((m >> b) & 1) offhi[m] |= 1ull << sg.hiq[b];
-            for (uint64_t c = 0; c < nchunks; ++c) {
-                qvg_state &W = *win[c & 1];
-                char *buf = static_cast<char *>(W.shards.bufs[0]);
-                const uint64_t base_off = pdep_host(c, sg.outmask);
-                for (uint64_t m = 0; m < npieces; ++m)
-                    cuda_check(cudaMemcpyAsync(buf + m * piece * S, h + (base_off + offhi[m]) * S, piece * S,
-                                               cudaMemcpyHostToDevice, W.stream),
-                               "out-of-core H2D");
-                chunk_ops(sg, ops, base_off, local);
-                run_local(W, buf, local.data(), local.size());
-                for (uint64_t m = 0; m < npieces; ++m)
-                    cuda_check(cudaMemcpyAsync(h + (base_off + offhi[m]) * S, buf + m * piece * S, piece * S,
-                                               cudaMemcpyDeviceToHost, W.stream),
-                               "out-of-core D2H");
-                host_bytes += 2 * (piece * npieces) * S;
-            }
-            // the next segment regroups the qubits: every chunk must be home first
-            for (auto *ws : win) cuda_check(cudaStreamSynchronize(ws->stream), "out-of-core sync");
-        }
-        if (stats_out) {
-            *stats_out = qvg_stats{};
-            for (auto *ws : win) {
-                stats_out->passes += ws->stats.passes;
-                stats_out->fused_passes += ws->stats.fused_passes;
-                stats_out->kernel_launches += ws->stats.kernel_launches;
-                stats_out->bytes_moved += ws->stats.bytes_moved;
-            }
-            stats_out->gates_applied = count;
-            stats_out->exchanges = segs.size();      // host round trips of the whole state
-            stats_out->exchange_bytes = host_bytes;  // PCIe bytes, both directions
-        }
+        const std::unique_ptr<OocIo> io = make_io(((uint64_t)(precision / 8)) << w);
+        ooc_run(*io, n, precision, w, ops, count, win, stats_out);
     });
     for (auto *ws : win)
         if (ws) qvg_destroy(ws);
     return rc;
+}
+
+}  // namespace
+
+extern "C" {
+
+int qvg_apply_host(void *host, uint32_t n, uint32_t precision, int device, uint32_t window_qubits,
+                   const qvg_gate *ops, uint64_t count, qvg_stats *stats_out) {
+    if (!host) {
+        g_last_error = "null host state";
+        return QVG_ERR_VALIDATION;
+    }
+    return ooc_entry(n, precision, device, window_qubits, ops, count, stats_out, [&](uint64_t) {
+        return std::unique_ptr<OocIo>(new HostMemIo(host, precision / 8));
+    });
+}
+
+int qvg_apply_stream(qvg_io_fn io, void *user, uint32_t n, uint32_t precision, int device, uint32_t window_qubits,
+                     const qvg_gate *ops, uint64_t count, qvg_stats *stats_out) {
+    if (!io) {
+        g_last_error = "null I/O callback";
+        return QVG_ERR_VALIDATION;
+    }
+    return ooc_entry(n, precision, device, window_qubits, ops, count, stats_out, [&](uint64_t window_bytes) {
+        return std::unique_ptr<OocIo>(new CallbackIo(io, user, precision / 8, window_bytes));
+    });
+}
+
+int qvg_device_memory(int device, uint64_t *free_bytes, uint64_t *total_bytes) {
+    return guarded([&] {
+        cuda_check(cudaSetDevice(device), "cudaSetDevice");
+        size_t f = 0, t = 0;
+        cuda_check(cudaMemGetInfo(&f, &t), "cudaMemGetInfo");
+        if (free_bytes) *free_bytes = f;
+        if (total_bytes) *total_bytes = t;
+    });
 }
 
 int qvg_plan_passes(uint32_t n_qubits, uint32_t precision, int fuse, uint32_t tile_qubits, uint32_t carriers,
