@@ -74,7 +74,10 @@ enum qvg_option {
     QVG_OPT_SUB_BITS = 7,    /* fused tile: 2^b register amplitudes per thread, b = 3 (default) or 4 */
     QVG_OPT_FMA = 8,         /* 1: fused-tile complex128 arithmetic with DFMA (faster, within 1e-15
                                 relative but NOT bit-identical to the reference); 0: exact (default) */
-    QVG_OPT_TIMING = 9       /* 1: bracket each qvg_apply with CUDA events; qvg_stats.kernel_ms sums them */
+    QVG_OPT_TIMING = 9,      /* 1: bracket each qvg_apply with CUDA events; qvg_stats.kernel_ms sums them */
+    QVG_OPT_EXCHANGE = 10    /* sharded states: 0 copy exchange (NCCL send/recv; virtual: swap kernel),
+                                1 peer-memory exchange kernel, 2 peer exchange fused with the gate that
+                                triggered it, -1 auto (default: 2 for NCCL ranks whose peers map, else 1) */
 };
 
 /* Counters (the reference's Metrics, metrics.hpp:14-30, plus the GPU pass
@@ -89,6 +92,7 @@ typedef struct qvg_stats {
     uint64_t exchanges;      /* pairwise half-shard exchanges */
     double kernel_ms;        /* device time of gate kernels (timed states only) */
     double exchange_ms;
+    uint64_t fused_exchanges; /* exchanges that also applied the gate that caused them (k_xchg) */
 } qvg_stats;
 
 typedef struct qvg_state qvg_state;

@@ -35,6 +35,7 @@ from ._core import (  # noqa: E402
     OPT_SUB_BITS,
     OPT_FMA,
     OPT_TIMING,
+    OPT_EXCHANGE,
     OPT_TILE_QUBITS,
     QVG_ABI_VERSION,
     CapacityError,

@@ -55,6 +55,7 @@ py::dict stats_dict(const qvg_stats &s) {
     d["exchange_bytes"] = s.exchange_bytes;
     d["exchanges"] = s.exchanges;
     d["kernel_ms"] = s.kernel_ms;
+    d["fused_exchanges"] = s.fused_exchanges;
     return d;
 }
 
@@ -391,4 +392,5 @@ PYBIND11_MODULE(_core, m) {
     m.attr("OPT_SUB_BITS") = (int)QVG_OPT_SUB_BITS;
     m.attr("OPT_FMA") = (int)QVG_OPT_FMA;
     m.attr("OPT_TIMING") = (int)QVG_OPT_TIMING;
+    m.attr("OPT_EXCHANGE") = (int)QVG_OPT_EXCHANGE;
 }

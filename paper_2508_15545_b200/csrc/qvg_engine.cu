@@ -97,6 +97,7 @@ struct qvg_state {
     uint32_t sub_bits = 3;     // fused tile: 2^sub register amplitudes per thread (3 measured faster)
     bool fma = false;          // fused tile c128: DFMA arithmetic (not bit-identical to the reference)
     bool timing = false;       // bracket each qvg_apply with CUDA events -> stats.kernel_ms
+    int exchange_mode = -1;    // QVG_OPT_EXCHANGE (-1 auto)
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
     // device scratch
     TileOp *d_ops = nullptr;
@@ -290,6 +291,7 @@ void shard_run_local(qvg_state &s, void *psi, const qvg_gate *ops, uint64_t coun
 cudaStream_t shard_stream(qvg_state &s) { return s.stream; }
 uint32_t shard_amp_bytes(const qvg_state &s) { return s.S; }
 qvg_stats &shard_stats(qvg_state &s) { return s.stats; }
+int shard_exchange_mode(const qvg_state &s) { return s.exchange_mode; }
 }  // namespace qvg
 
 extern "C" {
@@ -417,6 +419,10 @@ int qvg_set_option(qvg_state *s, int key, int64_t value) {
             break;
         case QVG_OPT_FMA: s->fma = value != 0; break;
         case QVG_OPT_TIMING: s->timing = value != 0; break;
+        case QVG_OPT_EXCHANGE:
+            if (value < -1 || value > 2) throw Validation("exchange mode must be -1, 0, 1 or 2");
+            s->exchange_mode = (int)value;
+            break;
         default: throw Validation("unknown option " + std::to_string(key));
         }
     });

@@ -250,6 +250,73 @@ k_swap_halves(typename Cplx<R>::T *__restrict__ p, typename Cplx<R>::T *__restri
     }
 }
 
+// K7: half-shard exchange over peer memory, optionally fused with the gate
+// that triggered it. Shard a has gpos bit 0 and shard b has gpos bit 1. t
+// enumerates local indices x0 whose bit lpos is 0, with x1 = x0 | 2^lpos.
+//
+// After the exchange:
+//   * a holds (a[x0], b[x0]) at (x0, x1);
+//   * b holds (a[x1], b[x1]) at (x0, x1).
+// The gate on the swapped-in qubit (now local bit lpos) pairs exactly those two
+// amplitudes. So each t owns four amplitudes that no other t reads or writes.
+// The t range can therefore be split between the two ranks (each rank streams
+// one half, with half its bytes local and half over NVLink) with no
+// synchronisation inside the kernel.
+//
+// Parameters:
+//   * mode bit 0 / bit 1: apply the gate on a's / b's pairs (each rank's
+//     predicate for a global control);
+//   * cbit: a local control bit (-1 = none); a pair whose cbit is 0 is only
+//     exchanged;
+//   * mode 0: the pure exchange a[x1] <-> b[x0], touching only those halves;
+//   * fence: the shards are on other GPUs; fence the stores system-wide
+//     before the stream-ordered barrier that follows the kernel.
+// The pair arithmetic is the reference formula (madd2), so a fused exchange
+// is bit-identical to exchange-then-gate.
+template <class R, int APT>
+__global__ void __launch_bounds__(256)
+k_xchg(typename Cplx<R>::T *a, typename Cplx<R>::T *b, int lpos, uint64_t t0, int cbit, int mode, int fence,
+       Mat<R> m) {
+    using T = typename Cplx<R>::T;
+    const uint64_t first = t0 + (uint64_t)blockIdx.x * (blockDim.x * APT) + threadIdx.x;
+    const uint64_t lb = 1ull << lpos;
+    uint64_t x0[APT];
+    if (mode == 0) {
+        T u[APT], v[APT];
+#pragma unroll
+        for (int k = 0; k < APT; ++k) {
+            x0[k] = ins0(first + (uint64_t)k * blockDim.x, lpos);
+            u[k] = ld_amp(a + (x0[k] | lb));
+            v[k] = ld_amp(b + x0[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < APT; ++k) {
+            st_amp(a + (x0[k] | lb), v[k]);
+            st_amp(b + x0[k], u[k]);
+        }
+    } else {
+        T a0[APT], a1[APT], b0[APT], b1[APT];
+#pragma unroll
+        for (int k = 0; k < APT; ++k) {
+            x0[k] = ins0(first + (uint64_t)k * blockDim.x, lpos);
+            a0[k] = ld_amp(a + x0[k]);
+            a1[k] = ld_amp(a + (x0[k] | lb));
+            b0[k] = ld_amp(b + x0[k]);
+            b1[k] = ld_amp(b + (x0[k] | lb));
+        }
+#pragma unroll
+        for (int k = 0; k < APT; ++k) {
+            const bool on = cbit < 0 || ((x0[k] >> cbit) & 1ull);
+            const bool ga = on && (mode & 1), gb = on && (mode & 2);
+            st_amp(a + x0[k], ga ? madd2(m.u[0], m.u[1], a0[k], m.u[2], m.u[3], b0[k]) : a0[k]);
+            st_amp(a + (x0[k] | lb), ga ? madd2(m.u[4], m.u[5], a0[k], m.u[6], m.u[7], b0[k]) : b0[k]);
+            st_amp(b + x0[k], gb ? madd2(m.u[0], m.u[1], a1[k], m.u[2], m.u[3], b1[k]) : a1[k]);
+            st_amp(b + (x0[k] | lb), gb ? madd2(m.u[4], m.u[5], a1[k], m.u[6], m.u[7], b1[k]) : b1[k]);
+        }
+    }
+    if (fence) __threadfence_system();
+}
+
 // ---------------------------------------------------------------------------
 // Readout.
 // Per-block partial sums of |a|^2 with a fixed grid, so the result is

@@ -1,14 +1,21 @@
 // qvg_shard.hpp — state sharding over G = 2^g GPUs, executing
 // the host schedule of qvg_schedule.hpp.
 //
-// Two transports behind one executor:
-//   * NCCL (one process per GPU, the deployment mode): a global-target gate
-//     triggers a pairwise half-shard exchange with ncclSend/ncclRecv over
-//     NVLink, chunked through a scratch buffer;
+// Three transports behind one executor:
+//   * peer memory (one process per GPU, the deployment mode on an NVSwitch
+//     box): the shards are mapped into every rank with CUDA IPC, and a
+//     global-target gate runs as ONE kernel (k_xchg) that exchanges the
+//     half-shards and applies the gate in the same pass. Each rank of a pair
+//     streams half of the pairs, half its bytes over NVLink. Stream-ordered
+//     NCCL barriers go before and after the kernel;
+//   * NCCL copy (when peers cannot be mapped): pairwise half-shard exchange
+//     with ncclSend/ncclRecv over NVLink, chunked through a scratch buffer;
 //   * virtual shards (all G shards on this device, one process): the same
-//     schedule with exchanges done as device-side range swaps. This is how the
-//     sharded path is tested bit-for-bit on a single GPU (the profiling guide
-//     forbids emulating ranks as processes that wait on each other).
+//     schedule and the same k_xchg kernel, with the "peer" pointer being
+//     another buffer on this device and one launch per rank role. This is how
+//     the sharded path, including the fused exchange, is tested bit-for-bit on
+//     a single GPU (the profiling guide forbids emulating ranks as processes
+//     that wait on each other).
 // The reference's only "nodes" are threads over one shared file
 // (reference parallel.cpp:55-143); it never exchanges data.
 #pragma once
@@ -38,6 +45,7 @@ void shard_run_local(qvg_state &s, void *psi, const qvg_gate *ops, uint64_t coun
 cudaStream_t shard_stream(qvg_state &s);
 uint32_t shard_amp_bytes(const qvg_state &s);
 qvg_stats &shard_stats(qvg_state &s);
+int shard_exchange_mode(const qvg_state &s);  // QVG_OPT_EXCHANGE value (-1 = auto)
 void cuda_throw(cudaError_t e, const char *what);
 
 inline void nccl_check(ncclResult_t r, const char *what) {
@@ -57,6 +65,8 @@ struct ShardSet {
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t received[2] = {nullptr, nullptr}, copied[2] = {nullptr, nullptr};
     double *d_scalar = nullptr;
+    std::vector<void *> peer;  // NCCL mode: every rank's shard, mapped here via CUDA IPC (own = bufs[0])
+    bool peer_ok = false;
 
     void init(qvg_state &s, uint32_t n_, uint32_t L_, uint32_t rank_, uint32_t world_, const void *nccl_id,
               bool virt) {
@@ -87,10 +97,52 @@ struct ShardSet {
                 cuda_throw(cudaEventCreateWithFlags(&received[b], cudaEventDisableTiming), "cudaEventCreate");
                 cuda_throw(cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming), "cudaEventCreate");
             }
+            open_peers();
         }
     }
 
+    // Map every rank's shard into this process (cudaIpcGetMemHandle, an
+    // ncclAllGather of the handles, cudaIpcOpenMemHandle). All ranks agree on
+    // the outcome (allreduce of a failure count); on failure the NCCL copy
+    // transport is used.
+    void open_peers() {
+        cudaIpcMemHandle_t mine{};
+        double fail = cudaIpcGetMemHandle(&mine, bufs[0]) == cudaSuccess ? 0.0 : 1.0;
+        (void)cudaGetLastError();
+        std::vector<cudaIpcMemHandle_t> all(world);
+        char *d = nullptr;
+        cuda_throw(cudaMalloc(&d, sizeof(cudaIpcMemHandle_t) * (world + 1)), "cudaMalloc(ipc handles)");
+        cuda_throw(cudaMemcpy(d, &mine, sizeof(mine), cudaMemcpyHostToDevice), "H2D ipc handle");
+        nccl_check(ncclAllGather(d, d + sizeof(mine), sizeof(mine), ncclChar, comm, nullptr), "ncclAllGather(ipc)");
+        cuda_throw(cudaMemcpy(all.data(), d + sizeof(mine), sizeof(mine) * world, cudaMemcpyDeviceToHost),
+                   "D2H ipc handles");
+        peer.assign(world, nullptr);
+        peer[rank] = bufs[0];
+        for (uint32_t r = 0; r < world && fail == 0.0; ++r) {
+            if (r == rank) continue;
+            if (cudaIpcOpenMemHandle(&peer[r], all[r], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                (void)cudaGetLastError();
+                peer[r] = nullptr;
+                fail = 1.0;
+            }
+        }
+        cuda_throw(cudaMemcpy(d, &fail, sizeof(fail), cudaMemcpyHostToDevice), "H2D flag");
+        nccl_check(ncclAllReduce(d, d, 1, ncclDouble, ncclSum, comm, nullptr), "ncclAllReduce(ipc ok)");
+        cuda_throw(cudaMemcpy(&fail, d, sizeof(fail), cudaMemcpyDeviceToHost), "D2H flag");
+        cudaFree(d);
+        peer_ok = fail == 0.0;
+        if (!peer_ok) close_peers();
+    }
+
+    void close_peers() {
+        for (uint32_t r = 0; r < peer.size(); ++r)
+            if (peer[r] && r != rank) cudaIpcCloseMemHandle(peer[r]);
+        peer.clear();
+        peer_ok = false;
+    }
+
     void release() {
+        close_peers();
         for (void *p : bufs) cudaFree(p);
         bufs.clear();
         ranks.clear();
@@ -179,36 +231,106 @@ inline void run_local_swap(qvg_state &s, ShardSet &set, uint32_t a, uint32_t b) 
     shard_stats(s).bytes_moved += set.bufs.size() * ((uint64_t)shard_amp_bytes(s) << set.L);
 }
 
+template <class R>
+inline void launch_xchg(cudaStream_t st, void *a, void *b, uint32_t lpos, uint64_t t0, uint64_t nt, int cbit,
+                        int mode, const double *u, int fence) {
+    using T = typename Cplx<R>::T;
+    Mat<R> m;
+    for (int i = 0; i < 8; ++i) m.u[i] = u ? (R)u[i] : R(0);
+    T *pa = static_cast<T *>(a), *pb = static_cast<T *>(b);
+    if (nt >= 1024) {
+        k_xchg<R, 4><<<(unsigned)(nt / 1024), 256, 0, st>>>(pa, pb, (int)lpos, t0, cbit, mode, fence, m);
+    } else {
+        const unsigned bs = (unsigned)std::min<uint64_t>(nt, 256);
+        k_xchg<R, 1><<<(unsigned)(nt / bs), bs, 0, st>>>(pa, pb, (int)lpos, t0, cbit, mode, fence, m);
+    }
+}
+
+// Stream-ordered barrier over all ranks: a one-element allreduce completes on
+// a rank only after every rank's earlier work on its state stream is done.
+inline void stream_barrier(ShardSet &set, cudaStream_t st) {
+    nccl_check(ncclAllReduce(set.d_scalar, set.d_scalar, 1, ncclDouble, ncclSum, set.comm, st), "ncclAllReduce(barrier)");
+}
+
 // Half-shard exchange swapping global physical qubit gpos with local qubit
-// lpos: a rank whose gpos bit is b sends the amplitudes whose local bit lpos is
-// 1-b (2^(L-1-lpos) blocks of 2^lpos contiguous amplitudes) and receives the
-// partner's matching half into the same places.
+// lpos. A rank whose gpos bit is b gives up the amplitudes whose local bit lpos
+// is 1-b (2^(L-1-lpos) blocks of 2^lpos contiguous amplitudes) and receives
+// the partner's matching half into the same places.
 //
-// NCCL transport: each block goes in chunks through two scratch buffers; the
-// send/recv of chunk i+1 (state stream) overlaps the scratch -> shard copy of
-// chunk i (copy stream), ordered by events. A chunk's copy waits for its own
+// `gate` (or null) is the local step that follows the exchange with its target
+// on lpos. The peer and virtual transports apply it inside the exchange kernel
+// when the exchange mode asks for it (returns true: the caller drops the
+// step). The NCCL copy transport never does.
+//
+// NCCL copy transport: each block goes in chunks through two scratch buffers.
+// The send/recv of chunk i+1 (state stream) overlaps the scratch -> shard copy
+// of chunk i (copy stream), ordered by events. A chunk's copy waits for its own
 // send/recv group, so the bytes it overwrites were already sent.
-inline void run_exchange(qvg_state &s, ShardSet &set, uint32_t gpos, uint32_t lpos) {
+inline bool run_exchange(qvg_state &s, ShardSet &set, uint32_t gpos, uint32_t lpos, const ShardStep *gate) {
     cudaStream_t st = shard_stream(s);
     const uint32_t S = shard_amp_bytes(s);
     const uint64_t half = 1ull << (set.L - 1);
     const uint64_t half_bytes = half * S;
     const uint32_t bit = 1u << (gpos - set.L);
+    // -1 auto: peer ranks fuse the gate (NVLink-bound, the local bytes are free);
+    // virtual shards only exchange (the gate usually joins a fused tile pass).
+    int mode = shard_exchange_mode(s);
+    if (mode < 0) mode = set.is_virtual ? 1 : 2;
+    const bool use_kernel = mode >= 1 && (set.is_virtual || set.peer_ok);
+    const bool fuse = use_kernel && mode == 2 && gate != nullptr;
+    int cbit = -1, flags = 0;
+    const double *u = nullptr;
+    auto pred = [&](uint32_t r) { return (r & gate->rank_mask) == gate->rank_value; };
+    if (fuse) {
+        cbit = gate->op.kind == QVG_OP_CONTROLLED ? gate->op.control : -1;
+        u = gate->op.u;
+    }
+    const bool dbl = S == 16;
+    auto xchg = [&](void *a, void *b, uint64_t t0, uint64_t nt, int fl, int fence) {
+        if (dbl) launch_xchg<double>(st, a, b, lpos, t0, nt, cbit, fl, u, fence);
+        else launch_xchg<float>(st, a, b, lpos, t0, nt, cbit, fl, u, fence);
+    };
+    const uint64_t quarter = half / 2;  // each rank of a pair streams half of the 2^(L-1) x0's
+    qvg_stats &stats = shard_stats(s);
     if (set.is_virtual) {
         for (size_t b = 0; b < set.bufs.size(); ++b) {
             const uint32_t r = set.ranks[b];
             if (r & bit) continue;
             const uint32_t partner = r | bit;
-            // r (bit 0) sends its lpos=1 half; partner (bit 1) its lpos=0 half.
-            if (S == 16) launch_swap_halves<double>(st, set.bufs[b], set.bufs[partner], set.L, lpos);
-            else launch_swap_halves<float>(st, set.bufs[b], set.bufs[partner], set.L, lpos);
+            if (!use_kernel) {
+                // r (bit 0) sends its lpos=1 half; partner (bit 1) its lpos=0 half.
+                if (dbl) launch_swap_halves<double>(st, set.bufs[b], set.bufs[partner], set.L, lpos);
+                else launch_swap_halves<float>(st, set.bufs[b], set.bufs[partner], set.L, lpos);
+                continue;
+            }
+            if (fuse) flags = (pred(r) ? 1 : 0) | (pred(partner) ? 2 : 0);
+            // one launch per rank role, exactly as the two ranks would split it
+            xchg(set.bufs[b], set.bufs[partner], 0, quarter, flags, 0);
+            xchg(set.bufs[b], set.bufs[partner], quarter, quarter, flags, 0);
+            stats.kernel_launches += 2;
         }
         cuda_throw(cudaGetLastError(), "exchange launch");
-        shard_stats(s).exchanges += 1;
-        shard_stats(s).exchange_bytes += half_bytes * set.world / 2;
-        return;
+        stats.exchanges += 1;
+        stats.exchange_bytes += half_bytes * set.world / 2;
+        if (fuse) stats.fused_exchanges += 1;
+        return fuse;
     }
-    const int partner = (int)(set.rank ^ bit);
+    const uint32_t partner = set.rank ^ bit;
+    if (use_kernel) {
+        const bool role_b = (set.rank & bit) != 0;
+        void *a = role_b ? set.peer[partner] : set.bufs[0];
+        void *b = role_b ? set.bufs[0] : set.peer[partner];
+        if (fuse) flags = (pred(set.rank & ~bit) ? 1 : 0) | (pred(set.rank | bit) ? 2 : 0);
+        stream_barrier(set, st);  // the partner's earlier passes over its shard are done
+        xchg(a, b, role_b ? quarter : 0, quarter, flags, 1);
+        cuda_throw(cudaGetLastError(), "exchange launch");
+        stream_barrier(set, st);  // both halves are in place before either rank goes on
+        stats.kernel_launches += 1;
+        stats.exchanges += 1;
+        stats.exchange_bytes += half_bytes;
+        if (fuse) stats.fused_exchanges += 1;
+        return fuse;
+    }
     const uint64_t sendbit = (set.rank & bit) ? 0 : 1;  // my half: local bit lpos == sendbit
     const uint64_t block_bytes = (uint64_t)S << lpos;
     const uint64_t nblocks = 1ull << (set.L - 1 - lpos);
@@ -221,8 +343,8 @@ inline void run_exchange(qvg_state &s, ShardSet &set, uint32_t gpos, uint32_t lp
             char *scr = static_cast<char *>(set.scratch) + (i & 1) * set.chunk_bytes;
             if (i >= 2) cuda_throw(cudaStreamWaitEvent(st, set.copied[i & 1], 0), "wait scratch");
             nccl_check(ncclGroupStart(), "ncclGroupStart");
-            nccl_check(ncclSend(blk + off, c, ncclChar, partner, set.comm, st), "ncclSend");
-            nccl_check(ncclRecv(scr, c, ncclChar, partner, set.comm, st), "ncclRecv");
+            nccl_check(ncclSend(blk + off, c, ncclChar, (int)partner, set.comm, st), "ncclSend");
+            nccl_check(ncclRecv(scr, c, ncclChar, (int)partner, set.comm, st), "ncclRecv");
             nccl_check(ncclGroupEnd(), "ncclGroupEnd");
             cuda_throw(cudaEventRecord(set.received[i & 1], st), "record received");
             cuda_throw(cudaStreamWaitEvent(set.copy_stream, set.received[i & 1], 0), "wait received");
@@ -232,13 +354,16 @@ inline void run_exchange(qvg_state &s, ShardSet &set, uint32_t gpos, uint32_t lp
     }
     for (int b = 0; b < 2 && (uint64_t)b < i; ++b)  // later work on the state stream sees every copy
         cuda_throw(cudaStreamWaitEvent(st, set.copied[b], 0), "wait copies");
-    shard_stats(s).exchanges += 1;
-    shard_stats(s).exchange_bytes += half_bytes;
+    stats.exchanges += 1;
+    stats.exchange_bytes += half_bytes;
+    return false;
 }
 
 // Execute a step list: consecutive local steps are batched per shard (each
 // shard keeps the ops whose rank predicate it satisfies) and planned together,
-// so fusion spans everything between two exchanges.
+// so fusion spans everything between two exchanges. The step right after an
+// exchange (the gate that caused it, target on the swapped-in qubit) is offered
+// to the exchange kernel.
 inline void run_steps(qvg_state &s, ShardSet &set, const std::vector<ShardStep> &steps) {
     std::vector<std::vector<qvg_gate>> batch(set.bufs.size());
     auto flush = [&] {
@@ -247,15 +372,22 @@ inline void run_steps(qvg_state &s, ShardSet &set, const std::vector<ShardStep> 
             batch[b].clear();
         }
     };
-    for (const ShardStep &st : steps) {
+    for (size_t i = 0; i < steps.size(); ++i) {
+        const ShardStep &st = steps[i];
         if (st.type == STEP_LOCAL) {
             for (size_t b = 0; b < set.bufs.size(); ++b)
                 if ((set.ranks[b] & st.rank_mask) == st.rank_value) batch[b].push_back(st.op);
             continue;
         }
         flush();
-        if (st.type == STEP_EXCHANGE) run_exchange(s, set, st.gpos, st.lpos);
-        else run_local_swap(s, set, st.lpos, st.lpos2);
+        if (st.type == STEP_EXCHANGE) {
+            const ShardStep *next = i + 1 < steps.size() ? &steps[i + 1] : nullptr;
+            const bool candidate = next && next->type == STEP_LOCAL && next->op.target == st.lpos &&
+                                   !op_is_diag(next->op);
+            if (run_exchange(s, set, st.gpos, st.lpos, candidate ? next : nullptr)) ++i;
+        } else {
+            run_local_swap(s, set, st.lpos, st.lpos2);
+        }
     }
     flush();
 }

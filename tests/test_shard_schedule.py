@@ -200,3 +200,125 @@ def test_gloo_multiprocess_bit_identical(world):
             p.join(120)
             assert p.exitcode == 0
         assert q.get(timeout=10) is True
+
+
+# --- peer-memory transport protocol (k_xchg over CUDA IPC) on CPU ----------------------
+# Each rank's shard is a shared-memory tensor mapped into every process (the
+# CUDA IPC mapping of qvg_shard.hpp's open_peers). An exchange is the k_xchg
+# protocol: barrier, each rank of the pair updates its own half of the x0
+# range in BOTH shards (fused with the gate that triggered the exchange when
+# the next step targets the swapped-in qubit), barrier. Ownership is disjoint,
+# so the real concurrent processes here must reproduce the oracle bit for bit.
+def _pair_gate(oracle, op, lo, hi):
+    """The reference pair formula on vectors (lo[i], hi[i]) via the oracle:
+    pack them as the two halves of a 2m-amplitude state, target its top qubit."""
+    m = lo.size
+    k = int(np.log2(m))
+    z = np.concatenate([lo, hi])
+    g = np.zeros(1, GATE_DTYPE)
+    g["kind"], g["target"], g["control"], g["u"] = 0, k, -1, op["u"]
+    oracle.apply(k + 1, z, g)
+    return z[:m], z[m:]
+
+
+def _xchg_role(oracle, shards, L, lpos, rank_a, rank_b, role, gate):
+    """One rank's share of k_xchg (qvg_kernels.cuh K7)."""
+    x0 = half_indices(L, lpos)
+    quarter = x0.size // 2
+    x0 = x0[role * quarter:(role + 1) * quarter]
+    x1 = x0 | (1 << lpos)
+    a, b = shards[rank_a], shards[rank_b]
+    a0, a1, b0, b1 = a[x0].copy(), a[x1].copy(), b[x0].copy(), b[x1].copy()
+    if gate is None:
+        a[x1], b[x0] = b0, a1
+        return
+    pred = lambda r: (r & int(gate["rank_mask"])) == int(gate["rank_value"])
+    op = gate["op"]
+    on = np.ones(x0.size, bool)
+    if int(op["kind"]) == 1:
+        on = ((x0 >> int(op["control"])) & 1).astype(bool)
+    na0, na1, nb0, nb1 = a0, b0, a1, b1
+    if pred(rank_a):
+        lo, hi = _pair_gate(oracle, op, a0, b0)
+        na0, na1 = np.where(on, lo, a0), np.where(on, hi, b0)
+    if pred(rank_b):
+        lo, hi = _pair_gate(oracle, op, a1, b1)
+        nb0, nb1 = np.where(on, lo, a1), np.where(on, hi, b1)
+    a[x0], a[x1], b[x0], b[x1] = na0, na1, nb0, nb1
+
+
+def _peer_worker(rank, world, port, fn, args, tensors, q):
+    import sys
+
+    import torch.distributed as dist
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    sys.path.insert(0, os.path.join(root, "tests"))
+    import paper_2508_15545_b200 as qv
+    from oracle.oracle import Oracle
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        oracle = Oracle()
+        c = build(qv, fn, args)
+        n = c.n_qubits
+        L = n - int(np.log2(world))
+        shards = [t.numpy().view(np.complex128) for t in tensors]  # every rank's shard, mapped
+        steps = schedule(qv, c, world)
+        fused = 0
+        i = 0
+        while i < len(steps):
+            st = steps[i]
+            if st["type"] == 1:
+                bit = 1 << (int(st["gpos"]) - L)
+                lpos = int(st["lpos"])
+                nxt = steps[i + 1] if i + 1 < len(steps) else None
+                gate = None
+                if (nxt is not None and nxt["type"] == 0 and int(nxt["op"]["target"]) == lpos
+                        and not (nxt["op"]["u"][2] == 0 and nxt["op"]["u"][3] == 0
+                                 and nxt["op"]["u"][4] == 0 and nxt["op"]["u"][5] == 0)):
+                    gate = nxt
+                dist.barrier()  # the partner's earlier work on its shard is done
+                _xchg_role(oracle, shards, L, lpos, rank & ~bit, rank | bit, 1 if rank & bit else 0, gate)
+                dist.barrier()  # both halves written before anyone goes on
+                if gate is not None:
+                    fused += 1
+                    i += 1
+            else:
+                run_local_steps(oracle, L, shards[rank], rank, [st])
+            i += 1
+        dist.barrier()
+        if rank == 0:
+            got = np.concatenate(shards)
+            want = oracle.simulate(n, gate_array(c))
+            q.put((bool(np.array_equal(got, want)), fused))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_gloo_peer_exchange_protocol_bit_identical(world):
+    import torch
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    for fn, args in [("u3_ladder_circuit", (10, 3, 5)), ("random_circuit", (8, 160, 4)),
+                     ("haar_sweep_circuit", (9, 3))]:
+        n = args[0]
+        L = n - int(np.log2(world))
+        tensors = [torch.zeros(2 << L, dtype=torch.float64).share_memory_() for _ in range(world)]
+        tensors[0][0] = 1.0
+        port = _free_port()
+        procs = [ctx.Process(target=_peer_worker, args=(r, world, port, fn, args, tensors, q)) for r in range(world)]
+        for p in procs:
+            p.start()
+        for p in procs:
+            p.join(120)
+            assert p.exitcode == 0
+        ok, fused = q.get(timeout=10)
+        assert ok, (fn, world)
+        assert fused > 0, (fn, world)
