@@ -75,9 +75,10 @@ enum qvg_option {
     QVG_OPT_FMA = 8,         /* 1: fused-tile complex128 arithmetic with DFMA (faster, within 1e-15
                                 relative but NOT bit-identical to the reference); 0: exact (default) */
     QVG_OPT_TIMING = 9,      /* 1: bracket each qvg_apply with CUDA events; qvg_stats.kernel_ms sums them */
-    QVG_OPT_EXCHANGE = 10    /* sharded states: 0 copy exchange (NCCL send/recv; virtual: swap kernel),
+    QVG_OPT_EXCHANGE = 10,   /* sharded states: 0 copy exchange (NCCL send/recv; virtual: swap kernel),
                                 1 peer-memory exchange kernel, 2 peer exchange fused with the gate that
                                 triggered it, -1 auto (default: 2 for NCCL ranks whose peers map, else 1) */
+    QVG_OPT_PREFETCH = 11    /* fused tile: 1 = cp.async prefetch of the CTA's next tile into shared memory */
 };
 
 /* Counters (the reference's Metrics, metrics.hpp:14-30, plus the GPU pass

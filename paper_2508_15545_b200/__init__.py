@@ -36,6 +36,7 @@ from ._core import (  # noqa: E402
     OPT_FMA,
     OPT_TIMING,
     OPT_EXCHANGE,
+    OPT_PREFETCH,
     OPT_TILE_QUBITS,
     QVG_ABI_VERSION,
     CapacityError,

@@ -393,4 +393,5 @@ PYBIND11_MODULE(_core, m) {
     m.attr("OPT_FMA") = (int)QVG_OPT_FMA;
     m.attr("OPT_TIMING") = (int)QVG_OPT_TIMING;
     m.attr("OPT_EXCHANGE") = (int)QVG_OPT_EXCHANGE;
+    m.attr("OPT_PREFETCH") = (int)QVG_OPT_PREFETCH;
 }

@@ -98,6 +98,7 @@ struct qvg_state {
     bool fma = false;          // fused tile c128: DFMA arithmetic (not bit-identical to the reference)
     bool timing = false;       // bracket each qvg_apply with CUDA events -> stats.kernel_ms
     int exchange_mode = -1;    // QVG_OPT_EXCHANGE (-1 auto)
+    bool prefetch = false;     // fused tile: cp.async prefetch of the next tile (QVG_OPT_PREFETCH)
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
     // device scratch
     TileOp *d_ops = nullptr;
@@ -205,15 +206,18 @@ void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *recs) {
     prm.g = g;
     std::memcpy(prm.ops, recs + p.op_begin, sizeof(TileOp) * g.nrec);
     const unsigned threads = 1u << (g.k - g.sub);  // one 2^sub-amplitude subcube per thread
+    const bool pf = s.prefetch && g.sub == 3;
     const size_t smem = (((sizeof(uint64_t) << g.nhi) + 15) & ~size_t(15)) +
-                        (g.ngroups > 1 ? (sizeof(T) << g.k) : 0);
+                        (g.ngroups > 1 ? (sizeof(T) << g.k) : 0) + (pf ? (sizeof(T) << g.k) : 0);
     const bool fma = s.fma && sizeof(R) == 8;  // complex64 always contracts
     const bool small = threads <= 256;
-    auto kern = g.sub == 4 ? (fma ? k_tile<R, 4, true, 256> : k_tile<R, 4, false, 256>)
-                : small    ? (fma ? k_tile<R, 3, true, 256> : k_tile<R, 3, false, 256>)
-                           : (fma ? k_tile<R, 3, true, 512> : k_tile<R, 3, false, 512>);
-    static bool attr_set[2][2][2][2] = {};
-    bool &set = attr_set[sizeof(R) == 8][g.sub == 4][fma][small];
+    auto kern = g.sub == 4 ? (fma ? k_tile<R, 4, true, 256, false> : k_tile<R, 4, false, 256, false>)
+                : pf ? (small ? (fma ? k_tile<R, 3, true, 256, true> : k_tile<R, 3, false, 256, true>)
+                              : (fma ? k_tile<R, 3, true, 512, true> : k_tile<R, 3, false, 512, true>))
+                : small ? (fma ? k_tile<R, 3, true, 256, false> : k_tile<R, 3, false, 256, false>)
+                        : (fma ? k_tile<R, 3, true, 512, false> : k_tile<R, 3, false, 512, false>);
+    static bool attr_set[2][2][2][2][2] = {};
+    bool &set = attr_set[sizeof(R) == 8][g.sub == 4][fma][small][pf];
     if (!set) {
         cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
                    "cudaFuncSetAttribute(k_tile)");
@@ -419,6 +423,7 @@ int qvg_set_option(qvg_state *s, int key, int64_t value) {
             break;
         case QVG_OPT_FMA: s->fma = value != 0; break;
         case QVG_OPT_TIMING: s->timing = value != 0; break;
+        case QVG_OPT_PREFETCH: s->prefetch = value != 0; break;
         case QVG_OPT_EXCHANGE:
             if (value < -1 || value > 2) throw Validation("exchange mode must be -1, 0, 1 or 2");
             s->exchange_mode = (int)value;

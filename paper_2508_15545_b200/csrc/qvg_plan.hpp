@@ -215,20 +215,40 @@ inline Plan make_plan(const qvg_gate *ops, uint64_t count, const PlanOptions &po
             int nb = 0;
             auto close_group = [&] {
                 if (group.empty()) return;
-                for (int b = 0; nb < g.sub && b < g.k; ++b) {  // pad with the lowest unused bits
-                    bool used = false;
-                    for (int x = 0; x < nb; ++x) used |= gbits[x] == b;
-                    if (!used) gbits[nb++] = b;
+                auto used = [&](int b) {
+                    for (int x = 0; x < nb; ++x)
+                        if (gbits[x] == b) return true;
+                    return false;
+                };
+                // Pad the free slots with the tile bits the group's diagonal
+                // ops use most (their multiplies then skip the elements the
+                // bit excludes at compile time), then the lowest unused bits.
+                int freq[64] = {};
+                for (const TileOp &t : group) {
+                    if (t.kind != TILE_DIAG) continue;
+                    if (t.tbit >= 0) freq[t.tbit] += 2;  // a target halves d0 == 1 work
+                    if (t.cbit >= 0) freq[t.cbit] += 1;
                 }
+                while (nb < g.sub) {
+                    int best = -1;
+                    for (int b = 0; b < g.k; ++b)
+                        if (freq[b] > 0 && !used(b) && (best < 0 || freq[b] > freq[best])) best = b;
+                    if (best < 0) break;
+                    gbits[nb++] = best;
+                }
+                for (int b = 0; nb < g.sub && b < g.k; ++b)
+                    if (!used(b)) gbits[nb++] = b;
                 std::sort(gbits, gbits + g.sub);
-                for (TileOp &t : group) {  // slot code 8*J + (K+1): target / control register slots
-                    if (t.kind != TILE_PAIR) continue;
+                for (TileOp &t : group) {
+                    // pair: slot = 8*J + (K+1); diag: slot = 64*(d0 != 1) + 8*(J+1) + (K+1),
+                    // J / K the target / control register slots (-1: not in the group)
                     int J = -1, K = -1;
                     for (int s = 0; s < g.sub; ++s) {
-                        if (gbits[s] == t.tbit) J = s;
+                        if (t.tbit >= 0 && gbits[s] == t.tbit) J = s;
                         if (t.cbit >= 0 && gbits[s] == t.cbit) K = s;
                     }
-                    t.slot = 8 * J + K + 1;
+                    if (t.kind == TILE_PAIR) t.slot = 8 * J + K + 1;
+                    else t.slot = (t.slot ? 0 : 64) + 8 * (J + 1) + K + 1;
                 }
                 TileOp h{};
                 h.kind = TILE_GROUP;
@@ -254,7 +274,7 @@ inline Plan make_plan(const qvg_gate *ops, uint64_t count, const PlanOptions &po
                     t.cbit = local_bit(o.control, g);
                     if (t.cbit < 0) t.greq = 1ull << o.control;
                 }
-                if (t.kind == TILE_DIAG) t.slot = (ops[x].u[0] == 1.0 && ops[x].u[1] == 0.0) ? 1 : 0;
+                if (t.kind == TILE_DIAG) t.slot = (ops[x].u[0] == 1.0 && ops[x].u[1] == 0.0) ? 1 : 0;  // d0 == 1, coded in close_group
                 if (t.kind == TILE_PAIR) {
                     // The target must be a register bit. An in-tile control is
                     // made one too: the control test is then the same for every

@@ -40,7 +40,7 @@ struct __align__(16) TileOp {
     int32_t kind;      // TileOpKind
     int32_t tbit;      // pair/diag: tile-local target bit (-1: diag target outside Q); group: op count
     int32_t cbit;      // tile-local control bit, -1 if none or outside Q
-    int32_t slot;      // pair: index of the target among the group's bits; diag: d0 == 1 exactly
+    int32_t slot;      // dispatch code: pair 8*J+(K+1), diag 64*(d0!=1)+8*(J+1)+(K+1) (J/K: register slots)
     uint64_t greq;     // global bits that must be 1 in the tile base (controls outside Q)
     uint64_t gtgt;     // diag: global target bit outside Q; group: packed bits b0 | b1<<8 | b2<<16 | b3<<24
     double u[8];       // matrix (diag uses u00 = u[0..1], u11 = u[6..7])
@@ -75,9 +75,14 @@ __device__ __forceinline__ uint32_t swz(uint32_t l) { return l ^ ((l >> 3) & 7u)
 // Pair op over the 2^SUB register amplitudes. Target on register slot J, control on slot K (-1: none / decided per tile):
 // both are compile-time, so a controlled op costs exactly its pairs and no
 // per-pair tests run (the instruction mix was 60% non-FP64 before this).
+// The matrix is read here, straight from the record in the parameter bank,
+// so each op loads only what its case uses.
 template <class R, int SUB, int J, int K, bool FMA>
-__device__ __forceinline__ void group_pair(typename Cplx<R>::T (&v)[1 << SUB], const R *u) {
+__device__ __forceinline__ void group_pair(typename Cplx<R>::T (&v)[1 << SUB], const double *uu) {
     if constexpr (J < SUB && K < SUB && J != K) {
+        R u[8];
+#pragma unroll
+        for (int x = 0; x < 8; ++x) u[x] = (R)uu[x];
 #pragma unroll
         for (int r = 0; r < (1 << SUB); ++r) {
             if ((r >> J) & 1) continue;
@@ -91,7 +96,7 @@ __device__ __forceinline__ void group_pair(typename Cplx<R>::T (&v)[1 << SUB], c
 
 // slot code = 8*J + (K+1)
 template <class R, int SUB, bool FMA>
-__device__ __forceinline__ void group_pair_dispatch(int code, typename Cplx<R>::T (&v)[1 << SUB], const R *u) {
+__device__ __forceinline__ void group_pair_dispatch(int code, typename Cplx<R>::T (&v)[1 << SUB], const double *u) {
 #define QVG_GP(J, K) \
     case 8 * (J) + (K) + 1: group_pair<R, SUB, J, K, FMA>(v, u); break;
     switch (code) {
@@ -104,29 +109,83 @@ __device__ __forceinline__ void group_pair_dispatch(int code, typename Cplx<R>::
 #undef QVG_GP
 }
 
-// Mask over the subcube: bit r set when element r has tile-local bit `bit`.
-template <int SUB>
-__device__ __forceinline__ uint32_t sub_mask(int bit, const int (&b)[SUB], uint32_t l0) {
-    constexpr uint32_t full = (1u << (1 << SUB)) - 1u;
-    if (bit < 0) return full;
-    uint32_t m = ((l0 >> bit) & 1u) ? full : 0u;
+// Diagonal op diag(d0, d1) over the register subcube. The target is on slot J
+// (-1: outside the group, then t1 is its value for this thread's whole
+// subcube). The control is on slot K (-1: none, or tested per thread/tile
+// before the call). D0: d0 != 1, so target-0 elements change too. All
+// compile-time, so e.g. a CZ with both bits in the group costs 2 complex
+// multiplies, not 8 predicated ones.
+template <class R, int SUB, int J, int K, bool D0, bool FMA>
+__device__ __forceinline__ void group_diag(typename Cplx<R>::T (&v)[1 << SUB], const double *uu, bool t1) {
+    if constexpr (J < SUB && K < SUB && (J != K || J < 0)) {
+        R u[8];
+        u[6] = (R)uu[6];
+        u[7] = (R)uu[7];
+        if constexpr (D0) {
+            u[0] = (R)uu[0];
+            u[1] = (R)uu[1];
+        } else {
+            u[0] = R(1);
+            u[1] = R(0);
+        }
+        if constexpr (J >= 0) {
 #pragma unroll
-    for (int j = 0; j < SUB; ++j) {
-        if (bit == b[j]) {
-            uint32_t mj = 0;
+            for (int r = 0; r < (1 << SUB); ++r) {
+                if (K >= 0 && !((r >> K) & 1)) continue;
+                if ((r >> J) & 1) v[r] = cmulx<FMA>(u[6], u[7], v[r]);
+                else if (D0) v[r] = cmulx<FMA>(u[0], u[1], v[r]);
+            }
+        } else {
+            if (!t1 && !D0) return;
+            const R dr = t1 ? u[6] : u[0], di = t1 ? u[7] : u[1];
 #pragma unroll
-            for (int r = 0; r < (1 << SUB); ++r) mj |= ((r >> j) & 1) ? (1u << r) : 0u;
-            m = mj;
+            for (int r = 0; r < (1 << SUB); ++r) {
+                if (K >= 0 && !((r >> K) & 1)) continue;
+                v[r] = cmulx<FMA>(dr, di, v[r]);
+            }
         }
     }
-    return m;
 }
+
+// diag code = 64*D0 + 8*(J+1) + (K+1)
+template <class R, int SUB, bool FMA>
+__device__ __forceinline__ void group_diag_dispatch(int code, typename Cplx<R>::T (&v)[1 << SUB], const double *u,
+                                                    bool t1) {
+#define QVG_GD(J, K)                                                                   \
+    case 8 * ((J) + 1) + (K) + 1: group_diag<R, SUB, J, K, false, FMA>(v, u, t1); break; \
+    case 64 + 8 * ((J) + 1) + (K) + 1: group_diag<R, SUB, J, K, true, FMA>(v, u, t1); break;
+    switch (code) {
+        QVG_GD(-1, -1) QVG_GD(-1, 0) QVG_GD(-1, 1) QVG_GD(-1, 2) QVG_GD(-1, 3)
+        QVG_GD(0, -1) QVG_GD(0, 1) QVG_GD(0, 2) QVG_GD(0, 3)
+        QVG_GD(1, -1) QVG_GD(1, 0) QVG_GD(1, 2) QVG_GD(1, 3)
+        QVG_GD(2, -1) QVG_GD(2, 0) QVG_GD(2, 1) QVG_GD(2, 3)
+        QVG_GD(3, -1) QVG_GD(3, 0) QVG_GD(3, 1) QVG_GD(3, 2)
+    default: break;
+    }
+#undef QVG_GD
+}
+
+// cp.async of one amplitude (16 B complex128, 8 B complex64) into shared memory.
+__device__ __forceinline__ void cp_async_amp(double2 *dst, const double2 *src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_amp(float2 *dst, const float2 *src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // MAXT: the largest CTA this instantiation serves (2^(k-SUB) threads). The
 // minimum-blocks hint keeps 4 CTAs/SM (64 registers) at 256 threads: measured
 // faster than 3 CTAs with 80 registers and no spills (C3 1278 vs 1356 ms).
-template <class R, int SUB, bool FMA, int MAXT>
-__global__ void __launch_bounds__(MAXT, (MAXT <= 256 && SUB == 3) ? 4 : 2)
+// PF: the CTA prefetches its next tile into a second shared buffer with
+// cp.async while it computes the current one, so the first group's HBM latency
+// is off the critical path (the top stall without it: a DMUL waiting on the
+// first group's loads, long_scoreboard, profiles/r01_ncu_summary.md).
+template <class R, int SUB, bool FMA, int MAXT, bool PF>
+__global__ void __launch_bounds__(MAXT, (MAXT <= 256 && SUB == 3) ? (PF ? 3 : 4) : 2)
 k_tile(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams prm) {
     using T = typename Cplx<R>::T;
     constexpr int E = 1 << SUB;
@@ -138,6 +197,7 @@ k_tile(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams
     const TileOp *ops = prm.ops;
     uint64_t *offhi = reinterpret_cast<uint64_t *>(smem_raw);
     T *sm = reinterpret_cast<T *>(smem_raw + (((sizeof(uint64_t) << g.nhi) + 15) & ~15ull));
+    T *pf = sm + (g.ngroups > 1 ? (1u << g.k) : 0u);  // PF: the next tile (after the transpose buffer)
     const uint32_t nhi = 1u << g.nhi;
     const uint32_t lowm = (1u << g.lowc) - 1u;
     {  // the high-qubit offset table
@@ -150,12 +210,33 @@ k_tile(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams
         }
     }
     __syncthreads();
-    for (uint64_t tile = blockIdx.x; tile < g.ntiles; tile += gridDim.x) {
-        // base index: the tile number spread over the qubits outside Q
+    // base index of a tile: the tile number spread over the qubits outside Q
+    auto tile_base = [&](uint64_t tile) {
         uint64_t base = tile << g.lowc;
 #pragma unroll
         for (int i = 0; i < 24; ++i)
             if (i < g.nhi) base = ins0(base, g.hiq[i]);
+        return base;
+    };
+    // PF: thread t copies local indices t + j*blockDim (coalesced segments)
+    auto prefetch = [&](uint64_t tile) {
+        const uint64_t b0 = tile_base(tile);
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+            const uint32_t l = threadIdx.x + (uint32_t)j * blockDim.x;
+            cp_async_amp(pf + swz(l), psi + (b0 | offhi[l >> g.lowc] | (l & lowm)));
+        }
+        cp_async_commit();
+    };
+    if constexpr (PF) {
+        if (blockIdx.x < g.ntiles) prefetch(blockIdx.x);
+    }
+    for (uint64_t tile = blockIdx.x; tile < g.ntiles; tile += gridDim.x) {
+        const uint64_t base = tile_base(tile);
+        if constexpr (PF) {
+            cp_async_wait_all();
+            __syncthreads();
+        }
         int rec = 0;
         for (int gi = 0; gi < g.ngroups; ++gi) {
             const int nops = ops[rec].tbit;
@@ -175,7 +256,12 @@ k_tile(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams
                 return l;
             };
             T v[E];
-            if (gi == 0) {
+            if (PF && gi == 0) {
+#pragma unroll
+                for (int r = 0; r < E; ++r) v[r] = pf[swz(lidx(r))];
+                __syncthreads();  // every thread has its subcube: refill the buffer
+                if (tile + gridDim.x < g.ntiles) prefetch(tile + gridDim.x);
+            } else if (gi == 0) {
 #pragma unroll
                 for (int r = 0; r < E; ++r) {
                     const uint32_t lr = lidx(r);
@@ -185,29 +271,18 @@ k_tile(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams
 #pragma unroll
                 for (int r = 0; r < E; ++r) v[r] = sm[swz(lidx(r))];
             }
-            // The next op's record is fetched from shared memory while the
-            // current one computes (its load latency was the top stall).
-            TileOp nxt = ops[rec];
             for (int i = 0; i < nops; ++i) {
-                const TileOp op = nxt;
-                if (i + 1 < nops) nxt = ops[rec + i + 1];
+                const TileOp &op = ops[rec + i];
                 if ((base & op.greq) != op.greq) continue;  // control outside the tile is 0
-                R u[8];
-#pragma unroll
-                for (int x = 0; x < 8; ++x) u[x] = (R)op.u[x];
                 if (op.kind == TILE_PAIR) {
-                    group_pair_dispatch<R, SUB, FMA>(op.slot, v, u);
+                    group_pair_dispatch<R, SUB, FMA>(op.slot, v, op.u);
                 } else {
-                    const uint32_t cm = sub_mask<SUB>(op.cbit, b, l0);
-                    const uint32_t tm = op.tbit >= 0 ? sub_mask<SUB>(op.tbit, b, l0)
-                                                     : ((base & op.gtgt) ? 0xFFFFu : 0u);
-                    // elements that change: control set and (d0 != 1 or target bit set)
-                    const uint32_t sel = cm & (op.slot != 0 ? tm : 0xFFFFu);
-#pragma unroll
-                    for (int r = 0; r < E; ++r) {
-                        if (!((sel >> r) & 1u)) continue;
-                        v[r] = ((tm >> r) & 1u) ? cmulx<FMA>(u[6], u[7], v[r]) : cmulx<FMA>(u[0], u[1], v[r]);
-                    }
+                    // tile bits outside the group are per-thread bits of l0
+                    if ((op.slot & 7) == 0 && op.cbit >= 0 && !((l0 >> op.cbit) & 1u)) continue;
+                    bool t1 = false;
+                    if ((op.slot & 0x38) == 0)
+                        t1 = op.tbit >= 0 ? ((l0 >> op.tbit) & 1u) != 0 : (base & op.gtgt) != 0;
+                    group_diag_dispatch<R, SUB, FMA>(op.slot, v, op.u, t1);
                 }
             }
             rec += nops;

@@ -194,14 +194,18 @@ def test_fma_mode_within_tolerance(qv, oracle):
         assert np.abs(got - want).max() <= 1e-12
 
 
-@pytest.mark.parametrize("sub", [3, 4])
-def test_tile_subcube_variants_bit_exact(qv, oracle, sub):
-    for c in [qv.u3_ladder_circuit(16, 6, 2), qv.grid_circuit(3, 5, 10, 4), qv.qft_circuit(14, 3)[0]]:
+@pytest.mark.parametrize("sub,pf,k", [(3, 0, 11), (4, 0, 11), (3, 1, 11), (3, 1, 12), (3, 1, 9)])
+def test_tile_subcube_variants_bit_exact(qv, oracle, sub, pf, k):
+    """Register subcube 2^3 / 2^4, cp.async next-tile prefetch, tile sizes."""
+    for c in [qv.u3_ladder_circuit(16, 6, 2), qv.grid_circuit(3, 5, 10, 4), qv.qft_circuit(14, 3)[0],
+              qv.random_circuit(15, 500, 12)]:
         n = c.n_qubits
         want = oracle.simulate(n, gate_array(c))
         st = qv.StateVector.create(n, 128, 0)
         st.set_option(qv.OPT_SUB_BITS, sub)
-        m = qv.apply_circuit(st, c)
+        st.set_option(qv.OPT_PREFETCH, pf)
+        st.set_option(qv.OPT_TILE_QUBITS, k)
+        m = qv.apply_circuit(st, c, tile_qubits=k)
         assert m["fused_passes"] > 0
         assert np.array_equal(st.read_state(), want)
 

@@ -17,9 +17,11 @@ import torch  # noqa: E402
 
 import paper_2508_15545_b200 as qv  # noqa: E402
 
-# (name, fuse, sub_bits, fma, tile qubits)
-VARIANTS = [("fused_sub3_k11", 1, 3, 0, 11), ("fused_sub3_k12", 1, 3, 0, 12), ("fused_sub4_k12", 1, 4, 0, 12),
-            ("fused_sub3_k10", 1, 3, 0, 10), ("fused_sub3_k11_fma", 1, 3, 1, 11), ("per_gate", 0, 3, 0, 11)]
+# (name, fuse, sub_bits, fma, tile qubits, prefetch)
+VARIANTS = [("fused_sub3_k11", 1, 3, 0, 11, 0), ("fused_sub3_k12", 1, 3, 0, 12, 0), ("fused_sub4_k12", 1, 4, 0, 12, 0),
+            ("fused_sub3_k10", 1, 3, 0, 10, 0), ("fused_sub3_k11_fma", 1, 3, 1, 11, 0),
+            ("fused_sub3_k11_pf", 1, 3, 0, 11, 1), ("fused_sub3_k10_pf", 1, 3, 0, 10, 1),
+            ("fused_sub3_k12_pf", 1, 3, 0, 12, 1), ("per_gate", 0, 3, 0, 11, 0)]
 
 
 def circuits(n):
@@ -36,7 +38,9 @@ def main():
     ap.add_argument("--n", type=int, default=30)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--precision", type=int, default=128)
+    ap.add_argument("--only", default="", help="comma-separated variant names (default: all)")
     a = ap.parse_args()
+    only = set(filter(None, a.only.split(",")))
     st = qv.StateVector.create(a.n, a.precision, 0)
     stream = torch.cuda.ExternalStream(st.stream())
     out = []
@@ -45,11 +49,14 @@ def main():
             continue
         g = c.gates()
         row = {"circuit": name, "ops": len(c)}
-        for vname, fuse, sub, fma, k in VARIANTS:
+        for vname, fuse, sub, fma, k, pf in VARIANTS:
+            if only and vname not in only:
+                continue
             st.set_option(qv.OPT_TILE_QUBITS, k)
             st.set_option(qv.OPT_FUSE, fuse)
             st.set_option(qv.OPT_SUB_BITS, sub)
             st.set_option(qv.OPT_FMA, fma)
+            st.set_option(qv.OPT_PREFETCH, pf)
             st.apply_gates(g)  # warm-up (and plan)
             st.reset_stats()
             ts = []
@@ -70,6 +77,7 @@ def main():
               file=sys.stderr)
     st.set_option(qv.OPT_SUB_BITS, 3)
     st.set_option(qv.OPT_FMA, 0)
+    st.set_option(qv.OPT_PREFETCH, 0)
     st.set_option(qv.OPT_FUSE, 1)
     st.set_option(qv.OPT_TILE_QUBITS, 11)
     print(json.dumps({"n": a.n, "precision": a.precision, "reps": a.reps, "rows": out}, indent=1))
