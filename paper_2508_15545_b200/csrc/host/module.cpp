@@ -289,10 +289,15 @@ PYBIND11_MODULE(_core, m) {
         .def("sync", &StateStore::sync);
 
     m.def("apply_circuit",
-          [](StateStore &store, const Circuit &circuit, const std::string &strategy, bool fuse, int device,
-             std::uint32_t window_qubits) {
+          [](StateStore &store, const Circuit &circuit, const std::string &strategy, std::uint64_t cache_bytes,
+             std::uint32_t workers, bool fuse, int device, std::uint32_t window_qubits) {
               const auto s = parse_strategy(strategy);
               if (!s) throw ValidationError("unknown strategy '" + strategy + "'");
+              // cache_bytes / workers: the reference's positional signature
+              // (reference bindings/module.cpp:118-139); the GPU strategy sizes
+              // its HBM windows itself and has no host worker pool.
+              if (workers == 0) throw ValidationError("workers must be >= 1");
+              (void)cache_bytes;
               RunConfig cfg;
               cfg.strategy = *s;
               cfg.fuse = fuse;
@@ -307,7 +312,8 @@ PYBIND11_MODULE(_core, m) {
               d["bytes_written"] = metrics.bytes_written;
               return d;
           },
-          py::arg("store"), py::arg("circuit"), py::arg("strategy") = "gpu", py::arg("fuse") = true,
+          py::arg("store"), py::arg("circuit"), py::arg("strategy") = "gpu",
+          py::arg("cache_bytes") = std::uint64_t{64} << 20, py::arg("workers") = 1, py::arg("fuse") = true,
           py::arg("device") = 0, py::arg("window_qubits") = 0,
           "File-backed apply: store -> HBM -> circuit on the GPU -> store; window_qubits > 0 (or a state larger "
           "than device memory) streams the file through two HBM windows instead");

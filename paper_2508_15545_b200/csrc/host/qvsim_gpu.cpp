@@ -255,6 +255,18 @@ Circuit parse_circuit(std::string_view text, std::optional<std::uint32_t> n_over
             declared = n;
             continue;
         }
+        if (m == "swap") {
+            // SWAP(a, b) = CX(a,b) CX(b,a) CX(a,b), the decomposition config 1's
+            // bit reversal uses; it serializes as those three cx lines
+            // (SURVEY §8f row 4).
+            if (tok.size() != 3) throw ParseError(line_no, "'swap' takes <qubit> <qubit>");
+            const std::uint32_t a = qubit_of(tok[1], line_no), b = qubit_of(tok[2], line_no);
+            if (a == b) throw ParseError(line_no, "swap of a qubit with itself (" + std::to_string(a) + ")");
+            ops.emplace_back(controlled_op("cx", a, b), line_no);
+            ops.emplace_back(controlled_op("cx", b, a), line_no);
+            ops.emplace_back(controlled_op("cx", a, b), line_no);
+            continue;
+        }
         if (const std::size_t ca = controlled_arity(m); ca != ~std::size_t{0}) {
             if (tok.size() != 3 + ca)
                 throw ParseError(line_no, "'" + m + "' takes <control> <target>" +

@@ -52,6 +52,22 @@ def test_extended_grammar_round_trips(qv):
     assert qv.parse_circuit(c.to_text()).gates().tobytes() == c.gates().tobytes()
 
 
+def test_swap_instruction_and_config_round_trips(qv):
+    """`swap a b` expands to cx a b / cx b a / cx a b (config 1's bit
+    reversal); every BASELINE config builder round-trips as text bit for bit
+    (SURVEY §8f row 4)."""
+    c = qv.parse_circuit("qubits 5\nswap 1 4\n")
+    assert c.to_text() == "qubits 5\ncx 1 4\ncx 4 1\ncx 1 4\n"
+    with pytest.raises(qv.ParseError, match="itself"):
+        qv.parse_circuit("qubits 3\nswap 2 2\n")
+    with pytest.raises(qv.ParseError, match="line 2"):
+        qv.parse_circuit("qubits 3\nswap 0 7\n")
+    for c in [qv.u3_ladder_circuit(20, 20, 1), qv.qft_circuit(26, 1)[0], qv.haar_sweep_circuit(30, 2508),
+              qv.grid_circuit(5, 6, 24, 1), qv.u3_ladder_circuit(35, 20, 4)]:
+        back = qv.parse_circuit(c.to_text())
+        assert back.gates().tobytes() == c.gates().tobytes()
+
+
 def test_errors_are_typed_with_lines(qv):
     # reference tests/python/test_smoke.py:110-123
     with pytest.raises(qv.QvsimError, match="line 2"):

@@ -133,3 +133,18 @@ def test_store_streamed_through_hbm_windows_matches_resident(qv, tmp_path, n, w)
         init = np.zeros(1 << n, np.complex128)
         init[0] = 1
         assert np.array_equal(o.apply(n, init, ops), got)
+
+
+@pytest.mark.gpu
+def test_reference_positional_signature(qv, tmp_path):
+    """apply_circuit(store, circuit, strategy, cache_bytes, workers) as the
+    reference binding orders it (reference bindings/module.cpp:118-139)."""
+    path = str(tmp_path / "p.qvs")
+    qv.StateStore.create(path, 12, block_amps=64)
+    c = qv.random_circuit(12, 100, 3)
+    m = qv.apply_circuit(qv.StateStore.open(path), c, "gpu", 64 << 20, 4)
+    assert m["gates_applied"] == 100
+    with pytest.raises(qv.ValidationError):
+        qv.apply_circuit(qv.StateStore.open(path), c, "gpu", 64 << 20, 0)
+    with pytest.raises(qv.ValidationError, match="paired-cached"):
+        qv.apply_circuit(qv.StateStore.open(path), c, "paired-cached")
