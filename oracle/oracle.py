@@ -120,6 +120,8 @@ class RefEngine:
         lib.qvr_store_open.argtypes = [ctypes.c_char_p]
         lib.qvr_store_open.restype = _P
         lib.qvr_store_close.argtypes = [_P]
+        lib.qvr_parse.argtypes = [ctypes.c_char_p, ctypes.c_int64, ctypes.c_int, _P, _U64, ctypes.POINTER(_U64),
+                                  ctypes.POINTER(_U32), ctypes.POINTER(_U64), ctypes.c_char_p, _U64]
         self.lib = lib
 
     def _check(self, rc: int):
@@ -131,6 +133,21 @@ class RefEngine:
         buf = ctypes.create_string_buffer(1 << 20)
         self._check(self.lib.qvr_random_circuit(n, depth, seed, _ptr(ops), buf, len(buf)))
         return ops, buf.value.decode()
+
+    def parse(self, text: str, qubits: int | None = None, strict: bool = False):
+        """The reference's parse_circuit: (n_qubits, ops, serialized text), or
+        ("ParseError", line) / ("Error", message) when it throws."""
+        cap = 4096
+        ops = np.zeros(cap, GATE_DTYPE)
+        count, n, line = _U64(0), _U32(0), _U64(0)
+        buf = ctypes.create_string_buffer(1 << 20)
+        rc = self.lib.qvr_parse(text.encode(), -1 if qubits is None else qubits, int(strict), _ptr(ops), cap,
+                                ctypes.byref(count), ctypes.byref(n), ctypes.byref(line), buf, len(buf))
+        if rc == 2:
+            return ("ParseError", line.value)
+        if rc:
+            return ("Error", self.lib.qvr_last_error().decode())
+        return n.value, ops[:count.value].copy(), buf.value.decode()
 
     def simulate_dense(self, n: int, ops: np.ndarray) -> np.ndarray:
         out = np.zeros(1 << n, np.complex128)

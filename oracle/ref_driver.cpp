@@ -12,11 +12,13 @@
 //   apply_circuit         reference engine.cpp:86-157
 //   read_full_state       reference engine.cpp:483-494
 //   BlockStore::norm      reference store.cpp:301-316
+//   parse_circuit         reference circuit_io.cpp:68-202 (differential parser tests)
 #include <cstdint>
 #include <cstring>
 #include <exception>
 #include <filesystem>
 #include <memory>
+#include <optional>
 #include <string>
 #include <algorithm>
 #include <unistd.h>
@@ -112,6 +114,35 @@ int qvr_random_circuit(std::uint32_t n, std::uint32_t depth, std::uint64_t seed,
             text[text_cap - 1] = 0;
         }
     });
+}
+
+// reference parse_circuit(text, n_override, strict): on success the ops, the
+// qubit count and the reference's own serialization; on ParseError returns 2
+// with its line number (reference error.hpp ParseError::line()).
+int qvr_parse(const char *text, std::int64_t n_override, int strict, Gate *out, std::uint64_t cap,
+              std::uint64_t *count, std::uint32_t *n_out, std::uint64_t *err_line, char *ser,
+              std::uint64_t ser_cap) {
+    try {
+        std::optional<std::uint32_t> ov;
+        if (n_override >= 0) ov = static_cast<std::uint32_t>(n_override);
+        const qvsim::Circuit c = qvsim::parse_circuit(text, ov, strict != 0);
+        *count = c.ops.size();
+        *n_out = c.n_qubits;
+        for (std::size_t k = 0; k < c.ops.size() && k < cap; ++k) from_op(c.ops[k], out[k]);
+        if (ser && ser_cap) {
+            const std::string s = qvsim::serialize_circuit(c);
+            std::strncpy(ser, s.c_str(), ser_cap - 1);
+            ser[ser_cap - 1] = 0;
+        }
+        return 0;
+    } catch (const qvsim::ParseError &e) {
+        g_err = e.what();
+        *err_line = e.line();
+        return 2;
+    } catch (const std::exception &e) {
+        g_err = e.what();
+        return 1;
+    }
 }
 
 // Dense oracle from |0..0> (n <= 12).
