@@ -107,6 +107,7 @@ class RefEngine:
     def __init__(self):
         lib = ctypes.CDLL(self.PATH)
         lib.qvr_last_error.restype = ctypes.c_char_p
+        lib.qvr_last_error_kind.restype = ctypes.c_char_p
         lib.qvr_random_circuit.argtypes = [_U32, _U32, _U64, _P, ctypes.c_char_p, _U64]
         lib.qvr_simulate_dense.argtypes = [_U32, _P, _U64, _P]
         lib.qvr_store_create.argtypes = [ctypes.c_char_p, _U32, _U64, _U64]
@@ -165,8 +166,22 @@ class RefEngine:
         st.eng, st.n, st.keep = self, n, True
         st.h = self.lib.qvr_store_open(path.encode())
         if not st.h:
-            raise RuntimeError(self.lib.qvr_last_error().decode())
+            raise RefError(self.lib.qvr_last_error_kind().decode(), self.lib.qvr_last_error().decode())
         return st
+
+    def open_error(self, path: str):
+        """None when the reference opens the file, else its error class name."""
+        h = self.lib.qvr_store_open(path.encode())
+        if h:
+            self.lib.qvr_store_close(h)
+            return None
+        return self.lib.qvr_last_error_kind().decode()
+
+
+class RefError(RuntimeError):
+    def __init__(self, kind: str, msg: str):
+        super().__init__(f"{kind}: {msg}")
+        self.kind = kind
 
 
 def default_scratch() -> str:

@@ -40,6 +40,16 @@ struct Gate {  // layout of qvg_gate (include/qvg.h)
 static_assert(sizeof(Gate) == 80, "qvg_gate layout");
 
 thread_local std::string g_err;
+thread_local std::string g_kind;  // reference error class of the last failure
+
+void note_kind(const std::exception &e) {
+    g_kind = dynamic_cast<const qvsim::FormatError *>(&e)       ? "FormatError"
+             : dynamic_cast<const qvsim::ValidationError *>(&e) ? "ValidationError"
+             : dynamic_cast<const qvsim::ParseError *>(&e)      ? "ParseError"
+             : dynamic_cast<const qvsim::CapacityError *>(&e)   ? "CapacityError"
+             : dynamic_cast<const qvsim::IoError *>(&e)         ? "IoError"
+                                                                 : "Error";
+}
 
 qvsim::GateMatrix to_matrix(const double *u) {
     return {qvsim::amp_t{u[0], u[1]}, qvsim::amp_t{u[2], u[3]},
@@ -88,6 +98,7 @@ template <class F> int guarded(F &&f) {
         return 0;
     } catch (const std::exception &e) {
         g_err = e.what();
+        note_kind(e);
         return 1;
     }
 }
@@ -101,6 +112,7 @@ struct Handle {
 extern "C" {
 
 const char *qvr_last_error() { return g_err.c_str(); }
+const char *qvr_last_error_kind() { return g_kind.c_str(); }
 
 // reference random_circuit(n, depth, seed); ops and the serialized text.
 int qvr_random_circuit(std::uint32_t n, std::uint32_t depth, std::uint64_t seed,

@@ -148,3 +148,43 @@ def test_reference_positional_signature(qv, tmp_path):
         qv.apply_circuit(qv.StateStore.open(path), c, "gpu", 64 << 20, 0)
     with pytest.raises(qv.ValidationError, match="paired-cached"):
         qv.apply_circuit(qv.StateStore.open(path), c, "paired-cached")
+
+
+def _header(magic=b"QVSV", version=1, n=4, block_amps=4, reserved=bytes(12)):
+    return (magic + version.to_bytes(4, "little") + n.to_bytes(4, "little") + block_amps.to_bytes(8, "little")
+            + reserved)
+
+
+FILES = {
+    "good": _header() + bytes(16 * 16),
+    "bad_magic": _header(magic=b"QVSX") + bytes(16 * 16),
+    "version_2": _header(version=2) + bytes(16 * 16),
+    "version_0": _header(version=0) + bytes(16 * 16),
+    "n_zero": _header(n=0) + bytes(16),
+    "n_huge": _header(n=60) + bytes(16),
+    "block_not_pow2": _header(block_amps=3) + bytes(16 * 16),
+    "block_zero": _header(block_amps=0) + bytes(16 * 16),
+    "block_over_state": _header(block_amps=32) + bytes(16 * 16),
+    "truncated_payload": _header() + bytes(16 * 15),
+    "extra_payload": _header() + bytes(16 * 17),
+    "short_header": b"QVSV" + bytes(20),
+    "empty": b"",
+    "reserved_nonzero": _header(reserved=b"\x01" + bytes(11)) + bytes(16 * 16),
+}
+
+
+@needs_ref
+@pytest.mark.parametrize("name", sorted(FILES))
+def test_open_errors_match_reference(qv, tmp_path, name):
+    """StateStore.open accepts exactly the files the reference's
+    BlockStore::open accepts, with the same error class
+    (reference store.cpp:135-149,216-245; tests/test_store.cpp:78-95,142-154)."""
+    p = tmp_path / f"{name}.qvs"
+    p.write_bytes(FILES[name])
+    want = RefEngine().open_error(str(p))
+    try:
+        qv.StateStore.open(str(p))
+        got = None
+    except qv.QvsimError as e:
+        got = type(e).__name__
+    assert got == want, (name, got, want)
