@@ -350,6 +350,45 @@ def e2e_leg(qv, st, circ, recs, line, args):
                            f"{E2E_CHUNKS} chunks, host wall clock"}
 
 
+def e2e_leg_sharded(qv, st, circ, line, args, rank, world, dist):
+    """e2e at N > 1: every rank copies its own 2^L-amplitude shard from pinned
+    host memory, the sweep runs through `apply_circuit(state, circuit)` (API
+    defaults: fused, exchanges over NCCL/NVLink), and every rank reads its
+    shard back (the read restores the canonical qubit order first). One state
+    per rank, steps back to back; the step time is the max over ranks."""
+    import torch
+
+    n = circ.n_qubits
+    L = n - int(math.log2(world))
+    local = 1 << L
+    h = torch.empty(local * 2, dtype=torch.float64, pin_memory=True)
+    buf = h.numpy().view(np.complex128)
+    buf[:] = 1.0 / math.sqrt(1 << n)
+    off = rank * local
+    steps = max(2, args.steps)
+    st.set_option(qv.OPT_FUSE, 1)
+    m = None
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        st.load_async(buf, off)
+        m = qv.apply_circuit(st, circ, sync=False)
+        st.read_async(buf, off)
+        st.sync()
+    ms = (time.perf_counter() - t0) * 1e3 / steps
+    t = torch.tensor([ms], device=f"cuda:{torch.cuda.current_device()}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    st.set_option(qv.OPT_FUSE, 0)
+    line["e2e"] = {"value": len(circ) * (1 << n) / (ms / 1e3), "unit": UNIT, "ms_per_step": ms, "steps": steps,
+                   "h2d_bytes_per_step": (1 << n) * 16, "d2h_bytes_per_step": (1 << n) * 16,
+                   "hbm_passes_per_step": m["traversals"] if m else None,
+                   "path": f"per step on each of {world} ranks: load_async(own pinned shard) -> apply_circuit(state, "
+                           "circuit) [API defaults: gpu, fused, exchanges] -> read_async(own shard); "
+                           "wall clock, max over ranks; bytes are whole-job totals"}
+
+
 def cpu_baseline(args, nops_hint=120):
     """The reference engine (oracle/_ref) on the host cores: a bounded sample of
     the same n=30 sweep (2 gate passes: a Haar U on q=0 and a CX), strategy
@@ -522,6 +561,8 @@ def main():
         fused_leg(qv, st, circ, line, args)
         if not args.no_e2e:
             e2e_leg(qv, st, circ, recs, line, args)
+    elif not args.no_e2e:
+        e2e_leg_sharded(qv, st, circ, line, args, rank, world, dist)
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
             try:
