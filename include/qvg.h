@@ -65,13 +65,14 @@ enum qvg_precision { QVG_C64 = 64, QVG_C128 = 128 };
 /* Option keys for qvg_set_option. */
 enum qvg_option {
     QVG_OPT_FUSE = 1,        /* 1: fused low/strided tile passes (default), 0: one pass per gate */
-    QVG_OPT_TILE_QUBITS = 2, /* qubits per fused tile, 5..12 (default 12) */
+    QVG_OPT_TILE_QUBITS = 2, /* qubits per fused tile, 5..12 (default 11) */
     QVG_OPT_CARRIERS = 3,    /* lowest qubits every tile keeps contiguous (default 3) */
     QVG_OPT_LOW_KERNEL = 4,  /* 1: warp-shuffle kernel for targets < 5, 0: k_pairs (default, measured faster) */
     QVG_OPT_MIN_RUN = 5,     /* bytes: a control/phase bit whose 1-runs are shorter is selected
                                 inside a dense pass instead of enumerated (default 32) */
     QVG_OPT_PRED_STORE = 6,  /* 1: skip stores of unselected amplitudes; 0: write them back (default) */
-    QVG_OPT_SUB_BITS = 7,    /* fused tile: 2^b register amplitudes per thread, b = 3 (default) or 4 */
+    QVG_OPT_SUB_BITS = 7,    /* fused tile: 2^b register amplitudes per thread, b = 3 or 4 (default 3
+                                complex128, 4 complex64) */
     QVG_OPT_FMA = 8,         /* 1: fused-tile complex128 arithmetic with DFMA (faster, within 1e-15
                                 relative but NOT bit-identical to the reference); 0: exact (default) */
     QVG_OPT_TIMING = 9,      /* 1: bracket each qvg_apply with CUDA events; qvg_stats.kernel_ms sums them */

@@ -89,12 +89,12 @@ struct qvg_state {
     int sm_count = 148;
     // options
     bool fuse = true;
-    uint32_t tile_qubits = 12;
+    uint32_t tile_qubits = 11;
     uint32_t carriers = 3;
     bool low_kernel = false;   // k_pairs measured faster for targets < 5 (profiles/r01_kernel_ab.json)
     uint32_t min_run = 32;     // bytes: shortest 1-run of a forced bit that is inserted
     bool pred_store = false;   // select-and-store-all for non-inserted forced bits
-    uint32_t sub_bits = 3;     // fused tile: 2^sub register amplitudes per thread (3 measured faster)
+    uint32_t sub_bits = 3;     // fused tile: 2^sub register amplitudes per thread (c128: 3, c64: 4, measured)
     bool fma = false;          // fused tile c128: DFMA arithmetic (not bit-identical to the reference)
     bool timing = false;       // bracket each qvg_apply with CUDA events -> stats.kernel_ms
     int exchange_mode = -1;    // QVG_OPT_EXCHANGE (-1 auto)
@@ -328,7 +328,10 @@ static int create_impl(uint32_t n, uint32_t precision, int device, uint32_t rank
         s->S = precision == QVG_C128 ? 16 : 8;
         s->rank = rank;
         s->world = world;
-        s->tile_qubits = 11;  // 2^11 amplitudes: 256 threads x 8; measured best (profiles/r01_fused_ab.json)
+        // Measured best tile shapes (profiles/r01_fused_ab.json, r01_fused_ab_c64.json):
+        // 2^11 amplitudes: complex128 as 256 threads x 8, complex64 as 128 threads x 16.
+        s->tile_qubits = 11;
+        s->sub_bits = precision == QVG_C128 ? 3 : 4;
         s->carriers = precision == QVG_C128 ? 3 : 4;
         try {
             set_device(s);
@@ -941,6 +944,7 @@ int qvg_plan_passes(uint32_t n_qubits, uint32_t precision, int fuse, uint32_t ti
         po.fuse = fuse != 0;
         po.tile_qubits = tile_qubits ? std::min<uint32_t>(tile_qubits, 12) : 11;
         po.carriers = carriers;
+        po.sub_bits = precision == QVG_C128 ? 3 : 4;  // the engine's defaults (create_impl)
         const Plan plan = make_plan(ops, count, po);
         uint64_t fused = 0, bytes = 0;
         for (const Pass &p : plan.passes) {
