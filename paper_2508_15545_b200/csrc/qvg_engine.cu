@@ -94,7 +94,7 @@ struct qvg_state {
     bool low_kernel = false;   // k_pairs measured faster for targets < 5 (profiles/r01_kernel_ab.json)
     uint32_t min_run = 32;     // bytes: shortest 1-run of a forced bit that is inserted
     bool pred_store = false;   // select-and-store-all for non-inserted forced bits
-    uint32_t sub_bits = 3;     // fused tile: 2^sub register amplitudes per thread (c128: 3, c64: 4, measured)
+    uint32_t sub_bits = 4;     // fused tile: 2^sub register amplitudes per thread (measured)
     bool fma = false;          // fused tile c128: DFMA arithmetic (not bit-identical to the reference)
     bool timing = false;       // bracket each qvg_apply with CUDA events -> stats.kernel_ms
     int exchange_mode = -1;    // QVG_OPT_EXCHANGE (-1 auto)
@@ -329,9 +329,10 @@ static int create_impl(uint32_t n, uint32_t precision, int device, uint32_t rank
         s->rank = rank;
         s->world = world;
         // Measured best tile shapes (profiles/r01_fused_ab.json, r01_fused_ab_c64.json):
-        // 2^11 amplitudes: complex128 as 256 threads x 8, complex64 as 128 threads x 16.
+        // 2^11 amplitudes as 128 threads x 16 register amplitudes
+        // (C2/C1/C3 4-11% faster than 256 x 8 for complex128, 10-15% for complex64).
         s->tile_qubits = 11;
-        s->sub_bits = precision == QVG_C128 ? 3 : 4;
+        s->sub_bits = 4;
         s->carriers = precision == QVG_C128 ? 3 : 4;
         try {
             set_device(s);
@@ -944,7 +945,7 @@ int qvg_plan_passes(uint32_t n_qubits, uint32_t precision, int fuse, uint32_t ti
         po.fuse = fuse != 0;
         po.tile_qubits = tile_qubits ? std::min<uint32_t>(tile_qubits, 12) : 11;
         po.carriers = carriers;
-        po.sub_bits = precision == QVG_C128 ? 3 : 4;  // the engine's defaults (create_impl)
+        po.sub_bits = 4;  // the engine's default (create_impl)
         const Plan plan = make_plan(ops, count, po);
         uint64_t fused = 0, bytes = 0;
         for (const Pass &p : plan.passes) {

@@ -87,7 +87,7 @@ def test_repeated_apply_reuses_plan_buffers(qv, oracle):
 
 
 @pytest.mark.parametrize("opt,val", [("OPT_TILE_QUBITS", 5), ("OPT_TILE_QUBITS", 12), ("OPT_CARRIERS", 0),
-                                     ("OPT_CARRIERS", 6), ("OPT_SUB_BITS", 4), ("OPT_LOW_KERNEL", 1),
+                                     ("OPT_CARRIERS", 6), ("OPT_SUB_BITS", 3), ("OPT_LOW_KERNEL", 1),
                                      ("OPT_MIN_RUN", 128), ("OPT_PRED_STORE", 1)])
 def test_options_keep_bits(qv, oracle, opt, val):
     c = qv.random_circuit(13, 400, 77)
