@@ -20,10 +20,11 @@
 // same for every tile) travel in the kernel's parameter bank.
 //
 // Measured limits (profiles/r01_fused_ab.json, r01_ncu_summary.md): the kernel
-// is compute/issue-bound, not HBM-bound — ~52% FP64 pipe, 64% issue slots;
-// a bit-exact FP64-instruction reduction for special matrices (real, or with
-// exact 0/2^k components) was tried and did not help (reverted), so the next
-// lever is latency and per-op overhead, not arithmetic.
+// is compute/latency-bound, not HBM-bound. The FP64 pipe is ~53% busy and issue
+// slots 65%. DFMA arithmetic (half the FP64 instructions) gains only 10-13%, and a
+// cp.async next-tile prefetch (fewer CTAs/SM) loses 10-15%. What helped: pair
+// and diagonal ops dispatched at compile time by register slot, per-case
+// record loads, and 16 register amplitudes per thread.
 #pragma once
 
 #include <cuda_runtime.h>
