@@ -37,6 +37,13 @@ py::dict metrics_dict(const Metrics &m, std::uint32_t n) {
     d["workers"] = m.workers;
     d["gates_applied"] = m.gates_applied;
     d["traversals"] = m.traversals;
+    d["blocks_read"] = m.blocks_read;
+    d["blocks_written"] = m.blocks_written;
+    d["bytes_read"] = m.bytes_read;
+    d["bytes_written"] = m.bytes_written;
+    d["cache_hits"] = m.cache_hits;
+    d["cache_misses"] = m.cache_misses;
+    d["peak_cache_bytes"] = m.peak_cache_bytes;
     d["fused_passes"] = m.fused_passes;
     d["bytes_moved"] = m.bytes_moved;
     d["exchange_bytes"] = m.exchange_bytes;

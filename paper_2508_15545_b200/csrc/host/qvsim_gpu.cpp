@@ -4,6 +4,7 @@
 #include "qvsim_gpu.hpp"
 
 #include <algorithm>
+#include <bit>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -680,6 +681,8 @@ void apply_circuit(StateVector &state, const Circuit &circuit, const RunConfig &
                               "' runs on the reference's block-store engine; a device state takes 'gpu'");
     metrics.strategy = strategy_tag(config.strategy);
     metrics.workers = state.world();
+    metrics.peak_cache_bytes = std::max<std::uint64_t>(
+        metrics.peak_cache_bytes, (std::uint64_t)(state.precision() == 128 ? 16 : 8) << (state.n_qubits() - std::countr_zero(state.world())));
     const double before = metrics.wall_ms;
     const auto t0 = std::chrono::steady_clock::now();
     const qvg_stats s0 = state.stats();

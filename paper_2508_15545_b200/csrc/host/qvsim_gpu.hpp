@@ -148,9 +148,19 @@ struct RunConfig {
     std::uint32_t window_qubits = 0;
 };
 
+// The reference's Metrics (reference metrics.hpp:14-30, to_json
+// metrics.cpp:25-41) plus the GPU pass accounting. Store fields count the QVSV
+// file traffic of a StateStore run; cache_* stay 0 (no host window);
+// peak_cache_bytes is the device memory holding the state (or the two
+// streaming windows).
 struct Metrics {
     std::uint64_t bytes_read = 0;     // state-file bytes read (StateStore path)
     std::uint64_t bytes_written = 0;  // state-file bytes written
+    std::uint64_t blocks_read = 0;    // state-file blocks read
+    std::uint64_t blocks_written = 0;
+    std::uint64_t cache_hits = 0;
+    std::uint64_t cache_misses = 0;
+    std::uint64_t peak_cache_bytes = 0;
     std::uint64_t gates_applied = 0;
     std::uint64_t traversals = 0;  // HBM passes (the reference's one traversal per gate)
     std::uint64_t fused_passes = 0;

@@ -250,6 +250,9 @@ void apply_circuit(StateStore &store, const Circuit &circuit, const RunConfig &c
         metrics.bytes_read += s.exchange_bytes / 2;
         metrics.bytes_written += s.exchange_bytes / 2;
         metrics.exchanges += s.exchanges;  // whole-state round trips (segments)
+        metrics.blocks_read += s.exchange_bytes / 2 / (store.block_amps() * 16);
+        metrics.blocks_written += s.exchange_bytes / 2 / (store.block_amps() * 16);
+        metrics.peak_cache_bytes = std::max<std::uint64_t>(metrics.peak_cache_bytes, 2 * (16ull << w));
         metrics.wall_ms =
             before + std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         return;
@@ -288,6 +291,8 @@ void apply_circuit(StateStore &store, const Circuit &circuit, const RunConfig &c
         store.write(static_cast<const amp_t *>(pin.buf[(k + 1) % 2]), pending_off, pending_c);
         metrics.bytes_written += pending_c * 16;
     }
+    metrics.blocks_read += store.n_blocks();
+    metrics.blocks_written += store.n_blocks();
     metrics.wall_ms = before + std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
 

@@ -99,6 +99,12 @@ def test_gpu_strategy_on_store_matches_reference_strategy(qv, tmp_path, n):
     m = qv.apply_circuit(qv.StateStore.open(b), c, strategy="gpu")
     assert m["strategy"] == "gpu" and m["gates_applied"] == len(c)
     assert m["bytes_read"] == m["bytes_written"] == 16 << n
+    # the reference's normative metrics fields (reference metrics.cpp:25-41)
+    for key in ("n_qubits", "strategy", "workers", "gates_applied", "traversals", "blocks_read", "blocks_written",
+                "bytes_read", "bytes_written", "cache_hits", "cache_misses", "peak_cache_bytes", "wall_ms"):
+        assert key in m, key
+    assert m["blocks_read"] == m["blocks_written"] == (1 << n) // min(1024, 1 << n)
+    assert m["peak_cache_bytes"] >= 16 << n
     got = qv.StateStore.open(b).read_state()
     assert np.array_equal(got, want)
     # and the reference can continue on our output
