@@ -78,7 +78,9 @@ enum qvg_option {
     QVG_OPT_EXCHANGE = 10,   /* sharded states: 0 copy exchange (NCCL send/recv; virtual: swap kernel),
                                 1 peer-memory exchange kernel, 2 peer exchange fused with the gate that
                                 triggered it, -1 auto (default: 2 for NCCL ranks whose peers map, else 1) */
-    QVG_OPT_PREFETCH = 11    /* fused tile: 1 = cp.async prefetch of the CTA's next tile into shared memory */
+    QVG_OPT_PREFETCH = 11,   /* fused tile: 1 = cp.async prefetch of the CTA's next tile into shared memory */
+    QVG_OPT_BATCH_EXCHANGE = 12 /* sharded: most global qubits one exchange swaps, 1..4 (default 4; 1 =
+                                   pairwise exchanges only) */
 };
 
 /* Counters (the reference's Metrics, metrics.hpp:14-30, plus the GPU pass
@@ -206,18 +208,21 @@ int qvg_plan_passes(uint32_t n_qubits, uint32_t precision, int fuse,
                     uint64_t *bytes_out);
 /* Schedule of a state sharded over `world` = 2^g ranks, as run
  * by qvg_apply on a sharded state; host-only, usable without a GPU. */
-enum qvg_step_type { QVG_STEP_LOCAL = 0, QVG_STEP_EXCHANGE = 1, QVG_STEP_LOCAL_SWAP = 2 };
+enum qvg_step_type { QVG_STEP_LOCAL = 0, QVG_STEP_EXCHANGE = 1, QVG_STEP_LOCAL_SWAP = 2, QVG_STEP_MULTI_EXCHANGE = 3 };
 typedef struct qvg_shard_step {
     uint32_t type;       /* qvg_step_type */
     uint32_t rank_mask;  /* LOCAL: runs on ranks with (rank & rank_mask) == rank_value */
     uint32_t rank_value;
-    uint32_t gpos;       /* EXCHANGE: global physical qubit (>= L) */
-    uint32_t lpos;       /* EXCHANGE: local qubit swapped with gpos; LOCAL_SWAP: first local qubit */
-    uint32_t lpos2;      /* LOCAL_SWAP: second local qubit */
+    uint32_t gpos;       /* EXCHANGE: global physical qubit (>= L); MULTI_EXCHANGE: the swapped global
+                            qubits as a rank-bit mask (bit j = physical qubit L + j) */
+    uint32_t lpos;       /* EXCHANGE: local qubit swapped with gpos; LOCAL_SWAP: first local qubit;
+                            MULTI_EXCHANGE: the local qubits, 8 bits each, in the mask's bit order */
+    uint32_t lpos2;      /* LOCAL_SWAP: second local qubit; MULTI_EXCHANGE: k, the number of pairs */
     qvg_gate op;         /* LOCAL: op on physical local qubits */
 } qvg_shard_step;
-/* Steps for ops[0..count) from the identity qubit map; with canonicalize != 0
- * the steps that restore the canonical order follow. Writes at most `cap`
+/* Steps for ops[0..count) from the identity qubit map. `canonicalize` is a
+ * flag word: bit 0 appends the steps that restore the canonical order; bits
+ * 8..11 give the most global qubits one exchange may swap (0/1: pairwise). Writes at most `cap`
  * steps and the total count to *nsteps (call with cap = 0 to size). */
 int qvg_shard_schedule(uint32_t n_qubits, uint32_t world, const qvg_gate *ops, uint64_t count,
                        int canonicalize, qvg_shard_step *steps, uint64_t cap, uint64_t *nsteps);

@@ -37,6 +37,7 @@ from ._core import (  # noqa: E402
     OPT_TIMING,
     OPT_EXCHANGE,
     OPT_PREFETCH,
+    OPT_BATCH_EXCHANGE,
     OPT_TILE_QUBITS,
     QVG_ABI_VERSION,
     CapacityError,

@@ -381,19 +381,23 @@ PYBIND11_MODULE(_core, m) {
           py::arg("tile_qubits") = 0, py::arg("carriers") = 3, "(passes, fused passes, algorithmic bytes)");
 
     m.def("shard_schedule",
-          [](std::uint32_t n, std::uint32_t world, py::buffer buf, bool canonicalize) {
+          [](std::uint32_t n, std::uint32_t world, py::buffer buf, bool canonicalize, std::uint32_t batch) {
               const py::buffer_info b = buf.request();
               std::size_t count = 0;
               const qvg_gate *g = gate_ptr(b, count);
               std::uint64_t nsteps = 0;
-              check_status(qvg_shard_schedule(n, world, g, count, canonicalize, nullptr, 0, &nsteps));
+              if (batch > 4) throw ValidationError("batch must be 0..4");
+              const int flags = (canonicalize ? 1 : 0) | (int)(batch << 8);
+              check_status(qvg_shard_schedule(n, world, g, count, flags, nullptr, 0, &nsteps));
               py::array_t<std::uint8_t> out(nsteps * sizeof(qvg_shard_step));
-              check_status(qvg_shard_schedule(n, world, g, count, canonicalize,
+              check_status(qvg_shard_schedule(n, world, g, count, flags,
                                               reinterpret_cast<qvg_shard_step *>(out.mutable_data()), nsteps, &nsteps));
               return out;
           },
           py::arg("n_qubits"), py::arg("world"), py::arg("gates"), py::arg("canonicalize") = true,
-          "Packed qvg_shard_step records (104 bytes each)");
+          py::arg("batch") = 1,
+          "Packed qvg_shard_step records (104 bytes each); batch = most global qubits one exchange swaps "
+          "(the engine's default is 4)");
 
     m.attr("QVG_ABI_VERSION") = qvg_abi_version();
     m.attr("OPT_FUSE") = (int)QVG_OPT_FUSE;
@@ -407,4 +411,5 @@ PYBIND11_MODULE(_core, m) {
     m.attr("OPT_TIMING") = (int)QVG_OPT_TIMING;
     m.attr("OPT_EXCHANGE") = (int)QVG_OPT_EXCHANGE;
     m.attr("OPT_PREFETCH") = (int)QVG_OPT_PREFETCH;
+    m.attr("OPT_BATCH_EXCHANGE") = (int)QVG_OPT_BATCH_EXCHANGE;
 }

@@ -99,6 +99,7 @@ struct qvg_state {
     bool timing = false;       // bracket each qvg_apply with CUDA events -> stats.kernel_ms
     int exchange_mode = -1;    // QVG_OPT_EXCHANGE (-1 auto)
     bool prefetch = false;     // fused tile: cp.async prefetch of the next tile (QVG_OPT_PREFETCH)
+    uint32_t batch_max = 4;    // sharded: most global qubits one exchange swaps (QVG_OPT_BATCH_EXCHANGE)
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
     // device scratch
     TileOp *d_ops = nullptr;
@@ -296,6 +297,7 @@ cudaStream_t shard_stream(qvg_state &s) { return s.stream; }
 uint32_t shard_amp_bytes(const qvg_state &s) { return s.S; }
 qvg_stats &shard_stats(qvg_state &s) { return s.stats; }
 int shard_exchange_mode(const qvg_state &s) { return s.exchange_mode; }
+uint32_t shard_batch_max(const qvg_state &s) { return s.batch_max; }
 }  // namespace qvg
 
 extern "C" {
@@ -428,6 +430,10 @@ int qvg_set_option(qvg_state *s, int key, int64_t value) {
         case QVG_OPT_FMA: s->fma = value != 0; break;
         case QVG_OPT_TIMING: s->timing = value != 0; break;
         case QVG_OPT_PREFETCH: s->prefetch = value != 0; break;
+        case QVG_OPT_BATCH_EXCHANGE:
+            if (value < 1 || value > 4) throw Validation("batch exchange must be 1..4 global qubits");
+            s->batch_max = (uint32_t)value;
+            break;
         case QVG_OPT_EXCHANGE:
             if (value < -1 || value > 2) throw Validation("exchange mode must be -1, 0, 1 or 2");
             s->exchange_mode = (int)value;
@@ -971,8 +977,11 @@ int qvg_shard_schedule(uint32_t n_qubits, uint32_t world, const qvg_gate *ops, u
         QubitMap map;
         map.reset(n_qubits);
         std::vector<ShardStep> out;
-        schedule_ops(n_qubits, L, ops, count, map, out);
-        if (canonicalize) schedule_canonicalize(n_qubits, L, map, out);
+        // flags: bit 0 canonicalize; bits 8..11 the most global qubits one
+        // exchange may swap (0 or 1: pairwise exchanges only)
+        const uint32_t kmax = std::max<uint32_t>(1, ((uint32_t)canonicalize >> 8) & 0xf);
+        schedule_ops(n_qubits, L, ops, count, map, out, kmax);
+        if (canonicalize & 1) schedule_canonicalize(n_qubits, L, map, out);
         if (nsteps) *nsteps = out.size();
         if (steps) std::memcpy(steps, out.data(), std::min<uint64_t>(cap, out.size()) * sizeof(ShardStep));
     });

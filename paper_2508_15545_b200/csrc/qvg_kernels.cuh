@@ -317,6 +317,62 @@ k_xchg(typename Cplx<R>::T *a, typename Cplx<R>::T *b, int lpos, uint64_t t0, in
     if (fence) __threadfence_system();
 }
 
+// K8: batched exchange of k global qubits over peer memory (STEP_MULTI_EXCHANGE
+// in qvg_schedule.hpp).
+//
+// This rank's shard `self` has value w on the k swapped rank bits. Round t
+// (1..2^k-1) pairs it with the rank whose bits read w^t (shard peer[t]): self's
+// amplitudes whose local bits at the k positions read w^t trade places with the
+// partner's that read w.
+//
+// Ownership: a (round, base) item is handled by one rank of its pair, the
+// one with the lower value taking the first half of the bases. So all ranks
+// run with no synchronisation inside the kernel. One grid row per round.
+template <class R>
+struct MxParams {
+    typename Cplx<R>::T *self;
+    typename Cplx<R>::T *peer[16];
+    int k;
+    int ps[4];     // the k local positions, ascending
+    int perm[4];   // value bit carried by ps[j]
+    uint32_t w;    // this rank's value on the swapped bits
+    uint64_t half; // bases per round owned by one rank: 2^(L-k) / 2
+    int fence;
+};
+
+template <class R>
+__device__ __forceinline__ uint64_t mx_deposit(uint64_t b, const MxParams<R> &p, uint32_t v) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+        if (j < p.k) b = ins0(b, p.ps[j]) | ((uint64_t)((v >> p.perm[j]) & 1u) << p.ps[j]);
+    return b;
+}
+
+template <class R, int APT>
+__global__ void __launch_bounds__(256) k_mxchg(const __grid_constant__ MxParams<R> p) {
+    using T = typename Cplx<R>::T;
+    const uint32_t t = blockIdx.y + 1;
+    const uint32_t wp = p.w ^ t;
+    T *peer = p.peer[t];
+    const uint64_t first = (p.w < wp ? 0 : p.half) + (uint64_t)blockIdx.x * (blockDim.x * APT) + threadIdx.x;
+    uint64_t xs[APT], xp[APT];
+    T a[APT], b[APT];
+#pragma unroll
+    for (int i = 0; i < APT; ++i) {
+        const uint64_t base = first + (uint64_t)i * blockDim.x;
+        xs[i] = mx_deposit(base, p, wp);
+        xp[i] = mx_deposit(base, p, p.w);
+        a[i] = ld_amp(p.self + xs[i]);
+        b[i] = ld_amp(peer + xp[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < APT; ++i) {
+        st_amp(p.self + xs[i], b[i]);
+        st_amp(peer + xp[i], a[i]);
+    }
+    if (p.fence) __threadfence_system();
+}
+
 // ---------------------------------------------------------------------------
 // Readout.
 // Per-block partial sums of |a|^2 with a fixed grid, so the result is

@@ -29,13 +29,21 @@
 
 namespace qvg {
 
-enum ShardStepType : uint32_t { STEP_LOCAL = 0, STEP_EXCHANGE = 1, STEP_LOCAL_SWAP = 2 };
+enum ShardStepType : uint32_t { STEP_LOCAL = 0, STEP_EXCHANGE = 1, STEP_LOCAL_SWAP = 2, STEP_MULTI_EXCHANGE = 3 };
 
 // One schedule step; the C layout is qvg_shard_step (include/qvg.h).
 // STEP_LOCAL runs `op` (physical local qubits) on ranks with
 // (rank & rank_mask) == rank_value; STEP_EXCHANGE swaps global physical qubit
 // gpos with local qubit lpos (= L-1); STEP_LOCAL_SWAP swaps local lpos, lpos2.
+// STEP_MULTI_EXCHANGE swaps k = lpos2 >= 2 global qubits at once: gpos is
+// their mask as rank bits (bit j = physical qubit L + j) and lpos packs the
+// local positions they trade with, 8 bits each, in the order of gpos's set
+// bits. It is an exchange among the 2^k ranks that differ only in those
+// bits: (1 - 2^-k) of each shard moves, against k/2 for k pairwise exchanges.
 using ShardStep = qvg_shard_step;
+
+// Local positions of a multi-exchange, in the order of the mask's set bits.
+inline uint32_t multi_pos(const ShardStep &st, uint32_t i) { return (st.lpos >> (8 * i)) & 0xffu; }
 
 struct QubitMap {
     std::vector<uint32_t> perm;  // logical -> physical
@@ -105,22 +113,74 @@ inline uint32_t pick_victim(uint32_t L, const qvg_gate *ops, uint64_t k, uint64_
     return best;
 }
 
+// Distance to the next op using logical qubit lq (as target, or as control
+// too when any_use), within the lookahead window; ~0 when unused there.
+inline uint64_t next_use(uint32_t lq, const qvg_gate *ops, uint64_t k, uint64_t count, bool any_use) {
+    constexpr uint64_t kLookahead = 1024;
+    for (uint64_t j = k; j < count && j < k + kLookahead; ++j) {
+        const qvg_gate &o = ops[j];
+        if (o.target == lq && (any_use || !op_is_diag(o))) return j - k;
+        if (any_use && o.kind == QVG_OP_CONTROLLED && (uint32_t)o.control == lq) return j - k;
+    }
+    return ~0ull;
+}
+
+// Batched exchange choice at op k (whose target is global): the global qubits
+// needed as non-diagonal targets soonest, paired with the local qubits (top
+// positions only) used furthest ahead, while each brought-in qubit is needed
+// before the qubit it displaces. Returns the (global, local) physical pairs;
+// one pair means a plain pairwise exchange is as good.
+inline std::vector<std::pair<uint32_t, uint32_t>> pick_batch(uint32_t n, uint32_t L, const qvg_gate *ops, uint64_t k,
+                                                             uint64_t count, const QubitMap &map, uint32_t kmax) {
+    std::vector<std::pair<uint64_t, uint32_t>> need, vic;
+    for (uint32_t p = L; p < n; ++p) {
+        const uint64_t d = next_use(map.inv[p], ops, k, count, false);
+        if (d != ~0ull) need.push_back({d, p});
+    }
+    for (uint32_t p = L; p-- > min_exchange_lpos(L);) vic.push_back({next_use(map.inv[p], ops, k, count, true), p});
+    std::stable_sort(need.begin(), need.end());
+    std::stable_sort(vic.begin(), vic.end(), [](const auto &a, const auto &b) { return a.first > b.first; });
+    std::vector<std::pair<uint32_t, uint32_t>> out;
+    for (size_t i = 0; i < need.size() && i < vic.size() && out.size() < kmax; ++i) {
+        if (i > 0 && !(need[i].first < vic[i].first)) break;
+        out.push_back({need[i].second, vic[i].second});
+    }
+    return out;
+}
+
+// kmax: most global qubits one exchange may swap (1 = pairwise exchanges only).
 inline void schedule_ops(uint32_t n, uint32_t L, const qvg_gate *ops, uint64_t count, QubitMap &map,
-                         std::vector<ShardStep> &out) {
+                         std::vector<ShardStep> &out, uint32_t kmax = 1) {
     for (uint64_t k = 0; k < count; ++k) {
         const qvg_gate &g = ops[k];
         const bool ctl = g.kind == QVG_OP_CONTROLLED;
         uint32_t pt = map.perm[g.target];
         const bool diag = op_is_diag(g);
         if (pt >= L && !diag) {
-            const uint32_t lpos = pick_victim(L, ops, k, count, map);
-            ShardStep ex{};
-            ex.type = STEP_EXCHANGE;
-            ex.gpos = pt;
-            ex.lpos = lpos;
-            out.push_back(ex);
-            map.swap_phys(pt, lpos);
-            pt = lpos;
+            auto batch = kmax >= 2 ? pick_batch(n, L, ops, k, count, map, std::min<uint32_t>(kmax, 4))
+                                   : std::vector<std::pair<uint32_t, uint32_t>>{};
+            if (batch.size() >= 2) {
+                std::sort(batch.begin(), batch.end());  // mask bit order
+                ShardStep ex{};
+                ex.type = STEP_MULTI_EXCHANGE;
+                for (size_t i = 0; i < batch.size(); ++i) {
+                    ex.gpos |= 1u << (batch[i].first - L);
+                    ex.lpos |= batch[i].second << (8 * i);
+                }
+                ex.lpos2 = (uint32_t)batch.size();
+                out.push_back(ex);
+                for (const auto &pr : batch) map.swap_phys(pr.first, pr.second);
+                pt = map.perm[g.target];
+            } else {
+                const uint32_t lpos = pick_victim(L, ops, k, count, map);
+                ShardStep ex{};
+                ex.type = STEP_EXCHANGE;
+                ex.gpos = pt;
+                ex.lpos = lpos;
+                out.push_back(ex);
+                map.swap_phys(pt, lpos);
+                pt = lpos;
+            }
         }
         const int32_t pc = ctl ? (int32_t)map.perm[(uint32_t)g.control] : -1;
         ShardStep st{};

@@ -46,6 +46,7 @@ cudaStream_t shard_stream(qvg_state &s);
 uint32_t shard_amp_bytes(const qvg_state &s);
 qvg_stats &shard_stats(qvg_state &s);
 int shard_exchange_mode(const qvg_state &s);  // QVG_OPT_EXCHANGE value (-1 = auto)
+uint32_t shard_batch_max(const qvg_state &s);  // QVG_OPT_BATCH_EXCHANGE: most global qubits per exchange
 void cuda_throw(cudaError_t e, const char *what);
 
 inline void nccl_check(ncclResult_t r, const char *what) {
@@ -359,6 +360,127 @@ inline bool run_exchange(qvg_state &s, ShardSet &set, uint32_t gpos, uint32_t lp
     return false;
 }
 
+// Bits of r at the set bits of mask, packed (pext) / spread back (pdep).
+inline uint32_t bits_pext(uint32_t r, uint32_t mask) {
+    uint32_t out = 0, i = 0;
+    for (uint32_t b = 0; b < 32; ++b)
+        if ((mask >> b) & 1u) out |= ((r >> b) & 1u) << i++;
+    return out;
+}
+inline uint32_t bits_pdep(uint32_t v, uint32_t mask) {
+    uint32_t out = 0, i = 0;
+    for (uint32_t b = 0; b < 32; ++b)
+        if ((mask >> b) & 1u) out |= ((v >> i++) & 1u) << b;
+    return out;
+}
+
+// Batched exchange (STEP_MULTI_EXCHANGE): the 2^k ranks that differ only in
+// the swapped rank bits trade, in 2^k - 1 XOR rounds, the regions whose
+// local bits at the k positions read the partner's value. Peer and virtual
+// transports run all rounds in one k_mxchg launch per rank. The NCCL copy
+// transport runs the rounds as pairwise chunked exchanges of those regions.
+inline void run_multi_exchange(qvg_state &s, ShardSet &set, const ShardStep &st) {
+    cudaStream_t stream = shard_stream(s);
+    const uint32_t S = shard_amp_bytes(s);
+    const uint32_t k = st.lpos2, mask = st.gpos;
+    if (k < 2 || k > 4 || (uint32_t)__builtin_popcount(mask) != k) throw std::runtime_error("internal: bad multi-exchange step");
+    int pos[4], idx[4] = {0, 1, 2, 3};
+    for (uint32_t i = 0; i < k; ++i) pos[i] = (int)multi_pos(st, i);
+    std::sort(idx, idx + k, [&](int a, int b) { return pos[a] < pos[b]; });
+    const uint64_t region = 1ull << (set.L - k);  // amplitudes per (rank, partner)
+    const uint32_t rounds = (1u << k) - 1;
+    qvg_stats &stats = shard_stats(s);
+    int mode = shard_exchange_mode(s);
+    const bool kernel = mode != 0 && (set.is_virtual || set.peer_ok);
+    auto launch = [&](auto tag, void *self, auto &&peer_of, uint32_t w, int fence) {
+        using R = decltype(tag);
+        using T = typename Cplx<R>::T;
+        MxParams<R> p{};
+        p.self = static_cast<T *>(self);
+        for (uint32_t t = 1; t <= rounds; ++t) p.peer[t] = static_cast<T *>(peer_of(t));
+        p.k = (int)k;
+        for (uint32_t j = 0; j < k; ++j) {
+            p.ps[j] = pos[idx[j]];
+            p.perm[j] = idx[j];
+        }
+        p.w = w;
+        p.half = region / 2;
+        p.fence = fence;
+        if (p.half >= 1024) {
+            k_mxchg<R, 4><<<dim3((unsigned)(p.half / 1024), rounds), 256, 0, stream>>>(p);
+        } else {
+            const unsigned bs = (unsigned)std::min<uint64_t>(p.half, 256);
+            k_mxchg<R, 1><<<dim3((unsigned)(p.half / bs), rounds), bs, 0, stream>>>(p);
+        }
+    };
+    auto launch_any = [&](void *self, auto &&peer_of, uint32_t w, int fence) {
+        if (S == 16) launch(double{}, self, peer_of, w, fence);
+        else launch(float{}, self, peer_of, w, fence);
+    };
+    const uint32_t gmask = mask;  // rank bits
+    if (set.is_virtual || kernel) {
+        if (set.is_virtual) {
+            for (size_t b = 0; b < set.bufs.size(); ++b) {
+                const uint32_t r = set.ranks[b];
+                launch_any(set.bufs[b], [&](uint32_t t) { return set.bufs[r ^ bits_pdep(t, gmask)]; },
+                           bits_pext(r, gmask), 0);
+                stats.kernel_launches += 1;
+            }
+            stats.exchange_bytes += (uint64_t)set.world * rounds * region * S;
+        } else {
+            const uint32_t r = set.rank;
+            stream_barrier(set, stream);
+            launch_any(set.bufs[0], [&](uint32_t t) { return set.peer[r ^ bits_pdep(t, gmask)]; }, bits_pext(r, gmask),
+                       1);
+            cuda_throw(cudaGetLastError(), "multi-exchange launch");
+            stream_barrier(set, stream);
+            stats.kernel_launches += 1;
+            stats.exchange_bytes += (uint64_t)rounds * region * S;
+        }
+        cuda_throw(cudaGetLastError(), "multi-exchange launch");
+        stats.exchanges += 1;
+        return;
+    }
+    // NCCL copy transport: round t is a pairwise exchange of the region whose
+    // local bits read the partner's value, in runs of 2^min(pos) amplitudes.
+    const uint32_t r = set.rank, w = bits_pext(r, gmask);
+    const int pmin = pos[idx[0]];
+    const uint64_t run_bytes = (uint64_t)S << pmin;
+    const uint64_t nruns = 1ull << (set.L - k - pmin);
+    char *base = static_cast<char *>(set.bufs[0]);
+    uint64_t i = 0;
+    for (uint32_t t = 1; t <= rounds; ++t) {
+        const int partner = (int)(r ^ bits_pdep(t, gmask));
+        const uint32_t v = w ^ t;  // region I send and receive into
+        for (uint64_t run = 0; run < nruns; ++run) {
+            uint64_t x = run << pmin;
+            for (uint32_t j = 0; j < k; ++j) {
+                const uint64_t low = (1ull << pos[idx[j]]) - 1;
+                x = ((x & ~low) << 1) | (x & low) | ((uint64_t)((v >> idx[j]) & 1u) << pos[idx[j]]);
+            }
+            char *blk = base + x * S;
+            for (uint64_t off = 0; off < run_bytes; off += set.chunk_bytes, ++i) {
+                const uint64_t c = std::min<uint64_t>(set.chunk_bytes, run_bytes - off);
+                char *scr = static_cast<char *>(set.scratch) + (i & 1) * set.chunk_bytes;
+                if (i >= 2) cuda_throw(cudaStreamWaitEvent(stream, set.copied[i & 1], 0), "wait scratch");
+                nccl_check(ncclGroupStart(), "ncclGroupStart");
+                nccl_check(ncclSend(blk + off, c, ncclChar, partner, set.comm, stream), "ncclSend");
+                nccl_check(ncclRecv(scr, c, ncclChar, partner, set.comm, stream), "ncclRecv");
+                nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+                cuda_throw(cudaEventRecord(set.received[i & 1], stream), "record received");
+                cuda_throw(cudaStreamWaitEvent(set.copy_stream, set.received[i & 1], 0), "wait received");
+                cuda_throw(cudaMemcpyAsync(blk + off, scr, c, cudaMemcpyDeviceToDevice, set.copy_stream),
+                           "exchange copy");
+                cuda_throw(cudaEventRecord(set.copied[i & 1], set.copy_stream), "record copied");
+            }
+        }
+    }
+    for (int b = 0; b < 2 && (uint64_t)b < i; ++b)
+        cuda_throw(cudaStreamWaitEvent(stream, set.copied[b], 0), "wait copies");
+    stats.exchanges += 1;
+    stats.exchange_bytes += (uint64_t)rounds * region * S;
+}
+
 // Execute a step list: consecutive local steps are batched per shard (each
 // shard keeps the ops whose rank predicate it satisfies) and planned together,
 // so fusion spans everything between two exchanges. The step right after an
@@ -385,6 +507,8 @@ inline void run_steps(qvg_state &s, ShardSet &set, const std::vector<ShardStep> 
             const bool candidate = next && next->type == STEP_LOCAL && next->op.target == st.lpos &&
                                    !op_is_diag(next->op);
             if (run_exchange(s, set, st.gpos, st.lpos, candidate ? next : nullptr)) ++i;
+        } else if (st.type == STEP_MULTI_EXCHANGE) {
+            run_multi_exchange(s, set, st);
         } else {
             run_local_swap(s, set, st.lpos, st.lpos2);
         }
@@ -398,7 +522,7 @@ inline void shard_apply(qvg_state &s, ShardSet &set, const qvg_gate *ops, uint64
         return;
     }
     std::vector<ShardStep> steps;
-    schedule_ops(set.n, set.L, ops, count, set.map, steps);
+    schedule_ops(set.n, set.L, ops, count, set.map, steps, shard_batch_max(s));
     run_steps(s, set, steps);
 }
 

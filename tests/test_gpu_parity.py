@@ -115,29 +115,34 @@ def test_virtual_shards_bit_identical(qv, oracle, world):
 def test_exchange_transports_bit_identical(qv, oracle, world):
     """QVG_OPT_EXCHANGE 0 (swap kernel), 1 (k_xchg, split in two rank-role
     launches like the peer transport) and 2 (k_xchg fused with the gate that
-    triggered the exchange, incl. local and global controls): all bit-exact
-    with the oracle."""
+    triggered the exchange, incl. local and global controls), with pairwise
+    exchanges only (QVG_OPT_BATCH_EXCHANGE 1) or batched ones (k_mxchg, up to
+    3 global qubits at once): all bit-exact with the oracle."""
     circuits = [qv.random_circuit(12, 400, 17), qv.haar_sweep_circuit(14, 5), qv.u3_ladder_circuit(13, 5, 8)]
     for c in circuits:
         n = c.n_qubits
         want = oracle.simulate(n, gate_array(c))
-        for mode in (0, 1, 2):
-            for fuse in (True, False):
-                st = qv.StateVector.create_sharded(n, 128, 0, 0, world, None)
-                st.set_option(qv.OPT_EXCHANGE, mode)
-                qv.apply_circuit(st, c, strategy="gpu", fuse=fuse)
-                s = st.stats()
-                assert np.array_equal(st.read_state(), want), (world, n, mode, fuse)
-                assert s["exchanges"] > 0
-                assert (s["fused_exchanges"] > 0) == (mode == 2), (mode, s)
+        for batch in (1, 4):
+            for mode in (0, 1, 2):
+                for fuse in (True, False):
+                    st = qv.StateVector.create_sharded(n, 128, 0, 0, world, None)
+                    st.set_option(qv.OPT_EXCHANGE, mode)
+                    st.set_option(qv.OPT_BATCH_EXCHANGE, batch)
+                    qv.apply_circuit(st, c, strategy="gpu", fuse=fuse)
+                    s = st.stats()
+                    assert np.array_equal(st.read_state(), want), (world, n, batch, mode, fuse)
+                    assert s["exchanges"] > 0
+                    if batch == 1:
+                        assert (s["fused_exchanges"] > 0) == (mode == 2), (mode, s)
 
 
 def test_exchange_fused_complex64(qv, oracle):
     c = qv.haar_sweep_circuit(14, 6)
     want = oracle.simulate(14, gate_array(c))
-    for mode in (0, 2):
+    for mode, batch in ((0, 1), (2, 1), (1, 4)):
         st = qv.StateVector.create_sharded(14, 64, 0, 0, 4, None)
         st.set_option(qv.OPT_EXCHANGE, mode)
+        st.set_option(qv.OPT_BATCH_EXCHANGE, batch)
         qv.apply_circuit(st, c, strategy="gpu")
         assert np.abs(st.read_state() - want).max() <= 1e-5
     with pytest.raises(qv.ValidationError):

@@ -21,9 +21,43 @@ STEP_DTYPE = np.dtype([("type", "<u4"), ("rank_mask", "<u4"), ("rank_value", "<u
 assert STEP_DTYPE.itemsize == 104
 
 
-def schedule(qv, circuit, world, canonicalize=True):
-    raw = qv.shard_schedule(circuit.n_qubits, world, circuit.gates(), canonicalize)
+def schedule(qv, circuit, world, canonicalize=True, batch=1):
+    raw = qv.shard_schedule(circuit.n_qubits, world, circuit.gates(), canonicalize, batch)
     return np.frombuffer(raw.tobytes(), STEP_DTYPE)
+
+
+# --- batched exchange (QVG_STEP_MULTI_EXCHANGE) helpers ---------------------------------
+def pext(r, mask):
+    out, i = 0, 0
+    for b in range(32):
+        if (mask >> b) & 1:
+            out |= ((r >> b) & 1) << i
+            i += 1
+    return out
+
+
+def pdep(v, mask):
+    out, i = 0, 0
+    for b in range(32):
+        if (mask >> b) & 1:
+            out |= ((v >> i) & 1) << b
+            i += 1
+    return out
+
+
+def multi_geometry(st):
+    """(rank-bit mask, local positions in the mask's bit order)."""
+    k = int(st["lpos2"])
+    return int(st["gpos"]), [(int(st["lpos"]) >> (8 * i)) & 0xFF for i in range(k)]
+
+
+def region(L, pos, v):
+    """Local indices whose bits at pos (in order) read v, ascending."""
+    x = np.arange(1 << L, dtype=np.int64)
+    val = np.zeros_like(x)
+    for i, p in enumerate(pos):
+        val |= ((x >> p) & 1) << i
+    return x[val == v]
 
 
 def half_indices(L, lpos):
@@ -68,6 +102,20 @@ def emulate(oracle, n, world, steps):
                 ri, pi = base | (1 << lpos), base
                 mine, theirs = shards[r][ri].copy(), shards[p][pi].copy()
                 shards[r][ri], shards[p][pi] = theirs, mine
+        elif st["type"] == 3:
+            # amplitude (r, x): its local bits at pos become r's swapped rank
+            # bits and vice versa
+            mask, pos = multi_geometry(st)
+            k = len(pos)
+            new = [a.copy() for a in shards]
+            for r in range(world):
+                w = pext(r, mask)
+                for v in range(1 << k):
+                    src = region(L, pos, v)
+                    dst_rank = (r & ~mask) | pdep(v, mask)
+                    dst = region(L, pos, w)
+                    new[dst_rank][dst] = shards[r][src]
+            shards = new
         else:
             for r in range(world):
                 run_local_steps(oracle, L, shards[r], r, [st])
@@ -88,14 +136,43 @@ def build(qv, fn, args):
     return out[0] if isinstance(out, tuple) else out
 
 
+@pytest.mark.parametrize("batch", [1, 4])
 @pytest.mark.parametrize("world", [2, 4, 8])
 @pytest.mark.parametrize("fn,args", CIRCUITS)
-def test_schedule_emulated_bit_identical(qv, oracle, world, fn, args):
+def test_schedule_emulated_bit_identical(qv, oracle, world, fn, args, batch):
     c = build(qv, fn, args)
-    steps = schedule(qv, c, world)
+    steps = schedule(qv, c, world, batch=batch)
+    if batch == 1 or world == 2:
+        assert 3 not in set(steps["type"])
     want = oracle.simulate(c.n_qubits, gate_array(c))
     got = emulate(oracle, c.n_qubits, world, steps)
     assert np.array_equal(got, want)
+
+
+def test_batched_exchange_moves_fewer_bytes(qv):
+    """Config 4's circuit at 4 and 8 shards: batched exchanges (1 - 2^-k of a
+    shard each) move less data than pairwise ones (1/2 each)."""
+    for n, world in [(34, 4), (35, 8)]:
+        c = qv.u3_ladder_circuit(n, 20, 1)
+        moved = {}
+        for batch in (1, 4):
+            s = schedule(qv, c, world, canonicalize=False, batch=batch)
+            vol = 0.0
+            for st in s:
+                if st["type"] == 1:
+                    vol += 0.5
+                elif st["type"] == 3:
+                    vol += 1 - 2.0 ** -int(st["lpos2"])
+            moved[batch] = vol
+            if batch == 4:
+                multi = s[s["type"] == 3]
+                assert len(multi) > 0
+                L = n - int(np.log2(world))
+                for st in multi:
+                    mask, pos = multi_geometry(st)
+                    assert bin(mask).count("1") == len(pos) >= 2
+                    assert min(pos) >= max(L - 12, L // 2) and len(set(pos)) == len(pos)
+        assert moved[4] < 0.85 * moved[1], (n, world, moved)
 
 
 def test_schedule_shape(qv):
@@ -134,7 +211,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, fn, args, q):
+def _worker(rank, world, port, fn, args, q, batch=1):
     import sys
 
     import torch
@@ -154,7 +231,7 @@ def _worker(rank, world, port, fn, args, q):
         c = build(qv, fn, args)
         n = c.n_qubits
         L = n - int(np.log2(world))
-        steps = schedule(qv, c, world)
+        steps = schedule(qv, c, world, batch=batch)
         shard = np.zeros(1 << L, np.complex128)
         if rank == 0:
             shard[0] = 1.0
@@ -172,6 +249,18 @@ def _worker(rank, world, port, fn, args, q):
                 for r in reqs:
                     r.wait()
                 shard[idx] = recv.numpy().view(np.complex128)
+            elif st["type"] == 3:  # batched: 2^k - 1 XOR rounds of region swaps
+                mask, pos = multi_geometry(st)
+                w = pext(rank, mask)
+                for t in range(1, 1 << len(pos)):
+                    partner = rank ^ pdep(t, mask)
+                    idx = region(L, pos, w ^ t)
+                    send = torch.from_numpy(shard[idx].view(np.float64).copy())
+                    recv = torch.empty_like(send)
+                    reqs = [dist.isend(send, partner), dist.irecv(recv, partner)]
+                    for r in reqs:
+                        r.wait()
+                    shard[idx] = recv.numpy().view(np.complex128)
             else:
                 run_local_steps(oracle, L, shard, rank, [st])
         parts = [torch.empty(2 << L, dtype=torch.float64) for _ in range(world)]
@@ -184,8 +273,8 @@ def _worker(rank, world, port, fn, args, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_gloo_multiprocess_bit_identical(world):
+@pytest.mark.parametrize("world,batch", [(2, 1), (4, 1), (4, 4)])
+def test_gloo_multiprocess_bit_identical(world, batch):
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
@@ -193,7 +282,7 @@ def test_gloo_multiprocess_bit_identical(world):
     port = _free_port()
     for fn, args in [("u3_ladder_circuit", (10, 3, 5)), ("random_circuit", (8, 120, 4))]:
         port = _free_port()
-        procs = [ctx.Process(target=_worker, args=(r, world, port, fn, args, q)) for r in range(world)]
+        procs = [ctx.Process(target=_worker, args=(r, world, port, fn, args, q, batch)) for r in range(world)]
         for p in procs:
             p.start()
         for p in procs:
@@ -247,7 +336,25 @@ def _xchg_role(oracle, shards, L, lpos, rank_a, rank_b, role, gate):
     a[x0], a[x1], b[x0], b[x1] = na0, na1, nb0, nb1
 
 
-def _peer_worker(rank, world, port, fn, args, tensors, q):
+def _mxchg_role(shards, L, mask, pos, rank):
+    """One rank's share of k_mxchg (qvg_kernels.cuh K8): for every round t,
+    the half of the bases this rank owns, swapped between its shard and the
+    partner's."""
+    k = len(pos)
+    w = pext(rank, mask)
+    for t in range(1, 1 << k):
+        wp = w ^ t
+        partner = rank ^ pdep(t, mask)
+        mine, theirs = region(L, pos, wp), region(L, pos, w)  # same base order
+        half = mine.size // 2
+        sl = slice(0, half) if w < wp else slice(half, mine.size)
+        a = shards[rank][mine[sl]].copy()
+        b = shards[partner][theirs[sl]].copy()
+        shards[rank][mine[sl]] = b
+        shards[partner][theirs[sl]] = a
+
+
+def _peer_worker(rank, world, port, fn, args, tensors, q, batch=1):
     import sys
 
     import torch.distributed as dist
@@ -267,7 +374,7 @@ def _peer_worker(rank, world, port, fn, args, tensors, q):
         n = c.n_qubits
         L = n - int(np.log2(world))
         shards = [t.numpy().view(np.complex128) for t in tensors]  # every rank's shard, mapped
-        steps = schedule(qv, c, world)
+        steps = schedule(qv, c, world, batch=batch)
         fused = 0
         i = 0
         while i < len(steps):
@@ -287,6 +394,11 @@ def _peer_worker(rank, world, port, fn, args, tensors, q):
                 if gate is not None:
                     fused += 1
                     i += 1
+            elif st["type"] == 3:
+                mask, pos = multi_geometry(st)
+                dist.barrier()
+                _mxchg_role(shards, L, mask, pos, rank)
+                dist.barrier()
             else:
                 run_local_steps(oracle, L, shards[rank], rank, [st])
             i += 1
@@ -299,8 +411,8 @@ def _peer_worker(rank, world, port, fn, args, tensors, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_gloo_peer_exchange_protocol_bit_identical(world):
+@pytest.mark.parametrize("world,batch", [(2, 1), (4, 1), (4, 4)])
+def test_gloo_peer_exchange_protocol_bit_identical(world, batch):
     import torch
     import torch.multiprocessing as mp
 
@@ -313,7 +425,8 @@ def test_gloo_peer_exchange_protocol_bit_identical(world):
         tensors = [torch.zeros(2 << L, dtype=torch.float64).share_memory_() for _ in range(world)]
         tensors[0][0] = 1.0
         port = _free_port()
-        procs = [ctx.Process(target=_peer_worker, args=(r, world, port, fn, args, tensors, q)) for r in range(world)]
+        procs = [ctx.Process(target=_peer_worker, args=(r, world, port, fn, args, tensors, q, batch))
+                 for r in range(world)]
         for p in procs:
             p.start()
         for p in procs:
@@ -321,4 +434,4 @@ def test_gloo_peer_exchange_protocol_bit_identical(world):
             assert p.exitcode == 0
         ok, fused = q.get(timeout=10)
         assert ok, (fn, world)
-        assert fused > 0, (fn, world)
+        assert fused > 0 or batch > 1, (fn, world)

@@ -1,7 +1,8 @@
 """Exchange-transport A/B on one GPU with virtual shards: config 4's layer
 circuit (U3 layers + CX ladder) at n qubits over G shards, with
 QVG_OPT_EXCHANGE 0 (swap kernel + separate gate), 1 (k_xchg exchange only)
-and 2 (k_xchg fused with the gate that triggered the exchange).
+and 2 (k_xchg fused with the gate that triggered the exchange), pairwise
+exchanges only, and batched exchanges (QVG_OPT_BATCH_EXCHANGE 4, k_mxchg).
 
 On one device every "remote" byte is an HBM byte, so this measures the
 kernels' HBM efficiency and the passes the fusion removes, not NVLink.
@@ -48,9 +49,10 @@ def main():
     for world in (2, 4, 8):
         for fuse in (True, False):
             ref = None
-            for mode in (0, 1, 2):
+            for mode, batch in ((0, 1), (1, 1), (2, 1), (1, 4)):
                 st = qv.StateVector.create_sharded(a.n, 128, 0, 0, world, None)
                 st.set_option(qv.OPT_EXCHANGE, mode)
+                st.set_option(qv.OPT_BATCH_EXCHANGE, batch)
                 ms, s = timed(st, circ, a.reps, fuse)
                 # bit-identity across modes on the same circuit
                 head = st.read_state(0, 1 << 20)
@@ -59,7 +61,7 @@ def main():
                     ref = head
                 else:
                     same = bool((head == ref).all())
-                row = {"n": a.n, "world": world, "fuse": fuse, "mode": mode, "ms": ms,
+                row = {"n": a.n, "world": world, "fuse": fuse, "mode": mode, "batch": batch, "ms": ms,
                        "passes": s["passes"] / a.reps, "exchanges": s["exchanges"] / a.reps,
                        "fused_exchanges": s["fused_exchanges"] / a.reps, "same_as_mode0": same}
                 rows.append(row)
