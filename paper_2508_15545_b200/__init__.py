@@ -38,6 +38,7 @@ from ._core import (  # noqa: E402
     OPT_EXCHANGE,
     OPT_PREFETCH,
     OPT_BATCH_EXCHANGE,
+    OPT_STAGE,
     OPT_TILE_QUBITS,
     QVG_ABI_VERSION,
     CapacityError,

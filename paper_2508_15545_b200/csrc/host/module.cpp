@@ -412,4 +412,5 @@ PYBIND11_MODULE(_core, m) {
     m.attr("OPT_EXCHANGE") = (int)QVG_OPT_EXCHANGE;
     m.attr("OPT_PREFETCH") = (int)QVG_OPT_PREFETCH;
     m.attr("OPT_BATCH_EXCHANGE") = (int)QVG_OPT_BATCH_EXCHANGE;
+    m.attr("OPT_STAGE") = (int)QVG_OPT_STAGE;
 }

@@ -100,6 +100,7 @@ struct qvg_state {
     int exchange_mode = -1;    // QVG_OPT_EXCHANGE (-1 auto)
     bool prefetch = false;     // fused tile: cp.async prefetch of the next tile (QVG_OPT_PREFETCH)
     uint32_t batch_max = 4;    // sharded: most global qubits one exchange swaps (QVG_OPT_BATCH_EXCHANGE)
+    uint32_t stage_bits = 3;   // fused tile: stage first/last group HBM access through shared memory (QVG_OPT_STAGE)
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
     // device scratch
     TileOp *d_ops = nullptr;
@@ -207,18 +208,23 @@ void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *recs) {
     prm.g = g;
     std::memcpy(prm.ops, recs + p.op_begin, sizeof(TileOp) * g.nrec);
     const unsigned threads = 1u << (g.k - g.sub);  // one 2^sub-amplitude subcube per thread
-    const bool pf = s.prefetch && g.sub == 3;
+    const bool pf = s.prefetch;
     const size_t smem = (((sizeof(uint64_t) << g.nhi) + 15) & ~size_t(15)) +
-                        (g.ngroups > 1 ? (sizeof(T) << g.k) : 0) + (pf ? (sizeof(T) << g.k) : 0);
+                        (g.ngroups > 1 || g.stage ? (sizeof(T) << g.k) : 0) + (pf ? (sizeof(T) << g.k) : 0);
     const bool fma = s.fma && sizeof(R) == 8;  // complex64 always contracts
     const bool small = threads <= 256;
-    auto kern = g.sub == 4 ? (fma ? k_tile<R, 4, true, 256, false> : k_tile<R, 4, false, 256, false>)
+    const bool tiny = threads <= 128;  // sub 4 at k <= 11: 128-thread CTAs, up to 168 registers
+    auto kern = g.sub == 4
+                    ? (tiny ? (pf ? (fma ? k_tile<R, 4, true, 128, true> : k_tile<R, 4, false, 128, true>)
+                                  : (fma ? k_tile<R, 4, true, 128, false> : k_tile<R, 4, false, 128, false>))
+                            : (pf ? (fma ? k_tile<R, 4, true, 256, true> : k_tile<R, 4, false, 256, true>)
+                                  : (fma ? k_tile<R, 4, true, 256, false> : k_tile<R, 4, false, 256, false>)))
                 : pf ? (small ? (fma ? k_tile<R, 3, true, 256, true> : k_tile<R, 3, false, 256, true>)
                               : (fma ? k_tile<R, 3, true, 512, true> : k_tile<R, 3, false, 512, true>))
                 : small ? (fma ? k_tile<R, 3, true, 256, false> : k_tile<R, 3, false, 256, false>)
                         : (fma ? k_tile<R, 3, true, 512, false> : k_tile<R, 3, false, 512, false>);
-    static bool attr_set[2][2][2][2][2] = {};
-    bool &set = attr_set[sizeof(R) == 8][g.sub == 4][fma][small][pf];
+    static bool attr_set[2][2][2][2][2][2] = {};
+    bool &set = attr_set[sizeof(R) == 8][g.sub == 4][fma][small][pf][tiny];
     if (!set) {
         cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
                    "cudaFuncSetAttribute(k_tile)");
@@ -241,6 +247,7 @@ PlanOptions plan_options(const qvg_state &s) {
     po.low_kernel = s.low_kernel;
     po.min_run = s.min_run;
     po.sub_bits = s.sub_bits;
+    po.stage_bits = s.stage_bits;
     return po;
 }
 
@@ -430,6 +437,10 @@ int qvg_set_option(qvg_state *s, int key, int64_t value) {
         case QVG_OPT_FMA: s->fma = value != 0; break;
         case QVG_OPT_TIMING: s->timing = value != 0; break;
         case QVG_OPT_PREFETCH: s->prefetch = value != 0; break;
+        case QVG_OPT_STAGE:
+            if (value < 0 || value > 12) throw Validation("stage must be 0 (never) .. 12");
+            s->stage_bits = (uint32_t)value;
+            break;
         case QVG_OPT_BATCH_EXCHANGE:
             if (value < 1 || value > 4) throw Validation("batch exchange must be 1..4 global qubits");
             s->batch_max = (uint32_t)value;

@@ -97,6 +97,9 @@ struct PlanOptions {
     bool low_kernel = false;
     uint32_t min_run = 32;   // see qvg_state::min_run
     uint32_t sub_bits = 3;   // tile register subcube: 2^sub amplitudes per thread (3 or 4)
+    uint32_t stage_bits = 3; // stage a first/last group through shared memory when its bits
+                             // include tile bits 0..stage_bits-1 (warp lanes >= 2^stage_bits
+                             // amplitudes apart); 0 = never
 };
 
 // Ops per fused pass: with at most one group header per op the records fit
@@ -211,6 +214,7 @@ inline Plan make_plan(const qvg_gate *ops, uint64_t count, const PlanOptions &po
             // Records: [group header, its ops]... Each group's pair ops touch
             // at most `sub` tile bits (the thread's register subcube).
             std::vector<TileOp> group;
+            uint32_t first_low = 0, last_low = 0;  // see PlanOptions::stage_bits
             int gbits[4];
             int nb = 0;
             auto close_group = [&] {
@@ -222,7 +226,7 @@ inline Plan make_plan(const qvg_gate *ops, uint64_t count, const PlanOptions &po
                 };
                 // Pad the free slots with the tile bits the group's diagonal
                 // ops use most (their multiplies then skip the elements the
-                // bit excludes at compile time), then the lowest unused bits.
+                // bit excludes at compile time).
                 int freq[64] = {};
                 for (const TileOp &t : group) {
                     if (t.kind != TILE_DIAG) continue;
@@ -236,7 +240,12 @@ inline Plan make_plan(const qvg_gate *ops, uint64_t count, const PlanOptions &po
                     if (best < 0) break;
                     gbits[nb++] = best;
                 }
-                for (int b = 0; nb < g.sub && b < g.k; ++b)
+                // Remaining slots take the HIGHEST unused tile bits: the
+                // lanes of a warp then run over the lowest tile bits, so the
+                // first group's HBM loads and the last group's stores are
+                // contiguous 512-B warp accesses and the shared-memory
+                // transposes stay conflict-free.
+                for (int b = g.k - 1; nb < g.sub && b >= 0; --b)
                     if (!used(b)) gbits[nb++] = b;
                 std::sort(gbits, gbits + g.sub);
                 for (TileOp &t : group) {
@@ -254,6 +263,10 @@ inline Plan make_plan(const qvg_gate *ops, uint64_t count, const PlanOptions &po
                 h.kind = TILE_GROUP;
                 h.tbit = (int32_t)group.size();
                 for (int s = 0; s < g.sub; ++s) h.gtgt |= (uint64_t)gbits[s] << (8 * s);
+                uint32_t low = 0;  // lowest tile bits the group holds: its lanes are 2^low amplitudes apart
+                while ((int)low < g.sub && gbits[low] == (int)low) ++low;
+                if (g.ngroups == 0) first_low = low;
+                last_low = low;
                 plan.tile_ops.push_back(h);
                 plan.tile_ops.insert(plan.tile_ops.end(), group.begin(), group.end());
                 group.clear();
@@ -301,6 +314,11 @@ inline Plan make_plan(const qvg_gate *ops, uint64_t count, const PlanOptions &po
                 group.push_back(t);
             }
             close_group();
+            g.stage = 0;
+            if (po.stage_bits > 0) {
+                if (first_low >= po.stage_bits) g.stage |= 1;
+                if (last_low >= po.stage_bits) g.stage |= 2;
+            }
             g.nrec = (int)(plan.tile_ops.size() - p.op_begin);
             p.geom = g;
             p.op_count = (uint32_t)(plan.tile_ops.size() - p.op_begin);

@@ -54,7 +54,7 @@ struct TileGeom {
     int ngroups;          // register groups in this pass
     int nrec;             // records (headers + ops)
     int sub;              // subcube bits per thread (3 or 4)
-    int pad;
+    int stage;            // bit 0: first group loads through shared memory; bit 1: last group stores through it
     int hiq[24];          // tile qubits >= lowc, ascending (tile-local bits lowc..k-1)
     uint64_t ntiles;      // 2^(n-k)
 };
@@ -186,7 +186,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // is off the critical path (the top stall without it: a DMUL waiting on the
 // first group's loads, long_scoreboard, profiles/r01_ncu_summary.md).
 template <class R, int SUB, bool FMA, int MAXT, bool PF>
-__global__ void __launch_bounds__(MAXT, (MAXT <= 256 && SUB == 3) ? (PF ? 3 : 4) : 2)
+__global__ void __launch_bounds__(MAXT, ((MAXT <= 256 && SUB == 3) || (MAXT <= 128 && SUB == 4)) ? (PF ? 3 : 4) : 2)
 k_tile(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams prm) {
     using T = typename Cplx<R>::T;
     constexpr int E = 1 << SUB;
@@ -198,7 +198,8 @@ k_tile(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams
     const TileOp *ops = prm.ops;
     uint64_t *offhi = reinterpret_cast<uint64_t *>(smem_raw);
     T *sm = reinterpret_cast<T *>(smem_raw + (((sizeof(uint64_t) << g.nhi) + 15) & ~15ull));
-    T *pf = sm + (g.ngroups > 1 ? (1u << g.k) : 0u);  // PF: the next tile (after the transpose buffer)
+    const bool use_sm = g.ngroups > 1 || g.stage != 0;
+    T *pf = sm + (use_sm ? (1u << g.k) : 0u);  // PF: the next tile (after the transpose buffer)
     const uint32_t nhi = 1u << g.nhi;
     const uint32_t lowm = (1u << g.lowc) - 1u;
     {  // the high-qubit offset table
@@ -262,6 +263,20 @@ k_tile(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams
                 for (int r = 0; r < E; ++r) v[r] = pf[swz(lidx(r))];
                 __syncthreads();  // every thread has its subcube: refill the buffer
                 if (tile + gridDim.x < g.ntiles) prefetch(tile + gridDim.x);
+            } else if (gi == 0 && (g.stage & 1)) {
+                // the group's bits include the lowest tile bits, so its lanes
+                // would stride through HBM: load the tile coalesced (lane =
+                // consecutive amplitudes) into shared memory first
+#pragma unroll
+                for (int j = 0; j < E; ++j) {  // all loads in flight before the first store
+                    const uint32_t l = threadIdx.x + (uint32_t)j * blockDim.x;
+                    v[j] = ld_amp(psi + (base | offhi[l >> g.lowc] | (l & lowm)));
+                }
+#pragma unroll
+                for (int j = 0; j < E; ++j) sm[swz(threadIdx.x + (uint32_t)j * blockDim.x)] = v[j];
+                __syncthreads();
+#pragma unroll
+                for (int r = 0; r < E; ++r) v[r] = sm[swz(lidx(r))];
             } else if (gi == 0) {
 #pragma unroll
                 for (int r = 0; r < E; ++r) {
@@ -287,7 +302,20 @@ k_tile(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams
                 }
             }
             rec += nops;
-            if (gi == g.ngroups - 1) {
+            if (gi == g.ngroups - 1 && (g.stage & 2)) {
+                // each thread rewrites only the slots it read, then the tile
+                // leaves coalesced
+#pragma unroll
+                for (int r = 0; r < E; ++r) sm[swz(lidx(r))] = v[r];
+                __syncthreads();
+#pragma unroll
+                for (int j = 0; j < E; ++j) v[j] = sm[swz(threadIdx.x + (uint32_t)j * blockDim.x)];
+#pragma unroll
+                for (int j = 0; j < E; ++j) {
+                    const uint32_t l = threadIdx.x + (uint32_t)j * blockDim.x;
+                    st_amp(psi + (base | offhi[l >> g.lowc] | (l & lowm)), v[j]);
+                }
+            } else if (gi == g.ngroups - 1) {
 #pragma unroll
                 for (int r = 0; r < E; ++r) {
                     const uint32_t lr = lidx(r);
@@ -299,7 +327,7 @@ k_tile(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams
                 __syncthreads();
             }
         }
-        if (g.ngroups > 1) __syncthreads();  // last group read sm; the next tile's groups write it
+        if (use_sm) __syncthreads();  // sm was read this tile; the next tile writes it
     }
 }
 

@@ -199,9 +199,11 @@ def test_fma_mode_within_tolerance(qv, oracle):
         assert np.abs(got - want).max() <= 1e-12
 
 
-@pytest.mark.parametrize("sub,pf,k", [(3, 0, 11), (4, 0, 11), (3, 1, 11), (3, 1, 12), (3, 1, 9)])
-def test_tile_subcube_variants_bit_exact(qv, oracle, sub, pf, k):
-    """Register subcube 2^3 / 2^4, cp.async next-tile prefetch, tile sizes."""
+@pytest.mark.parametrize("sub,pf,k,stage", [(3, 0, 11, 3), (4, 0, 11, 3), (3, 1, 11, 3), (3, 1, 12, 2), (3, 1, 9, 3),
+                                             (4, 1, 11, 1), (4, 0, 11, 0), (4, 0, 12, 1), (4, 0, 8, 2)])
+def test_tile_subcube_variants_bit_exact(qv, oracle, sub, pf, k, stage):
+    """Register subcube 2^3 / 2^4, cp.async next-tile prefetch, tile sizes,
+    first/last-group staging through shared memory."""
     for c in [qv.u3_ladder_circuit(16, 6, 2), qv.grid_circuit(3, 5, 10, 4), qv.qft_circuit(14, 3)[0],
               qv.random_circuit(15, 500, 12)]:
         n = c.n_qubits
@@ -209,6 +211,7 @@ def test_tile_subcube_variants_bit_exact(qv, oracle, sub, pf, k):
         st = qv.StateVector.create(n, 128, 0)
         st.set_option(qv.OPT_SUB_BITS, sub)
         st.set_option(qv.OPT_PREFETCH, pf)
+        st.set_option(qv.OPT_STAGE, stage)
         st.set_option(qv.OPT_TILE_QUBITS, k)
         m = qv.apply_circuit(st, c, tile_qubits=k)
         assert m["fused_passes"] > 0

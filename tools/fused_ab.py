@@ -21,7 +21,8 @@ import paper_2508_15545_b200 as qv  # noqa: E402
 VARIANTS = [("fused_sub3_k11", 1, 3, 0, 11, 0), ("fused_sub3_k12", 1, 3, 0, 12, 0), ("fused_sub4_k12", 1, 4, 0, 12, 0),
             ("fused_sub3_k10", 1, 3, 0, 10, 0), ("fused_sub3_k11_fma", 1, 3, 1, 11, 0),
             ("fused_sub3_k11_pf", 1, 3, 0, 11, 1), ("fused_sub3_k10_pf", 1, 3, 0, 10, 1),
-            ("fused_sub3_k12_pf", 1, 3, 0, 12, 1), ("fused_sub4_k11", 1, 4, 0, 11, 0), ("per_gate", 0, 3, 0, 11, 0)]
+            ("fused_sub3_k12_pf", 1, 3, 0, 12, 1), ("fused_sub4_k11", 1, 4, 0, 11, 0),
+            ("fused_sub4_k11_pf", 1, 4, 0, 11, 1), ("per_gate", 0, 3, 0, 11, 0)]
 
 
 def circuits(n):
@@ -39,6 +40,7 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--precision", type=int, default=128)
     ap.add_argument("--only", default="", help="comma-separated variant names (default: all)")
+    ap.add_argument("--stage", type=int, default=-1, help="QVG_OPT_STAGE for every variant (-1: default)")
     a = ap.parse_args()
     only = set(filter(None, a.only.split(",")))
     st = qv.StateVector.create(a.n, a.precision, 0)
@@ -57,6 +59,8 @@ def main():
             st.set_option(qv.OPT_SUB_BITS, sub)
             st.set_option(qv.OPT_FMA, fma)
             st.set_option(qv.OPT_PREFETCH, pf)
+            if a.stage >= 0:
+                st.set_option(qv.OPT_STAGE, a.stage)
             st.apply_gates(g)  # warm-up (and plan)
             st.reset_stats()
             ts = []
