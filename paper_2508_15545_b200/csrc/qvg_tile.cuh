@@ -54,7 +54,8 @@ struct TileGeom {
     int ngroups;          // register groups in this pass
     int nrec;             // records (headers + ops)
     int sub;              // subcube bits per thread (3 or 4)
-    int stage;            // bit 0: first group loads through shared memory; bit 1: last group stores through it
+    int stage;            // bit 0: first group loads through shared memory; bit 1: last group stores through it;
+                          // bit 2: prefetch the CTA's next tile into L2 (bulk prefetch per contiguous segment)
     int hiq[24];          // tile qubits >= lowc, ascending (tile-local bits lowc..k-1)
     uint64_t ntiles;      // 2^(n-k)
 };
@@ -175,6 +176,10 @@ __device__ __forceinline__ void cp_async_amp(float2 *dst, const float2 *src) {
     const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
 }
+// Bulk prefetch of `bytes` (multiple of 16) at a 16-B aligned address into L2.
+__device__ __forceinline__ void prefetch_l2(const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
@@ -235,6 +240,13 @@ k_tile(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams
     }
     for (uint64_t tile = blockIdx.x; tile < g.ntiles; tile += gridDim.x) {
         const uint64_t base = tile_base(tile);
+        if ((g.stage & 4) && tile + gridDim.x < g.ntiles) {
+            // the next tile's 2^nhi contiguous segments head for L2 while this
+            // tile computes; its loads then hit L2 instead of HBM
+            const uint64_t nb = tile_base(tile + gridDim.x);
+            const uint32_t seg = (uint32_t)sizeof(T) << g.lowc;
+            for (uint32_t h = threadIdx.x; h < nhi; h += blockDim.x) prefetch_l2(psi + (nb | offhi[h]), seg);
+        }
         if constexpr (PF) {
             cp_async_wait_all();
             __syncthreads();
