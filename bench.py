@@ -294,6 +294,32 @@ def fused_leg(qv, st, circ, line, args):
     st.set_option(qv.OPT_FUSE, 0)
 
 
+def pcie_bidir_gbs(host, st):
+    """The e2e roofline: pinned host<->device bandwidth with both directions
+    busy at once (what a pipelined e2e step needs), measured here on 4 GiB
+    each way with plain copies on two streams."""
+    import torch
+
+    nbytes = min(4 << 30, host.numel() * host.element_size())
+    h = host.view(torch.uint8)[:nbytes]
+    d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    h2 = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d2 = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    best = 0.0
+    for _ in range(2):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        with torch.cuda.stream(s1):
+            d.copy_(h, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h2.copy_(d2, non_blocking=True)
+        torch.cuda.synchronize()
+        best = max(best, 2 * nbytes / (time.perf_counter() - t0) / 1e9)
+    del d, d2, h2
+    return best
+
+
 def e2e_leg(qv, st, circ, recs, line, args):
     """The same metric through the public API with HOST buffers: every step
     copies a 16 GiB state from pinned host memory to the device, runs the sweep
@@ -341,7 +367,9 @@ def e2e_leg(qv, st, circ, recs, line, args):
         s.sync()
     ms = (time.perf_counter() - t0) * 1e3 / steps
     del states[1:]
+    pcie = pcie_bidir_gbs(bufs[0][0], st)
     line["e2e"] = {"value": len(circ) * count / (ms / 1e3), "unit": UNIT, "ms_per_step": ms,
+                   "pcie_bidir_gbs": pcie, "pcie_frac": (2 * count * 16 / (ms / 1e3) / 1e9) / pcie,
                    "latency_ms": latency, "latency_value": len(circ) * count / (latency / 1e3),
                    "steps": steps, "h2d_bytes_per_step": count * 16, "d2h_bytes_per_step": count * 16,
                    "hbm_passes_per_step": m["traversals"],
