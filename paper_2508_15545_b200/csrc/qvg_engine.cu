@@ -9,6 +9,7 @@
 #include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -204,7 +205,7 @@ void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *recs) {
     using T = typename Cplx<R>::T;
     const TileGeom &g = p.geom;
     if (g.nrec > kMaxTileRecs) throw std::runtime_error("internal: tile pass exceeds the record limit");
-    static TileParams prm;  // 25 KB; launch copies it into the parameter block
+    thread_local TileParams prm;  // 25 KB; the launch copies it into the parameter block (per host thread: states on different threads may launch concurrently)
     prm.g = g;
     std::memcpy(prm.ops, recs + p.op_begin, sizeof(TileOp) * g.nrec);
     const unsigned threads = 1u << (g.k - g.sub);  // one 2^sub-amplitude subcube per thread
@@ -223,12 +224,16 @@ void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *recs) {
                               : (fma ? k_tile<R, 3, true, 512, true> : k_tile<R, 3, false, 512, true>))
                 : small ? (fma ? k_tile<R, 3, true, 256, false> : k_tile<R, 3, false, 256, false>)
                         : (fma ? k_tile<R, 3, true, 512, false> : k_tile<R, 3, false, 512, false>);
-    static bool attr_set[2][2][2][2][2][2] = {};
-    bool &set = attr_set[sizeof(R) == 8][g.sub == 4][fma][small][pf][tiny];
-    if (!set) {
+    // The shared-memory opt-in is a per-device function attribute: set it once
+    // per (device, variant).
+    static std::atomic<uint64_t> attr_set[64];
+    const int variant = (sizeof(R) == 8 ? 1 : 0) | (g.sub == 4 ? 2 : 0) | (fma ? 4 : 0) | (small ? 8 : 0) |
+                        (pf ? 16 : 0) | (tiny ? 32 : 0);
+    std::atomic<uint64_t> &set = attr_set[s.device & 63];
+    if (!((set.load(std::memory_order_acquire) >> variant) & 1u)) {
         cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
                    "cudaFuncSetAttribute(k_tile)");
-        set = true;
+        set.fetch_or(1ull << variant, std::memory_order_acq_rel);
     }
     int per_sm = 0;
     cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (int)threads, smem), "occupancy(k_tile)");
