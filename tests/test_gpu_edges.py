@@ -135,3 +135,35 @@ def test_out_of_core_bit_identical(qv, oracle, prec):
             assert np.array_equal(host, oracle.simulate(n, gate_array(c)))
         else:  # complex64 contracts to FFMA differently per kernel plan: compare within 1e-6
             assert np.abs(host - want).max() <= 1e-6, (n, w)
+
+
+def test_states_on_concurrent_host_threads(qv, oracle):
+    """One state per host thread (the reference's single-owner rule,
+    reference cache.hpp:44-47); several threads may drive their own states at
+    once (the GIL is released). Fused passes build their parameter block per
+    thread, so concurrent launches do not race."""
+    import threading
+
+    circuits = [qv.random_circuit(14, 300, 100 + i) for i in range(4)]
+    wants = [oracle.simulate(14, gate_array(c)) for c in circuits]
+    got = [None] * len(circuits)
+    errors = []
+
+    def work(i):
+        try:
+            st = qv.StateVector.create(14, 128, 0)
+            for _ in range(5):
+                st.init_basis(0)
+                qv.apply_circuit(st, circuits[i])
+            got[i] = st.read_state()
+        except Exception as exc:  # surfaced below
+            errors.append(exc)
+
+    threads = [threading.Thread(target=work, args=(i,)) for i in range(len(circuits))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for i in range(len(circuits)):
+        assert np.array_equal(got[i], wants[i]), i
