@@ -78,8 +78,8 @@ enum qvg_option {
     QVG_OPT_EXCHANGE = 10,   /* sharded states: 0 copy exchange (NCCL send/recv; virtual: swap kernel),
                                 1 peer-memory exchange kernel, 2 peer exchange fused with the gate that
                                 triggered it, -1 auto (default: 2 for NCCL ranks whose peers map, else 1) */
-    QVG_OPT_PREFETCH = 11,   /* fused tile: prefetch of the CTA's next tile, 1 = cp.async into shared
-                                memory, 2 = bulk prefetch into L2 */
+    QVG_OPT_PREFETCH = 11,   /* fused tile: 1 = load the next tile's first-group amplitudes into
+                                registers during the current tile (8-amplitude subcubes only) */
     QVG_OPT_BATCH_EXCHANGE = 12, /* sharded: most global qubits one exchange swaps, 1..4 (default 4; 1 =
                                     pairwise exchanges only) */
     QVG_OPT_STAGE = 13       /* fused tile: a first/last register group holding tile bits 0..b-1 moves

@@ -99,7 +99,7 @@ struct qvg_state {
     bool fma = false;          // fused tile c128: DFMA arithmetic (not bit-identical to the reference)
     bool timing = false;       // bracket each qvg_apply with CUDA events -> stats.kernel_ms
     int exchange_mode = -1;    // QVG_OPT_EXCHANGE (-1 auto)
-    int prefetch_mode = 0;     // fused tile next-tile prefetch (QVG_OPT_PREFETCH): 1 cp.async to smem, 2 bulk to L2
+    int prefetch_mode = 0;     // fused tile next-tile prefetch (QVG_OPT_PREFETCH): 1 = into registers
     uint32_t batch_max = 4;    // sharded: most global qubits one exchange swaps (QVG_OPT_BATCH_EXCHANGE)
     uint32_t stage_bits = 3;   // fused tile: stage first/last group HBM access through shared memory (QVG_OPT_STAGE)
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
@@ -209,17 +209,14 @@ void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *recs) {
     prm.g = g;
     std::memcpy(prm.ops, recs + p.op_begin, sizeof(TileOp) * g.nrec);
     const unsigned threads = 1u << (g.k - g.sub);  // one 2^sub-amplitude subcube per thread
-    const bool pf = s.prefetch_mode == 1;
+    const bool pf = s.prefetch_mode == 1 && g.sub == 3;  // register prefetch needs the 8-amplitude subcube
     const size_t smem = (((sizeof(uint64_t) << g.nhi) + 15) & ~size_t(15)) +
-                        (g.ngroups > 1 || g.stage ? (sizeof(T) << g.k) : 0) + (pf ? (sizeof(T) << g.k) : 0);
+                        (g.ngroups > 1 || g.stage ? (sizeof(T) << g.k) : 0);
     const bool fma = s.fma && sizeof(R) == 8;  // complex64 always contracts
     const bool small = threads <= 256;
-    const bool tiny = threads <= 128;  // sub 4 at k <= 11: 128-thread CTAs, up to 168 registers
-    auto kern = g.sub == 4
-                    ? (tiny ? (pf ? (fma ? k_tile<R, 4, true, 128, true> : k_tile<R, 4, false, 128, true>)
-                                  : (fma ? k_tile<R, 4, true, 128, false> : k_tile<R, 4, false, 128, false>))
-                            : (pf ? (fma ? k_tile<R, 4, true, 256, true> : k_tile<R, 4, false, 256, true>)
-                                  : (fma ? k_tile<R, 4, true, 256, false> : k_tile<R, 4, false, 256, false>)))
+    const bool tiny = threads <= 128;  // sub 4 at k <= 11: 128-thread CTAs
+    auto kern = g.sub == 4 ? (tiny ? (fma ? k_tile<R, 4, true, 128, false> : k_tile<R, 4, false, 128, false>)
+                                   : (fma ? k_tile<R, 4, true, 256, false> : k_tile<R, 4, false, 256, false>))
                 : pf ? (small ? (fma ? k_tile<R, 3, true, 256, true> : k_tile<R, 3, false, 256, true>)
                               : (fma ? k_tile<R, 3, true, 512, true> : k_tile<R, 3, false, 512, true>))
                 : small ? (fma ? k_tile<R, 3, true, 256, false> : k_tile<R, 3, false, 256, false>)
@@ -253,7 +250,6 @@ PlanOptions plan_options(const qvg_state &s) {
     po.min_run = s.min_run;
     po.sub_bits = s.sub_bits;
     po.stage_bits = s.stage_bits;
-    po.l2_prefetch = s.prefetch_mode == 2;
     return po;
 }
 
@@ -443,7 +439,7 @@ int qvg_set_option(qvg_state *s, int key, int64_t value) {
         case QVG_OPT_FMA: s->fma = value != 0; break;
         case QVG_OPT_TIMING: s->timing = value != 0; break;
         case QVG_OPT_PREFETCH:
-            if (value < 0 || value > 2) throw Validation("prefetch must be 0, 1 (shared memory) or 2 (L2)");
+            if (value < 0 || value > 1) throw Validation("prefetch must be 0 or 1");
             s->prefetch_mode = (int)value;
             break;
         case QVG_OPT_STAGE:

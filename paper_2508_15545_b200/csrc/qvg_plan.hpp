@@ -100,7 +100,6 @@ struct PlanOptions {
     uint32_t stage_bits = 3; // stage a first/last group through shared memory when its bits
                              // include tile bits 0..stage_bits-1 (warp lanes >= 2^stage_bits
                              // amplitudes apart); 0 = never
-    bool l2_prefetch = false;  // tile passes prefetch each CTA's next tile into L2
 };
 
 // Ops per fused pass: with at most one group header per op the records fit
@@ -315,7 +314,7 @@ inline Plan make_plan(const qvg_gate *ops, uint64_t count, const PlanOptions &po
                 group.push_back(t);
             }
             close_group();
-            g.stage = po.l2_prefetch ? 4 : 0;
+            g.stage = 0;
             if (po.stage_bits > 0) {
                 if (first_low >= po.stage_bits) g.stage |= 1;
                 if (last_low >= po.stage_bits) g.stage |= 2;

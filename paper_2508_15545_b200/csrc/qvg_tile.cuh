@@ -54,8 +54,7 @@ struct TileGeom {
     int ngroups;          // register groups in this pass
     int nrec;             // records (headers + ops)
     int sub;              // subcube bits per thread (3 or 4)
-    int stage;            // bit 0: first group loads through shared memory; bit 1: last group stores through it;
-                          // bit 2: prefetch the CTA's next tile into L2 (bulk prefetch per contiguous segment)
+    int stage;            // bit 0: first group loads through shared memory; bit 1: last group stores through it
     int hiq[24];          // tile qubits >= lowc, ascending (tile-local bits lowc..k-1)
     uint64_t ntiles;      // 2^(n-k)
 };
@@ -167,31 +166,16 @@ __device__ __forceinline__ void group_diag_dispatch(int code, typename Cplx<R>::
 #undef QVG_GD
 }
 
-// cp.async of one amplitude (16 B complex128, 8 B complex64) into shared memory.
-__device__ __forceinline__ void cp_async_amp(double2 *dst, const double2 *src) {
-    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_amp(float2 *dst, const float2 *src) {
-    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
-}
-// Bulk prefetch of `bytes` (multiple of 16) at a 16-B aligned address into L2.
-__device__ __forceinline__ void prefetch_l2(const void *src, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
-
 // MAXT: the largest CTA this instantiation serves (2^(k-SUB) threads). The
 // minimum-blocks hint keeps 4 CTAs/SM (64 registers) at 256 threads: measured
 // faster than 3 CTAs with 80 registers and no spills (C3 1278 vs 1356 ms).
-// PF: the CTA prefetches its next tile into a second shared buffer with
-// cp.async while it computes the current one, so the first group's HBM latency
-// is off the critical path (the top stall without it: a DMUL waiting on the
-// first group's loads, long_scoreboard, profiles/r01_ncu_summary.md).
+// PF (SUB = 3 only): each thread loads the next tile's first-group amplitudes
+// into registers while it computes the current tile, so the first group's
+// HBM latency (the top stall without it: DMULs waiting on those loads,
+// long_scoreboard) overlaps compute. It costs 32 registers, so such CTAs run
+// at 2 per SM (16 warps, as many as the default 16-amplitude subcubes).
 template <class R, int SUB, bool FMA, int MAXT, bool PF>
-__global__ void __launch_bounds__(MAXT, ((MAXT <= 256 && SUB == 3) || (MAXT <= 128 && SUB == 4)) ? (PF ? 3 : 4) : 2)
+__global__ void __launch_bounds__(MAXT, PF ? 2 : (((MAXT <= 256 && SUB == 3) || (MAXT <= 128 && SUB == 4)) ? 4 : 2))
 k_tile(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams prm) {
     using T = typename Cplx<R>::T;
     constexpr int E = 1 << SUB;
@@ -204,7 +188,6 @@ k_tile(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams
     uint64_t *offhi = reinterpret_cast<uint64_t *>(smem_raw);
     T *sm = reinterpret_cast<T *>(smem_raw + (((sizeof(uint64_t) << g.nhi) + 15) & ~15ull));
     const bool use_sm = g.ngroups > 1 || g.stage != 0;
-    T *pf = sm + (use_sm ? (1u << g.k) : 0u);  // PF: the next tile (after the transpose buffer)
     const uint32_t nhi = 1u << g.nhi;
     const uint32_t lowm = (1u << g.lowc) - 1u;
     {  // the high-qubit offset table
@@ -225,32 +208,36 @@ k_tile(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams
             if (i < g.nhi) base = ins0(base, g.hiq[i]);
         return base;
     };
-    // PF: thread t copies local indices t + j*blockDim (coalesced segments)
-    auto prefetch = [&](uint64_t tile) {
-        const uint64_t b0 = tile_base(tile);
-#pragma unroll
-        for (int j = 0; j < E; ++j) {
-            const uint32_t l = threadIdx.x + (uint32_t)j * blockDim.x;
-            cp_async_amp(pf + swz(l), psi + (b0 | offhi[l >> g.lowc] | (l & lowm)));
-        }
-        cp_async_commit();
-    };
+    // The first group's layout is the same for every tile. A staged first
+    // group loads local indices t + j*blockDim (coalesced) and transposes
+    // through shared memory; otherwise each thread loads its own subcube.
+    uint32_t first_l0 = threadIdx.x;
+    int first_b[SUB];
     if constexpr (PF) {
-        if (blockIdx.x < g.ntiles) prefetch(blockIdx.x);
+        const uint64_t packed = ops[0].gtgt;
+#pragma unroll
+        for (int j = 0; j < SUB; ++j) first_b[j] = (int)((packed >> (8 * j)) & 0xff);
+#pragma unroll
+        for (int j = 0; j < SUB; ++j) first_l0 = (uint32_t)ins0(first_l0, first_b[j]);
+    }
+    auto load_first = [&](uint64_t tb, T(&dst)[E]) {
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+            uint32_t l = threadIdx.x + (uint32_t)r * blockDim.x;
+            if (!(g.stage & 1)) {
+                l = first_l0;
+#pragma unroll
+                for (int j = 0; j < SUB; ++j) l |= ((r >> j) & 1) ? (1u << first_b[j]) : 0u;
+            }
+            dst[r] = ld_amp(psi + (tb | offhi[l >> g.lowc] | (l & lowm)));
+        }
+    };
+    T nx[E];  // PF: the next tile's first-group amplitudes, in flight (unused otherwise)
+    if constexpr (PF) {
+        if (blockIdx.x < g.ntiles) load_first(tile_base(blockIdx.x), nx);
     }
     for (uint64_t tile = blockIdx.x; tile < g.ntiles; tile += gridDim.x) {
         const uint64_t base = tile_base(tile);
-        if ((g.stage & 4) && tile + gridDim.x < g.ntiles) {
-            // the next tile's 2^nhi contiguous segments head for L2 while this
-            // tile computes; its loads then hit L2 instead of HBM
-            const uint64_t nb = tile_base(tile + gridDim.x);
-            const uint32_t seg = (uint32_t)sizeof(T) << g.lowc;
-            for (uint32_t h = threadIdx.x; h < nhi; h += blockDim.x) prefetch_l2(psi + (nb | offhi[h]), seg);
-        }
-        if constexpr (PF) {
-            cp_async_wait_all();
-            __syncthreads();
-        }
         int rec = 0;
         for (int gi = 0; gi < g.ngroups; ++gi) {
             const int nops = ops[rec].tbit;
@@ -272,9 +259,15 @@ k_tile(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams
             T v[E];
             if (PF && gi == 0) {
 #pragma unroll
-                for (int r = 0; r < E; ++r) v[r] = pf[swz(lidx(r))];
-                __syncthreads();  // every thread has its subcube: refill the buffer
-                if (tile + gridDim.x < g.ntiles) prefetch(tile + gridDim.x);
+                for (int r = 0; r < E; ++r) v[r] = nx[r];
+                if (tile + gridDim.x < g.ntiles) load_first(tile_base(tile + gridDim.x), nx);
+                if (g.stage & 1) {  // v holds coalesced amplitudes: transpose to the group layout
+#pragma unroll
+                    for (int j = 0; j < E; ++j) sm[swz(threadIdx.x + (uint32_t)j * blockDim.x)] = v[j];
+                    __syncthreads();
+#pragma unroll
+                    for (int r = 0; r < E; ++r) v[r] = sm[swz(lidx(r))];
+                }
             } else if (gi == 0 && (g.stage & 1)) {
                 // the group's bits include the lowest tile bits, so its lanes
                 // would stride through HBM: load the tile coalesced (lane =

@@ -22,7 +22,6 @@ VARIANTS = [("fused_sub3_k11", 1, 3, 0, 11, 0), ("fused_sub3_k12", 1, 3, 0, 12, 
             ("fused_sub3_k10", 1, 3, 0, 10, 0), ("fused_sub3_k11_fma", 1, 3, 1, 11, 0),
             ("fused_sub3_k11_pf", 1, 3, 0, 11, 1), ("fused_sub3_k10_pf", 1, 3, 0, 10, 1),
             ("fused_sub3_k12_pf", 1, 3, 0, 12, 1), ("fused_sub4_k11", 1, 4, 0, 11, 0),
-            ("fused_sub4_k11_pf", 1, 4, 0, 11, 1), ("fused_sub4_k11_l2pf", 1, 4, 0, 11, 2),
             ("per_gate", 0, 3, 0, 11, 0)]
 
 
