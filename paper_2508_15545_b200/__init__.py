@@ -52,6 +52,7 @@ from ._core import (  # noqa: E402
     StateVector,
     ValidationError,
     top_amplitudes,
+    verify_equivalence,
     apply_circuit,
     apply_circuit_host,
     circuit_from_gates,

@@ -325,6 +325,47 @@ PYBIND11_MODULE(_core, m) {
           "File-backed apply: store -> HBM -> circuit on the GPU -> store; window_qubits > 0 (or a state larger "
           "than device memory) streams the file through two HBM windows instead");
 
+    m.def("verify_equivalence",
+          [](std::uint32_t max_qubits, std::uint64_t trials, std::uint32_t max_depth, std::uint64_t seed,
+             const std::string &scratch_dir, int device) {
+              (void)scratch_dir;  // the reference's store directory; device runs need none
+              VerifyOptions opts;
+              opts.max_qubits = max_qubits;
+              opts.trials = trials;
+              opts.max_depth = max_depth;
+              opts.seed = seed;
+              opts.device = device;
+              VerifyResult r;
+              {
+                  py::gil_scoped_release nogil;
+                  r = verify_equivalence(opts);
+              }
+              py::dict d;
+              d["trials"] = r.trials;
+              d["comparisons"] = r.comparisons;
+              d["max_deviation"] = r.max_deviation;
+              d["failures"] = r.failures.size();
+              d["passed"] = r.passed();
+              py::list details;
+              for (const VerifyFailure &f : r.failures) {
+                  py::dict e;
+                  e["trial"] = f.trial;
+                  e["n_qubits"] = f.n_qubits;
+                  e["depth"] = f.depth;
+                  e["config"] = f.config;
+                  e["deviation"] = f.deviation;
+                  if (f.first_divergent_gate) e["first_divergent_gate"] = *f.first_divergent_gate;
+                  else e["first_divergent_gate"] = py::none();
+                  details.append(e);
+              }
+              d["failure_details"] = details;
+              return d;
+          },
+          py::arg("max_qubits") = 10, py::arg("trials") = 200, py::arg("max_depth") = 30, py::arg("seed") = 1,
+          py::arg("scratch_dir") = "", py::arg("device") = 0,
+          "Random circuits (the reference's verify_equivalence draws) through every device configuration, "
+          "each compared with the one-pass-per-gate run");
+
     m.def("apply_circuit_host",
           [](py::buffer amps, const Circuit &circuit, std::uint32_t window_qubits, int device) {
               const py::buffer_info b = amps.request(true);

@@ -710,4 +710,95 @@ void apply_circuit(StateVector &state, const Circuit &circuit, const RunConfig &
     stamp();
 }
 
+// ---- verification (reference engine.cpp:253-340) -----------------------------------
+
+namespace {
+
+// reference engine.cpp:77-82
+std::uint64_t splitmix64(std::uint64_t x) {
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+
+// One device configuration run on ops[0..count) from |0...0>, read back.
+std::vector<amp_t> run_config(const std::string &cfg, std::uint32_t n, const std::vector<qvg_gate> &ops,
+                              std::size_t count, int device) {
+    std::vector<amp_t> out(std::size_t{1} << n);
+    if (cfg == "out-of-core") {
+        out.assign(out.size(), amp_t{0.0, 0.0});
+        out[0] = amp_t{1.0, 0.0};
+        qvg_stats st{};
+        check_status(qvg_apply_host(out.data(), n, 128, device, std::max<std::uint32_t>(4, n - 2), ops.data(), count,
+                                    &st));
+        return out;
+    }
+    std::uint32_t shards = 1;
+    if (cfg == "shards-2") shards = 2;
+    if (cfg == "shards-4") shards = 4;
+    StateVector sv = shards == 1 ? StateVector::create(n, 128, device)
+                                 : StateVector::create_sharded(n, 128, device, 0, shards, nullptr);
+    sv.set_option(QVG_OPT_FUSE, cfg == "per-gate" ? 0 : 1);
+    if (cfg == "fused-k5") sv.set_option(QVG_OPT_TILE_QUBITS, 5);
+    check_status(qvg_apply(sv.handle(), ops.data(), count));
+    sv.read(out.data(), 0, out.size());
+    return out;
+}
+
+double max_dev(const std::vector<amp_t> &a, const std::vector<amp_t> &b) {
+    double m = 0.0;
+    for (std::size_t i = 0; i < a.size(); ++i) {
+        const double d = std::abs(a[i] - b[i]);
+        if (!(d <= m)) m = d;  // NaN propagates
+    }
+    return m;
+}
+
+}  // namespace
+
+VerifyResult verify_equivalence(const VerifyOptions &opts) {
+    if (opts.min_qubits < 1 || opts.min_qubits > opts.max_qubits)
+        throw ValidationError("verify: qubit range must satisfy 1 <= min <= max");
+    if (opts.max_qubits > 24) throw ValidationError("verify: max qubits must be <= 24 (states are read back)");
+    if (opts.max_depth < 1) throw ValidationError("verify: depth must be >= 1");
+    VerifyResult result;
+    result.trials = opts.trials;
+    for (std::uint64_t trial = 0; trial < opts.trials; ++trial) {
+        std::mt19937_64 rng(splitmix64(opts.seed ^ (0x9e3779b97f4a7c15ull * (trial + 1))));
+        const auto n = static_cast<std::uint32_t>(opts.min_qubits +
+                                                  uniform_below(rng, opts.max_qubits - opts.min_qubits + 1));
+        const auto depth = static_cast<std::uint32_t>(1 + uniform_below(rng, opts.max_depth));
+        const Circuit circuit = random_circuit(rng, n, depth);
+        const std::vector<qvg_gate> ops = to_gates(circuit);
+        const std::vector<amp_t> reference = run_config("per-gate", n, ops, ops.size(), opts.device);
+        std::vector<std::string> configs = {"fused"};
+        if (n >= 5) configs.push_back("fused-k5");
+        if (n >= 3) configs.push_back("shards-2");
+        if (n >= 4) configs.push_back("shards-4");
+        if (n >= 6) configs.push_back("out-of-core");
+        for (const std::string &cfg : configs) {
+            const double dev = max_dev(reference, run_config(cfg, n, ops, ops.size(), opts.device));
+            result.comparisons += 1;
+            if (!(dev <= result.max_deviation)) result.max_deviation = dev;
+            if (dev <= opts.tolerance) continue;
+            VerifyFailure f;
+            f.trial = trial;
+            f.n_qubits = n;
+            f.depth = depth;
+            f.config = cfg;
+            f.deviation = dev;
+            for (std::size_t k = 1; k <= ops.size(); ++k) {  // first divergent prefix
+                if (!(max_dev(run_config("per-gate", n, ops, k, opts.device), run_config(cfg, n, ops, k, opts.device)) <=
+                      opts.tolerance)) {
+                    f.first_divergent_gate = k - 1;
+                    break;
+                }
+            }
+            result.failures.push_back(std::move(f));
+        }
+    }
+    return result;
+}
+
 }  // namespace qvsim

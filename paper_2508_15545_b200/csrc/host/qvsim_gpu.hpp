@@ -265,4 +265,40 @@ void apply_circuit(StateStore &store, const Circuit &circuit, const RunConfig &c
 // reference top_amplitudes (engine.cpp:511-544): k largest |a|^2, ties by index.
 std::vector<std::pair<std::uint64_t, amp_t>> top_amplitudes(const StateStore &store, std::size_t k);
 
+// reference verify_equivalence (engine.hpp:82-121, engine.cpp:253-340) for the
+// GPU strategy. Each trial draws the reference's own random circuit (same
+// per-trial seed derivation). Its reference run is one HBM pass per gate
+// (the kernels that restate apply_pair). It is compared against every other
+// device configuration: fused tiles (default and 5-qubit tiles), 2 and 4
+// virtual shards, and the out-of-core window path. A failure records the
+// first gate whose post-state already differs.
+struct VerifyOptions {
+    std::uint32_t min_qubits = 1;
+    std::uint32_t max_qubits = 10;
+    std::uint32_t max_depth = 30;
+    std::uint64_t trials = 200;
+    std::uint64_t seed = 1;
+    double tolerance = 1e-12;
+    int device = 0;
+};
+
+struct VerifyFailure {
+    std::uint64_t trial = 0;
+    std::uint32_t n_qubits = 0;
+    std::uint32_t depth = 0;
+    std::string config;
+    double deviation = 0.0;
+    std::optional<std::size_t> first_divergent_gate;
+};
+
+struct VerifyResult {
+    std::uint64_t trials = 0;
+    std::uint64_t comparisons = 0;
+    double max_deviation = 0.0;
+    std::vector<VerifyFailure> failures;
+    bool passed() const noexcept { return failures.empty(); }
+};
+
+VerifyResult verify_equivalence(const VerifyOptions &opts);
+
 }  // namespace qvsim

@@ -231,3 +231,15 @@ def test_timing_and_async_copies(qv):
     st.read_async(out)
     st.sync()
     assert np.array_equal(out, host)
+
+
+def test_verify_equivalence(qv):
+    """The reference's verify_equivalence draws (reference engine.cpp:253-340)
+    through every device configuration: each must equal the one-pass-per-gate
+    run bit for bit (max deviation exactly 0)."""
+    r = qv.verify_equivalence(max_qubits=12, trials=60, max_depth=40, seed=3)
+    assert r["passed"] and r["failures"] == 0 and r["failure_details"] == []
+    assert r["trials"] == 60 and r["comparisons"] >= 150
+    assert r["max_deviation"] == 0.0
+    with pytest.raises(qv.ValidationError):
+        qv.verify_equivalence(max_qubits=30)
