@@ -65,7 +65,7 @@ enum qvg_precision { QVG_C64 = 64, QVG_C128 = 128 };
 /* Option keys for qvg_set_option. */
 enum qvg_option {
     QVG_OPT_FUSE = 1,        /* 1: fused low/strided tile passes (default), 0: one pass per gate */
-    QVG_OPT_TILE_QUBITS = 2, /* qubits per fused tile, 5..12 (default 11) */
+    QVG_OPT_TILE_QUBITS = 2, /* qubits per fused tile, 5..12 (default 11; complex64 12) */
     QVG_OPT_CARRIERS = 3,    /* lowest qubits every tile keeps contiguous (default 3) */
     QVG_OPT_LOW_KERNEL = 4,  /* 1: warp-shuffle kernel for targets < 5, 0: k_pairs (default, measured faster) */
     QVG_OPT_MIN_RUN = 5,     /* bytes: a control/phase bit whose 1-runs are shorter is selected

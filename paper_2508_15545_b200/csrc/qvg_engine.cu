@@ -340,9 +340,10 @@ static int create_impl(uint32_t n, uint32_t precision, int device, uint32_t rank
         s->rank = rank;
         s->world = world;
         // Measured best tile shapes (profiles/r01_fused_ab.json, r01_fused_ab_c64.json):
-        // 2^11 amplitudes as 128 threads x 16 register amplitudes
-        // (C2/C1/C3 4-11% faster than 256 x 8 for complex128, 10-15% for complex64).
-        s->tile_qubits = 11;
+        // complex128: 2^11 amplitudes as 128 threads x 16 register amplitudes
+        // (C2/C1/C3 4-11% faster than 256 x 8); complex64: 2^12 as 256 x 16
+        // (C3 -11%, C2 -6% against 2^11; profiles/r01_fused_ab_c64.json).
+        s->tile_qubits = precision == QVG_C128 ? 11 : 12;
         s->sub_bits = 4;
         s->carriers = precision == QVG_C128 ? 3 : 4;
         try {

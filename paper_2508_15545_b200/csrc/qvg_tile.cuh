@@ -178,8 +178,15 @@ __device__ __forceinline__ void group_diag_dispatch(int code, typename Cplx<R>::
 #define QVG_SUB4_MINB 6  // CTAs/SM hint for 128-thread 16-amplitude tiles: 80 registers, no spills;
                          // measured faster than 4 CTAs with 128 (C1 -12%, C3 -3%, complex64 -4..15%)
 #endif
+#ifndef QVG_SUB4_256_MINB
+#define QVG_SUB4_256_MINB 3  // 256-thread 16-amplitude tiles (12-qubit tiles): 80 registers, no spills
+#endif
 template <class R, int SUB, bool FMA, int MAXT, bool PF>
-__global__ void __launch_bounds__(MAXT, PF ? 2 : (MAXT <= 128 && SUB == 4) ? QVG_SUB4_MINB : (MAXT <= 256 && SUB == 3) ? 4 : 2)
+__global__ void __launch_bounds__(MAXT, PF                         ? 2
+                                        : (MAXT <= 128 && SUB == 4) ? QVG_SUB4_MINB
+                                        : (MAXT <= 256 && SUB == 4) ? QVG_SUB4_256_MINB
+                                        : (MAXT <= 256 && SUB == 3) ? 4
+                                                                    : 2)
 k_tile(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams prm) {
     using T = typename Cplx<R>::T;
     constexpr int E = 1 << SUB;
