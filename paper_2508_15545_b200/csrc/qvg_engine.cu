@@ -104,8 +104,6 @@ struct qvg_state {
     uint32_t stage_bits = 3;   // fused tile: stage first/last group HBM access through shared memory (QVG_OPT_STAGE)
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
     // device scratch
-    TileOp *d_ops = nullptr;
-    size_t d_ops_cap = 0;
     double *d_partials = nullptr;
     double *d_probs = nullptr;
     qvg_stats stats{};
@@ -394,7 +392,6 @@ int qvg_destroy(qvg_state *s) {
             cudaEventDestroy(pr.second);
         }
         s->shards.release();
-        if (s->d_ops) cudaFree(s->d_ops);
         if (s->d_partials) cudaFree(s->d_partials);
         if (s->d_probs) cudaFree(s->d_probs);
         if (s->stream) cudaStreamDestroy(s->stream);
