@@ -294,16 +294,16 @@ def fused_leg(qv, st, circ, line, args):
     st.set_option(qv.OPT_FUSE, 0)
 
 
-def pcie_bidir_gbs(host, st):
+def pcie_bidir_gbs(host, host2):
     """The e2e roofline: pinned host<->device bandwidth with both directions
-    busy at once (what a pipelined e2e step needs), measured here on 4 GiB
-    each way with plain copies on two streams."""
+    busy at once (what a pipelined e2e step needs), measured here with a
+    state-sized (16 GiB) copy each way on two streams."""
     import torch
 
-    nbytes = min(4 << 30, host.numel() * host.element_size())
-    h = host.view(torch.uint8)[:nbytes]
+    nbytes = host.numel() * host.element_size()
+    h = host.view(torch.uint8)
+    h2 = host2.view(torch.uint8)
     d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
-    h2 = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
     d2 = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
     s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
     best = 0.0
@@ -316,7 +316,7 @@ def pcie_bidir_gbs(host, st):
             h2.copy_(d2, non_blocking=True)
         torch.cuda.synchronize()
         best = max(best, 2 * nbytes / (time.perf_counter() - t0) / 1e9)
-    del d, d2, h2
+    del d, d2
     return best
 
 
@@ -367,7 +367,7 @@ def e2e_leg(qv, st, circ, recs, line, args):
         s.sync()
     ms = (time.perf_counter() - t0) * 1e3 / steps
     del states[1:]
-    pcie = pcie_bidir_gbs(bufs[0][0], st)
+    pcie = pcie_bidir_gbs(bufs[0][0], bufs[1][0])
     line["e2e"] = {"value": len(circ) * count / (ms / 1e3), "unit": UNIT, "ms_per_step": ms,
                    "pcie_bidir_gbs": pcie, "pcie_frac": (2 * count * 16 / (ms / 1e3) / 1e9) / pcie,
                    "latency_ms": latency, "latency_value": len(circ) * count / (latency / 1e3),

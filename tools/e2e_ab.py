@@ -41,21 +41,25 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=30)
     ap.add_argument("--steps", type=int, default=6)
+    ap.add_argument("--states", default="2,3")
+    ap.add_argument("--chunks", default="1,8")
     a = ap.parse_args()
+    S_list = [int(x) for x in a.states.split(",")]
+    C_list = [int(x) for x in a.chunks.split(",")]
     n = a.n
     count = 1 << n
     circ = qv.haar_sweep_circuit(n, 2508)
     bufs = []
-    for _ in range(3):
+    for _ in range(max(S_list)):
         h = torch.empty(count * 2, dtype=torch.float64, pin_memory=True)
         arr = h.numpy().view(np.complex128)
         arr[:] = 1.0 / math.sqrt(count)
         bufs.append((h, arr))
     arrs = [b[1] for b in bufs]
-    states = [qv.StateVector.create(n, 128, 0) for _ in range(3)]
+    states = [qv.StateVector.create(n, 128, 0) for _ in range(max(S_list))]
     out = {}
-    for S in (2, 3):
-        for C in (1, 8):
+    for S in S_list:
+        for C in C_list:
             run(states[:S], arrs[:S], circ, 2, C)  # warm-up
             ms = run(states[:S], arrs[:S], circ, a.steps, C)
             out[f"states{S}_chunks{C}"] = {"ms_per_step": ms, "amp_updates_per_s": len(circ) * count / (ms / 1e3)}
