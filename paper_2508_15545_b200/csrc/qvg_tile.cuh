@@ -113,32 +113,34 @@ __device__ __forceinline__ void group_pair_dispatch(int code, typename Cplx<R>::
 // Diagonal op diag(d0, d1) over the register subcube. The target is on slot J
 // (-1: outside the group, then t1 is its value for this thread's whole
 // subcube). The control is on slot K (-1: none, or tested per thread/tile
-// before the call). D0: d0 != 1, so target-0 elements change too. All
-// compile-time, so e.g. a CZ with both bits in the group costs 2 complex
-// multiplies, not 8 predicated ones.
-template <class R, int SUB, int J, int K, bool D0, bool FMA>
-__device__ __forceinline__ void group_diag(typename Cplx<R>::T (&v)[1 << SUB], const double *uu, bool t1) {
+// before the call). J and K are compile-time, so e.g. a CZ with both bits in
+// the group costs 2 complex multiplies, not 8 predicated ones. Whether
+// d0 != 1 (target-0 elements change too) is a run-time flag: one body per
+// (J, K) keeps the kernel's code small, which measured 2-3% faster than a
+// body per (J, K, d0) (i-cache). Each element gets exactly one multiply, so
+// the bits are the same either way.
+template <class R, int SUB, int J, int K, bool FMA>
+__device__ __forceinline__ void group_diag_rt(typename Cplx<R>::T (&v)[1 << SUB], const double *uu, bool t1,
+                                              bool d0) {
     if constexpr (J < SUB && K < SUB && (J != K || J < 0)) {
-        R u[8];
-        u[6] = (R)uu[6];
-        u[7] = (R)uu[7];
-        if constexpr (D0) {
-            u[0] = (R)uu[0];
-            u[1] = (R)uu[1];
-        } else {
-            u[0] = R(1);
-            u[1] = R(0);
-        }
         if constexpr (J >= 0) {
+            const R d1r = (R)uu[6], d1i = (R)uu[7];
 #pragma unroll
             for (int r = 0; r < (1 << SUB); ++r) {
                 if (K >= 0 && !((r >> K) & 1)) continue;
-                if ((r >> J) & 1) v[r] = cmulx<FMA>(u[6], u[7], v[r]);
-                else if (D0) v[r] = cmulx<FMA>(u[0], u[1], v[r]);
+                if ((r >> J) & 1) v[r] = cmulx<FMA>(d1r, d1i, v[r]);
+            }
+            if (d0) {
+                const R d0r = (R)uu[0], d0i = (R)uu[1];
+#pragma unroll
+                for (int r = 0; r < (1 << SUB); ++r) {
+                    if (K >= 0 && !((r >> K) & 1)) continue;
+                    if (!((r >> J) & 1)) v[r] = cmulx<FMA>(d0r, d0i, v[r]);
+                }
             }
         } else {
-            if (!t1 && !D0) return;
-            const R dr = t1 ? u[6] : u[0], di = t1 ? u[7] : u[1];
+            if (!t1 && !d0) return;
+            const R dr = (R)(t1 ? uu[6] : uu[0]), di = (R)(t1 ? uu[7] : uu[1]);
 #pragma unroll
             for (int r = 0; r < (1 << SUB); ++r) {
                 if (K >= 0 && !((r >> K) & 1)) continue;
@@ -152,9 +154,11 @@ __device__ __forceinline__ void group_diag(typename Cplx<R>::T (&v)[1 << SUB], c
 template <class R, int SUB, bool FMA>
 __device__ __forceinline__ void group_diag_dispatch(int code, typename Cplx<R>::T (&v)[1 << SUB], const double *u,
                                                     bool t1) {
-#define QVG_GD(J, K)                                                                   \
-    case 8 * ((J) + 1) + (K) + 1: group_diag<R, SUB, J, K, false, FMA>(v, u, t1); break; \
-    case 64 + 8 * ((J) + 1) + (K) + 1: group_diag<R, SUB, J, K, true, FMA>(v, u, t1); break;
+#define QVG_GD(J, K)                                            \
+    case 8 * ((J) + 1) + (K) + 1:                               \
+    case 64 + 8 * ((J) + 1) + (K) + 1:                          \
+        group_diag_rt<R, SUB, J, K, FMA>(v, u, t1, code >= 64); \
+        break;
     switch (code) {
         QVG_GD(-1, -1) QVG_GD(-1, 0) QVG_GD(-1, 1) QVG_GD(-1, 2) QVG_GD(-1, 3)
         QVG_GD(0, -1) QVG_GD(0, 1) QVG_GD(0, 2) QVG_GD(0, 3)
