@@ -77,6 +77,8 @@ __device__ __forceinline__ float2 cmulx(float dr, float di, float2 a) {
 
 // Streaming loads/stores: every amplitude is touched once per pass, so mark
 // the lines evict-first in L2 (ld.global.cs / st.global.cs).
+// (Plain-cached loads/stores measured the same at n = 16..30, also for states
+// that fit in L2.)
 __device__ __forceinline__ double2 ld_amp(const double2 *p) { return __ldcs(p); }
 __device__ __forceinline__ float2 ld_amp(const float2 *p) { return __ldcs(p); }
 __device__ __forceinline__ void st_amp(double2 *p, double2 v) { __stcs(p, v); }
