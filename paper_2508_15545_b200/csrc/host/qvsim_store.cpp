@@ -7,13 +7,19 @@
 // file -> HBM load, the whole circuit on the device, and one HBM -> file store,
 // each in large pinned chunks double-buffered against the PCIe copies.
 #include <fcntl.h>
+#include <sys/mman.h>
 #include <sys/stat.h>
 #include <unistd.h>
 
 #include <algorithm>
+#include <exception>
+#include <mutex>
+#include <thread>
 #include <cerrno>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <queue>
 
@@ -25,7 +31,7 @@ namespace {
 
 constexpr std::uint64_t kHeaderBytes = 32;
 constexpr std::uint32_t kVersion = 1;
-constexpr std::uint64_t kChunkAmps = 1ull << 22;  // 64 MiB pinned staging chunks
+constexpr std::uint64_t kChunkAmps = 1ull << 24;  // 256 MiB pinned staging chunks
 
 [[noreturn]] void io_fail(const std::string &what, const std::string &path) {
     throw IoError(what + " '" + path + "': " + std::strerror(errno));
@@ -81,14 +87,42 @@ void pwrite_all(int fd, const void *src, std::uint64_t bytes, std::uint64_t off,
 }
 
 // Two pinned staging buffers from libqvg (cudaHostAlloc), freed on scope exit.
-struct Pinned {
+// Two page-locked staging buffers. Pinning 512 MiB costs ~0.3 s, more than
+// moving a 16 GiB state through them, so released buffers are kept in a
+// process-wide pool and reused by the next call (held until exit).
+class Pinned {
+  public:
     void *buf[2] = {nullptr, nullptr};
-    explicit Pinned(std::uint64_t bytes) {
-        for (auto &b : buf) check_status(qvg_host_alloc(bytes, &b));
+    explicit Pinned(std::uint64_t bytes) : bytes_(bytes) {
+        std::lock_guard<std::mutex> lock(mu());
+        auto &free = pool();
+        for (auto &b : buf) {
+            auto it = std::find_if(free.begin(), free.end(), [&](const auto &e) { return e.first == bytes; });
+            if (it != free.end()) {
+                b = it->second;
+                free.erase(it);
+            } else {
+                check_status(qvg_host_alloc(bytes, &b));
+            }
+        }
     }
     ~Pinned() {
+        std::lock_guard<std::mutex> lock(mu());
         for (auto *b : buf)
-            if (b) qvg_host_free(b);
+            if (b) pool().push_back({bytes_, b});
+    }
+    Pinned(const Pinned &) = delete;
+    Pinned &operator=(const Pinned &) = delete;
+
+  private:
+    std::uint64_t bytes_;
+    static std::mutex &mu() {
+        static std::mutex m;
+        return m;
+    }
+    static std::vector<std::pair<std::uint64_t, void *>> &pool() {
+        static auto *p = new std::vector<std::pair<std::uint64_t, void *>>();  // never destroyed: pinned until exit
+        return *p;
     }
 };
 
@@ -167,14 +201,68 @@ StateStore StateStore::open(const std::string &path) {
     }
 }
 
+namespace {
+
+// Large file transfers are split over host threads: a tmpfs / page-cache copy
+// is memcpy-bound at ~5 GB/s per thread, far below PCIe, and it dominates the
+// file-level drop-in (tools/store_e2e.py).
+template <class F> void split_io(std::uint64_t bytes, F &&piece) {
+    constexpr std::uint64_t kMinPiece = 4ull << 20;
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const std::uint64_t parts = std::min<std::uint64_t>({std::uint64_t{16}, hw, std::max<std::uint64_t>(1, bytes / kMinPiece)});
+    if (parts <= 1) {
+        piece(0, bytes);
+        return;
+    }
+    const std::uint64_t step = (bytes / parts + 15) & ~std::uint64_t{15};
+    std::vector<std::thread> pool;
+    std::vector<std::exception_ptr> errors(parts);
+    for (std::uint64_t i = 0; i < parts; ++i) {
+        const std::uint64_t a = std::min(bytes, i * step), b = std::min(bytes, a + step);
+        if (a >= b) break;
+        pool.emplace_back([&, i, a, b] {
+            try {
+                piece(a, b - a);
+            } catch (...) {
+                errors[i] = std::current_exception();
+            }
+        });
+    }
+    for (auto &t : pool) t.join();
+    for (auto &e : errors)
+        if (e) std::rethrow_exception(e);
+}
+
+}  // namespace
+
 void StateStore::read(amp_t *out, std::uint64_t offset, std::uint64_t count) const {
     if (offset > n_amps() || count > n_amps() - offset) throw ValidationError("amplitude range out of range");
-    pread_all(fd_, out, count * 16, kHeaderBytes + offset * 16, path_);
+    auto *dst = reinterpret_cast<unsigned char *>(out);
+    split_io(count * 16, [&](std::uint64_t at, std::uint64_t len) {
+        pread_all(fd_, dst + at, len, kHeaderBytes + offset * 16 + at, path_);
+    });
 }
 
 void StateStore::write(const amp_t *in, std::uint64_t offset, std::uint64_t count) {
     if (offset > n_amps() || count > n_amps() - offset) throw ValidationError("amplitude range out of range");
-    pwrite_all(fd_, in, count * 16, kHeaderBytes + offset * 16, path_);
+    const auto *src = reinterpret_cast<const unsigned char *>(in);
+    const std::uint64_t bytes = count * 16, start = kHeaderBytes + offset * 16;
+    // Concurrent pwrite()s to one file serialise on the inode lock, so large
+    // writes go through a shared mapping that many threads fill at once
+    // (5.9 -> tens of GB/s on tmpfs; tools/store_e2e.py). The file already
+    // has its full length (create() sizes it).
+    if (bytes >= (64ull << 20)) {
+        const std::uint64_t page = (std::uint64_t)::sysconf(_SC_PAGESIZE);
+        const std::uint64_t map_off = start & ~(page - 1), lead = start - map_off;
+        void *m = ::mmap(nullptr, lead + bytes, PROT_WRITE, MAP_SHARED, fd_, (off_t)map_off);
+        if (m != MAP_FAILED) {
+            unsigned char *dst = static_cast<unsigned char *>(m) + lead;
+            split_io(bytes, [&](std::uint64_t at, std::uint64_t len) { std::memcpy(dst + at, src + at, len); });
+            if (::munmap(m, lead + bytes) != 0) io_fail("munmap failed on", path_);
+            return;
+        }
+    }
+    split_io(bytes, [&](std::uint64_t at, std::uint64_t len) { pwrite_all(fd_, src + at, len, start + at, path_); });
 }
 
 amp_t StateStore::amplitude(std::uint64_t index) const {
@@ -261,18 +349,29 @@ void apply_circuit(StateStore &store, const Circuit &circuit, const RunConfig &c
     const std::uint64_t total = store.n_amps();
     const std::uint64_t chunk = std::min<std::uint64_t>(total, kChunkAmps);
     Pinned pin(chunk * 16);
-    // file -> pinned[i%2] -> HBM; the read of chunk i+1 overlaps the H2D of chunk i
+    const auto t_setup = std::chrono::steady_clock::now();
+    // file -> pinned[i%2] -> HBM; the read of chunk i+1 overlaps the H2D of
+    // chunk i. The buffer a read refills was last used by the H2D two chunks
+    // back, which the previous iteration's sync already waited for.
     std::uint64_t k = 0;
     for (std::uint64_t off = 0; off < total; off += chunk, ++k) {
         const std::uint64_t c = std::min(chunk, total - off);
-        if (k >= 2) sv.sync();  // the buffer about to be refilled was queued two chunks ago
         store.read(static_cast<amp_t *>(pin.buf[k % 2]), off, c);
+        sv.sync();  // the H2D of the previous chunk (it ran during this read)
         check_status(qvg_load_async(sv.handle(), pin.buf[k % 2], off, c));
         metrics.bytes_read += c * 16;
     }
+    const auto t_in = std::chrono::steady_clock::now();
     RunConfig dev_cfg = config;
     dev_cfg.sync = false;
     apply_circuit(sv, circuit, dev_cfg, metrics);
+    if (std::getenv("QVG_TRACE")) {
+        sv.sync();
+        std::fprintf(stderr, "[qvg] store apply: setup %.1f ms, file->HBM %.1f ms, gates %.1f ms\n",
+                     std::chrono::duration<double, std::milli>(t_setup - t0).count(),
+                     std::chrono::duration<double, std::milli>(t_in - t_setup).count(),
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_in).count());
+    }
     // HBM -> pinned[i%2] -> file; the D2H of chunk i+1 overlaps the write of chunk i
     k = 0;
     std::uint64_t pending_off = 0, pending_c = 0;
