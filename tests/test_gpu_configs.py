@@ -149,3 +149,30 @@ def test_config2_n28_bit_exact_vs_oracle(qv, oracle):
         st, _ = run(qv, c, fuse)
         assert np.array_equal(st.read_state(), want), fuse
         del st
+
+
+def test_config3_grid_n24_bit_exact_vs_oracle(qv, oracle):
+    """Config 3's generator on a 4x6 grid (n=24, 24 cycles of sqrt-X/Y/W and
+    CZ patterns, ~830 ops) against the oracle, fused and per gate."""
+    c = qv.grid_circuit(4, 6, 24, 1)
+    assert c.n_qubits == 24
+    want = oracle.simulate(24, gate_array(c))
+    for fuse in (True, False):
+        st, m = run(qv, c, fuse)
+        assert np.array_equal(st.read_state(), want), fuse
+        del st
+
+
+@pytest.mark.parametrize("world", [4, 8])
+def test_config4_layers_n24_sharded_bit_exact_vs_oracle(qv, oracle, world):
+    """Config 4's layer circuit at n=24 over 4 / 8 virtual shards (batched and
+    pairwise exchanges) against the oracle."""
+    c = qv.u3_ladder_circuit(24, 6, 4)
+    want = oracle.simulate(24, gate_array(c))
+    for batch in (1, 4):
+        st = qv.StateVector.create_sharded(24, 128, 0, 0, world, None)
+        st.set_option(qv.OPT_BATCH_EXCHANGE, batch)
+        m = qv.apply_circuit(st, c)
+        assert m["exchanges"] > 0
+        assert np.array_equal(st.read_state(), want), (world, batch)
+        del st
