@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define QVG_ABI_VERSION 1
+#define QVG_ABI_VERSION 2  /* 2: qvg_stats.fused_exchanges, multi-exchange steps, options 10-13 */
 
 /* Status codes -> reference exception types (error.hpp:10-50). */
 enum qvg_status {

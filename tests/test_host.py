@@ -171,7 +171,7 @@ def test_capi_exports_every_declared_symbol(qv):
     for name in names:
         assert hasattr(lib, name), name
     lib.qvg_abi_version.restype = ctypes.c_int
-    assert lib.qvg_abi_version() == qv.QVG_ABI_VERSION == 1
+    assert lib.qvg_abi_version() == qv.QVG_ABI_VERSION == 2
 
 
 @pytest.mark.skipif(cuda_present(), reason="checks the no-device error path")
