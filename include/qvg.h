@@ -82,8 +82,10 @@ enum qvg_option {
                                 registers during the current tile (8-amplitude subcubes only) */
     QVG_OPT_BATCH_EXCHANGE = 12, /* sharded: most global qubits one exchange swaps, 1..4 (default 4; 1 =
                                     pairwise exchanges only) */
-    QVG_OPT_STAGE = 13       /* fused tile: a first/last register group holding tile bits 0..b-1 moves
+    QVG_OPT_STAGE = 13,      /* fused tile: a first/last register group holding tile bits 0..b-1 moves
                                 its HBM data through shared memory, coalesced (default b = 3; 0 never) */
+    QVG_OPT_GRAPH = 14       /* 1: unsharded states replay a repeated op list as a captured CUDA graph
+                                (no per-pass host planning/launch cost; default 0) */
 };
 
 /* Counters (the reference's Metrics, metrics.hpp:14-30, plus the GPU pass

@@ -39,6 +39,7 @@ from ._core import (  # noqa: E402
     OPT_PREFETCH,
     OPT_BATCH_EXCHANGE,
     OPT_STAGE,
+    OPT_GRAPH,
     OPT_TILE_QUBITS,
     QVG_ABI_VERSION,
     CapacityError,

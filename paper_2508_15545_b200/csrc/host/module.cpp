@@ -454,4 +454,5 @@ PYBIND11_MODULE(_core, m) {
     m.attr("OPT_PREFETCH") = (int)QVG_OPT_PREFETCH;
     m.attr("OPT_BATCH_EXCHANGE") = (int)QVG_OPT_BATCH_EXCHANGE;
     m.attr("OPT_STAGE") = (int)QVG_OPT_STAGE;
+    m.attr("OPT_GRAPH") = (int)QVG_OPT_GRAPH;
 }

@@ -102,6 +102,16 @@ struct qvg_state {
     int prefetch_mode = 0;     // fused tile next-tile prefetch (QVG_OPT_PREFETCH): 1 = into registers
     uint32_t batch_max = 4;    // sharded: most global qubits one exchange swaps (QVG_OPT_BATCH_EXCHANGE)
     uint32_t stage_bits = 3;   // fused tile: stage first/last group HBM access through shared memory (QVG_OPT_STAGE)
+    bool graph = false;        // QVG_OPT_GRAPH: replay repeated op lists as captured CUDA graphs
+    struct GraphEntry {
+        uint64_t key = 0;
+        std::vector<qvg_gate> ops;
+        cudaGraphExec_t exec = nullptr;
+        qvg_stats delta{};
+        uint64_t last_use = 0;
+    };
+    std::vector<GraphEntry> graphs;  // small LRU cache
+    uint64_t graph_clock = 0;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
     // device scratch
     double *d_partials = nullptr;
@@ -280,6 +290,86 @@ void run_local(qvg_state &s, void *psi, const qvg_gate *ops, uint64_t count) {
     cuda_check(cudaGetLastError(), "kernel launch");
 }
 
+void drop_graphs(qvg_state &s) {
+    for (auto &g : s.graphs)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+    s.graphs.clear();
+}
+
+// Everything the plan of an op list depends on besides the ops themselves.
+uint64_t plan_signature(const qvg_state &s) {
+    uint64_t h = 1469598103934665603ull;
+    auto mix = [&](uint64_t v) { h = (h ^ v) * 1099511628211ull; };
+    mix(s.fuse); mix(s.tile_qubits); mix(s.carriers); mix(s.low_kernel); mix(s.min_run); mix(s.pred_store);
+    mix(s.sub_bits); mix(s.fma); mix(s.stage_bits); mix((uint64_t)s.prefetch_mode); mix(s.L); mix(s.precision);
+    return h;
+}
+
+uint64_t ops_hash(const qvg_gate *ops, uint64_t count, uint64_t seed) {
+    uint64_t h = seed;
+    const auto *b = reinterpret_cast<const unsigned char *>(ops);
+    for (uint64_t i = 0; i < count * sizeof(qvg_gate); ++i) h = (h ^ b[i]) * 1099511628211ull;
+    return h;
+}
+
+qvg_stats stats_diff(const qvg_stats &a, const qvg_stats &b) {
+    qvg_stats d{};
+    d.passes = a.passes - b.passes;
+    d.fused_passes = a.fused_passes - b.fused_passes;
+    d.kernel_launches = a.kernel_launches - b.kernel_launches;
+    d.bytes_moved = a.bytes_moved - b.bytes_moved;
+    return d;
+}
+
+// Unsharded states with QVG_OPT_GRAPH: an op list seen before (same bytes,
+// same plan options) replays as one captured CUDA graph; a new one is
+// captured while it runs. Removes the per-pass host planning and launch
+// cost that bounds small states.
+void apply_graph(qvg_state &s, const qvg_gate *ops, uint64_t count) {
+    const uint64_t key = ops_hash(ops, count, plan_signature(s));
+    for (auto &g : s.graphs) {
+        if (g.key == key && g.ops.size() == count &&
+            std::memcmp(g.ops.data(), ops, count * sizeof(qvg_gate)) == 0) {
+            cuda_check(cudaGraphLaunch(g.exec, s.stream), "cudaGraphLaunch");
+            s.stats.passes += g.delta.passes;
+            s.stats.fused_passes += g.delta.fused_passes;
+            s.stats.kernel_launches += g.delta.kernel_launches;
+            s.stats.bytes_moved += g.delta.bytes_moved;
+            g.last_use = ++s.graph_clock;
+            return;
+        }
+    }
+    const qvg_stats before = s.stats;
+    cudaGraph_t graph = nullptr;
+    cuda_check(cudaStreamBeginCapture(s.stream, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+    try {
+        run_local(s, s.shards.bufs[0], ops, count);
+    } catch (...) {
+        cudaStreamEndCapture(s.stream, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        s.stats = before;
+        throw;
+    }
+    cuda_check(cudaStreamEndCapture(s.stream, &graph), "cudaStreamEndCapture");
+    qvg_state::GraphEntry e;
+    e.key = key;
+    e.ops.assign(ops, ops + count);
+    e.delta = stats_diff(s.stats, before);
+    e.last_use = ++s.graph_clock;
+    const cudaError_t inst = cudaGraphInstantiate(&e.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    cuda_check(inst, "cudaGraphInstantiate");
+    cuda_check(cudaGraphLaunch(e.exec, s.stream), "cudaGraphLaunch");
+    constexpr size_t kMaxGraphs = 8;
+    if (s.graphs.size() >= kMaxGraphs) {
+        auto lru = std::min_element(s.graphs.begin(), s.graphs.end(),
+                                    [](const auto &a, const auto &b) { return a.last_use < b.last_use; });
+        cudaGraphExecDestroy(lru->exec);
+        s.graphs.erase(lru);
+    }
+    s.graphs.push_back(std::move(e));
+}
+
 void set_device(const qvg_state *s) { cuda_check(cudaSetDevice(s->device), "cudaSetDevice"); }
 
 void check_state(const qvg_state *s) {
@@ -391,6 +481,7 @@ int qvg_destroy(qvg_state *s) {
             cudaEventDestroy(pr.first);
             cudaEventDestroy(pr.second);
         }
+        drop_graphs(*s);
         s->shards.release();
         if (s->d_partials) cudaFree(s->d_partials);
         if (s->d_probs) cudaFree(s->d_probs);
@@ -439,6 +530,10 @@ int qvg_set_option(qvg_state *s, int key, int64_t value) {
         case QVG_OPT_PREFETCH:
             if (value < 0 || value > 1) throw Validation("prefetch must be 0 or 1");
             s->prefetch_mode = (int)value;
+            break;
+        case QVG_OPT_GRAPH:
+            s->graph = value != 0;
+            if (!s->graph) drop_graphs(*s);
             break;
         case QVG_OPT_STAGE:
             if (value < 0 || value > 12) throw Validation("stage must be 0 (never) .. 12");
@@ -533,7 +628,8 @@ int qvg_apply(qvg_state *s, const qvg_gate *ops, uint64_t count) {
             for (auto &e : ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
             cuda_check(cudaEventRecord(ev[0], s->stream), "cudaEventRecord");
         }
-        shard_apply(*s, s->shards, ops, count);
+        if (s->graph && s->world == 1 && count > 0) apply_graph(*s, ops, count);
+        else shard_apply(*s, s->shards, ops, count);
         if (s->timing) {
             cuda_check(cudaEventRecord(ev[1], s->stream), "cudaEventRecord");
             s->pending.push_back({ev[0], ev[1]});

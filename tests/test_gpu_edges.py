@@ -167,3 +167,31 @@ def test_states_on_concurrent_host_threads(qv, oracle):
     assert not errors, errors
     for i in range(len(circuits)):
         assert np.array_equal(got[i], wants[i]), i
+
+
+def test_graph_replay_bit_identical(qv, oracle):
+    """QVG_OPT_GRAPH: a repeated op list replays as a captured CUDA graph with
+    the same results and pass accounting; a changed option or op list
+    captures anew."""
+    n = 14
+    c = qv.random_circuit(n, 300, 5)
+    want = oracle.simulate(n, gate_array(c))
+    st = qv.StateVector.create(n, 128, 0)
+    st.set_option(qv.OPT_GRAPH, 1)
+    passes = []
+    for rep in range(3):
+        st.init_basis(0)
+        st.reset_stats()
+        qv.apply_circuit(st, c)
+        passes.append(st.stats()["passes"])
+        assert np.array_equal(st.read_state(), want), rep
+    assert passes[0] == passes[1] == passes[2] > 0
+    for fuse in (False, True):  # other plan options -> another graph
+        st.init_basis(0)
+        qv.apply_circuit(st, c, fuse=fuse)
+        assert np.array_equal(st.read_state(), want), fuse
+    c2 = qv.random_circuit(n, 50, 6)
+    st.init_basis(0)
+    qv.apply_circuit(st, c2)
+    assert np.array_equal(st.read_state(), oracle.simulate(n, gate_array(c2)))
+    st.set_option(qv.OPT_GRAPH, 0)
