@@ -1091,7 +1091,7 @@ int qvg_shard_schedule(uint32_t n_qubits, uint32_t world, const qvg_gate *ops, u
         // exchange may swap (0 or 1: pairwise exchanges only)
         const uint32_t kmax = std::max<uint32_t>(1, ((uint32_t)canonicalize >> 8) & 0xf);
         schedule_ops(n_qubits, L, ops, count, map, out, kmax);
-        if (canonicalize & 1) schedule_canonicalize(n_qubits, L, map, out);
+        if (canonicalize & 1) schedule_canonicalize(n_qubits, L, map, out, kmax);
         if (nsteps) *nsteps = out.size();
         if (steps) std::memcpy(steps, out.data(), std::min<uint64_t>(cap, out.size()) * sizeof(ShardStep));
     });

@@ -221,7 +221,29 @@ inline void schedule_ops(uint32_t n, uint32_t L, const qvg_gate *ops, uint64_t c
 }
 
 // Steps that bring the map back to the identity (canonical index order).
-inline void schedule_canonicalize(uint32_t n, uint32_t L, QubitMap &map, std::vector<ShardStep> &out) {
+inline void schedule_canonicalize(uint32_t n, uint32_t L, QubitMap &map, std::vector<ShardStep> &out,
+                                  uint32_t kmax = 1) {
+    // Batched first: every global position whose logical qubit sits on a
+    // high local position trades with it in one multi-exchange (k <= 4).
+    if (kmax >= 2) {
+        std::vector<std::pair<uint32_t, uint32_t>> batch;
+        for (uint32_t p = L; p < n && batch.size() < std::min<uint32_t>(kmax, 4); ++p) {
+            if (map.inv[p] == p) continue;
+            const uint32_t cur = map.perm[p];
+            if (cur < L && cur >= min_exchange_lpos(L)) batch.push_back({p, cur});
+        }
+        if (batch.size() >= 2) {
+            ShardStep ex{};
+            ex.type = STEP_MULTI_EXCHANGE;
+            for (size_t i = 0; i < batch.size(); ++i) {
+                ex.gpos |= 1u << (batch[i].first - L);
+                ex.lpos |= batch[i].second << (8 * i);
+            }
+            ex.lpos2 = (uint32_t)batch.size();
+            out.push_back(ex);
+            for (const auto &pr : batch) map.swap_phys(pr.first, pr.second);
+        }
+    }
     auto exchange = [&](uint32_t gpos, uint32_t lpos) {
         if (lpos < min_exchange_lpos(L)) {  // small blocks: move the qubit up first
             ShardStep sw{};

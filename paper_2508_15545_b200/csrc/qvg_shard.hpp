@@ -529,7 +529,7 @@ inline void shard_apply(qvg_state &s, ShardSet &set, const qvg_gate *ops, uint64
 inline void shard_canonicalize(qvg_state &s, ShardSet &set) {
     if (set.world == 1 || set.map.identity()) return;
     std::vector<ShardStep> steps;
-    schedule_canonicalize(set.n, set.L, set.map, steps);
+    schedule_canonicalize(set.n, set.L, set.map, steps, shard_batch_max(s));
     run_steps(s, set, steps);
 }
 
