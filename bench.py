@@ -145,6 +145,13 @@ def algorithmic_bytes(n, rec, S=16):
     return min(b * max(1, 32 // run) if run < 32 else b, 2 * (1 << n) * S)
 
 
+def gate_label(rec):
+    """'U q' for a single-qubit op, 'CX c->t' style for a controlled one."""
+    kind, target = (int(x) for x in np.frombuffer(rec[:8].tobytes(), np.uint32))
+    control = int(np.frombuffer(rec[8:12].tobytes(), np.int32)[0])
+    return f"U {target}" if kind == 0 else f"C{control}->{target}"
+
+
 def kernel_of(n, rec):
     """Launch class of a per-gate pass: every sweep op runs k_pairs (the
     warp-shuffle k_low is off by default, profiles/r01_kernel_ab.json);
@@ -262,6 +269,9 @@ def run_ours(args, rank, world, dist):
                      "launch_ms": dom_ms / dom_n, "share_of_step": dom_ms / mean_op.sum()},
         "per_kernel": {k: {"launches_per_step": v[2], "ms_per_launch": v[0] / v[2],
                            "gbs": (v[1] / v[2]) / ((v[0] / v[2]) / 1e3) / 1e9} for k, v in share.items()},
+        # per-gate time and HBM GB/s, individually
+        "per_gate": [{"op": i, "gate": gate_label(recs[i]), "ms": round(float(mean_op[i]), 4),
+                      "gbs": round(local_bytes[i] / (mean_op[i] / 1e3) / 1e9, 1)} for i in range(nops)],
         "gpu_launches": int(stats["kernel_launches"]),
         "exchanges_per_step": stats["exchanges"] / args.steps,
         "clocks": sampler.summary(),
