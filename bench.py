@@ -274,6 +274,13 @@ def run_ours(args, rank, world, dist):
                       "gbs": round(local_bytes[i] / (mean_op[i] / 1e3) / 1e9, 1)} for i in range(nops)],
         "gpu_launches": int(stats["kernel_launches"]),
         "exchanges_per_step": stats["exchanges"] / args.steps,
+        # N > 1: the exchange traffic's NVLink floor (per-GPU bytes sent at the
+        # measured 770 GB/s peer copy, B200_PROFILING.md) against the step
+        "exchange_roofline": None if world == 1 else {
+            "bound": "nvlink", "bytes_per_step_per_gpu": stats["exchange_bytes"] / args.steps,
+            "peak_gbs": 770.0, "peak_kind": "measured peer copy per direction (B200_PROFILING.md)",
+            "floor_ms": stats["exchange_bytes"] / args.steps / 770e9 * 1e3,
+            "floor_frac_of_step": (stats["exchange_bytes"] / args.steps / 770e9 * 1e3) / ms_step},
         "clocks": sampler.summary(),
     }
     return st, circ, recs, line, n
