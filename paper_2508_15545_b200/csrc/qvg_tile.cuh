@@ -181,8 +181,8 @@ __device__ __forceinline__ void group_diag_dispatch(int code, typename Cplx<R>::
 // long_scoreboard) overlaps compute. It costs 32 registers, so such CTAs run
 // at 2 per SM (16 warps, as many as the default 16-amplitude subcubes).
 #ifndef QVG_SUB4_MINB
-#define QVG_SUB4_MINB 6  // CTAs/SM hint for 128-thread 16-amplitude tiles: 80 registers, no spills;
-                         // measured faster than 4 CTAs with 128 (C1 -12%, C3 -3%, complex64 -4..15%)
+#define QVG_SUB4_MINB 5  // CTAs/SM hint for 128-thread 16-amplitude tiles: 96 registers, no spills.
+                         // 5 vs 6 (80 registers, spills): C2 -5%, C0-style -5%, C1 +3%; vs 4 (128): better everywhere
 #endif
 #ifndef QVG_SUB4_256_MINB
 #define QVG_SUB4_256_MINB 3  // 256-thread 16-amplitude tiles (12-qubit tiles): 80 registers, no spills
