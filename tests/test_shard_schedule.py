@@ -435,3 +435,23 @@ def test_gloo_peer_exchange_protocol_bit_identical(world, batch):
         ok, fused = q.get(timeout=10)
         assert ok, (fn, world)
         assert fused > 0 or batch > 1, (fn, world)
+
+
+# --- property test: random circuits, shard counts and batching ------------------------
+from hypothesis import given, settings, strategies as hs  # noqa: E402
+
+
+@settings(max_examples=40, deadline=None)
+@given(n=hs.integers(4, 9), g=hs.integers(1, 3), depth=hs.integers(1, 120), seed=hs.integers(0, 2**32 - 1),
+       batch=hs.sampled_from([1, 2, 4]))
+def test_schedule_property_random_circuits(qv, oracle, n, g, depth, seed, batch):
+    """Any seeded random circuit (the reference's generator), any shard count
+    with n >= g + 2, pairwise or batched exchanges: executing the schedule on
+    CPU shards reproduces the oracle bit for bit, and the canonical restore
+    leaves the qubit map at the identity."""
+    if n < g + 2:
+        return
+    c = qv.random_circuit(n, depth, seed)
+    steps = schedule(qv, c, 1 << g, canonicalize=True, batch=batch)
+    want = oracle.simulate(n, gate_array(c))
+    assert np.array_equal(emulate(oracle, n, 1 << g, steps), want)
