@@ -243,3 +243,27 @@ def test_verify_equivalence(qv):
     assert r["max_deviation"] == 0.0
     with pytest.raises(qv.ValidationError):
         qv.verify_equivalence(max_qubits=30)
+
+
+# --- property test: every option combination stays bit-exact -------------------------
+from hypothesis import HealthCheck, given, settings, strategies as hs  # noqa: E402
+
+
+@settings(max_examples=80, deadline=None, suppress_health_check=[HealthCheck.function_scoped_fixture])
+@given(n=hs.integers(2, 14), depth=hs.integers(1, 150), seed=hs.integers(0, 2**32 - 1),
+       fuse=hs.booleans(), tile=hs.integers(5, 12), sub=hs.sampled_from([3, 4]), stage=hs.integers(0, 3),
+       g=hs.integers(0, 2), exchange=hs.integers(0, 2), batch=hs.sampled_from([1, 4]), graph=hs.booleans())
+def test_random_options_bit_exact(qv, oracle, n, depth, seed, fuse, tile, sub, stage, g, exchange, batch, graph):
+    if n < 2 * g + 2:
+        g = 0
+    c = qv.random_circuit(n, depth, seed)
+    want = oracle.simulate(n, gate_array(c))
+    st = (qv.StateVector.create(n, 128, 0) if g == 0
+          else qv.StateVector.create_sharded(n, 128, 0, 0, 1 << g, None))
+    for key, val in ((qv.OPT_SUB_BITS, sub), (qv.OPT_STAGE, stage), (qv.OPT_EXCHANGE, exchange),
+                     (qv.OPT_BATCH_EXCHANGE, batch), (qv.OPT_GRAPH, int(graph))):
+        st.set_option(key, val)
+    for _ in range(2 if graph else 1):  # a graph replays on the second run
+        st.init_basis(0)
+        qv.apply_circuit(st, c, fuse=fuse, tile_qubits=tile)
+        assert np.array_equal(st.read_state(), want), (n, depth, seed, fuse, tile, sub, stage, g)
