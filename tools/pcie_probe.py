@@ -1,3 +1,8 @@
+"""Pinned host<->device copy bandwidth: H2D, D2H, and both at once on two
+streams (16 GiB each), the ceiling of bench.py's e2e leg.
+
+    python tools/pcie_probe.py
+"""
 import torch, time
 n = 16 << 30
 h1 = torch.empty(n, dtype=torch.uint8, pin_memory=True)

@@ -1,5 +1,13 @@
-import os, sys, time
-sys.path.insert(0, '/root/repo')
+"""Raw QVSV file read throughput through StateStore.read_state (n=30 file in
+/dev/shm) and the Kahan norm.
+
+    python tools/store_io_probe.py
+"""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import paper_2508_15545_b200 as qv
 n = 30

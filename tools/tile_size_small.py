@@ -1,5 +1,13 @@
-import sys, time, statistics
-sys.path.insert(0, '/root/repo')
+"""Tile size x register subcube at small n (config 0's circuit): passes and
+device ms per call.
+
+    python tools/tile_size_small.py
+"""
+import os
+import statistics
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2508_15545_b200 as qv
 for n in (16, 20, 22):
