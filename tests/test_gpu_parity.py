@@ -267,3 +267,26 @@ def test_random_options_bit_exact(qv, oracle, n, depth, seed, fuse, tile, sub, s
         st.init_basis(0)
         qv.apply_circuit(st, c, fuse=fuse, tile_qubits=tile)
         assert np.array_equal(st.read_state(), want), (n, depth, seed, fuse, tile, sub, stage, g)
+
+
+# --- direct parity with the unmodified reference engine (oracle/_ref) ----------------
+def test_bit_exact_vs_reference_engine_live(qv):
+    """The reference's own engine (compiled from its sources into oracle/_ref,
+    strategy paired-cached-parallel) and the GPU path on the same seeded
+    circuits at n = 10..18: identical amplitudes, bit for bit."""
+    from oracle.oracle import RefEngine
+
+    if not RefEngine.available():
+        pytest.skip("oracle/_ref not built")
+    eng = RefEngine()
+    rng = np.random.default_rng(11)
+    for trial in range(16):
+        n = int(rng.integers(10, 19))
+        c = qv.random_circuit(n, int(rng.integers(50, 400)), 500 + trial)
+        with eng.store(n, block_amps=1 << min(n - 2, 14)) as ref:
+            ref.apply(gate_array(c), "paired-cached-parallel", 4, 4 * 4 * (16 << min(n - 2, 14)))
+            want = ref.read()
+        for fuse in (True, False):
+            st = qv.StateVector.create(n, 128, 0)
+            qv.apply_circuit(st, c, fuse=fuse)
+            assert np.array_equal(st.read_state(), want), (trial, n, fuse)
