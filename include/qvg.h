@@ -84,8 +84,10 @@ enum qvg_option {
                                     pairwise exchanges only) */
     QVG_OPT_STAGE = 13,      /* fused tile: a first/last register group holding tile bits 0..b-1 moves
                                 its HBM data through shared memory, coalesced (default b = 3; 0 never) */
-    QVG_OPT_GRAPH = 14       /* 1: unsharded states replay a repeated op list as a captured CUDA graph
+    QVG_OPT_GRAPH = 14,      /* 1: unsharded states replay a repeated op list as a captured CUDA graph
                                 (no per-pass host planning/launch cost; default 0) */
+    QVG_OPT_REORDER = 15     /* 1: fusion may move an op ahead of ops on disjoint qubits (fewer passes;
+                                mathematically equal but NOT bit-identical to the reference; default 0) */
 };
 
 /* Counters (the reference's Metrics, metrics.hpp:14-30, plus the GPU pass

@@ -40,6 +40,7 @@ from ._core import (  # noqa: E402
     OPT_BATCH_EXCHANGE,
     OPT_STAGE,
     OPT_GRAPH,
+    OPT_REORDER,
     OPT_TILE_QUBITS,
     QVG_ABI_VERSION,
     CapacityError,

@@ -103,6 +103,7 @@ struct qvg_state {
     uint32_t batch_max = 4;    // sharded: most global qubits one exchange swaps (QVG_OPT_BATCH_EXCHANGE)
     uint32_t stage_bits = 3;   // fused tile: stage first/last group HBM access through shared memory (QVG_OPT_STAGE)
     bool graph = false;        // QVG_OPT_GRAPH: replay repeated op lists as captured CUDA graphs
+    bool reorder = false;      // QVG_OPT_REORDER: commutation-aware fusion order (not bit-exact)
     struct GraphEntry {
         uint64_t key = 0;
         std::vector<qvg_gate> ops;
@@ -258,13 +259,20 @@ PlanOptions plan_options(const qvg_state &s) {
     po.min_run = s.min_run;
     po.sub_bits = s.sub_bits;
     po.stage_bits = s.stage_bits;
+    po.reorder = s.reorder;
     return po;
 }
 
 // Run a batch of local ops (physical local qubit indices) on one shard buffer.
 void run_local(qvg_state &s, void *psi, const qvg_gate *ops, uint64_t count) {
     if (count == 0) return;
-    const Plan plan = make_plan(ops, count, plan_options(s));
+    const PlanOptions po = plan_options(s);
+    std::vector<qvg_gate> reordered;
+    if (po.reorder && po.fuse) {
+        reordered = reorder_for_tiles(ops, count, po);
+        ops = reordered.data();
+    }
+    const Plan plan = make_plan(ops, count, po);
     const bool dbl = s.precision == QVG_C128;
     for (const Pass &p : plan.passes) {
         switch (p.kind) {
@@ -302,6 +310,7 @@ uint64_t plan_signature(const qvg_state &s) {
     auto mix = [&](uint64_t v) { h = (h ^ v) * 1099511628211ull; };
     mix(s.fuse); mix(s.tile_qubits); mix(s.carriers); mix(s.low_kernel); mix(s.min_run); mix(s.pred_store);
     mix(s.sub_bits); mix(s.fma); mix(s.stage_bits); mix((uint64_t)s.prefetch_mode); mix(s.L); mix(s.precision);
+    mix(s.reorder);
     return h;
 }
 
@@ -531,6 +540,7 @@ int qvg_set_option(qvg_state *s, int key, int64_t value) {
             if (value < 0 || value > 1) throw Validation("prefetch must be 0 or 1");
             s->prefetch_mode = (int)value;
             break;
+        case QVG_OPT_REORDER: s->reorder = value != 0; break;
         case QVG_OPT_GRAPH:
             s->graph = value != 0;
             if (!s->graph) drop_graphs(*s);

@@ -97,6 +97,7 @@ struct PlanOptions {
     bool low_kernel = false;
     uint32_t min_run = 32;   // see qvg_state::min_run
     uint32_t sub_bits = 3;   // tile register subcube: 2^sub amplitudes per thread (3 or 4)
+    bool reorder = false;    // QVG_OPT_REORDER: commutation-aware op order (not bit-exact)
     uint32_t stage_bits = 3; // stage a first/last group through shared memory when its bits
                              // include tile bits 0..stage_bits-1 (warp lanes >= 2^stage_bits
                              // amplitudes apart); 0 = never
@@ -147,6 +148,52 @@ inline int local_bit(int q, const TileGeom &g) {
     for (int i = 0; i < g.nhi; ++i)
         if (g.hiq[i] == q) return g.lowc + i;
     return -1;
+}
+
+// Commutation-aware op order for fusion (QVG_OPT_REORDER, opt-in, NOT
+// bit-exact). The tile runs are built greedily as in make_plan, but an op that
+// does not fit the current run no longer ends it. Its qubits are marked
+// blocked, and later ops that touch no blocked qubit join the run: such an op
+// acts on qubits disjoint from every op it overtakes, so the two commute. The
+// product is mathematically the same, but amplitudes see the products in
+// another order, so results differ from the reference in the last bits
+// (tests bound them at 1e-12).
+inline std::vector<qvg_gate> reorder_for_tiles(const qvg_gate *ops, uint64_t count, const PlanOptions &po) {
+    constexpr uint64_t kWindow = 512;  // look-ahead per run
+    const uint32_t n = po.n;
+    const uint32_t k = std::min<uint32_t>(po.tile_qubits, n);
+    const uint32_t lowmin = std::min<uint32_t>(po.carriers, k);
+    std::vector<qvg_gate> out;
+    out.reserve(count);
+    std::vector<char> taken(count, 0);
+    uint64_t first = 0;  // lowest index not yet emitted
+    while (first < count) {
+        std::vector<int> high;
+        std::vector<char> blocked(n, 0);
+        uint64_t live = 0;
+        for (uint64_t j = first; j < count && j < first + kWindow && live < kMaxRunOps; ++j) {
+            if (taken[j]) continue;
+            const qvg_gate &g = ops[j];
+            const OpInfo o = classify(g);
+            const bool blk = blocked[o.target] || (o.control >= 0 && blocked[o.control]);
+            bool fits = !blk;
+            if (fits && !o.identity && !o.diag && (uint32_t)o.target >= lowmin &&
+                std::find(high.begin(), high.end(), o.target) == high.end()) {
+                if (high.size() == k - lowmin) fits = false;
+                else high.push_back(o.target);
+            }
+            if (!fits) {
+                blocked[o.target] = 1;
+                if (o.control >= 0) blocked[o.control] = 1;
+                continue;
+            }
+            taken[j] = 1;
+            out.push_back(g);
+            live += o.identity ? 0 : 1;
+        }
+        while (first < count && taken[first]) ++first;
+    }
+    return out;
 }
 
 inline Plan make_plan(const qvg_gate *ops, uint64_t count, const PlanOptions &po) {
