@@ -1,0 +1,142 @@
+// host_fuzz.cu — sanitizer harness for the host-side planning logic (no GPU
+// needed). Built with nvcc and -fsanitize=address,undefined by
+// tests/test_native_sanitizers.py. It drives:
+//   * make_plan / reorder_for_tiles (qvg_plan.hpp);
+//   * schedule_ops / schedule_canonicalize (qvg_schedule.hpp);
+// over random op lists, options and shard counts, and checks their
+// invariants. The reference has no sanitizer coverage (SURVEY §5:
+// "-Wall -Wextra" only); this is the B200 build's host-side equivalent of
+// compute-sanitizer on the kernels.
+#include <cstdio>
+#include <cstdlib>
+#include <random>
+#include <vector>
+
+#include "qvg_plan.hpp"
+#include "qvg_schedule.hpp"
+
+using namespace qvg;
+
+static int failures = 0;
+#define CHECK(c)                                                              \
+    do {                                                                      \
+        if (!(c)) {                                                           \
+            std::fprintf(stderr, "CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #c); \
+            ++failures;                                                       \
+        }                                                                     \
+    } while (0)
+
+static qvg_gate random_gate(std::mt19937_64 &rng, uint32_t n) {
+    qvg_gate g{};
+    std::uniform_int_distribution<uint32_t> q(0, n - 1);
+    g.target = q(rng);
+    g.control = -1;
+    g.kind = QVG_OP_SINGLE;
+    if (n >= 2 && rng() % 3 == 0) {
+        g.kind = QVG_OP_CONTROLLED;
+        do g.control = (int32_t)q(rng);
+        while ((uint32_t)g.control == g.target);
+    }
+    std::uniform_real_distribution<double> u(-1.0, 1.0);
+    const int kind = (int)(rng() % 4);  // dense, diag(1,d), diag(d0,d1), identity
+    for (double &x : g.u) x = u(rng);
+    if (kind >= 1) g.u[2] = g.u[3] = g.u[4] = g.u[5] = 0.0;
+    if (kind == 1 || kind == 3) { g.u[0] = 1.0; g.u[1] = 0.0; }
+    if (kind == 3) { g.u[6] = 1.0; g.u[7] = 0.0; }
+    return g;
+}
+
+static void check_plan(const std::vector<qvg_gate> &ops, const PlanOptions &po) {
+    std::vector<qvg_gate> list = ops;
+    if (po.reorder) {
+        list = reorder_for_tiles(ops.data(), ops.size(), po);
+        CHECK(list.size() == ops.size());
+    }
+    const Plan p = make_plan(list.data(), list.size(), po);
+    uint64_t covered = 0, live = 0;
+    for (const qvg_gate &g : list) live += classify(g).identity ? 0 : 1;
+    for (const Pass &pass : p.passes) {
+        covered += pass.kind == PASS_TILE ? 0 : 1;
+        if (pass.kind != PASS_TILE) continue;
+        const TileGeom &g = pass.geom;
+        CHECK(g.nrec <= kMaxTileRecs && g.nrec >= 2);
+        CHECK(g.k <= (int)po.n && g.lowc >= 0 && g.nhi == g.k - g.lowc);
+        CHECK(g.sub >= 2 && g.sub <= 4);
+        int rec = (int)pass.op_begin, groups = 0;
+        const int end = (int)pass.op_begin + g.nrec;
+        while (rec < end) {
+            const TileOp &h = p.tile_ops[rec];
+            CHECK(h.kind == TILE_GROUP);
+            for (int s = 0; s < g.sub; ++s) CHECK((int)((h.gtgt >> (8 * s)) & 0xff) < g.k);
+            const int nops = h.tbit;
+            CHECK(nops >= 1 && rec + 1 + nops <= end);
+            for (int i = 0; i < nops; ++i) {
+                const TileOp &t = p.tile_ops[rec + 1 + i];
+                CHECK(t.kind == TILE_PAIR || t.kind == TILE_DIAG);
+                if (t.kind == TILE_PAIR) {
+                    CHECK(t.slot >= 0 && t.slot < 8 * g.sub);  // 8*J + (K+1) with J >= 0 (target in the group)
+                    if (!(t.slot >= 0 && t.slot < 8 * g.sub) && failures < 5)
+                        std::fprintf(stderr, "  slot %d sub %d k %d tbit %d cbit %d\n", t.slot, g.sub, g.k, t.tbit, t.cbit);
+                }
+                else CHECK((t.slot & 63) < 8 * (g.sub + 1));
+                ++covered;
+            }
+            rec += 1 + nops;
+            ++groups;
+        }
+        CHECK(groups == g.ngroups);
+    }
+    CHECK(covered == live);  // every non-identity op exactly once
+}
+
+static void check_schedule(const std::vector<qvg_gate> &ops, uint32_t n, uint32_t g, uint32_t kmax) {
+    const uint32_t L = n - g;
+    QubitMap map;
+    map.reset(n);
+    std::vector<ShardStep> steps;
+    schedule_ops(n, L, ops.data(), ops.size(), map, steps, kmax);
+    schedule_canonicalize(n, L, map, steps, kmax);
+    CHECK(map.identity());
+    for (const ShardStep &st : steps) {
+        if (st.type == STEP_LOCAL) {
+            CHECK(st.op.target < L);
+            if (st.op.kind == QVG_OP_CONTROLLED) CHECK((uint32_t)st.op.control < L && (uint32_t)st.op.control != st.op.target);
+            CHECK((st.rank_value & ~st.rank_mask) == 0 && st.rank_mask < (1u << g));
+        } else if (st.type == STEP_EXCHANGE) {
+            CHECK(st.gpos >= L && st.gpos < n && st.lpos < L);
+        } else if (st.type == STEP_MULTI_EXCHANGE) {
+            const uint32_t k = st.lpos2;
+            CHECK(k >= 2 && k <= 4 && (uint32_t)__builtin_popcount(st.gpos) == k && st.gpos < (1u << g));
+            for (uint32_t i = 0; i < k; ++i) {
+                CHECK(multi_pos(st, i) >= min_exchange_lpos(L) && multi_pos(st, i) < L);
+                for (uint32_t j = 0; j < i; ++j) CHECK(multi_pos(st, i) != multi_pos(st, j));
+            }
+        } else {
+            CHECK(st.type == STEP_LOCAL_SWAP && st.lpos < L && st.lpos2 < L && st.lpos != st.lpos2);
+        }
+    }
+}
+
+int main(int argc, char **argv) {
+    const int trials = argc > 1 ? std::atoi(argv[1]) : 300;
+    std::mt19937_64 rng(2508);
+    for (int t = 0; t < trials; ++t) {
+        const uint32_t n = 2 + (uint32_t)(rng() % 29);  // 2..30
+        std::vector<qvg_gate> ops(1 + rng() % 400);
+        for (auto &g : ops) g = random_gate(rng, n);
+        PlanOptions po;
+        po.n = n;
+        po.amp_bytes = rng() % 2 ? 16 : 8;
+        po.fuse = rng() % 8 != 0;
+        po.tile_qubits = 5 + (uint32_t)(rng() % 8);
+        po.carriers = (uint32_t)(rng() % 5);
+        po.sub_bits = rng() % 2 ? 3 : 4;
+        po.stage_bits = (uint32_t)(rng() % 4);
+        po.reorder = rng() % 2;
+        check_plan(ops, po);
+        const uint32_t g = (uint32_t)(rng() % 4);
+        if (n >= g + 2) check_schedule(ops, n, g, 1 + (uint32_t)(rng() % 4));
+    }
+    std::printf("host_fuzz: %d trials, %d failures\n", trials, failures);
+    return failures ? 1 : 0;
+}
