@@ -268,7 +268,7 @@ void run_local(qvg_state &s, void *psi, const qvg_gate *ops, uint64_t count) {
     if (count == 0) return;
     const PlanOptions po = plan_options(s);
     std::vector<qvg_gate> reordered;
-    if (po.reorder && po.fuse) {
+    if (po.reorder && po.fuse && std::min(po.tile_qubits, po.n) >= 5) {  // only where tiles exist
         reordered = reorder_for_tiles(ops, count, po);
         ops = reordered.data();
     }
