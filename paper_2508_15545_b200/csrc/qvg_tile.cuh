@@ -187,10 +187,13 @@ __device__ __forceinline__ void group_diag_dispatch(int code, typename Cplx<R>::
 #ifndef QVG_SUB4_256_MINB
 #define QVG_SUB4_256_MINB 3  // 256-thread 16-amplitude tiles (12-qubit tiles): 80 registers, no spills
 #endif
+#ifndef QVG_C64_SUB4_256_MINB
+#define QVG_C64_SUB4_256_MINB 4  // complex64 (its default tile): 64 registers; 4-6% faster than 3 CTAs, 5 spills
+#endif
 template <class R, int SUB, bool FMA, int MAXT, bool PF>
 __global__ void __launch_bounds__(MAXT, PF                         ? 2
                                         : (MAXT <= 128 && SUB == 4) ? QVG_SUB4_MINB
-                                        : (MAXT <= 256 && SUB == 4) ? QVG_SUB4_256_MINB
+                                        : (MAXT <= 256 && SUB == 4) ? (sizeof(R) == 4 ? QVG_C64_SUB4_256_MINB : QVG_SUB4_256_MINB)
                                         : (MAXT <= 256 && SUB == 3) ? 4
                                                                     : 2)
 k_tile(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams prm) {
