@@ -86,8 +86,10 @@ enum qvg_option {
                                 its HBM data through shared memory, coalesced (default b = 3; 0 never) */
     QVG_OPT_GRAPH = 14,      /* 1: unsharded states replay a repeated op list as a captured CUDA graph
                                 (no per-pass host planning/launch cost; default 0) */
-    QVG_OPT_REORDER = 15     /* 1: fusion may move an op ahead of ops on disjoint qubits (fewer passes;
+    QVG_OPT_REORDER = 15,    /* 1: fusion may move an op ahead of ops on disjoint qubits (fewer passes;
                                 mathematically equal but NOT bit-identical to the reference; default 0) */
+    QVG_OPT_CLASSES = 16     /* fused tile: 1 = structured-matrix op bodies (real, X, entries +-1/2, Z),
+                                same values with fewer FP64 instructions (default); 0 = general bodies */
 };
 
 /* Counters (the reference's Metrics, metrics.hpp:14-30, plus the GPU pass

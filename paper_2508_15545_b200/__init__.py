@@ -41,6 +41,7 @@ from ._core import (  # noqa: E402
     OPT_STAGE,
     OPT_GRAPH,
     OPT_REORDER,
+    OPT_CLASSES,
     OPT_TILE_QUBITS,
     QVG_ABI_VERSION,
     CapacityError,

@@ -456,4 +456,5 @@ PYBIND11_MODULE(_core, m) {
     m.attr("OPT_STAGE") = (int)QVG_OPT_STAGE;
     m.attr("OPT_GRAPH") = (int)QVG_OPT_GRAPH;
     m.attr("OPT_REORDER") = (int)QVG_OPT_REORDER;
+    m.attr("OPT_CLASSES") = (int)QVG_OPT_CLASSES;
 }

@@ -16,6 +16,7 @@
 #include <new>
 #include <string>
 #include <functional>
+#include <type_traits>
 #include <memory>
 #include <vector>
 
@@ -104,6 +105,7 @@ struct qvg_state {
     uint32_t stage_bits = 3;   // fused tile: stage first/last group HBM access through shared memory (QVG_OPT_STAGE)
     bool graph = false;        // QVG_OPT_GRAPH: replay repeated op lists as captured CUDA graphs
     bool reorder = false;      // QVG_OPT_REORDER: commutation-aware fusion order (not bit-exact)
+    bool classes = true;       // QVG_OPT_CLASSES: structured-matrix op bodies in fused tiles
     struct GraphEntry {
         uint64_t key = 0;
         std::vector<qvg_gate> ops;
@@ -224,18 +226,26 @@ void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *recs) {
     const bool fma = s.fma && sizeof(R) == 8;  // complex64 always contracts
     const bool small = threads <= 256;
     const bool tiny = threads <= 128;  // sub 4 at k <= 11: 128-thread CTAs
-    auto kern = g.sub == 4 ? (tiny ? (fma ? k_tile<R, 4, true, 128, false> : k_tile<R, 4, false, 128, false>)
-                                   : (fma ? k_tile<R, 4, true, 256, false> : k_tile<R, 4, false, 256, false>))
-                : pf ? (small ? (fma ? k_tile<R, 3, true, 256, true> : k_tile<R, 3, false, 256, true>)
-                              : (fma ? k_tile<R, 3, true, 512, true> : k_tile<R, 3, false, 512, true>))
-                : small ? (fma ? k_tile<R, 3, true, 256, false> : k_tile<R, 3, false, 256, false>)
-                        : (fma ? k_tile<R, 3, true, 512, false> : k_tile<R, 3, false, 512, false>);
+    auto pick = [&](auto cm) {
+        constexpr int CM = decltype(cm)::value;
+        return g.sub == 4 ? (tiny ? (fma ? k_tile<R, 4, true, 128, false, CM> : k_tile<R, 4, false, 128, false, CM>)
+                                  : (fma ? k_tile<R, 4, true, 256, false, CM> : k_tile<R, 4, false, 256, false, CM>))
+               : pf ? (small ? (fma ? k_tile<R, 3, true, 256, true, CM> : k_tile<R, 3, false, 256, true, CM>)
+                             : (fma ? k_tile<R, 3, true, 512, true, CM> : k_tile<R, 3, false, 512, true, CM>))
+               : small ? (fma ? k_tile<R, 3, true, 256, false, CM> : k_tile<R, 3, false, 256, false, CM>)
+                       : (fma ? k_tile<R, 3, true, 512, false, CM> : k_tile<R, 3, false, 512, false, CM>);
+    };
+    // Passes without structured ops (classes off) use the REAL-set kernel:
+    // their records only name general bodies, which both sets compile.
+    const bool half_set = g.cls_set == kClsSetHalf;
+    auto kern = half_set ? pick(std::integral_constant<int, kClsSetHalf>{})
+                         : pick(std::integral_constant<int, kClsSetReal>{});
     // The shared-memory opt-in is a per-device function attribute: set it once
     // per (device, variant).
-    static std::atomic<uint64_t> attr_set[64];
+    static std::atomic<uint64_t> attr_set[64][2];  // [device][class set]: a bit per variant
     const int variant = (sizeof(R) == 8 ? 1 : 0) | (g.sub == 4 ? 2 : 0) | (fma ? 4 : 0) | (small ? 8 : 0) |
                         (pf ? 16 : 0) | (tiny ? 32 : 0);
-    std::atomic<uint64_t> &set = attr_set[s.device & 63];
+    std::atomic<uint64_t> &set = attr_set[s.device & 63][half_set ? 1 : 0];
     if (!((set.load(std::memory_order_acquire) >> variant) & 1u)) {
         cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
                    "cudaFuncSetAttribute(k_tile)");
@@ -260,6 +270,7 @@ PlanOptions plan_options(const qvg_state &s) {
     po.sub_bits = s.sub_bits;
     po.stage_bits = s.stage_bits;
     po.reorder = s.reorder;
+    po.classes = s.classes;
     return po;
 }
 
@@ -310,7 +321,7 @@ uint64_t plan_signature(const qvg_state &s) {
     auto mix = [&](uint64_t v) { h = (h ^ v) * 1099511628211ull; };
     mix(s.fuse); mix(s.tile_qubits); mix(s.carriers); mix(s.low_kernel); mix(s.min_run); mix(s.pred_store);
     mix(s.sub_bits); mix(s.fma); mix(s.stage_bits); mix((uint64_t)s.prefetch_mode); mix(s.L); mix(s.precision);
-    mix(s.reorder);
+    mix(s.reorder); mix(s.classes);
     return h;
 }
 
@@ -541,6 +552,7 @@ int qvg_set_option(qvg_state *s, int key, int64_t value) {
             s->prefetch_mode = (int)value;
             break;
         case QVG_OPT_REORDER: s->reorder = value != 0; break;
+        case QVG_OPT_CLASSES: s->classes = value != 0; break;
         case QVG_OPT_GRAPH:
             s->graph = value != 0;
             if (!s->graph) drop_graphs(*s);

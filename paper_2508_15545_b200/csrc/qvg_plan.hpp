@@ -37,9 +37,51 @@ struct OpInfo {
     bool diag = false;      // u01 == u10 == 0
     bool phase = false;     // diag and u00 == 1 + 0i
     bool identity = false;  // phase and u11 == 1 + 0i
+    bool neg = false;       // phase and u11 == -1 + 0i (Z, CZ): a sign flip in fused tiles
+    int cls = TILE_CLS_GEN; // non-diagonal: structured-matrix class for fused tiles (qvg_tile.cuh)
     int target = 0;
     int control = -1;
 };
+
+// Structured-matrix class of a non-diagonal 2x2 (fused tiles compute these
+// with fewer FP64 instructions and the reference's value, qvg_tile.cuh).
+inline int pair_class(const double *u) {
+    if (u[0] == 0.0 && u[1] == 0.0 && u[2] == 1.0 && u[3] == 0.0 && u[4] == 1.0 && u[5] == 0.0 && u[6] == 0.0 &&
+        u[7] == 0.0)
+        return TILE_CLS_SWAP;
+    if (u[1] == 0.0 && u[3] == 0.0 && u[5] == 0.0 && u[7] == 0.0) return TILE_CLS_REAL;
+    bool half = true;
+    for (int i = 0; i < 8; ++i) half = half && (u[i] == 0.5 || u[i] == -0.5);
+    return half ? TILE_CLS_HALF : TILE_CLS_GEN;
+}
+
+// The class set of one fused pass (k_tile compiles REAL or HALF bodies, not
+// both): whichever of the two covers more of the pass's ops; ops of the other
+// class run the general body.
+inline int tile_class_set(const OpInfo *info, uint64_t begin, uint64_t end) {
+    uint64_t real = 0, half = 0;
+    for (uint64_t x = begin; x < end; ++x) {
+        if (info[x].identity || info[x].diag) continue;
+        real += info[x].cls == TILE_CLS_REAL;
+        half += info[x].cls == TILE_CLS_HALF;
+    }
+    return half > real ? kClsSetHalf : kClsSetReal;
+}
+
+// The record's u[] for a HALF-class op: per output row (lo: u00 u01, hi: u10
+// u11) the four reals (s0/2, -s0 s1, -s2 s3, s0 s2) that half_apply
+// (qvg_tile.cuh) expects, s0..s3 the signs of the row's re/im entries.
+inline void half_record(const double *u, double *out) {
+    for (int row = 0; row < 2; ++row) {
+        const double *m = u + 4 * row;
+        const double s0 = m[0] > 0 ? 1.0 : -1.0, s1 = m[1] > 0 ? 1.0 : -1.0;
+        const double s2 = m[2] > 0 ? 1.0 : -1.0, s3 = m[3] > 0 ? 1.0 : -1.0;
+        out[4 * row + 0] = m[0];
+        out[4 * row + 1] = -s0 * s1;
+        out[4 * row + 2] = -s2 * s3;
+        out[4 * row + 3] = s0 * s2;
+    }
+}
 
 inline OpInfo classify(const qvg_gate &g) {
     OpInfo o;
@@ -47,6 +89,8 @@ inline OpInfo classify(const qvg_gate &g) {
     o.diag = u[2] == 0.0 && u[3] == 0.0 && u[4] == 0.0 && u[5] == 0.0;
     o.phase = o.diag && u[0] == 1.0 && u[1] == 0.0;
     o.identity = o.phase && u[6] == 1.0 && u[7] == 0.0;
+    o.neg = o.phase && u[6] == -1.0 && u[7] == 0.0;
+    if (!o.diag) o.cls = pair_class(u);
     o.target = (int)g.target;
     o.control = g.kind == QVG_OP_CONTROLLED ? g.control : -1;
     return o;
@@ -98,6 +142,7 @@ struct PlanOptions {
     uint32_t min_run = 32;   // see qvg_state::min_run
     uint32_t sub_bits = 3;   // tile register subcube: 2^sub amplitudes per thread (3 or 4)
     bool reorder = false;    // QVG_OPT_REORDER: commutation-aware op order (not bit-exact)
+    bool classes = true;     // QVG_OPT_CLASSES: structured-matrix op bodies in fused tiles
     uint32_t stage_bits = 3; // stage a first/last group through shared memory when its bits
                              // include tile bits 0..stage_bits-1 (warp lanes >= 2^stage_bits
                              // amplitudes apart); 0 = never
@@ -296,15 +341,17 @@ inline Plan make_plan(const qvg_gate *ops, uint64_t count, const PlanOptions &po
                     if (!used(b)) gbits[nb++] = b;
                 std::sort(gbits, gbits + g.sub);
                 for (TileOp &t : group) {
-                    // pair: slot = 8*J + (K+1); diag: slot = 64*(d0 != 1) + 8*(J+1) + (K+1),
-                    // J / K the target / control register slots (-1: not in the group)
+                    // pair: slot = 32*class + 8*J + (K+1); diag: slot = 128*neg + 64*(d0 != 1) +
+                    // 8*(J+1) + (K+1), J / K the target / control register slots (-1: not in
+                    // the group). Before this point slot holds the class (pair) or the
+                    // d0 == 1 / neg flags (diag, bits 0 / 1).
                     int J = -1, K = -1;
                     for (int s = 0; s < g.sub; ++s) {
                         if (t.tbit >= 0 && gbits[s] == t.tbit) J = s;
                         if (t.cbit >= 0 && gbits[s] == t.cbit) K = s;
                     }
-                    if (t.kind == TILE_PAIR) t.slot = 8 * J + K + 1;
-                    else t.slot = (t.slot ? 0 : 64) + 8 * (J + 1) + K + 1;
+                    if (t.kind == TILE_PAIR) t.slot = 32 * t.slot + 8 * J + K + 1;
+                    else t.slot = ((t.slot & 2) ? 128 : (t.slot & 1) ? 0 : 64) + 8 * (J + 1) + K + 1;
                 }
                 TileOp h{};
                 h.kind = TILE_GROUP;
@@ -321,6 +368,7 @@ inline Plan make_plan(const qvg_gate *ops, uint64_t count, const PlanOptions &po
                 g.ngroups += 1;
             };
             g.ngroups = 0;
+            g.cls_set = po.classes ? tile_class_set(info.data(), i, j) : (1 << TILE_CLS_GEN);
             for (uint64_t x = i; x < j; ++x) {
                 const OpInfo &o = info[x];
                 if (o.identity) continue;
@@ -334,7 +382,11 @@ inline Plan make_plan(const qvg_gate *ops, uint64_t count, const PlanOptions &po
                     t.cbit = local_bit(o.control, g);
                     if (t.cbit < 0) t.greq = 1ull << o.control;
                 }
-                if (t.kind == TILE_DIAG) t.slot = (ops[x].u[0] == 1.0 && ops[x].u[1] == 0.0) ? 1 : 0;  // d0 == 1, coded in close_group
+                if (t.kind == TILE_DIAG)  // d0 == 1 / neg flags, coded in close_group
+                    t.slot = (ops[x].u[0] == 1.0 && ops[x].u[1] == 0.0 ? 1 : 0) | (po.classes && o.neg ? 2 : 0);
+                else
+                    t.slot = ((g.cls_set >> o.cls) & 1) ? o.cls : TILE_CLS_GEN;
+                if (t.kind == TILE_PAIR && t.slot == TILE_CLS_HALF) half_record(ops[x].u, t.u);
                 if (t.kind == TILE_PAIR) {
                     // The target must be a register bit. An in-tile control is
                     // made one too: the control test is then the same for every

@@ -41,7 +41,8 @@ struct __align__(16) TileOp {
     int32_t kind;      // TileOpKind
     int32_t tbit;      // pair/diag: tile-local target bit (-1: diag target outside Q); group: op count
     int32_t cbit;      // tile-local control bit, -1 if none or outside Q
-    int32_t slot;      // dispatch code: pair 8*J+(K+1), diag 64*(d0!=1)+8*(J+1)+(K+1) (J/K: register slots)
+    int32_t slot;      // dispatch code: pair 32*class+8*J+(K+1), diag 128*neg+64*(d0!=1)+8*(J+1)+(K+1)
+                       // (J/K: register slots)
     uint64_t greq;     // global bits that must be 1 in the tile base (controls outside Q)
     uint64_t gtgt;     // diag: global target bit outside Q; group: packed bits b0 | b1<<8 | b2<<16 | b3<<24
     double u[8];       // matrix (diag uses u00 = u[0..1], u11 = u[6..7])
@@ -55,6 +56,7 @@ struct TileGeom {
     int nrec;             // records (headers + ops)
     int sub;              // subcube bits per thread (3 or 4)
     int stage;            // bit 0: first group loads through shared memory; bit 1: last group stores through it
+    int cls_set;          // structured-matrix classes this pass uses (kClsSetReal / kClsSetHalf)
     int hiq[24];          // tile qubits >= lowc, ascending (tile-local bits lowc..k-1)
     uint64_t ntiles;      // 2^(n-k)
 };
@@ -97,11 +99,133 @@ __device__ __forceinline__ void group_pair(typename Cplx<R>::T (&v)[1 << SUB], c
     }
 }
 
-// slot code = 8*J + (K+1)
-template <class R, int SUB, bool FMA>
+// Structured matrices (class chosen by the planner, qvg_plan.hpp
+// pair_class). Each computes the reference's value with fewer FP64
+// instructions; terms whose matrix entry is 0 contribute +-0, which changes
+// at most the sign of an exact-zero result.
+//   TILE_CLS_REAL: every imaginary part is 0 (H, real rotations):
+//     lo = (u00r*a.re + u01r*b.re, u00r*a.im + u01r*b.im), 12 instead of 28.
+//   TILE_CLS_SWAP: [[0,1],[1,0]] (X, the target of CX): a register swap.
+//   TILE_CLS_HALF: every |re| and |im| is 1/2 (sqrt(X), sqrt(Y), their
+//     adjoints): with u00 = (s0, s1)/2, u01 = (s2, s3)/2,
+//       lo.re = s0/2 * ((a.re - s0s1 a.im) + s0s2 (b.re - s2s3 b.im)),
+//     and likewise for lo.im and hi. Halving is exact and commutes with
+//     round-to-nearest, and so does negation, so this equals the
+//     reference's (s0/2 a.re - s1/2 a.im) + (s2/2 b.re - s3/2 b.im) bit for
+//     bit (unless an intermediate falls below 2^-1021 in magnitude, where
+//     halving rounds). 16 FP64 instructions instead of 28.
+enum TileCls : int32_t { TILE_CLS_GEN = 0, TILE_CLS_REAL = 1, TILE_CLS_SWAP = 2, TILE_CLS_HALF = 3 };
+
+__device__ __forceinline__ double xsgn(double x, uint32_t m) {
+    return __hiloint2double(__double2hiint(x) ^ (int)m, __double2loint(x));
+}
+__device__ __forceinline__ float xsgn(float x, uint32_t m) { return __int_as_float(__float_as_int(x) ^ (int)m); }
+template <class R> __device__ __forceinline__ R neg_rn(R x) { return xsgn(x, 0x80000000u); }
+// The SWAP class moves each component through one DADD with +0 (-0 becomes
+// +0, nothing else changes). Plain register renaming or inline-asm moves
+// made ptxas spill in the 96-register tile kernel: each switch case then
+// leaves the amplitudes in a different register assignment.
+__device__ __forceinline__ double2 mov_opaque(double2 x) {
+    return make_double2(__dadd_rn(x.x, 0.0), __dadd_rn(x.y, 0.0));
+}
+__device__ __forceinline__ float2 mov_opaque(float2 x) {
+    return make_float2(__fadd_rn(x.x, 0.0f), __fadd_rn(x.y, 0.0f));
+}
+
+// HALF-class records carry, per output row x (0 = lo, 1 = hi), four reals
+// u[4x..4x+3] = (s0/2, -s0 s1, -s2 s3, s0 s2) instead of the matrix
+// (pair_record, qvg_plan.hpp). A DFMA by +-1 is exact before its single
+// rounding, so fma(c, y, x) rounds exactly like x + c*y as DADD/DSUB: four
+// FP64 instructions per component, no sign-bit moves, and every constant is
+// a parameter-bank operand (ptxas reloads rather than spills it).
+template <class T, class R>
+__device__ __forceinline__ T half_apply(const double *uu, T a, T b) {
+    const R h = (R)uu[0], c1 = (R)uu[1], c2 = (R)uu[2], c3 = (R)uu[3];
+    T o;
+    if constexpr (sizeof(R) == 8) {
+        const double xr = __fma_rn(c1, a.y, a.x), yr = __fma_rn(c2, b.y, b.x);
+        const double xi = __fma_rn(-c1, a.x, a.y), yi = __fma_rn(-c2, b.x, b.y);
+        o.x = __dmul_rn(__fma_rn(c3, yr, xr), h);
+        o.y = __dmul_rn(__fma_rn(c3, yi, xi), h);
+    } else {
+        const R xr = fmaf(c1, a.y, a.x), yr = fmaf(c2, b.y, b.x);
+        const R xi = fmaf(-c1, a.x, a.y), yi = fmaf(-c2, b.x, b.y);
+        o.x = fmaf(c3, yr, xr) * h;
+        o.y = fmaf(c3, yi, xi) * h;
+    }
+    return o;
+}
+
+// REAL class: (m0*a.re + m1*b.re, m0*a.im + m1*b.im); the entries are read
+// at the point of use (parameter-bank operands, reloaded under pressure).
+template <class T, class R, bool FMA>
+__device__ __forceinline__ T real_apply(double m0, double m1, T a, T b) {
+    T o;
+    if constexpr (sizeof(R) == 8 && !FMA) {
+        o.x = __dadd_rn(__dmul_rn(m0, a.x), __dmul_rn(m1, b.x));
+        o.y = __dadd_rn(__dmul_rn(m0, a.y), __dmul_rn(m1, b.y));
+    } else {
+        o.x = (R)m0 * a.x + (R)m1 * b.x;
+        o.y = (R)m0 * a.y + (R)m1 * b.y;
+    }
+    return o;
+}
+
+// Class sets a k_tile instantiation compiles (CM: bit per TileCls). With all
+// four sets of bodies in one 96-register kernel ptxas spills inside the
+// bodies (~1 KB of local traffic per op); with three it does not. The planner
+// picks the set per pass (tile_class_set, qvg_plan.hpp).
+constexpr int kClsSetReal = (1 << TILE_CLS_GEN) | (1 << TILE_CLS_REAL) | (1 << TILE_CLS_SWAP);
+constexpr int kClsSetHalf = (1 << TILE_CLS_GEN) | (1 << TILE_CLS_HALF) | (1 << TILE_CLS_SWAP);
+template <class R, int SUB, int J, int K, bool FMA, int CLS, int CM>
+__device__ __forceinline__ void group_pair_cls(typename Cplx<R>::T (&v)[1 << SUB], const double *uu) {
+    using T = typename Cplx<R>::T;
+    if constexpr (J < SUB && K < SUB && J != K && ((CM >> CLS) & 1)) {
+        if constexpr (CLS == TILE_CLS_SWAP) {
+#pragma unroll
+            for (int r = 0; r < (1 << SUB); ++r) {
+                if ((r >> J) & 1) continue;
+                if (K >= 0 && !((r >> K) & 1)) continue;
+                const T a = v[r], b = v[r | (1 << J)];
+                v[r] = mov_opaque(b);
+                v[r | (1 << J)] = mov_opaque(a);
+            }
+        } else if constexpr (CLS == TILE_CLS_REAL) {
+#pragma unroll
+            for (int r = 0; r < (1 << SUB); ++r) {
+                if ((r >> J) & 1) continue;
+                if (K >= 0 && !((r >> K) & 1)) continue;
+                const T a = v[r], b = v[r | (1 << J)];
+                v[r] = real_apply<T, R, FMA>(uu[0], uu[2], a, b);
+                v[r | (1 << J)] = real_apply<T, R, FMA>(uu[4], uu[6], a, b);
+            }
+        } else {  // TILE_CLS_HALF
+#pragma unroll
+            for (int r = 0; r < (1 << SUB); ++r) {
+                if ((r >> J) & 1) continue;
+                if (K >= 0 && !((r >> K) & 1)) continue;
+                const T a = v[r], b = v[r | (1 << J)];
+                v[r] = half_apply<T, R>(uu, a, b);
+                v[r | (1 << J)] = half_apply<T, R>(uu + 4, a, b);
+            }
+        }
+    }
+}
+
+// slot code = 32*CLS + 8*J + (K+1)
+template <class R, int SUB, bool FMA, int CM>
 __device__ __forceinline__ void group_pair_dispatch(int code, typename Cplx<R>::T (&v)[1 << SUB], const double *u) {
-#define QVG_GP(J, K) \
-    case 8 * (J) + (K) + 1: group_pair<R, SUB, J, K, FMA>(v, u); break;
+#define QVG_GP(J, K)                                                                         \
+    case 8 * (J) + (K) + 1: group_pair<R, SUB, J, K, FMA>(v, u); break;                      \
+    case 32 * TILE_CLS_REAL + 8 * (J) + (K) + 1:                                              \
+        group_pair_cls<R, SUB, J, K, FMA, TILE_CLS_REAL, CM>(v, u);                               \
+        break;                                                                                \
+    case 32 * TILE_CLS_SWAP + 8 * (J) + (K) + 1:                                              \
+        group_pair_cls<R, SUB, J, K, FMA, TILE_CLS_SWAP, CM>(v, u);                               \
+        break;                                                                                \
+    case 32 * TILE_CLS_HALF + 8 * (J) + (K) + 1:                                              \
+        group_pair_cls<R, SUB, J, K, FMA, TILE_CLS_HALF, CM>(v, u);                               \
+        break;
     switch (code) {
         QVG_GP(0, -1) QVG_GP(0, 1) QVG_GP(0, 2) QVG_GP(0, 3)
         QVG_GP(1, -1) QVG_GP(1, 0) QVG_GP(1, 2) QVG_GP(1, 3)
@@ -120,17 +244,34 @@ __device__ __forceinline__ void group_pair_dispatch(int code, typename Cplx<R>::
 // d0 != 1 (target-0 elements change too) is a run-time flag: one body per
 // (J, K) keeps the kernel's code small, which measured 2-3% faster than a
 // body per (J, K, d0) (i-cache). Each element gets exactly one multiply, so
-// the bits are the same either way.
-template <class R, int SUB, int J, int K, bool FMA>
+// the bits are the same either way. NEG (planner class: d0 = 1, d1 = -1, i.e.
+// Z and CZ) flips the sign bits instead: (-1)*re - 0*im is -re up to the sign
+// of an exact zero, and no FP64 instruction is issued.
+template <class R, int SUB, int J, int K, bool FMA, bool NEG>
 __device__ __forceinline__ void group_diag_rt(typename Cplx<R>::T (&v)[1 << SUB], const double *uu, bool t1,
                                               bool d0) {
+    using T = typename Cplx<R>::T;
+    auto neg = [](T x) {
+        x.x = neg_rn(x.x);
+        x.y = neg_rn(x.y);
+        return x;
+    };
     if constexpr (J < SUB && K < SUB && (J != K || J < 0)) {
         if constexpr (J >= 0) {
-            const R d1r = (R)uu[6], d1i = (R)uu[7];
+            if constexpr (NEG) {
 #pragma unroll
-            for (int r = 0; r < (1 << SUB); ++r) {
-                if (K >= 0 && !((r >> K) & 1)) continue;
-                if ((r >> J) & 1) v[r] = cmulx<FMA>(d1r, d1i, v[r]);
+                for (int r = 0; r < (1 << SUB); ++r) {
+                    if (K >= 0 && !((r >> K) & 1)) continue;
+                    if ((r >> J) & 1) v[r] = neg(v[r]);
+                }
+                return;
+            } else {
+                const R d1r = (R)uu[6], d1i = (R)uu[7];
+#pragma unroll
+                for (int r = 0; r < (1 << SUB); ++r) {
+                    if (K >= 0 && !((r >> K) & 1)) continue;
+                    if ((r >> J) & 1) v[r] = cmulx<FMA>(d1r, d1i, v[r]);
+                }
             }
             if (d0) {
                 const R d0r = (R)uu[0], d0i = (R)uu[1];
@@ -142,24 +283,37 @@ __device__ __forceinline__ void group_diag_rt(typename Cplx<R>::T (&v)[1 << SUB]
             }
         } else {
             if (!t1 && !d0) return;
-            const R dr = (R)(t1 ? uu[6] : uu[0]), di = (R)(t1 ? uu[7] : uu[1]);
+            if constexpr (NEG) {
+                if (!t1) return;
 #pragma unroll
-            for (int r = 0; r < (1 << SUB); ++r) {
-                if (K >= 0 && !((r >> K) & 1)) continue;
-                v[r] = cmulx<FMA>(dr, di, v[r]);
+                for (int r = 0; r < (1 << SUB); ++r) {
+                    if (K >= 0 && !((r >> K) & 1)) continue;
+                    v[r] = neg(v[r]);
+                }
+                return;
+            } else {
+                const R dr = (R)(t1 ? uu[6] : uu[0]), di = (R)(t1 ? uu[7] : uu[1]);
+#pragma unroll
+                for (int r = 0; r < (1 << SUB); ++r) {
+                    if (K >= 0 && !((r >> K) & 1)) continue;
+                    v[r] = cmulx<FMA>(dr, di, v[r]);
+                }
             }
         }
     }
 }
 
-// diag code = 64*D0 + 8*(J+1) + (K+1)
+// diag code = 128*NEG + 64*D0 + 8*(J+1) + (K+1)
 template <class R, int SUB, bool FMA>
 __device__ __forceinline__ void group_diag_dispatch(int code, typename Cplx<R>::T (&v)[1 << SUB], const double *u,
                                                     bool t1) {
-#define QVG_GD(J, K)                                            \
-    case 8 * ((J) + 1) + (K) + 1:                               \
-    case 64 + 8 * ((J) + 1) + (K) + 1:                          \
-        group_diag_rt<R, SUB, J, K, FMA>(v, u, t1, code >= 64); \
+#define QVG_GD(J, K)                                                   \
+    case 8 * ((J) + 1) + (K) + 1:                                      \
+    case 64 + 8 * ((J) + 1) + (K) + 1:                                 \
+        group_diag_rt<R, SUB, J, K, FMA, false>(v, u, t1, code >= 64); \
+        break;                                                         \
+    case 128 + 8 * ((J) + 1) + (K) + 1:                                \
+        group_diag_rt<R, SUB, J, K, FMA, true>(v, u, t1, false);       \
         break;
     switch (code) {
         QVG_GD(-1, -1) QVG_GD(-1, 0) QVG_GD(-1, 1) QVG_GD(-1, 2) QVG_GD(-1, 3)
@@ -190,7 +344,7 @@ __device__ __forceinline__ void group_diag_dispatch(int code, typename Cplx<R>::
 #ifndef QVG_C64_SUB4_256_MINB
 #define QVG_C64_SUB4_256_MINB 4  // complex64 (its default tile): 64 registers; 4-6% faster than 3 CTAs, 5 spills
 #endif
-template <class R, int SUB, bool FMA, int MAXT, bool PF>
+template <class R, int SUB, bool FMA, int MAXT, bool PF, int CM>
 __global__ void __launch_bounds__(MAXT, PF                         ? 2
                                         : (MAXT <= 128 && SUB == 4) ? QVG_SUB4_MINB
                                         : (MAXT <= 256 && SUB == 4) ? (sizeof(R) == 4 ? QVG_C64_SUB4_256_MINB : QVG_SUB4_256_MINB)
@@ -316,7 +470,7 @@ k_tile(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams
                 const TileOp &op = ops[rec + i];
                 if ((base & op.greq) != op.greq) continue;  // control outside the tile is 0
                 if (op.kind == TILE_PAIR) {
-                    group_pair_dispatch<R, SUB, FMA>(op.slot, v, op.u);
+                    group_pair_dispatch<R, SUB, FMA, CM>(op.slot, v, op.u);
                 } else {
                     // tile bits outside the group are per-thread bits of l0
                     if ((op.slot & 7) == 0 && op.cbit >= 0 && !((l0 >> op.cbit) & 1u)) continue;

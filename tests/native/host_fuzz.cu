@@ -38,11 +38,17 @@ static qvg_gate random_gate(std::mt19937_64 &rng, uint32_t n) {
         while ((uint32_t)g.control == g.target);
     }
     std::uniform_real_distribution<double> u(-1.0, 1.0);
-    const int kind = (int)(rng() % 4);  // dense, diag(1,d), diag(d0,d1), identity
+    // dense, diag(1,d), diag(d0,d1), identity, then the structured classes:
+    // real, X, entries +-1/2, Z
+    const int kind = (int)(rng() % 8);
     for (double &x : g.u) x = u(rng);
-    if (kind >= 1) g.u[2] = g.u[3] = g.u[4] = g.u[5] = 0.0;
+    if (kind >= 1 && kind <= 3) g.u[2] = g.u[3] = g.u[4] = g.u[5] = 0.0;
     if (kind == 1 || kind == 3) { g.u[0] = 1.0; g.u[1] = 0.0; }
     if (kind == 3) { g.u[6] = 1.0; g.u[7] = 0.0; }
+    if (kind == 4) g.u[1] = g.u[3] = g.u[5] = g.u[7] = 0.0;
+    if (kind == 5) for (int i = 0; i < 8; ++i) g.u[i] = (i == 2 || i == 4) ? 1.0 : 0.0;
+    if (kind == 6) for (double &x : g.u) x = (rng() & 1) ? 0.5 : -0.5;
+    if (kind == 7) for (int i = 0; i < 8; ++i) g.u[i] = i == 0 ? 1.0 : i == 6 ? -1.0 : 0.0;
     return g;
 }
 
@@ -74,11 +80,23 @@ static void check_plan(const std::vector<qvg_gate> &ops, const PlanOptions &po) 
                 const TileOp &t = p.tile_ops[rec + 1 + i];
                 CHECK(t.kind == TILE_PAIR || t.kind == TILE_DIAG);
                 if (t.kind == TILE_PAIR) {
-                    CHECK(t.slot >= 0 && t.slot < 8 * g.sub);  // 8*J + (K+1) with J >= 0 (target in the group)
-                    if (!(t.slot >= 0 && t.slot < 8 * g.sub) && failures < 5)
+                    // 32*class + 8*J + (K+1) with J >= 0 (target in the group)
+                    const int cls = t.slot >> 5, js = t.slot & 31;
+                    CHECK(cls >= TILE_CLS_GEN && cls <= TILE_CLS_HALF && (po.classes || cls == TILE_CLS_GEN));
+                    CHECK(js < 8 * g.sub);
+                    if (!(js < 8 * g.sub) && failures < 5)
                         std::fprintf(stderr, "  slot %d sub %d k %d tbit %d cbit %d\n", t.slot, g.sub, g.k, t.tbit, t.cbit);
+                    if (cls == TILE_CLS_HALF)  // (s0/2, -s0 s1, -s2 s3, s0 s2) per row
+                        for (int row = 0; row < 2; ++row) {
+                            const double *m = t.u + 4 * row;
+                            CHECK((m[0] == 0.5 || m[0] == -0.5) && (m[1] == 1.0 || m[1] == -1.0) &&
+                                  (m[2] == 1.0 || m[2] == -1.0) && (m[3] == 1.0 || m[3] == -1.0));
+                        }
+                } else {
+                    CHECK((t.slot & 63) < 8 * (g.sub + 1));
+                    CHECK(t.slot >> 7 <= 1 && (po.classes || t.slot < 128));
+                    if (t.slot >= 128) CHECK(t.u[0] == 1.0 && t.u[6] == -1.0 && (t.slot & 64) == 0);
                 }
-                else CHECK((t.slot & 63) < 8 * (g.sub + 1));
                 ++covered;
             }
             rec += 1 + nops;
@@ -133,6 +151,7 @@ int main(int argc, char **argv) {
         po.sub_bits = rng() % 2 ? 3 : 4;
         po.stage_bits = (uint32_t)(rng() % 4);
         po.reorder = rng() % 2;
+        po.classes = rng() % 4 != 0;
         check_plan(ops, po);
         const uint32_t g = (uint32_t)(rng() % 4);
         if (n >= g + 2) check_schedule(ops, n, g, 1 + (uint32_t)(rng() % 4));

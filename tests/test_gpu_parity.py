@@ -314,3 +314,36 @@ def test_reorder_mode_within_tolerance(qv, oracle):
             else:
                 assert np.array_equal(got, want)
         assert passes[1] <= passes[0], (n, passes)
+
+
+# --- structured-matrix op bodies in fused tiles (QVG_OPT_CLASSES, qvg_tile.cuh) ---
+@pytest.mark.parametrize("n", [7, 12, 16])
+def test_structured_classes_bit_exact(qv, oracle, n):
+    """Real (H, ry), X (x, the CX target), entries +-1/2 (sx, sy and adjoint-like
+    sign patterns as `u`/`cu`) and Z/CZ take the reduced-FP64 bodies; results
+    are bit-identical to the oracle and to the general bodies, for every
+    register slot / control slot combination the planner produces."""
+    start = oracle.simulate(n, gate_array(qv.random_circuit(n, 30, 5)))
+    half = ["0.5 0.5 0.5 -0.5 0.5 -0.5 0.5 0.5", "0.5 -0.5 0.5 0.5 0.5 0.5 0.5 -0.5",
+            "0.5 0.5 -0.5 -0.5 0.5 0.5 0.5 0.5", "0.5 -0.5 0.5 -0.5 -0.5 0.5 0.5 -0.5"]
+    lines = [f"qubits {n}"]
+    for k in range(n):
+        c = (k + 1 + k % 3) % n
+        lines += [f"sx {k}", f"h {k}", f"cx {c} {k}", f"sy {k}", f"cz {c} {k}", f"z {k}",
+                  f"u {k} {half[k % 4]}", f"cu {c} {k} {half[(k + 1) % 4]}", f"ry {k} 0.4", f"x {k}",
+                  f"sw {k}", f"cx {k} {(k + 5) % n}"]
+    circ = qv.parse_circuit("\n".join(lines) + "\n")
+    want = oracle.apply(n, start.copy(), gate_array(circ))
+    for classes in (1, 0):
+        for tq, sub in ((0, 4), (7, 3), (5, 3)):
+            st = qv.StateVector.create(n, 128, 0)
+            st.load_state(start)
+            st.set_option(qv.OPT_CLASSES, classes)
+            st.set_option(qv.OPT_SUB_BITS, sub)
+            qv.apply_circuit(st, circ, strategy="gpu", fuse=True, tile_qubits=tq)
+            got = st.read_state()
+            assert np.array_equal(got, want), (classes, tq, sub, np.abs(got - want).max())
+    st = qv.StateVector.create(n, 64, 0)
+    st.load_state(start.astype(np.complex64))
+    qv.apply_circuit(st, circ, strategy="gpu", fuse=True)
+    assert np.abs(st.read_state() - want).max() <= 1e-5

@@ -24,7 +24,7 @@ VARIANTS = [("fused_sub3_k11", 1, 3, 0, 11, 0), ("fused_sub3_k12", 1, 3, 0, 12, 
             ("fused_sub3_k10", 1, 3, 0, 10, 0), ("fused_sub3_k11_fma", 1, 3, 1, 11, 0),
             ("fused_sub3_k11_pf", 1, 3, 0, 11, 1), ("fused_sub3_k10_pf", 1, 3, 0, 10, 1),
             ("fused_sub3_k12_pf", 1, 3, 0, 12, 1), ("fused_sub4_k11", 1, 4, 0, 11, 0),
-            ("fused_reorder", 1, 4, 0, 11, 0), ("per_gate", 0, 3, 0, 11, 0)]
+            ("fused_reorder", 1, 4, 0, 11, 0), ("fused_sub4_k11_noclass", 1, 4, 0, 11, 0), ("per_gate", 0, 3, 0, 11, 0)]
 
 
 def circuits(n):
@@ -62,6 +62,8 @@ def main():
             st.set_option(qv.OPT_FMA, fma)
             st.set_option(qv.OPT_PREFETCH, pf)
             st.set_option(qv.OPT_REORDER, 1 if vname.endswith("reorder") else 0)
+            if hasattr(qv, "OPT_CLASSES"):
+                st.set_option(qv.OPT_CLASSES, 0 if vname.endswith("noclass") else 1)
             if a.stage >= 0:
                 st.set_option(qv.OPT_STAGE, a.stage)
             st.apply_gates(g)  # warm-up (and plan)
