@@ -82,7 +82,7 @@ def main():
                           "amp_updates_per_s": len(c) * (1 << a.n) / (ms / 1e3),
                           "hbm_gbs": s["bytes_moved"] / a.reps / (ms / 1e3) / 1e9}
         out.append(row)
-        print(name, " ".join(f"{k}={v['ms']:.1f}ms/{v['passes']:.0f}p" for k, v in row.items() if isinstance(v, dict)),
+        print(name, " ".join(f"{k}={v['ms']:.3f}ms/{v['passes']:.0f}p" for k, v in row.items() if isinstance(v, dict)),
               file=sys.stderr)
     st.set_option(qv.OPT_SUB_BITS, 3)
     st.set_option(qv.OPT_FMA, 0)
