@@ -237,15 +237,16 @@ void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *recs) {
     };
     // Passes without structured ops (classes off) use the REAL-set kernel:
     // their records only name general bodies, which both sets compile.
-    const bool half_set = g.cls_set == kClsSetHalf;
-    auto kern = half_set ? pick(std::integral_constant<int, kClsSetHalf>{})
-                         : pick(std::integral_constant<int, kClsSetReal>{});
+    const int set_idx = g.cls_set == kClsSetHalf ? 1 : g.cls_set == kClsSetHalfW ? 2 : 0;
+    auto kern = set_idx == 1   ? pick(std::integral_constant<int, kClsSetHalf>{})
+                : set_idx == 2 ? pick(std::integral_constant<int, kClsSetHalfW>{})
+                               : pick(std::integral_constant<int, kClsSetReal>{});
     // The shared-memory opt-in is a per-device function attribute: set it once
     // per (device, variant).
-    static std::atomic<uint64_t> attr_set[64][2];  // [device][class set]: a bit per variant
+    static std::atomic<uint64_t> attr_set[64][3];  // [device][class set]: a bit per variant
     const int variant = (sizeof(R) == 8 ? 1 : 0) | (g.sub == 4 ? 2 : 0) | (fma ? 4 : 0) | (small ? 8 : 0) |
                         (pf ? 16 : 0) | (tiny ? 32 : 0);
-    std::atomic<uint64_t> &set = attr_set[s.device & 63][half_set ? 1 : 0];
+    std::atomic<uint64_t> &set = attr_set[s.device & 63][set_idx];
     if (!((set.load(std::memory_order_acquire) >> variant) & 1u)) {
         cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
                    "cudaFuncSetAttribute(k_tile)");

@@ -50,21 +50,38 @@ inline int pair_class(const double *u) {
         u[7] == 0.0)
         return TILE_CLS_SWAP;
     if (u[1] == 0.0 && u[3] == 0.0 && u[5] == 0.0 && u[7] == 0.0) return TILE_CLS_REAL;
+    auto h = [&](int i) { return u[i] == 0.5 || u[i] == -0.5; };
     bool half = true;
-    for (int i = 0; i < 8; ++i) half = half && (u[i] == 0.5 || u[i] == -0.5);
-    return half ? TILE_CLS_HALF : TILE_CLS_GEN;
+    for (int i = 0; i < 8; ++i) half = half && h(i);
+    if (half) return TILE_CLS_HALF;
+    if (h(0) && h(1) && h(6) && h(7) && u[2] == 0.0 && u[3] != 0.0 && u[4] != 0.0 && u[5] == 0.0)
+        return TILE_CLS_SQW;
+    return TILE_CLS_GEN;
 }
 
-// The class set of one fused pass (k_tile compiles REAL or HALF bodies, not
-// both): whichever of the two covers more of the pass's ops; ops of the other
-// class run the general body.
+// The record's u[] for an SQW-class op: (s0/2, -s0 s1, q) for lo (u00 and
+// u01 = (0, q)) and (s0'/2, -s0' s1', p) for hi (u11 and u10 = (p, 0)), as
+// sqw_lo / sqw_hi (qvg_tile.cuh) expect.
+inline void sqw_record(const double *u, double *out) {
+    auto sg = [](double x) { return x > 0 ? 1.0 : -1.0; };
+    double r[8] = {u[0], -sg(u[0]) * sg(u[1]), u[3], 0.0, u[6], -sg(u[6]) * sg(u[7]), u[4], 0.0};
+    std::memcpy(out, r, sizeof(r));
+}
+
+// The class set of one fused pass: a k_tile instantiation compiles at most
+// three sets of pair bodies without spilling (qvg_tile.cuh), so the pass
+// takes the set that saves the most FP64 instructions per pair (real 16,
+// X 24, +-1/2 12, sqrt(W) 16); ops of other classes run the general body.
 inline int tile_class_set(const OpInfo *info, uint64_t begin, uint64_t end) {
-    uint64_t real = 0, half = 0;
+    uint64_t n[5] = {};
     for (uint64_t x = begin; x < end; ++x) {
         if (info[x].identity || info[x].diag) continue;
-        real += info[x].cls == TILE_CLS_REAL;
-        half += info[x].cls == TILE_CLS_HALF;
+        n[info[x].cls] += 1;
     }
+    const uint64_t real = 16 * n[TILE_CLS_REAL] + 24 * n[TILE_CLS_SWAP];
+    const uint64_t half = 12 * n[TILE_CLS_HALF] + 24 * n[TILE_CLS_SWAP];
+    const uint64_t halfw = 12 * n[TILE_CLS_HALF] + 16 * n[TILE_CLS_SQW];
+    if (halfw > real && halfw > half) return kClsSetHalfW;
     return half > real ? kClsSetHalf : kClsSetReal;
 }
 
@@ -387,6 +404,7 @@ inline Plan make_plan(const qvg_gate *ops, uint64_t count, const PlanOptions &po
                 else
                     t.slot = ((g.cls_set >> o.cls) & 1) ? o.cls : TILE_CLS_GEN;
                 if (t.kind == TILE_PAIR && t.slot == TILE_CLS_HALF) half_record(ops[x].u, t.u);
+                if (t.kind == TILE_PAIR && t.slot == TILE_CLS_SQW) sqw_record(ops[x].u, t.u);
                 if (t.kind == TILE_PAIR) {
                     // The target must be a register bit. An in-tile control is
                     // made one too: the control test is then the same for every

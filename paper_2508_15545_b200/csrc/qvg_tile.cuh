@@ -114,7 +114,18 @@ __device__ __forceinline__ void group_pair(typename Cplx<R>::T (&v)[1 << SUB], c
 //     reference's (s0/2 a.re - s1/2 a.im) + (s2/2 b.re - s3/2 b.im) bit for
 //     bit (unless an intermediate falls below 2^-1021 in magnitude, where
 //     halving rounds). 16 FP64 instructions instead of 28.
-enum TileCls : int32_t { TILE_CLS_GEN = 0, TILE_CLS_REAL = 1, TILE_CLS_SWAP = 2, TILE_CLS_HALF = 3 };
+//   TILE_CLS_SQW: diagonal entries as in HALF, u01 = (0, q) imaginary and
+//     u10 = (p, 0) real (sqrt(W) of the grid circuits): with u00 = (s0, s1)/2,
+//       lo.re = fma(s0/2, a.re - s0s1 a.im, -(q*b.im)),
+//     where s0/2 times the bracket is exact, so the DFMA rounds like the
+//     reference's final DADD, and 0*b.re contributes +-0. 12 instead of 28.
+enum TileCls : int32_t {
+    TILE_CLS_GEN = 0,
+    TILE_CLS_REAL = 1,
+    TILE_CLS_SWAP = 2,
+    TILE_CLS_HALF = 3,
+    TILE_CLS_SQW = 4
+};
 
 __device__ __forceinline__ double xsgn(double x, uint32_t m) {
     return __hiloint2double(__double2hiint(x) ^ (int)m, __double2loint(x));
@@ -171,12 +182,44 @@ __device__ __forceinline__ T real_apply(double m0, double m1, T a, T b) {
     return o;
 }
 
+// SQW-class records carry per output row the half entry's (s0/2, -s0 s1)
+// and the off-diagonal entry's non-zero part: lo (u00, u01 = (0, q)) in
+// u[0..2] = (s0/2, -s0 s1, q), hi (u11, u10 = (p, 0)) in u[4..6] =
+// (s0'/2, -s0' s1', p) (sqw_record, qvg_plan.hpp).
+template <class T, class R>
+__device__ __forceinline__ T sqw_lo(const double *uu, T a, T b) {  // u00 a + (0, q) b
+    const R s = (R)uu[0], c1 = (R)uu[1], q = (R)uu[2];
+    T r;
+    if constexpr (sizeof(R) == 8) {
+        r.x = __fma_rn(s, __fma_rn(c1, a.y, a.x), -__dmul_rn(q, b.y));
+        r.y = __fma_rn(s, __fma_rn(-c1, a.x, a.y), __dmul_rn(q, b.x));
+    } else {
+        r.x = fmaf(s, fmaf(c1, a.y, a.x), -(q * b.y));
+        r.y = fmaf(s, fmaf(-c1, a.x, a.y), q * b.x);
+    }
+    return r;
+}
+template <class T, class R>
+__device__ __forceinline__ T sqw_hi(const double *uu, T a, T b) {  // (p, 0) a + u11 b
+    const R s = (R)uu[4], c1 = (R)uu[5], p = (R)uu[6];
+    T r;
+    if constexpr (sizeof(R) == 8) {
+        r.x = __fma_rn(s, __fma_rn(c1, b.y, b.x), __dmul_rn(p, a.x));
+        r.y = __fma_rn(s, __fma_rn(-c1, b.x, b.y), __dmul_rn(p, a.y));
+    } else {
+        r.x = fmaf(s, fmaf(c1, b.y, b.x), p * a.x);
+        r.y = fmaf(s, fmaf(-c1, b.x, b.y), p * a.y);
+    }
+    return r;
+}
+
 // Class sets a k_tile instantiation compiles (CM: bit per TileCls). With all
 // four sets of bodies in one 96-register kernel ptxas spills inside the
 // bodies (~1 KB of local traffic per op); with three it does not. The planner
 // picks the set per pass (tile_class_set, qvg_plan.hpp).
 constexpr int kClsSetReal = (1 << TILE_CLS_GEN) | (1 << TILE_CLS_REAL) | (1 << TILE_CLS_SWAP);
 constexpr int kClsSetHalf = (1 << TILE_CLS_GEN) | (1 << TILE_CLS_HALF) | (1 << TILE_CLS_SWAP);
+constexpr int kClsSetHalfW = (1 << TILE_CLS_GEN) | (1 << TILE_CLS_HALF) | (1 << TILE_CLS_SQW);
 template <class R, int SUB, int J, int K, bool FMA, int CLS, int CM>
 __device__ __forceinline__ void group_pair_cls(typename Cplx<R>::T (&v)[1 << SUB], const double *uu) {
     using T = typename Cplx<R>::T;
@@ -198,6 +241,15 @@ __device__ __forceinline__ void group_pair_cls(typename Cplx<R>::T (&v)[1 << SUB
                 const T a = v[r], b = v[r | (1 << J)];
                 v[r] = real_apply<T, R, FMA>(uu[0], uu[2], a, b);
                 v[r | (1 << J)] = real_apply<T, R, FMA>(uu[4], uu[6], a, b);
+            }
+        } else if constexpr (CLS == TILE_CLS_SQW) {
+#pragma unroll
+            for (int r = 0; r < (1 << SUB); ++r) {
+                if ((r >> J) & 1) continue;
+                if (K >= 0 && !((r >> K) & 1)) continue;
+                const T a = v[r], b = v[r | (1 << J)];
+                v[r] = sqw_lo<T, R>(uu, a, b);
+                v[r | (1 << J)] = sqw_hi<T, R>(uu, a, b);
             }
         } else {  // TILE_CLS_HALF
 #pragma unroll
@@ -225,6 +277,9 @@ __device__ __forceinline__ void group_pair_dispatch(int code, typename Cplx<R>::
         break;                                                                                \
     case 32 * TILE_CLS_HALF + 8 * (J) + (K) + 1:                                              \
         group_pair_cls<R, SUB, J, K, FMA, TILE_CLS_HALF, CM>(v, u);                               \
+        break;                                                                                \
+    case 32 * TILE_CLS_SQW + 8 * (J) + (K) + 1:                                               \
+        group_pair_cls<R, SUB, J, K, FMA, TILE_CLS_SQW, CM>(v, u);                                \
         break;
     switch (code) {
         QVG_GP(0, -1) QVG_GP(0, 1) QVG_GP(0, 2) QVG_GP(0, 3)

@@ -39,8 +39,8 @@ static qvg_gate random_gate(std::mt19937_64 &rng, uint32_t n) {
     }
     std::uniform_real_distribution<double> u(-1.0, 1.0);
     // dense, diag(1,d), diag(d0,d1), identity, then the structured classes:
-    // real, X, entries +-1/2, Z
-    const int kind = (int)(rng() % 8);
+    // real, X, entries +-1/2, Z, sqrt(W)-like
+    const int kind = (int)(rng() % 9);
     for (double &x : g.u) x = u(rng);
     if (kind >= 1 && kind <= 3) g.u[2] = g.u[3] = g.u[4] = g.u[5] = 0.0;
     if (kind == 1 || kind == 3) { g.u[0] = 1.0; g.u[1] = 0.0; }
@@ -49,6 +49,13 @@ static qvg_gate random_gate(std::mt19937_64 &rng, uint32_t n) {
     if (kind == 5) for (int i = 0; i < 8; ++i) g.u[i] = (i == 2 || i == 4) ? 1.0 : 0.0;
     if (kind == 6) for (double &x : g.u) x = (rng() & 1) ? 0.5 : -0.5;
     if (kind == 7) for (int i = 0; i < 8; ++i) g.u[i] = i == 0 ? 1.0 : i == 6 ? -1.0 : 0.0;
+    if (kind == 8) {
+        for (double &x : g.u) x = (rng() & 1) ? 0.5 : -0.5;
+        g.u[2] = 0.0;
+        g.u[5] = 0.0;
+        g.u[3] = u(rng);
+        g.u[4] = u(rng);
+    }
     return g;
 }
 
@@ -82,7 +89,13 @@ static void check_plan(const std::vector<qvg_gate> &ops, const PlanOptions &po) 
                 if (t.kind == TILE_PAIR) {
                     // 32*class + 8*J + (K+1) with J >= 0 (target in the group)
                     const int cls = t.slot >> 5, js = t.slot & 31;
-                    CHECK(cls >= TILE_CLS_GEN && cls <= TILE_CLS_HALF && (po.classes || cls == TILE_CLS_GEN));
+                    CHECK(cls >= TILE_CLS_GEN && cls <= TILE_CLS_SQW && (po.classes || cls == TILE_CLS_GEN));
+                    CHECK((g.cls_set >> cls) & 1);
+                    if (cls == TILE_CLS_SQW)  // (s0/2, -s0 s1, q, 0) per row
+                        for (int row = 0; row < 2; ++row) {
+                            const double *m = t.u + 4 * row;
+                            CHECK((m[0] == 0.5 || m[0] == -0.5) && (m[1] == 1.0 || m[1] == -1.0) && m[3] == 0.0);
+                        }
                     CHECK(js < 8 * g.sub);
                     if (!(js < 8 * g.sub) && failures < 5)
                         std::fprintf(stderr, "  slot %d sub %d k %d tbit %d cbit %d\n", t.slot, g.sub, g.k, t.tbit, t.cbit);

@@ -347,3 +347,30 @@ def test_structured_classes_bit_exact(qv, oracle, n):
     st.load_state(start.astype(np.complex64))
     qv.apply_circuit(st, circ, strategy="gpu", fuse=True)
     assert np.abs(st.read_state() - want).max() <= 1e-5
+
+
+@pytest.mark.parametrize("n", [8, 13])
+def test_grid_gate_set_bit_exact(qv, oracle, n):
+    """Passes of sqrt(X)/sqrt(Y)/sqrt(W) + CZ only (config 3's gate set) take the
+    {general, +-1/2, sqrt(W)} body set; bit-identical to the oracle, with
+    every register-slot and control-slot combination."""
+    start = oracle.simulate(n, gate_array(qv.random_circuit(n, 20, 8)))
+    rng = np.random.default_rng(n)
+    lines = [f"qubits {n}"]
+    for _ in range(12):
+        for k in range(n):
+            lines.append(f"{['sx', 'sy', 'sw'][int(rng.integers(3))]} {k}")
+        for k in range(n):
+            c = int(rng.integers(n))
+            if c != k:
+                lines.append(f"cz {c} {k}")
+                lines.append(f"cu {c} {k} 0.5 0.5 0 -0.7071067811865476 0.7071067811865476 0 0.5 0.5")
+    circ = qv.parse_circuit("\n".join(lines) + "\n")
+    want = oracle.apply(n, start.copy(), gate_array(circ))
+    for tq, sub in ((0, 4), (6, 3)):
+        st = qv.StateVector.create(n, 128, 0)
+        st.load_state(start)
+        st.set_option(qv.OPT_SUB_BITS, sub)
+        qv.apply_circuit(st, circ, strategy="gpu", fuse=True, tile_qubits=tq)
+        got = st.read_state()
+        assert np.array_equal(got, want), (tq, sub, np.abs(got - want).max())
