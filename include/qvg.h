@@ -86,8 +86,10 @@ enum qvg_option {
                                 its HBM data through shared memory, coalesced (default b = 3; 0 never) */
     QVG_OPT_GRAPH = 14,      /* 1: unsharded states replay a repeated op list as a captured CUDA graph
                                 (no per-pass host planning/launch cost; default 0) */
-    QVG_OPT_REORDER = 15,    /* 1: fusion may move an op ahead of ops on disjoint qubits (fewer passes;
-                                mathematically equal but NOT bit-identical to the reference; default 0) */
+    QVG_OPT_REORDER = 15,    /* fusion may move an op ahead of ops on disjoint qubits (fewer passes):
+                                2 = only moves that keep every bit (an X/CX permutation or a Z/CZ sign
+                                flip on either side; default), 1 = any such move (mathematically equal,
+                                NOT bit-identical to the reference), 0 = circuit order */
     QVG_OPT_CLASSES = 16     /* fused tile: 1 = structured-matrix op bodies (real, X, entries +-1/2, Z),
                                 same values with fewer FP64 instructions (default); 0 = general bodies */
 };

@@ -104,7 +104,7 @@ struct qvg_state {
     uint32_t batch_max = 4;    // sharded: most global qubits one exchange swaps (QVG_OPT_BATCH_EXCHANGE)
     uint32_t stage_bits = 3;   // fused tile: stage first/last group HBM access through shared memory (QVG_OPT_STAGE)
     bool graph = false;        // QVG_OPT_GRAPH: replay repeated op lists as captured CUDA graphs
-    bool reorder = false;      // QVG_OPT_REORDER: commutation-aware fusion order (not bit-exact)
+    uint32_t reorder = REORDER_EXACT;  // QVG_OPT_REORDER: commutation-aware fusion order (qvg_plan.hpp)
     bool classes = true;       // QVG_OPT_CLASSES: structured-matrix op bodies in fused tiles
     struct GraphEntry {
         uint64_t key = 0;
@@ -279,12 +279,7 @@ PlanOptions plan_options(const qvg_state &s) {
 void run_local(qvg_state &s, void *psi, const qvg_gate *ops, uint64_t count) {
     if (count == 0) return;
     const PlanOptions po = plan_options(s);
-    std::vector<qvg_gate> reordered;
-    if (po.reorder && po.fuse && std::min(po.tile_qubits, po.n) >= 5) {  // only where tiles exist
-        reordered = reorder_for_tiles(ops, count, po);
-        ops = reordered.data();
-    }
-    const Plan plan = make_plan(ops, count, po);
+    const Plan plan = plan_ops(ops, count, po);
     const bool dbl = s.precision == QVG_C128;
     for (const Pass &p : plan.passes) {
         switch (p.kind) {
@@ -552,7 +547,10 @@ int qvg_set_option(qvg_state *s, int key, int64_t value) {
             if (value < 0 || value > 1) throw Validation("prefetch must be 0 or 1");
             s->prefetch_mode = (int)value;
             break;
-        case QVG_OPT_REORDER: s->reorder = value != 0; break;
+        case QVG_OPT_REORDER:
+            if (value < 0 || value > 2) throw Validation("reorder must be 0 (never), 1 (any commuting move) or 2 (bit-exact moves)");
+            s->reorder = (uint32_t)value;
+            break;
         case QVG_OPT_CLASSES: s->classes = value != 0; break;
         case QVG_OPT_GRAPH:
             s->graph = value != 0;
@@ -1085,7 +1083,7 @@ int qvg_plan_passes(uint32_t n_qubits, uint32_t precision, int fuse, uint32_t ti
         po.tile_qubits = tile_qubits ? std::min<uint32_t>(tile_qubits, 12) : 11;
         po.carriers = carriers;
         po.sub_bits = 4;  // the engine's default (create_impl)
-        const Plan plan = make_plan(ops, count, po);
+        const Plan plan = plan_ops(ops, count, po);  // as run_local (default reorder mode)
         uint64_t fused = 0, bytes = 0;
         for (const Pass &p : plan.passes) {
             fused += p.kind == PASS_TILE;

@@ -62,8 +62,21 @@ static qvg_gate random_gate(std::mt19937_64 &rng, uint32_t n) {
 static void check_plan(const std::vector<qvg_gate> &ops, const PlanOptions &po) {
     std::vector<qvg_gate> list = ops;
     if (po.reorder) {
-        list = reorder_for_tiles(ops.data(), ops.size(), po);
-        CHECK(list.size() == ops.size());
+        std::vector<uint64_t> order;
+        list = reorder_for_tiles(ops.data(), ops.size(), po, &order);
+        CHECK(list.size() == ops.size() && order.size() == ops.size());
+        // every inverted pair acts on disjoint qubits; in the bit-exact mode
+        // one of the two is a permutation or a +-1 phase
+        std::vector<uint64_t> pos(ops.size());
+        for (uint64_t x = 0; x < order.size(); ++x) pos[order[x]] = x;
+        for (uint64_t a = 0; a < ops.size(); ++a)
+            for (uint64_t b = a + 1; b < ops.size(); ++b) {
+                if (pos[a] < pos[b]) continue;
+                const OpInfo oa = classify(ops[a]), ob = classify(ops[b]);
+                auto touches = [](const OpInfo &o, int q) { return o.target == q || o.control == q; };
+                CHECK(!touches(oa, ob.target) && (ob.control < 0 || !touches(oa, ob.control)));
+                if (po.reorder == REORDER_EXACT) CHECK(exact_commuter(oa) || exact_commuter(ob));
+            }
     }
     const Plan p = make_plan(list.data(), list.size(), po);
     uint64_t covered = 0, live = 0;
@@ -163,7 +176,7 @@ int main(int argc, char **argv) {
         po.carriers = (uint32_t)(rng() % 5);
         po.sub_bits = rng() % 2 ? 3 : 4;
         po.stage_bits = (uint32_t)(rng() % 4);
-        po.reorder = rng() % 2;
+        po.reorder = (uint32_t)(rng() % 3);
         po.classes = rng() % 4 != 0;
         check_plan(ops, po);
         const uint32_t g = (uint32_t)(rng() % 4);

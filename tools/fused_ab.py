@@ -24,7 +24,10 @@ VARIANTS = [("fused_sub3_k11", 1, 3, 0, 11, 0), ("fused_sub3_k12", 1, 3, 0, 12, 
             ("fused_sub3_k10", 1, 3, 0, 10, 0), ("fused_sub3_k11_fma", 1, 3, 1, 11, 0),
             ("fused_sub3_k11_pf", 1, 3, 0, 11, 1), ("fused_sub3_k10_pf", 1, 3, 0, 10, 1),
             ("fused_sub3_k12_pf", 1, 3, 0, 12, 1), ("fused_sub4_k11", 1, 4, 0, 11, 0),
-            ("fused_reorder", 1, 4, 0, 11, 0), ("fused_sub4_k11_noclass", 1, 4, 0, 11, 0), ("per_gate", 0, 3, 0, 11, 0)]
+            ("fused_reorder", 1, 4, 0, 11, 0), ("fused_sub4_k11_noclass", 1, 4, 0, 11, 0),
+            ("fused_sub4_k11_inorder", 1, 4, 0, 11, 0), ("per_gate", 0, 3, 0, 11, 0)]
+# OPT_REORDER per variant: *_reorder = 1 (any commuting move, not bit-exact),
+# *_inorder = 0 (circuit order), otherwise the default 2 (bit-exact moves)
 
 
 def circuits(n):
@@ -61,7 +64,7 @@ def main():
             st.set_option(qv.OPT_SUB_BITS, sub)
             st.set_option(qv.OPT_FMA, fma)
             st.set_option(qv.OPT_PREFETCH, pf)
-            st.set_option(qv.OPT_REORDER, 1 if vname.endswith("reorder") else 0)
+            st.set_option(qv.OPT_REORDER, 1 if vname.endswith("reorder") else 0 if vname.endswith("inorder") else 2)
             if hasattr(qv, "OPT_CLASSES"):
                 st.set_option(qv.OPT_CLASSES, 0 if vname.endswith("noclass") else 1)
             if a.stage >= 0:
@@ -87,7 +90,7 @@ def main():
     st.set_option(qv.OPT_SUB_BITS, 3)
     st.set_option(qv.OPT_FMA, 0)
     st.set_option(qv.OPT_PREFETCH, 0)
-    st.set_option(qv.OPT_REORDER, 0)
+    st.set_option(qv.OPT_REORDER, 2)
     st.set_option(qv.OPT_FUSE, 1)
     st.set_option(qv.OPT_TILE_QUBITS, 11)
     print(json.dumps({"n": a.n, "precision": a.precision, "reps": a.reps, "rows": out}, indent=1))

@@ -1,0 +1,43 @@
+"""Per-pass view of a fused circuit for ncu: applies one BASELINE circuit
+(fused, default options) once so that an ncu launch list shows every tile
+pass with its duration, FP64-pipe and DRAM activity.
+
+    ncu --metrics gpu__time_duration.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,\
+dram__throughput.avg.pct_of_peak_sustained_elapsed,smsp__issue_active.avg.pct_of_peak_sustained_active \
+        -k regex:k_tile --csv python tools/pass_profile.py --circuit grid
+"""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2508_15545_b200 as qv  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=30)
+    ap.add_argument("--circuit", default="sweep", choices=["sweep", "grid", "ladder", "qft"])
+    ap.add_argument("--sub", type=int, default=4)
+    ap.add_argument("--prefetch", type=int, default=0)
+    ap.add_argument("--tile", type=int, default=11)
+    a = ap.parse_args()
+    n = a.n
+    c = {"sweep": lambda: qv.haar_sweep_circuit(n, 2508),
+         "grid": lambda: qv.grid_circuit(5, 6, 24, 1) if n == 30 else qv.grid_circuit(4, n // 4, 24, 1),
+         "ladder": lambda: qv.u3_ladder_circuit(n, 4, 1),
+         "qft": lambda: qv.qft_circuit(n, 1)[0]}[a.circuit]()
+    st = qv.StateVector.create(n, 128, 0)
+    st.apply_gates(qv.make_benchmark_circuit(n).gates())
+    st.set_option(qv.OPT_SUB_BITS, a.sub)
+    st.set_option(qv.OPT_PREFETCH, a.prefetch)
+    st.set_option(qv.OPT_TILE_QUBITS, a.tile)
+    st.apply_gates(c.gates())
+    st.sync()
+    print("ok", st.stats())
+
+
+if __name__ == "__main__":
+    main()
