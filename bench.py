@@ -311,6 +311,71 @@ def fused_leg(qv, st, circ, line, args):
     st.set_option(qv.OPT_FUSE, 0)
 
 
+def c64_leg(qv, circ, recs, line, args):
+    """BASELINE config 2 also names complex64: the same per-gate sweep on an
+    8 GiB complex64 state (fusion off, per-launch events on the state's
+    stream), its dominant launch class against the HBM roofline, per-gate ms
+    and GB/s, and the fused time. Not the headline (the metric is c128)."""
+    import torch
+
+    n = circ.n_qubits
+    nops = len(recs)
+    st = qv.StateVector.create(n, 64, torch.cuda.current_device())
+    st.set_option(qv.OPT_FUSE, 0)
+    stream = torch.cuda.ExternalStream(st.stream())
+    st.apply_gates(qv.make_benchmark_circuit(n).gates())
+    for _ in range(args.warmup):
+        for i in range(nops):
+            st.apply_gates(recs[i], sync=False)
+    st.sync()
+    steps = max(1, args.steps)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nops + 1)] for _ in range(steps)]
+    for k in range(steps):
+        evs[k][0].record(stream)
+        for i in range(nops):
+            st.apply_gates(recs[i], sync=False)
+            evs[k][i + 1].record(stream)
+    st.sync()
+    per_op = np.array([[evs[k][i].elapsed_time(evs[k][i + 1]) for i in range(nops)] for k in range(steps)])
+    mean_op = per_op.mean(axis=0)
+    ms_step = float(per_op.sum(axis=1).mean())
+    nbytes = [algorithmic_bytes(n, recs[i], S=8) for i in range(nops)]
+    share = {}
+    for i in range(nops):
+        k = kernel_of(n, recs[i]).replace("double", "float")
+        share.setdefault(k, [0.0, 0, 0])
+        share[k][0] += mean_op[i]
+        share[k][1] += nbytes[i]
+        share[k][2] += 1
+    dom = max(share, key=lambda k: share[k][0])
+    dom_ms, dom_bytes, dom_n = share[dom]
+    hbm_peak, peak_kind = peaks()
+    achieved = (dom_bytes / dom_n) / ((dom_ms / dom_n) / 1e3) / 1e9
+    st.set_option(qv.OPT_FUSE, 1)
+    st.apply_gates(circ.gates())
+    st.sync()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        st.apply_gates(circ.gates(), sync=False)
+    b.record(stream)
+    st.sync()
+    fused_ms = a.elapsed_time(b) / steps
+    line["c64"] = {
+        "value": nops * (1 << n) / (ms_step / 1e3), "unit": UNIT, "ms_per_step": ms_step, "dtype": "c64 (f32)",
+        "hbm_gbs_step": sum(nbytes) / (ms_step / 1e3) / 1e9,
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak, "peak_kind": peak_kind,
+                     "unit": "GB/s", "frac": achieved / hbm_peak, "launch_ms": dom_ms / dom_n,
+                     "algorithmic_bytes_per_launch": dom_bytes / dom_n},
+        "per_kernel": {k: {"launches_per_step": v[2], "ms_per_launch": v[0] / v[2],
+                           "gbs": (v[1] / v[2]) / ((v[0] / v[2]) / 1e3) / 1e9} for k, v in share.items()},
+        "per_gate": [{"op": i, "gate": gate_label(recs[i]), "ms": round(float(mean_op[i]), 4),
+                      "gbs": round(nbytes[i] / (mean_op[i] / 1e3) / 1e9, 1)} for i in range(nops)],
+        "fused": {"ms_per_step": fused_ms, "value": nops * (1 << n) / (fused_ms / 1e3)},
+    }
+    del st
+
+
 def pcie_bidir_gbs(host, host2):
     """The e2e roofline: pinned host<->device bandwidth with both directions
     busy at once (what a pipelined e2e step needs), measured here with a
@@ -611,6 +676,7 @@ def main():
         fused_leg(qv, st, circ, line, args)
         if not args.no_e2e:
             e2e_leg(qv, st, circ, recs, line, args)
+        c64_leg(qv, circ, recs, line, args)
     elif not args.no_e2e:
         e2e_leg_sharded(qv, st, circ, line, args, rank, world, dist)
     if rank == 0:
