@@ -376,17 +376,24 @@ inline Plan make_plan(const qvg_gate *ops, uint64_t count, const PlanOptions &po
                     if (!used(b)) gbits[nb++] = b;
                 std::sort(gbits, gbits + g.sub);
                 for (TileOp &t : group) {
-                    // pair: slot = 32*class + 8*J + (K+1); diag: slot = 128*neg + 64*(d0 != 1) +
-                    // 8*(J+1) + (K+1), J / K the target / control register slots (-1: not in
-                    // the group). Before this point slot holds the class (pair) or the
-                    // d0 == 1 / neg flags (diag, bits 0 / 1).
+                    // slot = dispatch index | flags (op_dispatch, qvg_tile.cuh), J / K the
+                    // target / control register slots (-1: not in the group). Before this
+                    // point slot holds the class (pair) or the d0 == 1 / neg flags (diag,
+                    // bits 0 / 1).
                     int J = -1, K = -1;
                     for (int s = 0; s < g.sub; ++s) {
                         if (t.tbit >= 0 && gbits[s] == t.tbit) J = s;
                         if (t.cbit >= 0 && gbits[s] == t.cbit) K = s;
                     }
-                    if (t.kind == TILE_PAIR) t.slot = 32 * t.slot + 8 * J + K + 1;
-                    else t.slot = ((t.slot & 2) ? 128 : (t.slot & 1) ? 0 : 64) + 8 * (J + 1) + K + 1;
+                    if (t.kind == TILE_PAIR) {
+                        t.slot = 20 * t.slot + 5 * J + K + 1;
+                    } else {
+                        const bool neg = (t.slot & 2) != 0, d0one = (t.slot & 1) != 0;
+                        t.slot = kDispDiag + (neg ? 25 : 0) + 5 * (J + 1) + K + 1;
+                        if (K < 0 && t.cbit >= 0) t.slot |= kSlotCtlTest;
+                        if (J < 0) t.slot |= kSlotT1;
+                        if (!neg && !d0one) t.slot |= kSlotD0;
+                    }
                 }
                 TileOp h{};
                 h.kind = TILE_GROUP;

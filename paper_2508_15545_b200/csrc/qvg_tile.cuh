@@ -41,8 +41,8 @@ struct __align__(16) TileOp {
     int32_t kind;      // TileOpKind
     int32_t tbit;      // pair/diag: tile-local target bit (-1: diag target outside Q); group: op count
     int32_t cbit;      // tile-local control bit, -1 if none or outside Q
-    int32_t slot;      // dispatch code: pair 32*class+8*J+(K+1), diag 128*neg+64*(d0!=1)+8*(J+1)+(K+1)
-                       // (J/K: register slots)
+    int32_t slot;      // dispatch index | flags (op_dispatch): pair 20*class+5*J+(K+1), diag
+                       // 100+25*neg+5*(J+1)+(K+1); J/K: register slots
     uint64_t greq;     // global bits that must be 1 in the tile base (controls outside Q)
     uint64_t gtgt;     // diag: global target bit outside Q; group: packed bits b0 | b1<<8 | b2<<16 | b3<<24
     double u[8];       // matrix (diag uses u00 = u[0..1], u11 = u[6..7])
@@ -264,33 +264,6 @@ __device__ __forceinline__ void group_pair_cls(typename Cplx<R>::T (&v)[1 << SUB
     }
 }
 
-// slot code = 32*CLS + 8*J + (K+1)
-template <class R, int SUB, bool FMA, int CM>
-__device__ __forceinline__ void group_pair_dispatch(int code, typename Cplx<R>::T (&v)[1 << SUB], const double *u) {
-#define QVG_GP(J, K)                                                                         \
-    case 8 * (J) + (K) + 1: group_pair<R, SUB, J, K, FMA>(v, u); break;                      \
-    case 32 * TILE_CLS_REAL + 8 * (J) + (K) + 1:                                              \
-        group_pair_cls<R, SUB, J, K, FMA, TILE_CLS_REAL, CM>(v, u);                               \
-        break;                                                                                \
-    case 32 * TILE_CLS_SWAP + 8 * (J) + (K) + 1:                                              \
-        group_pair_cls<R, SUB, J, K, FMA, TILE_CLS_SWAP, CM>(v, u);                               \
-        break;                                                                                \
-    case 32 * TILE_CLS_HALF + 8 * (J) + (K) + 1:                                              \
-        group_pair_cls<R, SUB, J, K, FMA, TILE_CLS_HALF, CM>(v, u);                               \
-        break;                                                                                \
-    case 32 * TILE_CLS_SQW + 8 * (J) + (K) + 1:                                               \
-        group_pair_cls<R, SUB, J, K, FMA, TILE_CLS_SQW, CM>(v, u);                                \
-        break;
-    switch (code) {
-        QVG_GP(0, -1) QVG_GP(0, 1) QVG_GP(0, 2) QVG_GP(0, 3)
-        QVG_GP(1, -1) QVG_GP(1, 0) QVG_GP(1, 2) QVG_GP(1, 3)
-        QVG_GP(2, -1) QVG_GP(2, 0) QVG_GP(2, 1) QVG_GP(2, 3)
-        QVG_GP(3, -1) QVG_GP(3, 0) QVG_GP(3, 1) QVG_GP(3, 2)
-    default: break;
-    }
-#undef QVG_GP
-}
-
 // Diagonal op diag(d0, d1) over the register subcube. The target is on slot J
 // (-1: outside the group, then t1 is its value for this thread's whole
 // subcube). The control is on slot K (-1: none, or tested per thread/tile
@@ -358,19 +331,45 @@ __device__ __forceinline__ void group_diag_rt(typename Cplx<R>::T (&v)[1 << SUB]
     }
 }
 
-// diag code = 128*NEG + 64*D0 + 8*(J+1) + (K+1)
-template <class R, int SUB, bool FMA>
-__device__ __forceinline__ void group_diag_dispatch(int code, typename Cplx<R>::T (&v)[1 << SUB], const double *u,
-                                                    bool t1) {
-#define QVG_GD(J, K)                                                   \
-    case 8 * ((J) + 1) + (K) + 1:                                      \
-    case 64 + 8 * ((J) + 1) + (K) + 1:                                 \
-        group_diag_rt<R, SUB, J, K, FMA, false>(v, u, t1, code >= 64); \
-        break;                                                         \
-    case 128 + 8 * ((J) + 1) + (K) + 1:                                \
-        group_diag_rt<R, SUB, J, K, FMA, true>(v, u, t1, false);       \
+// One dense dispatch index per op (TileOp::slot & 0xff), so the switch
+// compiles to a single jump table (one indirect branch per op). Sparse codes
+// compiled to a compare-and-branch tree, and the instruction-fetch bubbles
+// after its branches were the kernel's top stall (no_instruction).
+//   pair:     20*class + 5*J + (K+1)              0..99
+//   diagonal: 100 + 25*neg + 5*(J+1) + (K+1)     100..149
+constexpr int kDispDiag = 100;
+constexpr int kSlotCtlTest = 256;  // diagonal: control in the tile but not in the group: test per thread
+constexpr int kSlotT1 = 512;       // diagonal: target not in the group: t1 per thread / tile
+constexpr int kSlotD0 = 1024;      // diagonal: d0 != 1
+template <class R, int SUB, bool FMA, int CM>
+__device__ __forceinline__ void op_dispatch(int d, typename Cplx<R>::T (&v)[1 << SUB], const double *u, bool t1,
+                                            bool d0) {
+#define QVG_GP(J, K)                                                                          \
+    case 20 * TILE_CLS_GEN + 5 * (J) + (K) + 1: group_pair<R, SUB, J, K, FMA>(v, u); break;   \
+    case 20 * TILE_CLS_REAL + 5 * (J) + (K) + 1:                                              \
+        group_pair_cls<R, SUB, J, K, FMA, TILE_CLS_REAL, CM>(v, u);                           \
+        break;                                                                                \
+    case 20 * TILE_CLS_SWAP + 5 * (J) + (K) + 1:                                              \
+        group_pair_cls<R, SUB, J, K, FMA, TILE_CLS_SWAP, CM>(v, u);                           \
+        break;                                                                                \
+    case 20 * TILE_CLS_HALF + 5 * (J) + (K) + 1:                                              \
+        group_pair_cls<R, SUB, J, K, FMA, TILE_CLS_HALF, CM>(v, u);                           \
+        break;                                                                                \
+    case 20 * TILE_CLS_SQW + 5 * (J) + (K) + 1:                                               \
+        group_pair_cls<R, SUB, J, K, FMA, TILE_CLS_SQW, CM>(v, u);                            \
         break;
-    switch (code) {
+#define QVG_GD(J, K)                                                  \
+    case kDispDiag + 5 * ((J) + 1) + (K) + 1:                         \
+        group_diag_rt<R, SUB, J, K, FMA, false>(v, u, t1, d0);        \
+        break;                                                        \
+    case kDispDiag + 25 + 5 * ((J) + 1) + (K) + 1:                    \
+        group_diag_rt<R, SUB, J, K, FMA, true>(v, u, t1, false);      \
+        break;
+    switch (d) {
+        QVG_GP(0, -1) QVG_GP(0, 1) QVG_GP(0, 2) QVG_GP(0, 3)
+        QVG_GP(1, -1) QVG_GP(1, 0) QVG_GP(1, 2) QVG_GP(1, 3)
+        QVG_GP(2, -1) QVG_GP(2, 0) QVG_GP(2, 1) QVG_GP(2, 3)
+        QVG_GP(3, -1) QVG_GP(3, 0) QVG_GP(3, 1) QVG_GP(3, 2)
         QVG_GD(-1, -1) QVG_GD(-1, 0) QVG_GD(-1, 1) QVG_GD(-1, 2) QVG_GD(-1, 3)
         QVG_GD(0, -1) QVG_GD(0, 1) QVG_GD(0, 2) QVG_GD(0, 3)
         QVG_GD(1, -1) QVG_GD(1, 0) QVG_GD(1, 2) QVG_GD(1, 3)
@@ -378,6 +377,7 @@ __device__ __forceinline__ void group_diag_dispatch(int code, typename Cplx<R>::
         QVG_GD(3, -1) QVG_GD(3, 0) QVG_GD(3, 1) QVG_GD(3, 2)
     default: break;
     }
+#undef QVG_GP
 #undef QVG_GD
 }
 
@@ -524,16 +524,12 @@ k_tile(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams
             for (int i = 0; i < nops; ++i) {
                 const TileOp &op = ops[rec + i];
                 if ((base & op.greq) != op.greq) continue;  // control outside the tile is 0
-                if (op.kind == TILE_PAIR) {
-                    group_pair_dispatch<R, SUB, FMA, CM>(op.slot, v, op.u);
-                } else {
-                    // tile bits outside the group are per-thread bits of l0
-                    if ((op.slot & 7) == 0 && op.cbit >= 0 && !((l0 >> op.cbit) & 1u)) continue;
-                    bool t1 = false;
-                    if ((op.slot & 0x38) == 0)
-                        t1 = op.tbit >= 0 ? ((l0 >> op.tbit) & 1u) != 0 : (base & op.gtgt) != 0;
-                    group_diag_dispatch<R, SUB, FMA>(op.slot, v, op.u, t1);
-                }
+                const int sl = op.slot;
+                // tile bits outside the group are per-thread bits of l0
+                if ((sl & kSlotCtlTest) && !((l0 >> op.cbit) & 1u)) continue;
+                bool t1 = false;
+                if (sl & kSlotT1) t1 = op.tbit >= 0 ? ((l0 >> op.tbit) & 1u) != 0 : (base & op.gtgt) != 0;
+                op_dispatch<R, SUB, FMA, CM>(sl & 0xff, v, op.u, t1, (sl & kSlotD0) != 0);
             }
             rec += nops;
             if (gi == g.ngroups - 1 && (g.stage & 2)) {

@@ -100,8 +100,9 @@ static void check_plan(const std::vector<qvg_gate> &ops, const PlanOptions &po) 
                 const TileOp &t = p.tile_ops[rec + 1 + i];
                 CHECK(t.kind == TILE_PAIR || t.kind == TILE_DIAG);
                 if (t.kind == TILE_PAIR) {
-                    // 32*class + 8*J + (K+1) with J >= 0 (target in the group)
-                    const int cls = t.slot >> 5, js = t.slot & 31;
+                    // 20*class + 5*J + (K+1) with J >= 0 (target in the group)
+                    CHECK((t.slot & ~0xff) == 0 && t.slot < kDispDiag);
+                    const int cls = t.slot / 20, js = 8 * ((t.slot % 20) / 5);
                     CHECK(cls >= TILE_CLS_GEN && cls <= TILE_CLS_SQW && (po.classes || cls == TILE_CLS_GEN));
                     CHECK((g.cls_set >> cls) & 1);
                     if (cls == TILE_CLS_SQW)  // (s0/2, -s0 s1, q, 0) per row
@@ -119,9 +120,15 @@ static void check_plan(const std::vector<qvg_gate> &ops, const PlanOptions &po) 
                                   (m[2] == 1.0 || m[2] == -1.0) && (m[3] == 1.0 || m[3] == -1.0));
                         }
                 } else {
-                    CHECK((t.slot & 63) < 8 * (g.sub + 1));
-                    CHECK(t.slot >> 7 <= 1 && (po.classes || t.slot < 128));
-                    if (t.slot >= 128) CHECK(t.u[0] == 1.0 && t.u[6] == -1.0 && (t.slot & 64) == 0);
+                    const int d = t.slot & 0xff;  // 100 + 25*neg + 5*(J+1) + (K+1)
+                    CHECK(d >= kDispDiag && d < kDispDiag + 50);
+                    const int neg = (d - kDispDiag) / 25, J = ((d - kDispDiag) % 25) / 5 - 1,
+                              K = (d - kDispDiag) % 5 - 1;
+                    CHECK(J < g.sub && K < g.sub && (J < 0 || J != K));
+                    CHECK(po.classes || !neg);
+                    if (neg) CHECK(t.u[0] == 1.0 && t.u[6] == -1.0 && !(t.slot & kSlotD0));
+                    CHECK(((t.slot & kSlotT1) != 0) == (J < 0));
+                    CHECK(((t.slot & kSlotCtlTest) != 0) == (K < 0 && t.cbit >= 0));
                 }
                 ++covered;
             }
