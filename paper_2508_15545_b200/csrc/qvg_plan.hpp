@@ -393,6 +393,17 @@ inline Plan make_plan(const qvg_gate *ops, uint64_t count, const PlanOptions &po
                         if (K < 0 && t.cbit >= 0) t.slot |= kSlotCtlTest;
                         if (J < 0) t.slot |= kSlotT1;
                         if (!neg && !d0one) t.slot |= kSlotD0;
+                        // A tile bit outside the group is a bit of the thread index:
+                        // store that position, so the kernel tests threadIdx.x (which
+                        // it can re-read) instead of the subcube base l0 (which it
+                        // spilled under the 96-register limit and reloaded per op).
+                        auto tpos = [&](int p) {
+                            int below = 0;
+                            for (int x = 0; x < g.sub; ++x) below += gbits[x] < p;
+                            return p - below;
+                        };
+                        if (K < 0 && t.cbit >= 0) t.cbit = tpos(t.cbit);
+                        if (J < 0 && t.tbit >= 0) t.tbit = tpos(t.tbit);
                     }
                 }
                 TileOp h{};

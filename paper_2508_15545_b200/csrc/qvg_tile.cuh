@@ -39,8 +39,10 @@ enum TileOpKind : int32_t { TILE_PAIR = 0, TILE_DIAG = 1, TILE_GROUP = 2 };
 // One record of a tile pass: a group header followed by its ops.
 struct __align__(16) TileOp {
     int32_t kind;      // TileOpKind
-    int32_t tbit;      // pair/diag: tile-local target bit (-1: diag target outside Q); group: op count
-    int32_t cbit;      // tile-local control bit, -1 if none or outside Q
+    int32_t tbit;      // pair/diag: tile-local target bit (-1: diag target outside Q; diag target
+                       // in Q but not in the group: its thread-index bit); group: op count
+    int32_t cbit;      // tile-local control bit, -1 if none or outside Q (diag control in Q but
+                       // not in the group: its thread-index bit)
     int32_t slot;      // dispatch index | flags (op_dispatch): pair 20*class+5*J+(K+1), diag
                        // 100+25*neg+5*(J+1)+(K+1); J/K: register slots
     uint64_t greq;     // global bits that must be 1 in the tile base (controls outside Q)
@@ -525,10 +527,11 @@ k_tile(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams
                 const TileOp &op = ops[rec + i];
                 if ((base & op.greq) != op.greq) continue;  // control outside the tile is 0
                 const int sl = op.slot;
-                // tile bits outside the group are per-thread bits of l0
-                if ((sl & kSlotCtlTest) && !((l0 >> op.cbit) & 1u)) continue;
+                // tile bits outside the group are bits of the thread index
+                // (the planner stores their thread-bit positions)
+                if ((sl & kSlotCtlTest) && !((threadIdx.x >> op.cbit) & 1u)) continue;
                 bool t1 = false;
-                if (sl & kSlotT1) t1 = op.tbit >= 0 ? ((l0 >> op.tbit) & 1u) != 0 : (base & op.gtgt) != 0;
+                if (sl & kSlotT1) t1 = op.tbit >= 0 ? ((threadIdx.x >> op.tbit) & 1u) != 0 : (base & op.gtgt) != 0;
                 op_dispatch<R, SUB, FMA, CM>(sl & 0xff, v, op.u, t1, (sl & kSlotD0) != 0);
             }
             rec += nops;
