@@ -441,6 +441,12 @@ inline Plan make_plan(const qvg_gate *ops, uint64_t count, const PlanOptions &po
                     t.slot = ((g.cls_set >> o.cls) & 1) ? o.cls : TILE_CLS_GEN;
                 if (t.kind == TILE_PAIR && t.slot == TILE_CLS_HALF) half_record(ops[x].u, t.u);
                 if (t.kind == TILE_PAIR && t.slot == TILE_CLS_SQW) sqw_record(ops[x].u, t.u);
+                if (po.amp_bytes == 8) {  // complex64: the kernel reads 8 floats (no F2F per use)
+                    float f[8];
+                    for (int e = 0; e < 8; ++e) f[e] = (float)t.u[e];
+                    std::memset(t.u, 0, sizeof(t.u));
+                    std::memcpy(t.u, f, sizeof(f));
+                }
                 if (t.kind == TILE_PAIR) {
                     // The target must be a register bit. An in-tile control is
                     // made one too: the control test is then the same for every

@@ -47,7 +47,8 @@ struct __align__(16) TileOp {
                        // 100+25*neg+5*(J+1)+(K+1); J/K: register slots
     uint64_t greq;     // global bits that must be 1 in the tile base (controls outside Q)
     uint64_t gtgt;     // diag: global target bit outside Q; group: packed bits b0 | b1<<8 | b2<<16 | b3<<24
-    double u[8];       // matrix (diag uses u00 = u[0..1], u11 = u[6..7])
+    double u[8];       // matrix (diag uses u00 = u[0..1], u11 = u[6..7]); complex64 passes: the same
+                       // 8 values as floats in the first 32 bytes (no per-use conversion)
 };
 static_assert(sizeof(TileOp) == 96, "TileOp layout");
 
@@ -85,11 +86,11 @@ __device__ __forceinline__ uint32_t swz(uint32_t l) { return l ^ ((l >> 3) & 7u)
 // The matrix is read here, straight from the record in the parameter bank,
 // so each op loads only what its case uses.
 template <class R, int SUB, int J, int K, bool FMA>
-__device__ __forceinline__ void group_pair(typename Cplx<R>::T (&v)[1 << SUB], const double *uu) {
+__device__ __forceinline__ void group_pair(typename Cplx<R>::T (&v)[1 << SUB], const R *uu) {
     if constexpr (J < SUB && K < SUB && J != K) {
         R u[8];
 #pragma unroll
-        for (int x = 0; x < 8; ++x) u[x] = (R)uu[x];
+        for (int x = 0; x < 8; ++x) u[x] = uu[x];
 #pragma unroll
         for (int r = 0; r < (1 << SUB); ++r) {
             if ((r >> J) & 1) continue;
@@ -152,8 +153,8 @@ __device__ __forceinline__ float2 mov_opaque(float2 x) {
 // FP64 instructions per component, no sign-bit moves, and every constant is
 // a parameter-bank operand (ptxas reloads rather than spills it).
 template <class T, class R>
-__device__ __forceinline__ T half_apply(const double *uu, T a, T b) {
-    const R h = (R)uu[0], c1 = (R)uu[1], c2 = (R)uu[2], c3 = (R)uu[3];
+__device__ __forceinline__ T half_apply(const R *uu, T a, T b) {
+    const R h = uu[0], c1 = uu[1], c2 = uu[2], c3 = uu[3];
     T o;
     if constexpr (sizeof(R) == 8) {
         const double xr = __fma_rn(c1, a.y, a.x), yr = __fma_rn(c2, b.y, b.x);
@@ -172,7 +173,7 @@ __device__ __forceinline__ T half_apply(const double *uu, T a, T b) {
 // REAL class: (m0*a.re + m1*b.re, m0*a.im + m1*b.im); the entries are read
 // at the point of use (parameter-bank operands, reloaded under pressure).
 template <class T, class R, bool FMA>
-__device__ __forceinline__ T real_apply(double m0, double m1, T a, T b) {
+__device__ __forceinline__ T real_apply(R m0, R m1, T a, T b) {
     T o;
     if constexpr (sizeof(R) == 8 && !FMA) {
         o.x = __dadd_rn(__dmul_rn(m0, a.x), __dmul_rn(m1, b.x));
@@ -189,8 +190,8 @@ __device__ __forceinline__ T real_apply(double m0, double m1, T a, T b) {
 // u[0..2] = (s0/2, -s0 s1, q), hi (u11, u10 = (p, 0)) in u[4..6] =
 // (s0'/2, -s0' s1', p) (sqw_record, qvg_plan.hpp).
 template <class T, class R>
-__device__ __forceinline__ T sqw_lo(const double *uu, T a, T b) {  // u00 a + (0, q) b
-    const R s = (R)uu[0], c1 = (R)uu[1], q = (R)uu[2];
+__device__ __forceinline__ T sqw_lo(const R *uu, T a, T b) {  // u00 a + (0, q) b
+    const R s = uu[0], c1 = uu[1], q = uu[2];
     T r;
     if constexpr (sizeof(R) == 8) {
         r.x = __fma_rn(s, __fma_rn(c1, a.y, a.x), -__dmul_rn(q, b.y));
@@ -202,8 +203,8 @@ __device__ __forceinline__ T sqw_lo(const double *uu, T a, T b) {  // u00 a + (0
     return r;
 }
 template <class T, class R>
-__device__ __forceinline__ T sqw_hi(const double *uu, T a, T b) {  // (p, 0) a + u11 b
-    const R s = (R)uu[4], c1 = (R)uu[5], p = (R)uu[6];
+__device__ __forceinline__ T sqw_hi(const R *uu, T a, T b) {  // (p, 0) a + u11 b
+    const R s = uu[4], c1 = uu[5], p = uu[6];
     T r;
     if constexpr (sizeof(R) == 8) {
         r.x = __fma_rn(s, __fma_rn(c1, b.y, b.x), __dmul_rn(p, a.x));
@@ -223,7 +224,7 @@ constexpr int kClsSetReal = (1 << TILE_CLS_GEN) | (1 << TILE_CLS_REAL) | (1 << T
 constexpr int kClsSetHalf = (1 << TILE_CLS_GEN) | (1 << TILE_CLS_HALF) | (1 << TILE_CLS_SWAP);
 constexpr int kClsSetHalfW = (1 << TILE_CLS_GEN) | (1 << TILE_CLS_HALF) | (1 << TILE_CLS_SQW);
 template <class R, int SUB, int J, int K, bool FMA, int CLS, int CM>
-__device__ __forceinline__ void group_pair_cls(typename Cplx<R>::T (&v)[1 << SUB], const double *uu) {
+__device__ __forceinline__ void group_pair_cls(typename Cplx<R>::T (&v)[1 << SUB], const R *uu) {
     using T = typename Cplx<R>::T;
     if constexpr (J < SUB && K < SUB && J != K && ((CM >> CLS) & 1)) {
         if constexpr (CLS == TILE_CLS_SWAP) {
@@ -278,7 +279,7 @@ __device__ __forceinline__ void group_pair_cls(typename Cplx<R>::T (&v)[1 << SUB
 // Z and CZ) flips the sign bits instead: (-1)*re - 0*im is -re up to the sign
 // of an exact zero, and no FP64 instruction is issued.
 template <class R, int SUB, int J, int K, bool FMA, bool NEG>
-__device__ __forceinline__ void group_diag_rt(typename Cplx<R>::T (&v)[1 << SUB], const double *uu, bool t1,
+__device__ __forceinline__ void group_diag_rt(typename Cplx<R>::T (&v)[1 << SUB], const R *uu, bool t1,
                                               bool d0) {
     using T = typename Cplx<R>::T;
     auto neg = [](T x) {
@@ -296,7 +297,7 @@ __device__ __forceinline__ void group_diag_rt(typename Cplx<R>::T (&v)[1 << SUB]
                 }
                 return;
             } else {
-                const R d1r = (R)uu[6], d1i = (R)uu[7];
+                const R d1r = uu[6], d1i = uu[7];
 #pragma unroll
                 for (int r = 0; r < (1 << SUB); ++r) {
                     if (K >= 0 && !((r >> K) & 1)) continue;
@@ -304,7 +305,7 @@ __device__ __forceinline__ void group_diag_rt(typename Cplx<R>::T (&v)[1 << SUB]
                 }
             }
             if (d0) {
-                const R d0r = (R)uu[0], d0i = (R)uu[1];
+                const R d0r = uu[0], d0i = uu[1];
 #pragma unroll
                 for (int r = 0; r < (1 << SUB); ++r) {
                     if (K >= 0 && !((r >> K) & 1)) continue;
@@ -322,7 +323,7 @@ __device__ __forceinline__ void group_diag_rt(typename Cplx<R>::T (&v)[1 << SUB]
                 }
                 return;
             } else {
-                const R dr = (R)(t1 ? uu[6] : uu[0]), di = (R)(t1 ? uu[7] : uu[1]);
+                const R dr = t1 ? uu[6] : uu[0], di = t1 ? uu[7] : uu[1];
 #pragma unroll
                 for (int r = 0; r < (1 << SUB); ++r) {
                     if (K >= 0 && !((r >> K) & 1)) continue;
@@ -344,7 +345,7 @@ constexpr int kSlotCtlTest = 256;  // diagonal: control in the tile but not in t
 constexpr int kSlotT1 = 512;       // diagonal: target not in the group: t1 per thread / tile
 constexpr int kSlotD0 = 1024;      // diagonal: d0 != 1
 template <class R, int SUB, bool FMA, int CM>
-__device__ __forceinline__ void op_dispatch(int d, typename Cplx<R>::T (&v)[1 << SUB], const double *u, bool t1,
+__device__ __forceinline__ void op_dispatch(int d, typename Cplx<R>::T (&v)[1 << SUB], const R *u, bool t1,
                                             bool d0) {
 #define QVG_GP(J, K)                                                                          \
     case 20 * TILE_CLS_GEN + 5 * (J) + (K) + 1: group_pair<R, SUB, J, K, FMA>(v, u); break;   \
@@ -532,7 +533,8 @@ k_tile(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams
                 if ((sl & kSlotCtlTest) && !((threadIdx.x >> op.cbit) & 1u)) continue;
                 bool t1 = false;
                 if (sl & kSlotT1) t1 = op.tbit >= 0 ? ((threadIdx.x >> op.tbit) & 1u) != 0 : (base & op.gtgt) != 0;
-                op_dispatch<R, SUB, FMA, CM>(sl & 0xff, v, op.u, t1, (sl & kSlotD0) != 0);
+                // complex64 records carry the matrix as 8 floats (tile_record_precision)
+                op_dispatch<R, SUB, FMA, CM>(sl & 0xff, v, reinterpret_cast<const R *>(op.u), t1, (sl & kSlotD0) != 0);
             }
             rec += nops;
             if (gi == g.ngroups - 1 && (g.stage & 2)) {

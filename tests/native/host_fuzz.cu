@@ -98,6 +98,10 @@ static void check_plan(const std::vector<qvg_gate> &ops, const PlanOptions &po) 
             CHECK(nops >= 1 && rec + 1 + nops <= end);
             for (int i = 0; i < nops; ++i) {
                 const TileOp &t = p.tile_ops[rec + 1 + i];
+                // record values: 8 doubles, or 8 floats for complex64 passes
+                double uv[8];
+                for (int e = 0; e < 8; ++e)
+                    uv[e] = po.amp_bytes == 8 ? (double)reinterpret_cast<const float *>(t.u)[e] : t.u[e];
                 CHECK(t.kind == TILE_PAIR || t.kind == TILE_DIAG);
                 if (t.kind == TILE_PAIR) {
                     // 20*class + 5*J + (K+1) with J >= 0 (target in the group)
@@ -107,7 +111,7 @@ static void check_plan(const std::vector<qvg_gate> &ops, const PlanOptions &po) 
                     CHECK((g.cls_set >> cls) & 1);
                     if (cls == TILE_CLS_SQW)  // (s0/2, -s0 s1, q, 0) per row
                         for (int row = 0; row < 2; ++row) {
-                            const double *m = t.u + 4 * row;
+                            const double *m = uv + 4 * row;
                             CHECK((m[0] == 0.5 || m[0] == -0.5) && (m[1] == 1.0 || m[1] == -1.0) && m[3] == 0.0);
                         }
                     CHECK(js < 8 * g.sub);
@@ -115,7 +119,7 @@ static void check_plan(const std::vector<qvg_gate> &ops, const PlanOptions &po) 
                         std::fprintf(stderr, "  slot %d sub %d k %d tbit %d cbit %d\n", t.slot, g.sub, g.k, t.tbit, t.cbit);
                     if (cls == TILE_CLS_HALF)  // (s0/2, -s0 s1, -s2 s3, s0 s2) per row
                         for (int row = 0; row < 2; ++row) {
-                            const double *m = t.u + 4 * row;
+                            const double *m = uv + 4 * row;
                             CHECK((m[0] == 0.5 || m[0] == -0.5) && (m[1] == 1.0 || m[1] == -1.0) &&
                                   (m[2] == 1.0 || m[2] == -1.0) && (m[3] == 1.0 || m[3] == -1.0));
                         }
@@ -126,7 +130,7 @@ static void check_plan(const std::vector<qvg_gate> &ops, const PlanOptions &po) 
                               K = (d - kDispDiag) % 5 - 1;
                     CHECK(J < g.sub && K < g.sub && (J < 0 || J != K));
                     CHECK(po.classes || !neg);
-                    if (neg) CHECK(t.u[0] == 1.0 && t.u[6] == -1.0 && !(t.slot & kSlotD0));
+                    if (neg) CHECK(uv[0] == 1.0 && uv[6] == -1.0 && !(t.slot & kSlotD0));
                     CHECK(((t.slot & kSlotT1) != 0) == (J < 0));
                     CHECK(((t.slot & kSlotCtlTest) != 0) == (K < 0 && t.cbit >= 0));
                 }

@@ -22,18 +22,20 @@ def main():
     ap.add_argument("--circuit", default="sweep", choices=["sweep", "grid", "ladder", "qft"])
     ap.add_argument("--sub", type=int, default=4)
     ap.add_argument("--prefetch", type=int, default=0)
-    ap.add_argument("--tile", type=int, default=11)
+    ap.add_argument("--tile", type=int, default=0, help="tile qubits (0: the precision's default)")
+    ap.add_argument("--precision", type=int, default=128)
     a = ap.parse_args()
     n = a.n
     c = {"sweep": lambda: qv.haar_sweep_circuit(n, 2508),
          "grid": lambda: qv.grid_circuit(5, 6, 24, 1) if n == 30 else qv.grid_circuit(4, n // 4, 24, 1),
          "ladder": lambda: qv.u3_ladder_circuit(n, 4, 1),
          "qft": lambda: qv.qft_circuit(n, 1)[0]}[a.circuit]()
-    st = qv.StateVector.create(n, 128, 0)
+    st = qv.StateVector.create(n, a.precision, 0)
     st.apply_gates(qv.make_benchmark_circuit(n).gates())
     st.set_option(qv.OPT_SUB_BITS, a.sub)
     st.set_option(qv.OPT_PREFETCH, a.prefetch)
-    st.set_option(qv.OPT_TILE_QUBITS, a.tile)
+    if a.tile:
+        st.set_option(qv.OPT_TILE_QUBITS, a.tile)
     st.apply_gates(c.gates())
     st.sync()
     print("ok", st.stats())
