@@ -205,6 +205,12 @@ inline Pass single_pass(const qvg_gate &g, const OpInfo &o, const PlanOptions &p
     return p;
 }
 
+// Global index offset of tile-local bit p: the low carriers map to
+// themselves, bits >= lowc to their high qubits.
+inline uint64_t tile_bit_offset(const TileGeom &g, int p) {
+    return p < g.lowc ? 1ull << p : 1ull << g.hiq[p - g.lowc];
+}
+
 inline int local_bit(int q, const TileGeom &g) {
     if (q < g.lowc) return q;
     for (int i = 0; i < g.nhi; ++i)
@@ -335,6 +341,7 @@ inline Plan make_plan(const qvg_gate *ops, uint64_t count, const PlanOptions &po
                 if (inq[q]) g.hiq[g.nhi++] = (int)q;
             g.ntiles = 1ull << (n - k);
             g.sub = (int)std::min<uint32_t>(sub, k - 2);
+            for (int s = 0; s < g.sub; ++s) g.sdep[s] = tile_bit_offset(g, g.k - g.sub + s);
             Pass p;
             p.kind = PASS_TILE;
             p.op_begin = (uint32_t)plan.tile_ops.size();
@@ -410,6 +417,10 @@ inline Plan make_plan(const qvg_gate *ops, uint64_t count, const PlanOptions &po
                 h.kind = TILE_GROUP;
                 h.tbit = (int32_t)group.size();
                 for (int s = 0; s < g.sub; ++s) h.gtgt |= (uint64_t)gbits[s] << (8 * s);
+                for (int s = 0; s < g.sub; ++s) {  // global offsets of the group's bits
+                    const uint64_t d = tile_bit_offset(g, gbits[s]);
+                    std::memcpy(&h.u[s], &d, sizeof(d));
+                }
                 uint32_t low = 0;  // lowest tile bits the group holds: its lanes are 2^low amplitudes apart
                 while ((int)low < g.sub && gbits[low] == (int)low) ++low;
                 if (g.ngroups == 0) first_low = low;

@@ -47,7 +47,7 @@ struct __align__(16) TileOp {
                        // 100+25*neg+5*(J+1)+(K+1); J/K: register slots
     uint64_t greq;     // global bits that must be 1 in the tile base (controls outside Q)
     uint64_t gtgt;     // diag: global target bit outside Q; group: packed bits b0 | b1<<8 | b2<<16 | b3<<24
-    double u[8];       // matrix (diag uses u00 = u[0..1], u11 = u[6..7]); complex64 passes: the same
+    double u[8];       // group: u[j] holds (as bits) the global offset of tile-local bit b_j; op: matrix (diag uses u00 = u[0..1], u11 = u[6..7]); complex64 passes: the same
                        // 8 values as floats in the first 32 bytes (no per-use conversion)
 };
 static_assert(sizeof(TileOp) == 96, "TileOp layout");
@@ -62,6 +62,8 @@ struct TileGeom {
     int cls_set;          // structured-matrix classes this pass uses (kClsSetReal / kClsSetHalf)
     int hiq[24];          // tile qubits >= lowc, ascending (tile-local bits lowc..k-1)
     uint64_t ntiles;      // 2^(n-k)
+    uint64_t sdep[4];     // global offset of tile-local bit (k - sub + i): the staged (coalesced)
+                          // layout's index t + j*blockDim is t | j << (k - sub)
 };
 
 // Records per fused pass; they travel as the kernel's parameter block
@@ -474,6 +476,11 @@ k_tile(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams
         for (int gi = 0; gi < g.ngroups; ++gi) {
             const int nops = ops[rec].tbit;
             const uint64_t packed = ops[rec].gtgt;
+            // global offsets of the group's bits (the planner's group header):
+            // amplitude r of the subcube sits at base | dep(l0) | OR_j r_j gdep[j],
+            // so an address needs one shared-memory lookup per group, not one per
+            // amplitude (those LDS fed every global load and store address)
+            const uint64_t *gdep = reinterpret_cast<const uint64_t *>(ops[rec].u);
             ++rec;
             int b[SUB];
 #pragma unroll
@@ -487,6 +494,39 @@ k_tile(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams
 #pragma unroll
                 for (int j = 0; j < SUB; ++j) l |= ((r >> j) & 1) ? (1u << b[j]) : 0u;
                 return l;
+            };
+            // complex128 (FP64-issue bound) takes the offsets; complex64 (ALU-issue
+            // bound) measured faster with the per-amplitude lookups (64-bit ORs
+            // cost it more than the LDS latency): C3 c64 525 vs 597 ms
+            constexpr bool kDep = sizeof(R) == 8;
+            const bool direct = (gi == 0 && !(g.stage & 1) && !PF) || (gi == g.ngroups - 1 && !(g.stage & 2));
+            uint64_t dl0 = 0;
+            if (kDep && direct) dl0 = base | offhi[l0 >> g.lowc] | (l0 & lowm);
+            auto gaddr = [&](int r) {  // global index of subcube amplitude r
+                if constexpr (kDep) {
+                    uint64_t a = dl0;
+#pragma unroll
+                    for (int j = 0; j < SUB; ++j)
+                        if ((r >> j) & 1) a |= gdep[j];
+                    return a;
+                } else {
+                    const uint32_t lr = lidx(r);
+                    return base | offhi[lr >> g.lowc] | (lr & lowm);
+                }
+            };
+            // staged (coalesced) layout: index t + j*blockDim = t | j << (k - sub)
+            const uint32_t t = threadIdx.x;
+            auto saddr = [&](uint64_t dt, int j) {
+                if constexpr (kDep) {
+                    uint64_t a = dt;
+#pragma unroll
+                    for (int i = 0; i < SUB; ++i)
+                        if ((j >> i) & 1) a |= g.sdep[i];
+                    return a;
+                } else {
+                    const uint32_t l = t + (uint32_t)j * blockDim.x;
+                    return base | offhi[l >> g.lowc] | (l & lowm);
+                }
             };
             T v[E];
             if (PF && gi == 0) {
@@ -504,11 +544,9 @@ k_tile(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams
                 // the group's bits include the lowest tile bits, so its lanes
                 // would stride through HBM: load the tile coalesced (lane =
                 // consecutive amplitudes) into shared memory first
+                const uint64_t dt = kDep ? base | offhi[t >> g.lowc] | (t & lowm) : 0;
 #pragma unroll
-                for (int j = 0; j < E; ++j) {  // all loads in flight before the first store
-                    const uint32_t l = threadIdx.x + (uint32_t)j * blockDim.x;
-                    v[j] = ld_amp(psi + (base | offhi[l >> g.lowc] | (l & lowm)));
-                }
+                for (int j = 0; j < E; ++j) v[j] = ld_amp(psi + saddr(dt, j));  // all loads in flight first
 #pragma unroll
                 for (int j = 0; j < E; ++j) sm[swz(threadIdx.x + (uint32_t)j * blockDim.x)] = v[j];
                 __syncthreads();
@@ -516,10 +554,7 @@ k_tile(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams
                 for (int r = 0; r < E; ++r) v[r] = sm[swz(lidx(r))];
             } else if (gi == 0) {
 #pragma unroll
-                for (int r = 0; r < E; ++r) {
-                    const uint32_t lr = lidx(r);
-                    v[r] = ld_amp(psi + (base | offhi[lr >> g.lowc] | (lr & lowm)));
-                }
+                for (int r = 0; r < E; ++r) v[r] = ld_amp(psi + gaddr(r));
             } else {
 #pragma unroll
                 for (int r = 0; r < E; ++r) v[r] = sm[swz(lidx(r))];
@@ -545,17 +580,12 @@ k_tile(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams
                 __syncthreads();
 #pragma unroll
                 for (int j = 0; j < E; ++j) v[j] = sm[swz(threadIdx.x + (uint32_t)j * blockDim.x)];
+                const uint64_t dt = kDep ? base | offhi[t >> g.lowc] | (t & lowm) : 0;
 #pragma unroll
-                for (int j = 0; j < E; ++j) {
-                    const uint32_t l = threadIdx.x + (uint32_t)j * blockDim.x;
-                    st_amp(psi + (base | offhi[l >> g.lowc] | (l & lowm)), v[j]);
-                }
+                for (int j = 0; j < E; ++j) st_amp(psi + saddr(dt, j), v[j]);
             } else if (gi == g.ngroups - 1) {
 #pragma unroll
-                for (int r = 0; r < E; ++r) {
-                    const uint32_t lr = lidx(r);
-                    st_amp(psi + (base | offhi[lr >> g.lowc] | (lr & lowm)), v[r]);
-                }
+                for (int r = 0; r < E; ++r) st_amp(psi + gaddr(r), v[r]);
             } else {
 #pragma unroll
                 for (int r = 0; r < E; ++r) sm[swz(lidx(r))] = v[r];
