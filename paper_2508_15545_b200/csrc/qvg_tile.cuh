@@ -20,11 +20,12 @@
 // same for every tile) travel in the kernel's parameter bank.
 //
 // Measured limits (profiles/r01_fused_ab.json, r01_ncu_summary.md): the kernel
-// is compute/latency-bound, not HBM-bound. The FP64 pipe is ~53% busy and issue
-// slots 65%. DFMA arithmetic (half the FP64 instructions) gains only 10-13%, and a
-// cp.async next-tile prefetch (fewer CTAs/SM) loses 10-15%. What helped: pair
-// and diagonal ops dispatched at compile time by register slot, per-case
-// record loads, and 16 register amplitudes per thread.
+// is compute/latency-bound, not HBM-bound (issue slots ~59%, FP64 pipe ~42% on
+// a grid pass). DFMA arithmetic (half the FP64 instructions) gains only 10-13%,
+// and a cp.async next-tile prefetch (fewer CTAs/SM) loses 10-15%. What helped:
+// pair and diagonal ops dispatched at compile time by register slot, one jump
+// table per op dispatch, structured-matrix bodies, per-case record loads, and
+// 16 register amplitudes per thread.
 #pragma once
 
 #include <cuda_runtime.h>
