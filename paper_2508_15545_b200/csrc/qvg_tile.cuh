@@ -499,11 +499,13 @@ k_tile(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams
             // complex128 (FP64-issue bound) takes the offsets; complex64 (ALU-issue
             // bound) measured faster with the per-amplitude lookups (64-bit ORs
             // cost it more than the LDS latency): C3 c64 525 vs 597 ms
+            // (loads only: dl0 is computed right before them and is dead after;
+            // the last group's stores keep the per-amplitude lookups, which
+            // measured no slower and need no register live across the op loop,
+            // where the extra two spilled up to 780 bytes in some class sets)
             constexpr bool kDep = sizeof(R) == 8;
-            const bool direct = (gi == 0 && !(g.stage & 1) && !PF) || (gi == g.ngroups - 1 && !(g.stage & 2));
-            uint64_t dl0 = 0;
-            if (kDep && direct) dl0 = base | offhi[l0 >> g.lowc] | (l0 & lowm);
-            auto gaddr = [&](int r) {  // global index of subcube amplitude r
+            auto dep_l0 = [&]() { return kDep ? base | offhi[l0 >> g.lowc] | (l0 & lowm) : 0; };
+            auto gaddr = [&](uint64_t dl0, int r) {  // global index of subcube amplitude r
                 if constexpr (kDep) {
                     uint64_t a = dl0;
 #pragma unroll
@@ -554,8 +556,9 @@ k_tile(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams
 #pragma unroll
                 for (int r = 0; r < E; ++r) v[r] = sm[swz(lidx(r))];
             } else if (gi == 0) {
+                const uint64_t dl0 = dep_l0();
 #pragma unroll
-                for (int r = 0; r < E; ++r) v[r] = ld_amp(psi + gaddr(r));
+                for (int r = 0; r < E; ++r) v[r] = ld_amp(psi + gaddr(dl0, r));
             } else {
 #pragma unroll
                 for (int r = 0; r < E; ++r) v[r] = sm[swz(lidx(r))];
@@ -586,7 +589,10 @@ k_tile(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams
                 for (int j = 0; j < E; ++j) st_amp(psi + saddr(dt, j), v[j]);
             } else if (gi == g.ngroups - 1) {
 #pragma unroll
-                for (int r = 0; r < E; ++r) st_amp(psi + gaddr(r), v[r]);
+                for (int r = 0; r < E; ++r) {
+                    const uint32_t lr = lidx(r);
+                    st_amp(psi + (base | offhi[lr >> g.lowc] | (lr & lowm)), v[r]);
+                }
             } else {
 #pragma unroll
                 for (int r = 0; r < E; ++r) sm[swz(lidx(r))] = v[r];
