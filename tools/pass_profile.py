@@ -31,7 +31,9 @@ def main():
          "ladder": lambda: qv.u3_ladder_circuit(n, 4, 1),
          "qft": lambda: qv.qft_circuit(n, 1)[0]}[a.circuit]()
     st = qv.StateVector.create(n, a.precision, 0)
+    st.set_option(qv.OPT_FUSE, 0)  # the start state: n per-gate H launches (skip them with ncu -s n)
     st.apply_gates(qv.make_benchmark_circuit(n).gates())
+    st.set_option(qv.OPT_FUSE, 1)
     st.set_option(qv.OPT_SUB_BITS, a.sub)
     st.set_option(qv.OPT_PREFETCH, a.prefetch)
     if a.tile:
