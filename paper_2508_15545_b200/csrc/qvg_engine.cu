@@ -237,13 +237,14 @@ void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *recs) {
     };
     // Passes without structured ops (classes off) use the REAL-set kernel:
     // their records only name general bodies, which both sets compile.
-    const int set_idx = g.cls_set == kClsSetHalf ? 1 : g.cls_set == kClsSetHalfW ? 2 : 0;
+    const int set_idx = g.cls_set == kClsSetHalf ? 1 : g.cls_set == kClsSetHalfW ? 2 : g.cls_set == kClsSetU3 ? 3 : 0;
     auto kern = set_idx == 1   ? pick(std::integral_constant<int, kClsSetHalf>{})
                 : set_idx == 2 ? pick(std::integral_constant<int, kClsSetHalfW>{})
+                : set_idx == 3 ? pick(std::integral_constant<int, kClsSetU3>{})
                                : pick(std::integral_constant<int, kClsSetReal>{});
     // The shared-memory opt-in is a per-device function attribute: set it once
     // per (device, variant).
-    static std::atomic<uint64_t> attr_set[64][3];  // [device][class set]: a bit per variant
+    static std::atomic<uint64_t> attr_set[64][4];  // [device][class set]: a bit per variant
     const int variant = (sizeof(R) == 8 ? 1 : 0) | (g.sub == 4 ? 2 : 0) | (fma ? 4 : 0) | (small ? 8 : 0) |
                         (pf ? 16 : 0) | (tiny ? 32 : 0);
     std::atomic<uint64_t> &set = attr_set[s.device & 63][set_idx];

@@ -56,6 +56,7 @@ inline int pair_class(const double *u) {
     if (half) return TILE_CLS_HALF;
     if (h(0) && h(1) && h(6) && h(7) && u[2] == 0.0 && u[3] != 0.0 && u[4] != 0.0 && u[5] == 0.0)
         return TILE_CLS_SQW;
+    if (u[1] == 0.0) return TILE_CLS_U00R;
     return TILE_CLS_GEN;
 }
 
@@ -71,9 +72,10 @@ inline void sqw_record(const double *u, double *out) {
 // The class set of one fused pass: a k_tile instantiation compiles at most
 // three sets of pair bodies without spilling (qvg_tile.cuh), so the pass
 // takes the set that saves the most FP64 instructions per pair (real 16,
-// X 24, +-1/2 12, sqrt(W) 16); ops of other classes run the general body.
+// X 24, +-1/2 12, sqrt(W) 16, real u00 4); ops of other classes run the
+// general body.
 inline int tile_class_set(const OpInfo *info, uint64_t begin, uint64_t end) {
-    uint64_t n[5] = {};
+    uint64_t n[6] = {};
     for (uint64_t x = begin; x < end; ++x) {
         if (info[x].identity || info[x].diag) continue;
         n[info[x].cls] += 1;
@@ -81,7 +83,9 @@ inline int tile_class_set(const OpInfo *info, uint64_t begin, uint64_t end) {
     const uint64_t real = 16 * n[TILE_CLS_REAL] + 24 * n[TILE_CLS_SWAP];
     const uint64_t half = 12 * n[TILE_CLS_HALF] + 24 * n[TILE_CLS_SWAP];
     const uint64_t halfw = 12 * n[TILE_CLS_HALF] + 16 * n[TILE_CLS_SQW];
-    if (halfw > real && halfw > half) return kClsSetHalfW;
+    const uint64_t u3 = 4 * n[TILE_CLS_U00R] + 24 * n[TILE_CLS_SWAP];
+    if (halfw > real && halfw > half && halfw > u3) return kClsSetHalfW;
+    if (u3 > real && u3 > half) return kClsSetU3;
     return half > real ? kClsSetHalf : kClsSetReal;
 }
 

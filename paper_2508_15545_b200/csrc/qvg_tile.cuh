@@ -45,7 +45,7 @@ struct __align__(16) TileOp {
     int32_t cbit;      // tile-local control bit, -1 if none or outside Q (diag control in Q but
                        // not in the group: its thread-index bit)
     int32_t slot;      // dispatch index | flags (op_dispatch): pair 20*class+5*J+(K+1), diag
-                       // 100+25*neg+5*(J+1)+(K+1); J/K: register slots
+                       // 120+25*neg+5*(J+1)+(K+1); J/K: register slots
     uint64_t greq;     // global bits that must be 1 in the tile base (controls outside Q)
     uint64_t gtgt;     // diag: global target bit outside Q; group: packed bits b0 | b1<<8 | b2<<16 | b3<<24
     double u[8];       // group: u[j] holds (as bits) the global offset of tile-local bit b_j; op: matrix (diag uses u00 = u[0..1], u11 = u[6..7]); complex64 passes: the same
@@ -125,12 +125,16 @@ __device__ __forceinline__ void group_pair(typename Cplx<R>::T (&v)[1 << SUB], c
 //       lo.re = fma(s0/2, a.re - s0s1 a.im, -(q*b.im)),
 //     where s0/2 times the bracket is exact, so the DFMA rounds like the
 //     reference's final DADD, and 0*b.re contributes +-0. 12 instead of 28.
+//   TILE_CLS_U00R: u00 real (U3: u00 = cos(theta/2)), the rest general:
+//     lo.re = u00r*a.re + (u01r*b.re - u01i*b.im), the reference's 0*a.im
+//     term being +-0. 24 instead of 28.
 enum TileCls : int32_t {
     TILE_CLS_GEN = 0,
     TILE_CLS_REAL = 1,
     TILE_CLS_SWAP = 2,
     TILE_CLS_HALF = 3,
-    TILE_CLS_SQW = 4
+    TILE_CLS_SQW = 4,
+    TILE_CLS_U00R = 5
 };
 
 __device__ __forceinline__ double xsgn(double x, uint32_t m) {
@@ -226,6 +230,7 @@ __device__ __forceinline__ T sqw_hi(const R *uu, T a, T b) {  // (p, 0) a + u11 
 constexpr int kClsSetReal = (1 << TILE_CLS_GEN) | (1 << TILE_CLS_REAL) | (1 << TILE_CLS_SWAP);
 constexpr int kClsSetHalf = (1 << TILE_CLS_GEN) | (1 << TILE_CLS_HALF) | (1 << TILE_CLS_SWAP);
 constexpr int kClsSetHalfW = (1 << TILE_CLS_GEN) | (1 << TILE_CLS_HALF) | (1 << TILE_CLS_SQW);
+constexpr int kClsSetU3 = (1 << TILE_CLS_GEN) | (1 << TILE_CLS_U00R) | (1 << TILE_CLS_SWAP);
 template <class R, int SUB, int J, int K, bool FMA, int CLS, int CM>
 __device__ __forceinline__ void group_pair_cls(typename Cplx<R>::T (&v)[1 << SUB], const R *uu) {
     using T = typename Cplx<R>::T;
@@ -256,6 +261,22 @@ __device__ __forceinline__ void group_pair_cls(typename Cplx<R>::T (&v)[1 << SUB
                 const T a = v[r], b = v[r | (1 << J)];
                 v[r] = sqw_lo<T, R>(uu, a, b);
                 v[r | (1 << J)] = sqw_hi<T, R>(uu, a, b);
+            }
+        } else if constexpr (CLS == TILE_CLS_U00R) {
+#pragma unroll
+            for (int r = 0; r < (1 << SUB); ++r) {
+                if ((r >> J) & 1) continue;
+                if (K >= 0 && !((r >> K) & 1)) continue;
+                const T a = v[r], b = v[r | (1 << J)];
+                if constexpr (sizeof(R) == 8) {
+                    v[r] = make_double2(
+                        __dadd_rn(__dmul_rn(uu[0], a.x), __dsub_rn(__dmul_rn(uu[2], b.x), __dmul_rn(uu[3], b.y))),
+                        __dadd_rn(__dmul_rn(uu[0], a.y), __dadd_rn(__dmul_rn(uu[2], b.y), __dmul_rn(uu[3], b.x))));
+                } else {
+                    v[r].x = uu[0] * a.x + (uu[2] * b.x - uu[3] * b.y);
+                    v[r].y = uu[0] * a.y + (uu[2] * b.y + uu[3] * b.x);
+                }
+                v[r | (1 << J)] = madd2x<FMA>(uu[4], uu[5], a, uu[6], uu[7], b);
             }
         } else {  // TILE_CLS_HALF
 #pragma unroll
@@ -341,9 +362,9 @@ __device__ __forceinline__ void group_diag_rt(typename Cplx<R>::T (&v)[1 << SUB]
 // compiles to a single jump table (one indirect branch per op). Sparse codes
 // compiled to a compare-and-branch tree, and the instruction-fetch bubbles
 // after its branches were the kernel's top stall (no_instruction).
-//   pair:     20*class + 5*J + (K+1)              0..99
-//   diagonal: 100 + 25*neg + 5*(J+1) + (K+1)     100..149
-constexpr int kDispDiag = 100;
+//   pair:     20*class + 5*J + (K+1)              0..119
+//   diagonal: 120 + 25*neg + 5*(J+1) + (K+1)     120..169
+constexpr int kDispDiag = 120;
 constexpr int kSlotCtlTest = 256;  // diagonal: control in the tile but not in the group: test per thread
 constexpr int kSlotT1 = 512;       // diagonal: target not in the group: t1 per thread / tile
 constexpr int kSlotD0 = 1024;      // diagonal: d0 != 1
@@ -363,6 +384,9 @@ __device__ __forceinline__ void op_dispatch(int d, typename Cplx<R>::T (&v)[1 <<
         break;                                                                                \
     case 20 * TILE_CLS_SQW + 5 * (J) + (K) + 1:                                               \
         group_pair_cls<R, SUB, J, K, FMA, TILE_CLS_SQW, CM>(v, u);                            \
+        break;                                                                                \
+    case 20 * TILE_CLS_U00R + 5 * (J) + (K) + 1:                                              \
+        group_pair_cls<R, SUB, J, K, FMA, TILE_CLS_U00R, CM>(v, u);                           \
         break;
 #define QVG_GD(J, K)                                                  \
     case kDispDiag + 5 * ((J) + 1) + (K) + 1:                         \

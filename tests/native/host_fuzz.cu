@@ -39,8 +39,8 @@ static qvg_gate random_gate(std::mt19937_64 &rng, uint32_t n) {
     }
     std::uniform_real_distribution<double> u(-1.0, 1.0);
     // dense, diag(1,d), diag(d0,d1), identity, then the structured classes:
-    // real, X, entries +-1/2, Z, sqrt(W)-like
-    const int kind = (int)(rng() % 9);
+    // real, X, entries +-1/2, Z, sqrt(W)-like, real u00 (U3)
+    const int kind = (int)(rng() % 10);
     for (double &x : g.u) x = u(rng);
     if (kind >= 1 && kind <= 3) g.u[2] = g.u[3] = g.u[4] = g.u[5] = 0.0;
     if (kind == 1 || kind == 3) { g.u[0] = 1.0; g.u[1] = 0.0; }
@@ -49,6 +49,7 @@ static qvg_gate random_gate(std::mt19937_64 &rng, uint32_t n) {
     if (kind == 5) for (int i = 0; i < 8; ++i) g.u[i] = (i == 2 || i == 4) ? 1.0 : 0.0;
     if (kind == 6) for (double &x : g.u) x = (rng() & 1) ? 0.5 : -0.5;
     if (kind == 7) for (int i = 0; i < 8; ++i) g.u[i] = i == 0 ? 1.0 : i == 6 ? -1.0 : 0.0;
+    if (kind == 9) g.u[1] = 0.0;
     if (kind == 8) {
         for (double &x : g.u) x = (rng() & 1) ? 0.5 : -0.5;
         g.u[2] = 0.0;
@@ -107,7 +108,7 @@ static void check_plan(const std::vector<qvg_gate> &ops, const PlanOptions &po) 
                     // 20*class + 5*J + (K+1) with J >= 0 (target in the group)
                     CHECK((t.slot & ~0xff) == 0 && t.slot < kDispDiag);
                     const int cls = t.slot / 20, js = 8 * ((t.slot % 20) / 5);
-                    CHECK(cls >= TILE_CLS_GEN && cls <= TILE_CLS_SQW && (po.classes || cls == TILE_CLS_GEN));
+                    CHECK(cls >= TILE_CLS_GEN && cls <= TILE_CLS_U00R && (po.classes || cls == TILE_CLS_GEN));
                     CHECK((g.cls_set >> cls) & 1);
                     if (cls == TILE_CLS_SQW)  // (s0/2, -s0 s1, q, 0) per row
                         for (int row = 0; row < 2; ++row) {
