@@ -152,6 +152,15 @@ def test_planner_bytes_and_fusion(qv):
     assert f == p and p < len(c3) / 8
 
 
+def test_planner_bit_exact_reorder(qv):
+    # The default plan lets X/CX permutations and Z/CZ sign flips move past
+    # ops on other qubits (bit-exact, qvg_plan.hpp reorder_for_tiles); the
+    # U3 + CX ladder then needs about half the passes of circuit order
+    # (27 at n=30, 4 layers).
+    p, f, _ = qv.plan_passes(30, qv.u3_ladder_circuit(30, 4, 1).gates())
+    assert f == p and p == 14
+
+
 def test_planner_rejects_bad_ops(qv):
     with pytest.raises(qv.ValidationError):
         qv.plan_passes(3, qv.parse_circuit("qubits 4\nh 3\n").gates())
