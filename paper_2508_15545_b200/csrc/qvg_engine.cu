@@ -25,6 +25,7 @@
 #include "qvg_ooc.hpp"
 #include "qvg_plan.hpp"
 #include "qvg_shard.hpp"
+#include "qvg_tile_select.hpp"
 
 using namespace qvg;
 
@@ -226,22 +227,10 @@ void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *recs) {
     const bool fma = s.fma && sizeof(R) == 8;  // complex64 always contracts
     const bool small = threads <= 256;
     const bool tiny = threads <= 128;  // sub 4 at k <= 11: 128-thread CTAs
-    auto pick = [&](auto cm) {
-        constexpr int CM = decltype(cm)::value;
-        return g.sub == 4 ? (tiny ? (fma ? k_tile<R, 4, true, 128, false, CM> : k_tile<R, 4, false, 128, false, CM>)
-                                  : (fma ? k_tile<R, 4, true, 256, false, CM> : k_tile<R, 4, false, 256, false, CM>))
-               : pf ? (small ? (fma ? k_tile<R, 3, true, 256, true, CM> : k_tile<R, 3, false, 256, true, CM>)
-                             : (fma ? k_tile<R, 3, true, 512, true, CM> : k_tile<R, 3, false, 512, true, CM>))
-               : small ? (fma ? k_tile<R, 3, true, 256, false, CM> : k_tile<R, 3, false, 256, false, CM>)
-                       : (fma ? k_tile<R, 3, true, 512, false, CM> : k_tile<R, 3, false, 512, false, CM>);
-    };
     // Passes without structured ops (classes off) use the REAL-set kernel:
-    // their records only name general bodies, which both sets compile.
-    const int set_idx = g.cls_set == kClsSetHalf ? 1 : g.cls_set == kClsSetHalfW ? 2 : g.cls_set == kClsSetU3 ? 3 : 0;
-    auto kern = set_idx == 1   ? pick(std::integral_constant<int, kClsSetHalf>{})
-                : set_idx == 2 ? pick(std::integral_constant<int, kClsSetHalfW>{})
-                : set_idx == 3 ? pick(std::integral_constant<int, kClsSetU3>{})
-                               : pick(std::integral_constant<int, kClsSetReal>{});
+    // their records only name general bodies, which every set compiles.
+    const int set_idx = class_set_index(g.cls_set);
+    const TileKernel<R> kern = tile_kernel<R>(set_idx, TileVariant{g.sub, tiny, small, fma, pf});
     // The shared-memory opt-in is a per-device function attribute: set it once
     // per (device, variant).
     static std::atomic<uint64_t> attr_set[64][4];  // [device][class set]: a bit per variant
