@@ -46,6 +46,7 @@ def main():
     ap.add_argument("--precision", type=int, default=128)
     ap.add_argument("--only", default="", help="comma-separated variant names (default: all)")
     ap.add_argument("--stage", type=int, default=-1, help="QVG_OPT_STAGE for every variant (-1: default)")
+    ap.add_argument("--carriers", type=int, default=-1, help="QVG_OPT_CARRIERS for every variant (-1: default)")
     a = ap.parse_args()
     only = set(filter(None, a.only.split(",")))
     st = qv.StateVector.create(a.n, a.precision, 0)
@@ -69,6 +70,8 @@ def main():
                 st.set_option(qv.OPT_CLASSES, 0 if vname.endswith("noclass") else 1)
             if a.stage >= 0:
                 st.set_option(qv.OPT_STAGE, a.stage)
+            if a.carriers >= 0:
+                st.set_option(qv.OPT_CARRIERS, a.carriers)
             st.apply_gates(g)  # warm-up (and plan)
             st.reset_stats()
             ts = []
