@@ -530,10 +530,15 @@ def cpu_baseline(args, nops_hint=120):
         for _ in range(2):
             wall = store.apply(sample, "paired-cached-parallel", cores, cores * (64 << 20))
             best = min(best, wall)
+        # also the single-threaded column (the paper's 1-worker
+        # paired_cached with a 64 MiB window), one gate pass
+        single = store.apply(sample[:1], "paired-cached", 1, 64 << 20)
     return {"value": len(sample) * (1 << n) / (best / 1e3), "unit": UNIT, "cores": cores, "kind": "reference",
             "ms_per_gate": best / len(sample),
             "sample": "2 gate passes of the n=30 sweep (Haar U q=0, CX 0->1), paired-cached-parallel, "
-                      f"workers={cores}, block_amps=65536, store on {scratch}, min of 2"}
+                      f"workers={cores}, block_amps=65536, store on {scratch}, min of 2",
+            "single_thread": {"value": (1 << n) / (single / 1e3), "unit": UNIT, "cores": 1, "ms_per_gate": single,
+                              "sample": "1 gate pass (Haar U q=0), paired-cached, 1 worker, 64 MiB window"}}
 
 
 def run_reference(args, rank, world):
