@@ -305,9 +305,11 @@ def fused_leg(qv, st, circ, line, args):
     st.sync()
     ms = a.elapsed_time(b) / reps
     s = st.stats()
+    hbm = s["bytes_moved"] / reps / (ms / 1e3) / 1e9
     line["fused"] = {"ms_per_step": ms, "value": len(circ) * (1 << circ.n_qubits) / (ms / 1e3),
                      "passes_per_step": s["passes"] / reps, "fused_passes_per_step": s["fused_passes"] / reps,
-                     "hbm_gbs": s["bytes_moved"] / reps / (ms / 1e3) / 1e9}
+                     "hbm_gbs": hbm, "hbm_frac": hbm / peaks()[0],
+                     "note": "compute/latency-bound tile passes (profiles/r01_fused_passes.json)"}
     st.set_option(qv.OPT_FUSE, 0)
 
 
