@@ -71,7 +71,8 @@ enum qvg_option {
     QVG_OPT_MIN_RUN = 5,     /* bytes: a control/phase bit whose 1-runs are shorter is selected
                                 inside a dense pass instead of enumerated (default 32) */
     QVG_OPT_PRED_STORE = 6,  /* 1: skip stores of unselected amplitudes; 0: write them back (default) */
-    QVG_OPT_SUB_BITS = 7,    /* fused tile: 2^b register amplitudes per thread, b = 3 or 4 (default 4) */
+    QVG_OPT_SUB_BITS = 7,    /* fused tile: 2^b register amplitudes per thread, b = 3 or 4 (default 4);
+                                complex64 also 5 (its default) */
     QVG_OPT_FMA = 8,         /* 1: fused-tile complex128 arithmetic with DFMA (faster, within 1e-15
                                 relative but NOT bit-identical to the reference); 0: exact (default) */
     QVG_OPT_TIMING = 9,      /* 1: bracket each qvg_apply with CUDA events; qvg_stats.kernel_ms sums them */

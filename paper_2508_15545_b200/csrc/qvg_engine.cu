@@ -233,14 +233,15 @@ void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *recs) {
     const TileKernel<R> kern = tile_kernel<R>(set_idx, TileVariant{g.sub, tiny, small, fma, pf});
     // The shared-memory opt-in is a per-device function attribute: set it once
     // per (device, variant).
-    static std::atomic<uint64_t> attr_set[64][4];  // [device][class set]: a bit per variant
+    static std::atomic<uint64_t> attr_set[64][4][2];  // [device][class set][variant / 64]: a bit per variant
     const int variant = (sizeof(R) == 8 ? 1 : 0) | (g.sub == 4 ? 2 : 0) | (fma ? 4 : 0) | (small ? 8 : 0) |
-                        (pf ? 16 : 0) | (tiny ? 32 : 0);
-    std::atomic<uint64_t> &set = attr_set[s.device & 63][set_idx];
-    if (!((set.load(std::memory_order_acquire) >> variant) & 1u)) {
+                        (pf ? 16 : 0) | (tiny ? 32 : 0) | (g.sub == 5 ? 64 : 0);
+    std::atomic<uint64_t> &set = attr_set[s.device & 63][set_idx][variant >> 6];
+    const uint64_t bit = 1ull << (variant & 63);
+    if (!(set.load(std::memory_order_acquire) & bit)) {
         cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
                    "cudaFuncSetAttribute(k_tile)");
-        set.fetch_or(1ull << variant, std::memory_order_acq_rel);
+        set.fetch_or(bit, std::memory_order_acq_rel);
     }
     int per_sm = 0;
     cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (int)threads, smem), "occupancy(k_tile)");
@@ -433,12 +434,12 @@ static int create_impl(uint32_t n, uint32_t precision, int device, uint32_t rank
         s->S = precision == QVG_C128 ? 16 : 8;
         s->rank = rank;
         s->world = world;
-        // Measured best tile shapes (profiles/r01_fused_ab.json, r01_fused_ab_c64.json):
-        // complex128: 2^11 amplitudes as 128 threads x 16 register amplitudes
-        // (C2/C1/C3 4-11% faster than 256 x 8); complex64: 2^12 as 256 x 16
-        // (C3 -11%, C2 -6% against 2^11; profiles/r01_fused_ab_c64.json).
+        // Measured best tile shapes (profiles/r01_fused_ab.json, r01_fused_ab_c64.json,
+        // r01_sub5_ab.json): complex128: 2^11 amplitudes as 128 threads x 16 register
+        // amplitudes (C2/C1/C3 4-11% faster than 256 x 8); complex64: 2^12 as
+        // 128 threads x 32 (C2 -16%, C1 -12% against 256 x 16, C3 +1%).
         s->tile_qubits = precision == QVG_C128 ? 11 : 12;
-        s->sub_bits = 4;
+        s->sub_bits = precision == QVG_C128 ? 4 : 5;
         s->carriers = precision == QVG_C128 ? 3 : 4;
         try {
             set_device(s);
@@ -528,7 +529,8 @@ int qvg_set_option(qvg_state *s, int key, int64_t value) {
             break;
         case QVG_OPT_PRED_STORE: s->pred_store = value != 0; break;
         case QVG_OPT_SUB_BITS:
-            if (value != 3 && value != 4) throw Validation("sub_bits must be 3 or 4");
+            if (value < 3 || value > (s->precision == QVG_C64 ? 5 : 4))
+                throw Validation("sub_bits must be 3 or 4 (complex64: 3..5)");
             s->sub_bits = (uint32_t)value;
             break;
         case QVG_OPT_FMA: s->fma = value != 0; break;

@@ -161,7 +161,7 @@ struct PlanOptions {
     uint32_t carriers = 3;
     bool low_kernel = false;
     uint32_t min_run = 32;   // see qvg_state::min_run
-    uint32_t sub_bits = 3;   // tile register subcube: 2^sub amplitudes per thread (3 or 4)
+    uint32_t sub_bits = 3;   // tile register subcube: 2^sub amplitudes per thread (3..5; 5 complex64 only)
     uint32_t reorder = 2;    // QVG_OPT_REORDER: ReorderMode (below); 2 keeps every bit
     bool classes = true;     // QVG_OPT_CLASSES: structured-matrix op bodies in fused tiles
     uint32_t stage_bits = 3; // stage a first/last group through shared memory when its bits
@@ -353,7 +353,7 @@ inline Plan make_plan(const qvg_gate *ops, uint64_t count, const PlanOptions &po
             // at most `sub` tile bits (the thread's register subcube).
             std::vector<TileOp> group;
             uint32_t first_low = 0, last_low = 0;  // see PlanOptions::stage_bits
-            int gbits[4];
+            int gbits[5];
             int nb = 0;
             auto close_group = [&] {
                 if (group.empty()) return;
@@ -397,10 +397,10 @@ inline Plan make_plan(const qvg_gate *ops, uint64_t count, const PlanOptions &po
                         if (t.cbit >= 0 && gbits[s] == t.cbit) K = s;
                     }
                     if (t.kind == TILE_PAIR) {
-                        t.slot = 20 * t.slot + 5 * J + K + 1;
+                        t.slot = 30 * t.slot + 6 * J + K + 1;
                     } else {
                         const bool neg = (t.slot & 2) != 0, d0one = (t.slot & 1) != 0;
-                        t.slot = kDispDiag + (neg ? 25 : 0) + 5 * (J + 1) + K + 1;
+                        t.slot = kDispDiag + (neg ? 36 : 0) + 6 * (J + 1) + K + 1;
                         if (K < 0 && t.cbit >= 0) t.slot |= kSlotCtlTest;
                         if (J < 0) t.slot |= kSlotT1;
                         if (!neg && !d0one) t.slot |= kSlotD0;

@@ -44,8 +44,8 @@ struct __align__(16) TileOp {
                        // in Q but not in the group: its thread-index bit); group: op count
     int32_t cbit;      // tile-local control bit, -1 if none or outside Q (diag control in Q but
                        // not in the group: its thread-index bit)
-    int32_t slot;      // dispatch index | flags (op_dispatch): pair 20*class+5*J+(K+1), diag
-                       // 120+25*neg+5*(J+1)+(K+1); J/K: register slots
+    int32_t slot;      // dispatch index | flags (op_dispatch): pair 30*class+6*J+(K+1), diag
+                       // 180+36*neg+6*(J+1)+(K+1); J/K: register slots
     uint64_t greq;     // global bits that must be 1 in the tile base (controls outside Q)
     uint64_t gtgt;     // diag: global target bit outside Q; group: packed bits b0 | b1<<8 | b2<<16 | b3<<24
     double u[8];       // group: u[j] holds (as bits) the global offset of tile-local bit b_j; op: matrix (diag uses u00 = u[0..1], u11 = u[6..7]); complex64 passes: the same
@@ -63,7 +63,7 @@ struct TileGeom {
     int cls_set;          // structured-matrix classes this pass uses (kClsSetReal / kClsSetHalf)
     int hiq[24];          // tile qubits >= lowc, ascending (tile-local bits lowc..k-1)
     uint64_t ntiles;      // 2^(n-k)
-    uint64_t sdep[4];     // global offset of tile-local bit (k - sub + i): the staged (coalesced)
+    uint64_t sdep[5];     // global offset of tile-local bit (k - sub + i): the staged (coalesced)
                           // layout's index t + j*blockDim is t | j << (k - sub)
 };
 
@@ -362,9 +362,10 @@ __device__ __forceinline__ void group_diag_rt(typename Cplx<R>::T (&v)[1 << SUB]
 // compiles to a single jump table (one indirect branch per op). Sparse codes
 // compiled to a compare-and-branch tree, and the instruction-fetch bubbles
 // after its branches were the kernel's top stall (no_instruction).
-//   pair:     20*class + 5*J + (K+1)              0..119
-//   diagonal: 120 + 25*neg + 5*(J+1) + (K+1)     120..169
-constexpr int kDispDiag = 120;
+//   pair:     30*class + 6*J + (K+1)              0..179
+//   diagonal: 180 + 36*neg + 6*(J+1) + (K+1)     180..251
+// (J, K < 5: register slots of up to 32-amplitude subcubes)
+constexpr int kDispDiag = 180;
 constexpr int kSlotCtlTest = 256;  // diagonal: control in the tile but not in the group: test per thread
 constexpr int kSlotT1 = 512;       // diagonal: target not in the group: t1 per thread / tile
 constexpr int kSlotD0 = 1024;      // diagonal: d0 != 1
@@ -372,39 +373,41 @@ template <class R, int SUB, bool FMA, int CM>
 __device__ __forceinline__ void op_dispatch(int d, typename Cplx<R>::T (&v)[1 << SUB], const R *u, bool t1,
                                             bool d0) {
 #define QVG_GP(J, K)                                                                          \
-    case 20 * TILE_CLS_GEN + 5 * (J) + (K) + 1: group_pair<R, SUB, J, K, FMA>(v, u); break;   \
-    case 20 * TILE_CLS_REAL + 5 * (J) + (K) + 1:                                              \
+    case 30 * TILE_CLS_GEN + 6 * (J) + (K) + 1: group_pair<R, SUB, J, K, FMA>(v, u); break;   \
+    case 30 * TILE_CLS_REAL + 6 * (J) + (K) + 1:                                              \
         group_pair_cls<R, SUB, J, K, FMA, TILE_CLS_REAL, CM>(v, u);                           \
         break;                                                                                \
-    case 20 * TILE_CLS_SWAP + 5 * (J) + (K) + 1:                                              \
+    case 30 * TILE_CLS_SWAP + 6 * (J) + (K) + 1:                                              \
         group_pair_cls<R, SUB, J, K, FMA, TILE_CLS_SWAP, CM>(v, u);                           \
         break;                                                                                \
-    case 20 * TILE_CLS_HALF + 5 * (J) + (K) + 1:                                              \
+    case 30 * TILE_CLS_HALF + 6 * (J) + (K) + 1:                                              \
         group_pair_cls<R, SUB, J, K, FMA, TILE_CLS_HALF, CM>(v, u);                           \
         break;                                                                                \
-    case 20 * TILE_CLS_SQW + 5 * (J) + (K) + 1:                                               \
+    case 30 * TILE_CLS_SQW + 6 * (J) + (K) + 1:                                               \
         group_pair_cls<R, SUB, J, K, FMA, TILE_CLS_SQW, CM>(v, u);                            \
         break;                                                                                \
-    case 20 * TILE_CLS_U00R + 5 * (J) + (K) + 1:                                              \
+    case 30 * TILE_CLS_U00R + 6 * (J) + (K) + 1:                                              \
         group_pair_cls<R, SUB, J, K, FMA, TILE_CLS_U00R, CM>(v, u);                           \
         break;
 #define QVG_GD(J, K)                                                  \
-    case kDispDiag + 5 * ((J) + 1) + (K) + 1:                         \
+    case kDispDiag + 6 * ((J) + 1) + (K) + 1:                         \
         group_diag_rt<R, SUB, J, K, FMA, false>(v, u, t1, d0);        \
         break;                                                        \
-    case kDispDiag + 25 + 5 * ((J) + 1) + (K) + 1:                    \
+    case kDispDiag + 36 + 6 * ((J) + 1) + (K) + 1:                    \
         group_diag_rt<R, SUB, J, K, FMA, true>(v, u, t1, false);      \
         break;
     switch (d) {
-        QVG_GP(0, -1) QVG_GP(0, 1) QVG_GP(0, 2) QVG_GP(0, 3)
-        QVG_GP(1, -1) QVG_GP(1, 0) QVG_GP(1, 2) QVG_GP(1, 3)
-        QVG_GP(2, -1) QVG_GP(2, 0) QVG_GP(2, 1) QVG_GP(2, 3)
-        QVG_GP(3, -1) QVG_GP(3, 0) QVG_GP(3, 1) QVG_GP(3, 2)
-        QVG_GD(-1, -1) QVG_GD(-1, 0) QVG_GD(-1, 1) QVG_GD(-1, 2) QVG_GD(-1, 3)
-        QVG_GD(0, -1) QVG_GD(0, 1) QVG_GD(0, 2) QVG_GD(0, 3)
-        QVG_GD(1, -1) QVG_GD(1, 0) QVG_GD(1, 2) QVG_GD(1, 3)
-        QVG_GD(2, -1) QVG_GD(2, 0) QVG_GD(2, 1) QVG_GD(2, 3)
-        QVG_GD(3, -1) QVG_GD(3, 0) QVG_GD(3, 1) QVG_GD(3, 2)
+        QVG_GP(0, -1) QVG_GP(0, 1) QVG_GP(0, 2) QVG_GP(0, 3) QVG_GP(0, 4)
+        QVG_GP(1, -1) QVG_GP(1, 0) QVG_GP(1, 2) QVG_GP(1, 3) QVG_GP(1, 4)
+        QVG_GP(2, -1) QVG_GP(2, 0) QVG_GP(2, 1) QVG_GP(2, 3) QVG_GP(2, 4)
+        QVG_GP(3, -1) QVG_GP(3, 0) QVG_GP(3, 1) QVG_GP(3, 2) QVG_GP(3, 4)
+        QVG_GP(4, -1) QVG_GP(4, 0) QVG_GP(4, 1) QVG_GP(4, 2) QVG_GP(4, 3)
+        QVG_GD(-1, -1) QVG_GD(-1, 0) QVG_GD(-1, 1) QVG_GD(-1, 2) QVG_GD(-1, 3) QVG_GD(-1, 4)
+        QVG_GD(0, -1) QVG_GD(0, 1) QVG_GD(0, 2) QVG_GD(0, 3) QVG_GD(0, 4)
+        QVG_GD(1, -1) QVG_GD(1, 0) QVG_GD(1, 2) QVG_GD(1, 3) QVG_GD(1, 4)
+        QVG_GD(2, -1) QVG_GD(2, 0) QVG_GD(2, 1) QVG_GD(2, 3) QVG_GD(2, 4)
+        QVG_GD(3, -1) QVG_GD(3, 0) QVG_GD(3, 1) QVG_GD(3, 2) QVG_GD(3, 4)
+        QVG_GD(4, -1) QVG_GD(4, 0) QVG_GD(4, 1) QVG_GD(4, 2) QVG_GD(4, 3)
     default: break;
     }
 #undef QVG_GP
@@ -429,8 +432,13 @@ __device__ __forceinline__ void op_dispatch(int d, typename Cplx<R>::T (&v)[1 <<
 #ifndef QVG_C64_SUB4_256_MINB
 #define QVG_C64_SUB4_256_MINB 4  // complex64 (its default tile): 64 registers; 4-6% faster than 3 CTAs, 5 spills
 #endif
+#ifndef QVG_SUB5_MINB
+#define QVG_SUB5_MINB 5  // complex64 32-amplitude subcubes, 128 threads: 96 registers
+                         // (vs 4 CTAs at 128: C1 -5%, C3 -4%; profiles/r01_sub5_ab.json)
+#endif
 template <class R, int SUB, bool FMA, int MAXT, bool PF, int CM>
 __global__ void __launch_bounds__(MAXT, PF                         ? 2
+                                        : (SUB == 5) ? (MAXT <= 128 ? QVG_SUB5_MINB : 2)
                                         : (MAXT <= 128 && SUB == 4) ? QVG_SUB4_MINB
                                         : (MAXT <= 256 && SUB == 4) ? (sizeof(R) == 4 ? QVG_C64_SUB4_256_MINB : QVG_SUB4_256_MINB)
                                         : (MAXT <= 256 && SUB == 3) ? 4

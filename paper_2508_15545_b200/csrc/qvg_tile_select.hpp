@@ -12,7 +12,7 @@ template <class R>
 using TileKernel = void (*)(typename Cplx<R>::T *, const TileParams);
 
 struct TileVariant {
-    int sub;     // register subcube bits (3 or 4)
+    int sub;     // register subcube bits (3, 4; 5 complex64)
     bool tiny;   // <= 128 threads
     bool small;  // <= 256 threads
     bool fma;    // complex128 DFMA arithmetic (QVG_OPT_FMA)
@@ -60,6 +60,9 @@ inline TileKernel<R> tile_kernel(int set_idx, const TileVariant &v) {
 // qvg_tile_inst.cu only.
 template <class R, int CM>
 TileKernel<R> tile_kernel_pick(const TileVariant &v) {
+    if constexpr (sizeof(R) == 4) {  // 32-amplitude subcubes: complex64 only (64 data registers)
+        if (v.sub == 5) return v.tiny ? k_tile<R, 5, false, 128, false, CM> : k_tile<R, 5, false, 256, false, CM>;
+    }
     if (v.sub == 4)
         return v.tiny ? (v.fma ? k_tile<R, 4, true, 128, false, CM> : k_tile<R, 4, false, 128, false, CM>)
                       : (v.fma ? k_tile<R, 4, true, 256, false, CM> : k_tile<R, 4, false, 256, false, CM>);

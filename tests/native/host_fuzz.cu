@@ -88,7 +88,7 @@ static void check_plan(const std::vector<qvg_gate> &ops, const PlanOptions &po) 
         const TileGeom &g = pass.geom;
         CHECK(g.nrec <= kMaxTileRecs && g.nrec >= 2);
         CHECK(g.k <= (int)po.n && g.lowc >= 0 && g.nhi == g.k - g.lowc);
-        CHECK(g.sub >= 2 && g.sub <= 4);
+        CHECK(g.sub >= 2 && g.sub <= 5);
         int rec = (int)pass.op_begin, groups = 0;
         const int end = (int)pass.op_begin + g.nrec;
         while (rec < end) {
@@ -105,9 +105,9 @@ static void check_plan(const std::vector<qvg_gate> &ops, const PlanOptions &po) 
                     uv[e] = po.amp_bytes == 8 ? (double)reinterpret_cast<const float *>(t.u)[e] : t.u[e];
                 CHECK(t.kind == TILE_PAIR || t.kind == TILE_DIAG);
                 if (t.kind == TILE_PAIR) {
-                    // 20*class + 5*J + (K+1) with J >= 0 (target in the group)
+                    // 30*class + 6*J + (K+1) with J >= 0 (target in the group)
                     CHECK((t.slot & ~0xff) == 0 && t.slot < kDispDiag);
-                    const int cls = t.slot / 20, js = 8 * ((t.slot % 20) / 5);
+                    const int cls = t.slot / 30, js = 8 * ((t.slot % 30) / 6);
                     CHECK(cls >= TILE_CLS_GEN && cls <= TILE_CLS_U00R && (po.classes || cls == TILE_CLS_GEN));
                     CHECK((g.cls_set >> cls) & 1);
                     if (cls == TILE_CLS_SQW)  // (s0/2, -s0 s1, q, 0) per row
@@ -125,10 +125,10 @@ static void check_plan(const std::vector<qvg_gate> &ops, const PlanOptions &po) 
                                   (m[2] == 1.0 || m[2] == -1.0) && (m[3] == 1.0 || m[3] == -1.0));
                         }
                 } else {
-                    const int d = t.slot & 0xff;  // 100 + 25*neg + 5*(J+1) + (K+1)
-                    CHECK(d >= kDispDiag && d < kDispDiag + 50);
-                    const int neg = (d - kDispDiag) / 25, J = ((d - kDispDiag) % 25) / 5 - 1,
-                              K = (d - kDispDiag) % 5 - 1;
+                    const int d = t.slot & 0xff;  // 180 + 36*neg + 6*(J+1) + (K+1)
+                    CHECK(d >= kDispDiag && d < kDispDiag + 72);
+                    const int neg = (d - kDispDiag) / 36, J = ((d - kDispDiag) % 36) / 6 - 1,
+                              K = (d - kDispDiag) % 6 - 1;
                     CHECK(J < g.sub && K < g.sub && (J < 0 || J != K));
                     CHECK(po.classes || !neg);
                     if (neg) CHECK(uv[0] == 1.0 && uv[6] == -1.0 && !(t.slot & kSlotD0));
@@ -186,7 +186,7 @@ int main(int argc, char **argv) {
         po.fuse = rng() % 8 != 0;
         po.tile_qubits = 5 + (uint32_t)(rng() % 8);
         po.carriers = (uint32_t)(rng() % 5);
-        po.sub_bits = rng() % 2 ? 3 : 4;
+        po.sub_bits = 3 + (uint32_t)(rng() % 3);
         po.stage_bits = (uint32_t)(rng() % 4);
         po.reorder = (uint32_t)(rng() % 3);
         po.classes = rng() % 4 != 0;

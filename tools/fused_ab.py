@@ -25,7 +25,9 @@ VARIANTS = [("fused_sub3_k11", 1, 3, 0, 11, 0), ("fused_sub3_k12", 1, 3, 0, 12, 
             ("fused_sub3_k11_pf", 1, 3, 0, 11, 1), ("fused_sub3_k10_pf", 1, 3, 0, 10, 1),
             ("fused_sub3_k12_pf", 1, 3, 0, 12, 1), ("fused_sub4_k11", 1, 4, 0, 11, 0),
             ("fused_reorder", 1, 4, 0, 11, 0), ("fused_sub4_k11_noclass", 1, 4, 0, 11, 0),
-            ("fused_sub4_k11_inorder", 1, 4, 0, 11, 0), ("per_gate", 0, 3, 0, 11, 0)]
+            ("fused_sub4_k11_inorder", 1, 4, 0, 11, 0), ("fused_sub4_k10", 1, 4, 0, 10, 0),
+            ("fused_sub5_k12", 1, 5, 0, 12, 0), ("fused_sub5_k11", 1, 5, 0, 11, 0),
+            ("per_gate", 0, 3, 0, 11, 0)]
 # OPT_REORDER per variant: *_reorder = 1 (any commuting move, not bit-exact),
 # *_inorder = 0 (circuit order), otherwise the default 2 (bit-exact moves)
 
