@@ -107,6 +107,7 @@ struct qvg_state {
     bool graph = false;        // QVG_OPT_GRAPH: replay repeated op lists as captured CUDA graphs
     uint32_t reorder = REORDER_EXACT;  // QVG_OPT_REORDER: commutation-aware fusion order (qvg_plan.hpp)
     bool classes = true;       // QVG_OPT_CLASSES: structured-matrix op bodies in fused tiles
+    bool shape_set = false;    // tile_qubits / sub_bits set by the caller (no small-state default)
     struct GraphEntry {
         uint64_t key = 0;
         std::vector<qvg_gate> ops;
@@ -263,6 +264,14 @@ PlanOptions plan_options(const qvg_state &s) {
     po.stage_bits = s.stage_bits;
     po.reorder = s.reorder;
     po.classes = s.classes;
+    // Small complex128 states: 2^10-amplitude tiles of 8-amplitude subcubes
+    // (4x the CTAs of the default 2^11 x 16 shape) unless the caller chose a
+    // shape. tools/tile_size_small.py, config 0's circuit: n=16 0.64-0.65 ->
+    // 0.57-0.61 ms on two boxes; from n=18 on the default shape is as fast or faster.
+    if (!s.shape_set && s.precision == QVG_C128 && s.L <= 17) {
+        po.tile_qubits = std::min<uint32_t>(10, s.L);
+        po.sub_bits = 3;
+    }
     return po;
 }
 
@@ -308,7 +317,7 @@ uint64_t plan_signature(const qvg_state &s) {
     auto mix = [&](uint64_t v) { h = (h ^ v) * 1099511628211ull; };
     mix(s.fuse); mix(s.tile_qubits); mix(s.carriers); mix(s.low_kernel); mix(s.min_run); mix(s.pred_store);
     mix(s.sub_bits); mix(s.fma); mix(s.stage_bits); mix((uint64_t)s.prefetch_mode); mix(s.L); mix(s.precision);
-    mix(s.reorder); mix(s.classes);
+    mix(s.reorder); mix(s.classes); mix(s.shape_set);
     return h;
 }
 
@@ -516,6 +525,7 @@ int qvg_set_option(qvg_state *s, int key, int64_t value) {
             const int64_t maxk = 12;  // k_tile runs 2^(k-3) <= 512 threads
             if (value < 2 || value > maxk) throw Validation("tile_qubits out of range");
             s->tile_qubits = (uint32_t)value;
+            s->shape_set = true;
             break;
         }
         case QVG_OPT_CARRIERS:
@@ -532,6 +542,7 @@ int qvg_set_option(qvg_state *s, int key, int64_t value) {
             if (value < 3 || value > (s->precision == QVG_C64 ? 5 : 4))
                 throw Validation("sub_bits must be 3 or 4 (complex64: 3..5)");
             s->sub_bits = (uint32_t)value;
+            s->shape_set = true;
             break;
         case QVG_OPT_FMA: s->fma = value != 0; break;
         case QVG_OPT_TIMING: s->timing = value != 0; break;

@@ -111,7 +111,8 @@ __device__ __forceinline__ void group_pair(typename Cplx<R>::T (&v)[1 << SUB], c
 // at most the sign of an exact-zero result.
 //   TILE_CLS_REAL: every imaginary part is 0 (H, real rotations):
 //     lo = (u00r*a.re + u01r*b.re, u00r*a.im + u01r*b.im), 12 instead of 28.
-//   TILE_CLS_SWAP: [[0,1],[1,0]] (X, the target of CX): a register swap.
+//   TILE_CLS_SWAP: [[0,1],[1,0]] (X, the target of CX): a swap, each component
+//     moved through one DADD with +0 (mov_opaque).
 //   TILE_CLS_HALF: every |re| and |im| is 1/2 (sqrt(X), sqrt(Y), their
 //     adjoints): with u00 = (s0, s1)/2, u01 = (s2, s3)/2,
 //       lo.re = s0/2 * ((a.re - s0s1 a.im) + s0s2 (b.re - s2s3 b.im)),

@@ -24,3 +24,14 @@ for n in (16, 20, 22):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream); st.apply_gates(g, sync=False); e1.record(stream); st.sync(); ts.append(e0.elapsed_time(e1))
             print(n, k, sub, st.stats()['passes'] / 10, round(statistics.median(ts), 3), flush=True)
+# the engine's own choice (no shape option set)
+for n in (12, 14, 16, 17, 18, 20):
+    c = qv.u3_ladder_circuit(n, 20, 1); g = c.gates()
+    st = qv.StateVector.create(n, 128, 0)
+    stream = torch.cuda.ExternalStream(st.stream())
+    for _ in range(3): st.apply_gates(g)
+    st.reset_stats(); ts = []
+    for _ in range(10):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream); st.apply_gates(g, sync=False); e1.record(stream); st.sync(); ts.append(e0.elapsed_time(e1))
+    print(n, "auto", st.stats()['passes'] / 10, round(statistics.median(ts), 3), flush=True)
