@@ -20,7 +20,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=30)
     ap.add_argument("--circuit", default="sweep", choices=["sweep", "grid", "ladder", "qft"])
-    ap.add_argument("--sub", type=int, default=4)
+    ap.add_argument("--sub", type=int, default=0, help="register subcube bits (0: the engine's default)")
     ap.add_argument("--prefetch", type=int, default=0)
     ap.add_argument("--tile", type=int, default=0, help="tile qubits (0: the precision's default)")
     ap.add_argument("--precision", type=int, default=128)
@@ -34,7 +34,8 @@ def main():
     st.set_option(qv.OPT_FUSE, 0)  # the start state: n per-gate H launches (skip them with ncu -s n)
     st.apply_gates(qv.make_benchmark_circuit(n).gates())
     st.set_option(qv.OPT_FUSE, 1)
-    st.set_option(qv.OPT_SUB_BITS, a.sub)
+    if a.sub:
+        st.set_option(qv.OPT_SUB_BITS, a.sub)
     st.set_option(qv.OPT_PREFETCH, a.prefetch)
     if a.tile:
         st.set_option(qv.OPT_TILE_QUBITS, a.tile)
