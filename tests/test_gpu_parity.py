@@ -376,3 +376,21 @@ def test_grid_gate_set_bit_exact(qv, oracle, n):
         qv.apply_circuit(st, circ, strategy="gpu", fuse=True, tile_qubits=tq)
         got = st.read_state()
         assert np.array_equal(got, want), (tq, sub, np.abs(got - want).max())
+
+
+def test_subcube_option_bounds(qv, oracle):
+    """QVG_OPT_SUB_BITS: complex128 takes 3..4, complex64 3..5 (its default is
+    5: 32 register amplitudes); a complex64 run at each size stays within
+    1e-5 of the oracle."""
+    st = qv.StateVector.create(10, 128, 0)
+    with pytest.raises(qv.ValidationError):
+        st.set_option(qv.OPT_SUB_BITS, 5)
+    c = qv.random_circuit(13, 200, 4)
+    want = oracle.simulate(13, gate_array(c))
+    for sub in (3, 4, 5):
+        st = qv.StateVector.create(13, 64, 0)
+        st.set_option(qv.OPT_SUB_BITS, sub)
+        qv.apply_circuit(st, c)
+        assert np.abs(st.read_state() - want).max() <= 1e-5, sub
+    with pytest.raises(qv.ValidationError):
+        qv.StateVector.create(10, 64, 0).set_option(qv.OPT_SUB_BITS, 6)
