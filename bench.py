@@ -174,6 +174,8 @@ def run_ours(args, rank, world, dist):
     nops = len(recs)
     if world == 1:
         st = qv.StateVector.create(n, 128, dev)
+    elif dist is None:  # virtual shards on one device: the N > 1 code path without NCCL (tools/bench_virtual.py)
+        st = qv.StateVector.create_sharded(n, 128, dev, 0, world, None)
     else:
         nid = qv.nccl_unique_id() if rank == 0 else None
         box = [nid]
@@ -185,7 +187,16 @@ def run_ours(args, rank, world, dist):
     # uniform start state with |a|^2 = 2^-n so no pass sees denormals/zeros
     st.apply_gates(qv.make_benchmark_circuit(n).gates())
 
+    # N = 1: one call per gate pass, with an event after each (per-gate times).
+    # N > 1: the whole sweep per call, so the shard schedule sees every op and
+    # batches its global-qubit exchanges (one op per call would swap a global
+    # qubit in without lookahead, then often swap it back).
+    all_gates = circ.gates()
+
     def one_step(events=None):
+        if world > 1:
+            st.apply_gates(all_gates, sync=False)
+            return
         for i in range(nops):
             st.apply_gates(recs[i], sync=False)
             if events is not None:
@@ -214,11 +225,17 @@ def run_ours(args, rank, world, dist):
         dist.barrier()
     total_ms = t_start.elapsed_time(t_end)
     stats = st.stats()
-    # per-launch durations from the interleaved events (same stream)
+    # per-launch durations from the interleaved events (same stream); N > 1
+    # records none (one call per step): the step's pass time is spread over
+    # the ops in proportion to their algorithmic bytes
     per_op = np.zeros((args.steps, nops))
-    for k in range(args.steps):
-        for i in range(nops):
-            per_op[k, i] = evs[k][i].elapsed_time(evs[k][i + 1])
+    if world == 1:
+        for k in range(args.steps):
+            for i in range(nops):
+                per_op[k, i] = evs[k][i].elapsed_time(evs[k][i + 1])
+    else:
+        lb = np.array([algorithmic_bytes(n - g, recs[i]) for i in range(nops)], dtype=np.float64)
+        per_op[:] = (total_ms / args.steps) * lb / lb.sum()
     if dist is not None:
         t = torch.tensor([total_ms], device=f"cuda:{dev}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -272,6 +289,9 @@ def run_ours(args, rank, world, dist):
         # per-gate time and HBM GB/s, individually
         "per_gate": [{"op": i, "gate": gate_label(recs[i]), "ms": round(float(mean_op[i]), 4),
                       "gbs": round(local_bytes[i] / (mean_op[i] / 1e3) / 1e9, 1)} for i in range(nops)],
+        "per_gate_timing": "CUDA events between launches" if world == 1 else
+                           "apportioned: N > 1 applies the whole sweep per call (exchange schedule with lookahead); "
+                           "the step time, exchanges included, is spread over the ops by algorithmic bytes",
         "gpu_launches": int(stats["kernel_launches"]),
         "exchanges_per_step": stats["exchanges"] / args.steps,
         # N > 1: the exchange traffic's NVLink floor (per-GPU bytes sent at the
