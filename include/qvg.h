@@ -32,7 +32,9 @@
 extern "C" {
 #endif
 
-#define QVG_ABI_VERSION 2  /* 2: qvg_stats.fused_exchanges, multi-exchange steps, options 10-13 */
+#define QVG_ABI_VERSION 3  /* 3: qvg_exchange_plan, qvg_set_step_hook, QVG_OPT_XCHG_CHUNK, per-segment
+                              sharded timing (kernel_ms / exchange_ms); 2: qvg_stats.fused_exchanges,
+                              multi-exchange steps, options 10-13 */
 
 /* Status codes -> reference exception types (error.hpp:10-50). */
 enum qvg_status {
@@ -75,7 +77,8 @@ enum qvg_option {
                                 complex64 also 5 (its default) */
     QVG_OPT_FMA = 8,         /* 1: fused-tile complex128 arithmetic with DFMA (faster, within 1e-15
                                 relative but NOT bit-identical to the reference); 0: exact (default) */
-    QVG_OPT_TIMING = 9,      /* 1: bracket each qvg_apply with CUDA events; qvg_stats.kernel_ms sums them */
+    QVG_OPT_TIMING = 9,      /* 1: CUDA events around each qvg_apply (sharded: around every local-pass
+                                batch and exchange); qvg_stats.kernel_ms / exchange_ms sum them */
     QVG_OPT_EXCHANGE = 10,   /* sharded states: 0 copy exchange (NCCL send/recv; virtual: swap kernel),
                                 1 peer-memory exchange kernel, 2 peer exchange fused with the gate that
                                 triggered it, -1 auto (default: 2 for NCCL ranks whose peers map, else 1) */
@@ -91,8 +94,10 @@ enum qvg_option {
                                 2 = only moves that keep every bit (an X/CX permutation or a Z/CZ sign
                                 flip on either side; default), 1 = any such move (mathematically equal,
                                 NOT bit-identical to the reference), 0 = circuit order */
-    QVG_OPT_CLASSES = 16     /* fused tile: 1 = structured-matrix op bodies (real, X, entries +-1/2, Z),
+    QVG_OPT_CLASSES = 16,    /* fused tile: 1 = structured-matrix op bodies (real, X, entries +-1/2, Z),
                                 same values with fewer FP64 instructions (default); 0 = general bodies */
+    QVG_OPT_XCHG_CHUNK = 17  /* sharded: copy-transport chunk bytes (multiple of 16; 0 = default 256 MiB,
+                                capped by the NCCL scratch); tests use small chunks to split runs */
 };
 
 /* Counters (the reference's Metrics, metrics.hpp:14-30, plus the GPU pass
@@ -105,8 +110,8 @@ typedef struct qvg_stats {
     uint64_t bytes_moved;    /* algorithmic HBM bytes, read + write */
     uint64_t exchange_bytes; /* bytes sent over NVLink (sharded states) */
     uint64_t exchanges;      /* pairwise half-shard exchanges */
-    double kernel_ms;        /* device time of gate kernels (timed states only) */
-    double exchange_ms;
+    double kernel_ms;        /* device time of gate passes (QVG_OPT_TIMING states only) */
+    double exchange_ms;      /* device time of exchanges (QVG_OPT_TIMING, sharded states) */
     uint64_t fused_exchanges; /* exchanges that also applied the gate that caused them (k_xchg) */
 } qvg_stats;
 
@@ -238,6 +243,31 @@ typedef struct qvg_shard_step {
  * steps and the total count to *nsteps (call with cap = 0 to size). */
 int qvg_shard_schedule(uint32_t n_qubits, uint32_t world, const qvg_gate *ops, uint64_t count,
                        int canonicalize, qvg_shard_step *steps, uint64_t cap, uint64_t *nsteps);
+/* The copy transport's chunk plan for one exchange step on one rank
+ * (qvg_schedule.hpp exchange_chunks), in issue order: chunk i is one grouped
+ * send/recv with `partner` of the `bytes` at `offset_bytes` of this rank's
+ * shard, received into the same place; chunk i of a rank and of its partner
+ * carry each other's data. The plan the NCCL and virtual-shard copy
+ * transports execute; host-only (tests drive it over gloo). Writes at most
+ * `cap` entries and the total to *count. */
+typedef struct qvg_xchunk {
+    uint32_t round;   /* 1-based round (multi-exchange: 1 .. 2^k - 1) */
+    uint32_t partner;
+    uint64_t offset_bytes;
+    uint64_t bytes;
+} qvg_xchunk;
+int qvg_exchange_plan(uint32_t n_qubits, uint32_t world, uint32_t rank, uint32_t precision,
+                      const qvg_shard_step *step, uint64_t chunk_bytes, qvg_xchunk *out,
+                      uint64_t cap, uint64_t *count);
+/* Test instrumentation around every executed segment of a sharded apply (a
+ * batch of local passes or one exchange; the reference's ExecHooks,
+ * parallel.hpp:40-45): fn(user, rank, segment, step_type, phase) with phase 0
+ * before the segment is enqueued and 1 after its device work completed (the
+ * state's stream is synchronised while a hook is installed). A nonzero
+ * return is an injected fault: qvg_apply fails with QVG_ERR_IO and no later
+ * segment runs. NULL removes the hook. */
+typedef int (*qvg_step_hook_fn)(void *user, uint32_t rank, uint64_t segment, uint32_t step_type, uint32_t phase);
+int qvg_set_step_hook(qvg_state *s, qvg_step_hook_fn fn, void *user);
 /* Thread-local message of the last failing call ("" when none). */
 const char *qvg_last_error(void);
 int qvg_abi_version(void);

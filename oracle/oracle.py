@@ -121,6 +121,7 @@ class RefEngine:
         lib.qvr_store_open.argtypes = [ctypes.c_char_p]
         lib.qvr_store_open.restype = _P
         lib.qvr_store_close.argtypes = [_P]
+        lib.qvr_store_path.argtypes = [_P, ctypes.c_char_p, _U64]
         lib.qvr_parse.argtypes = [ctypes.c_char_p, ctypes.c_int64, ctypes.c_int, _P, _U64, ctypes.POINTER(_U64),
                                   ctypes.POINTER(_U32), ctypes.POINTER(_U64), ctypes.c_char_p, _U64]
         self.lib = lib
@@ -224,6 +225,17 @@ class RefStore:
 
     def sync(self):
         self.eng._check(self.eng.lib.qvr_store_sync(self.h))
+
+    def path(self) -> str:
+        buf = ctypes.create_string_buffer(4096)
+        self.eng._check(self.eng.lib.qvr_store_path(self.h, buf, len(buf)))
+        return buf.value.decode()
+
+    def amplitudes(self) -> np.ndarray:
+        """Read-only memory map of the store's amplitude payload (the QVSV
+        layout: a 32-byte header, then 2^n little-endian complex128,
+        reference store.hpp:13-29). Call sync() first."""
+        return np.memmap(self.path(), dtype=np.complex128, mode="r", offset=32, shape=(1 << self.n,))
 
     def close(self):
         if self.h:

@@ -199,6 +199,16 @@ void *qvr_store_open(const char *path) {
     return h;
 }
 
+// The store's file path (the QVSV file the reference engine streams; read
+// back with a memory map for multi-GiB states instead of read_full_state).
+int qvr_store_path(void *h, char *out, std::uint64_t cap) {
+    return guarded([&] {
+        const std::string s = static_cast<Handle *>(h)->store.path().string();
+        if (s.size() + 1 > cap) throw qvsim::ValidationError("path buffer too small");
+        std::memcpy(out, s.c_str(), s.size() + 1);
+    });
+}
+
 // Close without deleting the file.
 void qvr_store_close(void *h) { delete static_cast<Handle *>(h); }
 

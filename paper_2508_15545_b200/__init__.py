@@ -26,86 +26,13 @@ except ImportError as exc:  # pragma: no cover - exercised only on a broken buil
         f"({exc}); build it with `make -C {_HERE}` or __graft_entry__.build()"
     ) from exc
 
-from ._core import (  # noqa: E402
-    OPT_CARRIERS,
-    OPT_FUSE,
-    OPT_LOW_KERNEL,
-    OPT_MIN_RUN,
-    OPT_PRED_STORE,
-    OPT_SUB_BITS,
-    OPT_FMA,
-    OPT_TIMING,
-    OPT_EXCHANGE,
-    OPT_PREFETCH,
-    OPT_BATCH_EXCHANGE,
-    OPT_STAGE,
-    OPT_GRAPH,
-    OPT_REORDER,
-    OPT_CLASSES,
-    OPT_TILE_QUBITS,
-    QVG_ABI_VERSION,
-    CapacityError,
-    Circuit,
-    FormatError,
-    IoError,
-    ParseError,
-    QvsimError,
-    DEFAULT_BLOCK_AMPS,
-    StateStore,
-    StateVector,
-    ValidationError,
-    top_amplitudes,
-    verify_equivalence,
-    apply_circuit,
-    apply_circuit_host,
-    circuit_from_gates,
-    grid_circuit,
-    haar_sweep_circuit,
-    make_benchmark_circuit,
-    make_gate,
-    nccl_unique_id,
-    parse_circuit,
-    plan_passes,
-    qft_circuit,
-    random_circuit,
-    serialize_circuit,
-    shard_schedule,
-    strategy_tags,
-    u3_ladder_circuit,
-)
+# Every public name of the native module (circuit builders, StateVector /
+# StateStore, apply_circuit*, error classes, OPT_* option keys, planner and
+# schedule queries) is re-exported as is.
+globals().update({k: getattr(_core, k) for k in dir(_core) if not k.startswith("_")})
 
 LIBQVG = _os.path.join(_HERE, "libqvg.so")
 
-__all__ = [
-    "CapacityError",
-    "Circuit",
-    "FormatError",
-    "IoError",
-    "LIBQVG",
-    "OPT_CARRIERS",
-    "OPT_FUSE",
-    "OPT_LOW_KERNEL",
-    "OPT_TILE_QUBITS",
-    "ParseError",
-    "QVG_ABI_VERSION",
-    "QvsimError",
-    "StateVector",
-    "ValidationError",
-    "apply_circuit",
-    "circuit_from_gates",
-    "grid_circuit",
-    "haar_sweep_circuit",
-    "make_benchmark_circuit",
-    "make_gate",
-    "nccl_unique_id",
-    "parse_circuit",
-    "plan_passes",
-    "qft_circuit",
-    "random_circuit",
-    "serialize_circuit",
-    "shard_schedule",
-    "strategy_tags",
-    "u3_ladder_circuit",
-]
+__all__ = sorted([k for k in dir(_core) if not k.startswith("_")] + ["LIBQVG"])
 
-__version__ = "0.1.0"
+__version__ = "0.2.0"

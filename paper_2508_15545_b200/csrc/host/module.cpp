@@ -62,6 +62,7 @@ py::dict stats_dict(const qvg_stats &s) {
     d["exchange_bytes"] = s.exchange_bytes;
     d["exchanges"] = s.exchanges;
     d["kernel_ms"] = s.kernel_ms;
+    d["exchange_ms"] = s.exchange_ms;
     d["fused_exchanges"] = s.fused_exchanges;
     return d;
 }
@@ -228,6 +229,8 @@ PYBIND11_MODULE(_core, m) {
         }, py::arg("other"), "max_i |a_i - b_i| on the device")
         .def("set_option", &StateVector::set_option, py::arg("key"), py::arg("value"))
         .def("stats", [](const StateVector &s) { return stats_dict(s.stats()); })
+        .def("handle", [](const StateVector &s) { return reinterpret_cast<std::uintptr_t>(s.handle()); },
+             "the qvg_state* of this state (for C-ABI calls through ctypes, e.g. qvg_set_step_hook)")
         .def("reset_stats", [](StateVector &s) { check_status(qvg_stats_reset(s.handle())); })
         .def("sync", [](const StateVector &s) {
             py::gil_scoped_release nogil;
@@ -419,7 +422,9 @@ PYBIND11_MODULE(_core, m) {
               return py::make_tuple(passes, fused, bytes);
           },
           py::arg("n_qubits"), py::arg("gates"), py::arg("precision") = 128, py::arg("fuse") = true,
-          py::arg("tile_qubits") = 0, py::arg("carriers") = 3, "(passes, fused passes, algorithmic bytes)");
+          py::arg("tile_qubits") = 0, py::arg("carriers") = 0,
+          "(passes, fused passes, algorithmic bytes) as qvg_apply plans them on an unsharded state "
+          "(tile_qubits / carriers 0 = the engine's defaults for the precision and width)");
 
     m.def("shard_schedule",
           [](std::uint32_t n, std::uint32_t world, py::buffer buf, bool canonicalize, std::uint32_t batch) {
@@ -457,4 +462,5 @@ PYBIND11_MODULE(_core, m) {
     m.attr("OPT_GRAPH") = (int)QVG_OPT_GRAPH;
     m.attr("OPT_REORDER") = (int)QVG_OPT_REORDER;
     m.attr("OPT_CLASSES") = (int)QVG_OPT_CLASSES;
+    m.attr("OPT_XCHG_CHUNK") = (int)QVG_OPT_XCHG_CHUNK;
 }

@@ -117,7 +117,13 @@ struct qvg_state {
     };
     std::vector<GraphEntry> graphs;  // small LRU cache
     uint64_t graph_clock = 0;
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
+    struct Timed {
+        cudaEvent_t a, b;
+        int kind;  // 0: gate passes -> kernel_ms, 1: exchange -> exchange_ms
+    };
+    std::vector<Timed> pending;
+    qvg_step_hook_fn hook = nullptr;  // qvg_set_step_hook (tests)
+    void *hook_user = nullptr;
     // device scratch
     double *d_partials = nullptr;
     double *d_probs = nullptr;
@@ -251,6 +257,26 @@ void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *recs) {
     kern<<<(unsigned)grid, threads, smem, s.stream>>>(static_cast<T *>(psi), prm);
 }
 
+// The engine's default tile shape for a precision (create_impl; measured in
+// profiles/r01_fused_ab.json, r01_fused_ab_c64.json, r01_sub5_ab.json).
+struct TileShape {
+    uint32_t tile_qubits, sub_bits, carriers;
+};
+TileShape default_shape(uint32_t precision) {
+    return precision == QVG_C128 ? TileShape{11, 4, 3} : TileShape{12, 5, 4};
+}
+
+// Small complex128 states: 2^10-amplitude tiles of 8-amplitude subcubes
+// (4x the CTAs of the default 2^11 x 16 shape) unless the caller chose a
+// shape. tools/tile_size_small.py, config 0's circuit: n=16 0.64-0.65 ->
+// 0.57-0.61 ms on two boxes; from n=18 on the default shape is as fast or faster.
+void small_state_shape(PlanOptions &po, uint32_t precision, uint32_t L, bool shape_set) {
+    if (!shape_set && precision == QVG_C128 && L <= 17) {
+        po.tile_qubits = std::min<uint32_t>(10, L);
+        po.sub_bits = 3;
+    }
+}
+
 PlanOptions plan_options(const qvg_state &s) {
     PlanOptions po;
     po.n = s.L;
@@ -264,14 +290,7 @@ PlanOptions plan_options(const qvg_state &s) {
     po.stage_bits = s.stage_bits;
     po.reorder = s.reorder;
     po.classes = s.classes;
-    // Small complex128 states: 2^10-amplitude tiles of 8-amplitude subcubes
-    // (4x the CTAs of the default 2^11 x 16 shape) unless the caller chose a
-    // shape. tools/tile_size_small.py, config 0's circuit: n=16 0.64-0.65 ->
-    // 0.57-0.61 ms on two boxes; from n=18 on the default shape is as fast or faster.
-    if (!s.shape_set && s.precision == QVG_C128 && s.L <= 17) {
-        po.tile_qubits = std::min<uint32_t>(10, s.L);
-        po.sub_bits = 3;
-    }
+    small_state_shape(po, s.precision, s.L, s.shape_set);
     return po;
 }
 
@@ -410,6 +429,12 @@ cudaStream_t shard_stream(qvg_state &s) { return s.stream; }
 uint32_t shard_amp_bytes(const qvg_state &s) { return s.S; }
 qvg_stats &shard_stats(qvg_state &s) { return s.stats; }
 int shard_exchange_mode(const qvg_state &s) { return s.exchange_mode; }
+bool shard_timing(const qvg_state &s) { return s.timing; }
+void shard_time_push(qvg_state &s, cudaEvent_t a, cudaEvent_t b, int kind) { s.pending.push_back({a, b, kind}); }
+bool shard_has_hook(const qvg_state &s) { return s.hook != nullptr; }
+int shard_step_hook(qvg_state &s, uint32_t rank, uint64_t segment, uint32_t type, uint32_t phase) {
+    return s.hook ? s.hook(s.hook_user, rank, segment, type, phase) : 0;
+}
 uint32_t shard_batch_max(const qvg_state &s) { return s.batch_max; }
 }  // namespace qvg
 
@@ -447,9 +472,10 @@ static int create_impl(uint32_t n, uint32_t precision, int device, uint32_t rank
         // r01_sub5_ab.json): complex128: 2^11 amplitudes as 128 threads x 16 register
         // amplitudes (C2/C1/C3 4-11% faster than 256 x 8); complex64: 2^12 as
         // 128 threads x 32 (C2 -16%, C1 -12% against 256 x 16, C3 +1%).
-        s->tile_qubits = precision == QVG_C128 ? 11 : 12;
-        s->sub_bits = precision == QVG_C128 ? 4 : 5;
-        s->carriers = precision == QVG_C128 ? 3 : 4;
+        const TileShape shape = default_shape(precision);
+        s->tile_qubits = shape.tile_qubits;
+        s->sub_bits = shape.sub_bits;
+        s->carriers = shape.carriers;
         try {
             set_device(s);
             cuda_check(cudaDeviceGetAttribute(&s->sm_count, cudaDevAttrMultiProcessorCount, device), "sm count");
@@ -494,8 +520,8 @@ int qvg_destroy(qvg_state *s) {
         cudaSetDevice(s->device);
         if (s->stream) cudaStreamSynchronize(s->stream);
         for (auto &pr : s->pending) {
-            cudaEventDestroy(pr.first);
-            cudaEventDestroy(pr.second);
+            cudaEventDestroy(pr.a);
+            cudaEventDestroy(pr.b);
         }
         drop_graphs(*s);
         s->shards.release();
@@ -570,6 +596,10 @@ int qvg_set_option(qvg_state *s, int key, int64_t value) {
         case QVG_OPT_EXCHANGE:
             if (value < -1 || value > 2) throw Validation("exchange mode must be -1, 0, 1 or 2");
             s->exchange_mode = (int)value;
+            break;
+        case QVG_OPT_XCHG_CHUNK:
+            if (value < 0 || (value % 16) != 0) throw Validation("exchange chunk must be a multiple of 16 bytes (0 = default)");
+            s->shards.chunk_override = (uint64_t)value;
             break;
         default: throw Validation("unknown option " + std::to_string(key));
         }
@@ -647,16 +677,20 @@ int qvg_apply(qvg_state *s, const qvg_gate *ops, uint64_t count) {
         for (uint64_t i = 0; i < count; ++i) validate_op(ops[i], s->n, i);
         set_device(s);
         nvtxRangePushA("qvg_apply");
+        // Timing: an unsharded apply is one bracketed interval (kernel_ms); a
+        // sharded one is timed per segment inside the executor (local passes
+        // -> kernel_ms, exchanges -> exchange_ms, qvg_shard.hpp run_steps).
+        const bool whole = s->timing && s->world == 1;
         cudaEvent_t ev[2] = {nullptr, nullptr};
-        if (s->timing) {
+        if (whole) {
             for (auto &e : ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
             cuda_check(cudaEventRecord(ev[0], s->stream), "cudaEventRecord");
         }
         if (s->graph && s->world == 1 && count > 0) apply_graph(*s, ops, count);
         else shard_apply(*s, s->shards, ops, count);
-        if (s->timing) {
+        if (whole) {
             cuda_check(cudaEventRecord(ev[1], s->stream), "cudaEventRecord");
-            s->pending.push_back({ev[0], ev[1]});
+            s->pending.push_back({ev[0], ev[1], 0});
         }
         nvtxRangePop();
         s->stats.gates_applied += count;
@@ -841,11 +875,11 @@ int qvg_stats_get(const qvg_state *s, qvg_stats *out) {
         auto *m = const_cast<qvg_state *>(s);
         for (auto &pr : m->pending) {
             float ms = 0.f;
-            cuda_check(cudaEventSynchronize(pr.second), "cudaEventSynchronize");
-            cuda_check(cudaEventElapsedTime(&ms, pr.first, pr.second), "cudaEventElapsedTime");
-            m->stats.kernel_ms += ms;
-            cudaEventDestroy(pr.first);
-            cudaEventDestroy(pr.second);
+            cuda_check(cudaEventSynchronize(pr.b), "cudaEventSynchronize");
+            cuda_check(cudaEventElapsedTime(&ms, pr.a, pr.b), "cudaEventElapsedTime");
+            (pr.kind ? m->stats.exchange_ms : m->stats.kernel_ms) += ms;
+            cudaEventDestroy(pr.a);
+            cudaEventDestroy(pr.b);
         }
         m->pending.clear();
         *out = s->stats;
@@ -1079,13 +1113,17 @@ int qvg_plan_passes(uint32_t n_qubits, uint32_t precision, int fuse, uint32_t ti
         if (n_qubits < 1 || n_qubits > 40) throw Validation("n_qubits must be in [1, 40]");
         if (count && !ops) throw Validation("null op array");
         for (uint64_t i = 0; i < count; ++i) validate_op(ops[i], n_qubits, i);
+        // the same options qvg_apply plans with on an unsharded state of this
+        // precision and width (create_impl defaults + plan_options): 0 = default
+        const TileShape shape = default_shape(precision);
         PlanOptions po;
         po.n = n_qubits;
         po.amp_bytes = precision == QVG_C128 ? 16 : 8;
         po.fuse = fuse != 0;
-        po.tile_qubits = tile_qubits ? std::min<uint32_t>(tile_qubits, 12) : 11;
-        po.carriers = carriers;
-        po.sub_bits = 4;  // the engine's default (create_impl)
+        po.tile_qubits = tile_qubits ? std::min<uint32_t>(tile_qubits, 12) : shape.tile_qubits;
+        po.carriers = carriers ? carriers : shape.carriers;
+        po.sub_bits = shape.sub_bits;
+        small_state_shape(po, precision, n_qubits, tile_qubits != 0);
         const Plan plan = plan_ops(ops, count, po);  // as run_local (default reorder mode)
         uint64_t fused = 0, bytes = 0;
         for (const Pass &p : plan.passes) {
@@ -1095,6 +1133,41 @@ int qvg_plan_passes(uint32_t n_qubits, uint32_t precision, int fuse, uint32_t ti
         if (passes_out) *passes_out = plan.passes.size();
         if (fused_out) *fused_out = fused;
         if (bytes_out) *bytes_out = bytes;
+    });
+}
+
+int qvg_set_step_hook(qvg_state *s, qvg_step_hook_fn fn, void *user) {
+    return guarded([&] {
+        check_state(s);
+        s->hook = fn;
+        s->hook_user = user;
+    });
+}
+
+int qvg_exchange_plan(uint32_t n_qubits, uint32_t world, uint32_t rank, uint32_t precision, const qvg_shard_step *step,
+                      uint64_t chunk_bytes, qvg_xchunk *out, uint64_t cap, uint64_t *count) {
+    return guarded([&] {
+        if (world < 2 || (world & (world - 1)) != 0) throw Validation("world size must be a power of two >= 2");
+        if (rank >= world) throw Validation("rank out of range");
+        if (precision != QVG_C64 && precision != QVG_C128) throw Validation("precision must be 64 or 128");
+        if (!step) throw Validation("null step");
+        uint32_t g = 0;
+        while ((1u << g) < world) ++g;
+        if (n_qubits < g + 2 || n_qubits > 40) throw Validation("too few qubits for this many shards");
+        if (step->type == STEP_EXCHANGE && (step->gpos >= n_qubits))
+            throw Validation("exchange step: gpos out of range");
+        if (step->type == STEP_MULTI_EXCHANGE && (step->gpos >> g) != 0)
+            throw Validation("multi-exchange mask has bits beyond the rank bits");
+        if (chunk_bytes == 0 || chunk_bytes % 16) throw Validation("chunk_bytes must be a positive multiple of 16");
+        std::vector<XChunk> plan;
+        try {
+            plan = exchange_chunks(n_qubits - g, precision == QVG_C128 ? 16 : 8, chunk_bytes, rank, *step);
+        } catch (const std::invalid_argument &e) {
+            throw Validation(e.what());
+        }
+        if (count) *count = plan.size();
+        static_assert(sizeof(XChunk) == sizeof(qvg_xchunk), "qvg_xchunk layout");
+        if (out) std::memcpy(out, plan.data(), std::min<uint64_t>(cap, plan.size()) * sizeof(XChunk));
     });
 }
 

@@ -229,29 +229,6 @@ k_swap_bits(typename Cplx<R>::T *__restrict__ psi, int a, int b) {
     }
 }
 
-// K6: virtual-shard half exchange (both shards on this device): p's
-// amplitudes with local bit lpos = 1 trade places with q's with bit lpos = 0,
-// which is what the NCCL transport does between two ranks.
-template <class R, int APT>
-__global__ void __launch_bounds__(256)
-k_swap_halves(typename Cplx<R>::T *__restrict__ p, typename Cplx<R>::T *__restrict__ q, int lpos) {
-    using T = typename Cplx<R>::T;
-    const uint64_t first = (uint64_t)blockIdx.x * (blockDim.x * APT) + threadIdx.x;
-    uint64_t i0[APT];
-    T x[APT], y[APT];
-#pragma unroll
-    for (int k = 0; k < APT; ++k) {
-        i0[k] = ins0(first + (uint64_t)k * blockDim.x, lpos);
-        x[k] = ld_amp(p + (i0[k] | (1ull << lpos)));
-        y[k] = ld_amp(q + i0[k]);
-    }
-#pragma unroll
-    for (int k = 0; k < APT; ++k) {
-        st_amp(p + (i0[k] | (1ull << lpos)), y[k]);
-        st_amp(q + i0[k], x[k]);
-    }
-}
-
 // K7: half-shard exchange over peer memory, optionally fused with the gate
 // that triggered it. Shard a has gpos bit 0 and shard b has gpos bit 1. t
 // enumerates local indices x0 whose bit lpos is 0, with x1 = x0 | 2^lpos.

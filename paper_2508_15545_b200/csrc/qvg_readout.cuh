@@ -85,7 +85,10 @@ constexpr int kTopkBins = 2048;
 template <class R>
 __global__ void __launch_bounds__(256)
 k_topk_hist(const typename Cplx<R>::T *__restrict__ psi, uint64_t count, uint64_t prefix, int shift, int width,
-            unsigned int *__restrict__ hist) {
+            unsigned long long *__restrict__ hist) {
+    // per-block counts fit 32 bits (a block visits <= 2^33 / 4096 keys); the
+    // global bins are 64-bit: a state of >= 2^32 amplitudes (n >= 32 on one
+    // B200, or sharded) can put that many keys in one bin
     __shared__ unsigned int sh[kTopkBins];
     for (int i = threadIdx.x; i < kTopkBins; i += blockDim.x) sh[i] = 0;
     __syncthreads();
@@ -99,7 +102,7 @@ k_topk_hist(const typename Cplx<R>::T *__restrict__ psi, uint64_t count, uint64_
     }
     __syncthreads();
     for (int i = threadIdx.x; i < kTopkBins; i += blockDim.x)
-        if (sh[i]) atomicAdd(&hist[i], sh[i]);
+        if (sh[i]) atomicAdd(&hist[i], (unsigned long long)sh[i]);
 }
 
 // Append every amplitude with key > tau (at most k of them by construction).
@@ -139,6 +142,17 @@ k_topk_tie_counts(const typename Cplx<R>::T *__restrict__ psi, uint64_t count, u
         __syncthreads();
     }
     if (threadIdx.x == 0) counts[c] = red[0];
+}
+
+// flags[j] = 1 iff amplitude chunk_off + j has key == tau: the tie test stays
+// on the device (the host never recomputes |a|^2, whose rounding could differ
+// under FMA contraction on another host ISA).
+template <class R>
+__global__ void __launch_bounds__(256)
+k_topk_tie_flags(const typename Cplx<R>::T *__restrict__ psi, uint64_t chunk_off, uint64_t len, uint64_t tau,
+                 unsigned char *__restrict__ flags) {
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < len; j += (uint64_t)gridDim.x * blockDim.x)
+        flags[j] = prob_key(psi[chunk_off + j]) == tau;
 }
 
 }  // namespace qvg

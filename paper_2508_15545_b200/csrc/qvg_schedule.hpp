@@ -1,6 +1,7 @@
 // qvg_schedule.hpp — host-only schedule for a state sharded over G = 2^g
 // ranks. No CUDA; exported through qvg_shard_schedule so the
-// logic is testable on CPU (tests/test_shard_gloo.py runs it over gloo).
+// logic is testable on CPU (tests/test_shard_schedule.py runs it emulated and
+// over gloo).
 //
 // Layout: rank r owns physical indices [r*2^L, (r+1)*2^L), L = n - g — the
 // reference's contiguous Eq. 9 partition (reference parallel.cpp:13-37,
@@ -44,6 +45,87 @@ using ShardStep = qvg_shard_step;
 
 // Local positions of a multi-exchange, in the order of the mask's set bits.
 inline uint32_t multi_pos(const ShardStep &st, uint32_t i) { return (st.lpos >> (8 * i)) & 0xffu; }
+
+// Bits of r at the set bits of mask, packed (pext) / spread back (pdep).
+inline uint32_t bits_pext(uint32_t r, uint32_t mask) {
+    uint32_t out = 0, i = 0;
+    for (uint32_t b = 0; b < 32; ++b)
+        if ((mask >> b) & 1u) out |= ((r >> b) & 1u) << i++;
+    return out;
+}
+inline uint32_t bits_pdep(uint32_t v, uint32_t mask) {
+    uint32_t out = 0, i = 0;
+    for (uint32_t b = 0; b < 32; ++b)
+        if ((mask >> b) & 1u) out |= ((v >> i++) & 1u) << b;
+    return out;
+}
+
+// The copy transport's chunk plan for one exchange step on one rank, in issue
+// order (the layout is qvg_xchunk, include/qvg.h). Each chunk is one grouped
+// send/recv with `partner`: this rank sends the `bytes` at `offset` of its
+// shard and receives the partner's chunk of the same index into the same
+// place. Chunk i of a rank and chunk i of its partner (same round) carry each
+// other's data, so the plan needs no coordination beyond the order.
+//   STEP_EXCHANGE (gpos, lpos): a rank whose gpos bit is b sends the
+//     amplitudes whose local bit lpos is 1 - b: 2^(L-1-lpos) runs of 2^lpos;
+//   STEP_MULTI_EXCHANGE (k qubits): round t = 1 .. 2^k - 1 pairs rank r with
+//     r ^ pdep(t, mask); r sends (and receives into) the region whose local
+//     bits at the k positions read w ^ t, w = pext(r, mask), in runs of
+//     2^min(pos) amplitudes.
+// Runs longer than chunk_bytes are split. Used by the NCCL copy transport and
+// by virtual shards in exchange mode 0 (qvg_shard.hpp), and exported as
+// qvg_exchange_plan for the CPU tests (emulated and over gloo).
+struct XChunk {
+    uint32_t round;    // 1-based exchange round (pairwise: 1)
+    uint32_t partner;  // rank this chunk is traded with
+    uint64_t offset;   // byte offset into this rank's shard
+    uint64_t bytes;
+};
+
+inline std::vector<XChunk> exchange_chunks(uint32_t L, uint32_t S, uint64_t chunk_bytes, uint32_t rank,
+                                           const ShardStep &st) {
+    std::vector<XChunk> out;
+    if (chunk_bytes == 0) throw std::invalid_argument("chunk_bytes must be > 0");
+    auto emit = [&](uint32_t round, uint32_t partner, uint64_t off, uint64_t len) {
+        for (uint64_t o = 0; o < len; o += chunk_bytes)
+            out.push_back(XChunk{round, partner, off + o, std::min<uint64_t>(chunk_bytes, len - o)});
+    };
+    if (st.type == STEP_EXCHANGE) {
+        if (st.gpos < L || st.lpos >= L) throw std::invalid_argument("exchange step: gpos must be global, lpos local");
+        const uint32_t bit = 1u << (st.gpos - L);
+        const uint64_t sendbit = (rank & bit) ? 0 : 1;
+        const uint64_t run = (uint64_t)S << st.lpos;
+        const uint64_t nruns = 1ull << (L - 1 - st.lpos);
+        for (uint64_t k = 0; k < nruns; ++k) emit(1, rank ^ bit, ((k << 1) | sendbit) * run, run);
+        return out;
+    }
+    if (st.type != STEP_MULTI_EXCHANGE) throw std::invalid_argument("not an exchange step");
+    const uint32_t k = st.lpos2, mask = st.gpos;
+    if (k < 2 || k > 4 || (uint32_t)__builtin_popcount(mask) != k) throw std::invalid_argument("bad multi-exchange step");
+    int pos[4], idx[4] = {0, 1, 2, 3};
+    for (uint32_t i = 0; i < k; ++i) {
+        pos[i] = (int)multi_pos(st, i);
+        if ((uint32_t)pos[i] >= L) throw std::invalid_argument("multi-exchange local position out of range");
+    }
+    std::sort(idx, idx + k, [&](int a, int b) { return pos[a] < pos[b]; });
+    const uint32_t w = bits_pext(rank, mask);
+    const int pmin = pos[idx[0]];
+    const uint64_t run = (uint64_t)S << pmin;
+    const uint64_t nruns = 1ull << (L - k - pmin);
+    for (uint32_t t = 1; t < (1u << k); ++t) {
+        const uint32_t partner = rank ^ bits_pdep(t, mask);
+        const uint32_t v = w ^ t;  // the region this rank sends and receives into
+        for (uint64_t r = 0; r < nruns; ++r) {
+            uint64_t x = r << pmin;
+            for (uint32_t j = 0; j < k; ++j) {
+                const uint64_t low = (1ull << pos[idx[j]]) - 1;
+                x = ((x & ~low) << 1) | (x & low) | ((uint64_t)((v >> idx[j]) & 1u) << pos[idx[j]]);
+            }
+            emit(t, partner, x * S, run);
+        }
+    }
+    return out;
+}
 
 struct QubitMap {
     std::vector<uint32_t> perm;  // logical -> physical

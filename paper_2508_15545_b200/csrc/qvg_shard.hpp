@@ -48,6 +48,15 @@ qvg_stats &shard_stats(qvg_state &s);
 int shard_exchange_mode(const qvg_state &s);  // QVG_OPT_EXCHANGE value (-1 = auto)
 uint32_t shard_batch_max(const qvg_state &s);  // QVG_OPT_BATCH_EXCHANGE: most global qubits per exchange
 void cuda_throw(cudaError_t e, const char *what);
+// QVG_OPT_TIMING on a sharded state: CUDA events around every executed
+// segment (a batch of local passes, or an exchange), folded into
+// qvg_stats.kernel_ms (kind 0) and exchange_ms (kind 1) by qvg_stats_get.
+bool shard_timing(const qvg_state &s);
+void shard_time_push(qvg_state &s, cudaEvent_t a, cudaEvent_t b, int kind);
+// qvg_set_step_hook: test instrumentation around every executed segment
+// (the reference's ExecHooks, parallel.hpp:40-45). Returns the hook's value.
+bool shard_has_hook(const qvg_state &s);
+int shard_step_hook(qvg_state &s, uint32_t rank, uint64_t segment, uint32_t type, uint32_t phase);
 
 inline void nccl_check(ncclResult_t r, const char *what) {
     if (r != ncclSuccess) throw std::runtime_error(std::string(what) + ": " + ncclGetErrorString(r));
@@ -63,6 +72,7 @@ struct ShardSet {
     void *scratch = nullptr;
     uint64_t scratch_bytes = 0;
     uint64_t chunk_bytes = 0;
+    uint64_t chunk_override = 0;  // QVG_OPT_XCHG_CHUNK: copy-transport chunk bytes (tests)
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t received[2] = {nullptr, nullptr}, copied[2] = {nullptr, nullptr};
     double *d_scalar = nullptr;
@@ -149,6 +159,7 @@ struct ShardSet {
         ranks.clear();
         if (scratch) cudaFree(scratch);
         scratch = nullptr;
+        scratch_bytes = 0;
         if (copy_stream) cudaStreamDestroy(copy_stream);
         copy_stream = nullptr;
         for (int b = 0; b < 2; ++b) {
@@ -160,6 +171,22 @@ struct ShardSet {
         d_scalar = nullptr;
         if (comm) ncclCommDestroy(comm);
         comm = nullptr;
+    }
+
+    // Chunk size of the copy transport: the NCCL scratch halves; virtual
+    // shards use the same 256 MiB cap (or a test override).
+    uint64_t copy_chunk_bytes(uint32_t S) const {
+        if (chunk_override) return chunk_bytes ? std::min(chunk_override, chunk_bytes) : chunk_override;
+        if (chunk_bytes) return chunk_bytes;
+        return std::min<uint64_t>(((uint64_t)S << L) / 2, 256ull << 20);
+    }
+    void ensure_scratch(uint64_t bytes) {
+        if (scratch_bytes >= bytes) return;
+        if (scratch) cudaFree(scratch);
+        scratch = nullptr;
+        scratch_bytes = 0;
+        cuda_throw(cudaMalloc(&scratch, bytes), "cudaMalloc(exchange scratch)");
+        scratch_bytes = bytes;
     }
 
     std::vector<void *> local_buffers() const { return bufs; }
@@ -204,22 +231,6 @@ inline void launch_swap_bits(cudaStream_t st, void *psi, uint32_t L, uint32_t a,
     }
 }
 
-// Virtual-shard exchange: p's amplitudes with local bit lpos = 1 trade places
-// with q's amplitudes with local bit lpos = 0.
-template <class R>
-inline void launch_swap_halves(cudaStream_t st, void *p, void *q, uint32_t L, uint32_t lpos) {
-    using T = typename Cplx<R>::T;
-    const uint64_t count = 1ull << (L - 1);
-    if (count >= 1024)
-        k_swap_halves<R, 4><<<(unsigned)(count / 1024), 256, 0, st>>>(static_cast<T *>(p), static_cast<T *>(q),
-                                                                       (int)lpos);
-    else {
-        const unsigned bs = (unsigned)std::min<uint64_t>(count, 256);
-        k_swap_halves<R, 1><<<(unsigned)(count / bs), bs, 0, st>>>(static_cast<T *>(p), static_cast<T *>(q),
-                                                                    (int)lpos);
-    }
-}
-
 inline void run_local_swap(qvg_state &s, ShardSet &set, uint32_t a, uint32_t b) {
     cudaStream_t st = shard_stream(s);
     for (void *psi : set.bufs) {
@@ -251,6 +262,67 @@ inline void launch_xchg(cudaStream_t st, void *a, void *b, uint32_t lpos, uint64
 // a rank only after every rank's earlier work on its state stream is done.
 inline void stream_barrier(ShardSet &set, cudaStream_t st) {
     nccl_check(ncclAllReduce(set.d_scalar, set.d_scalar, 1, ncclDouble, ncclSum, set.comm, st), "ncclAllReduce(barrier)");
+}
+
+// Copy transport for one exchange step, driven by the host chunk plan
+// (exchange_chunks, qvg_schedule.hpp) — the same plan on every transport:
+//   * NCCL ranks: chunk i is a grouped ncclSend/ncclRecv with the partner into
+//     one of two scratch buffers; its scratch -> shard copy runs on the copy
+//     stream and overlaps the send/recv of chunk i+1 (event-ordered; a chunk's
+//     copy waits for its own group, so the bytes it overwrites were sent);
+//   * virtual shards (one device): chunk i of rank r and chunk i of its
+//     partner trade places through a scratch buffer with D2D copies, the
+//     pair driven once by its lower rank. The bytes land exactly where the
+//     NCCL transport puts them, so the plan runs bit-exactly on one GPU.
+inline void copy_exchange(qvg_state &s, ShardSet &set, const ShardStep &step) {
+    cudaStream_t st = shard_stream(s);
+    const uint32_t S = shard_amp_bytes(s);
+    const uint64_t chunk = set.copy_chunk_bytes(S);
+    if (set.is_virtual) {
+        set.ensure_scratch(chunk);
+        for (size_t b = 0; b < set.bufs.size(); ++b) {
+            const uint32_t r = set.ranks[b];
+            const std::vector<XChunk> mine = exchange_chunks(set.L, S, chunk, r, step);
+            std::vector<XChunk> theirs;
+            uint32_t cur = ~0u;
+            for (size_t i = 0; i < mine.size(); ++i) {
+                const XChunk &c = mine[i];
+                if (c.partner < r) continue;  // driven by the partner
+                if (c.partner != cur) {
+                    theirs = exchange_chunks(set.L, S, chunk, c.partner, step);
+                    cur = c.partner;
+                }
+                const XChunk &d = theirs[i];
+                if (d.partner != r || d.bytes != c.bytes || d.round != c.round)
+                    throw std::runtime_error("internal: exchange chunk plans of a pair disagree");
+                char *pa = static_cast<char *>(set.bufs[r]) + c.offset;
+                char *pb = static_cast<char *>(set.bufs[c.partner]) + d.offset;
+                cuda_throw(cudaMemcpyAsync(set.scratch, pa, c.bytes, cudaMemcpyDeviceToDevice, st), "exchange copy");
+                cuda_throw(cudaMemcpyAsync(pa, pb, c.bytes, cudaMemcpyDeviceToDevice, st), "exchange copy");
+                cuda_throw(cudaMemcpyAsync(pb, set.scratch, c.bytes, cudaMemcpyDeviceToDevice, st), "exchange copy");
+            }
+        }
+        return;
+    }
+    const std::vector<XChunk> plan = exchange_chunks(set.L, S, chunk, set.rank, step);
+    char *base = static_cast<char *>(set.bufs[0]);
+    uint64_t i = 0;
+    for (const XChunk &c : plan) {
+        char *scr = static_cast<char *>(set.scratch) + (i & 1) * set.chunk_bytes;
+        if (i >= 2) cuda_throw(cudaStreamWaitEvent(st, set.copied[i & 1], 0), "wait scratch");
+        nccl_check(ncclGroupStart(), "ncclGroupStart");
+        nccl_check(ncclSend(base + c.offset, c.bytes, ncclChar, (int)c.partner, set.comm, st), "ncclSend");
+        nccl_check(ncclRecv(scr, c.bytes, ncclChar, (int)c.partner, set.comm, st), "ncclRecv");
+        nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+        cuda_throw(cudaEventRecord(set.received[i & 1], st), "record received");
+        cuda_throw(cudaStreamWaitEvent(set.copy_stream, set.received[i & 1], 0), "wait received");
+        cuda_throw(cudaMemcpyAsync(base + c.offset, scr, c.bytes, cudaMemcpyDeviceToDevice, set.copy_stream),
+                   "exchange copy");
+        cuda_throw(cudaEventRecord(set.copied[i & 1], set.copy_stream), "record copied");
+        ++i;
+    }
+    for (int b = 0; b < 2 && (uint64_t)b < i; ++b)  // later work on the state stream sees every copy
+        cuda_throw(cudaStreamWaitEvent(st, set.copied[b], 0), "wait copies");
 }
 
 // Half-shard exchange swapping global physical qubit gpos with local qubit
@@ -293,17 +365,21 @@ inline bool run_exchange(qvg_state &s, ShardSet &set, uint32_t gpos, uint32_t lp
     };
     const uint64_t quarter = half / 2;  // each rank of a pair streams half of the 2^(L-1) x0's
     qvg_stats &stats = shard_stats(s);
+    if (!use_kernel) {  // copy transport (NCCL send/recv, or D2D copies between virtual shards)
+        ShardStep xs{};
+        xs.type = STEP_EXCHANGE;
+        xs.gpos = gpos;
+        xs.lpos = lpos;
+        copy_exchange(s, set, xs);
+        stats.exchanges += 1;
+        stats.exchange_bytes += set.is_virtual ? half_bytes * set.world / 2 : half_bytes;
+        return false;
+    }
     if (set.is_virtual) {
         for (size_t b = 0; b < set.bufs.size(); ++b) {
             const uint32_t r = set.ranks[b];
             if (r & bit) continue;
             const uint32_t partner = r | bit;
-            if (!use_kernel) {
-                // r (bit 0) sends its lpos=1 half; partner (bit 1) its lpos=0 half.
-                if (dbl) launch_swap_halves<double>(st, set.bufs[b], set.bufs[partner], set.L, lpos);
-                else launch_swap_halves<float>(st, set.bufs[b], set.bufs[partner], set.L, lpos);
-                continue;
-            }
             if (fuse) flags = (pred(r) ? 1 : 0) | (pred(partner) ? 2 : 0);
             // one launch per rank role, exactly as the two ranks would split it
             xchg(set.bufs[b], set.bufs[partner], 0, quarter, flags, 0);
@@ -332,46 +408,7 @@ inline bool run_exchange(qvg_state &s, ShardSet &set, uint32_t gpos, uint32_t lp
         if (fuse) stats.fused_exchanges += 1;
         return fuse;
     }
-    const uint64_t sendbit = (set.rank & bit) ? 0 : 1;  // my half: local bit lpos == sendbit
-    const uint64_t block_bytes = (uint64_t)S << lpos;
-    const uint64_t nblocks = 1ull << (set.L - 1 - lpos);
-    char *base = static_cast<char *>(set.bufs[0]);
-    uint64_t i = 0;
-    for (uint64_t k = 0; k < nblocks; ++k) {
-        char *blk = base + (((k << 1) | sendbit) * block_bytes);
-        for (uint64_t off = 0; off < block_bytes; off += set.chunk_bytes, ++i) {
-            const uint64_t c = std::min<uint64_t>(set.chunk_bytes, block_bytes - off);
-            char *scr = static_cast<char *>(set.scratch) + (i & 1) * set.chunk_bytes;
-            if (i >= 2) cuda_throw(cudaStreamWaitEvent(st, set.copied[i & 1], 0), "wait scratch");
-            nccl_check(ncclGroupStart(), "ncclGroupStart");
-            nccl_check(ncclSend(blk + off, c, ncclChar, (int)partner, set.comm, st), "ncclSend");
-            nccl_check(ncclRecv(scr, c, ncclChar, (int)partner, set.comm, st), "ncclRecv");
-            nccl_check(ncclGroupEnd(), "ncclGroupEnd");
-            cuda_throw(cudaEventRecord(set.received[i & 1], st), "record received");
-            cuda_throw(cudaStreamWaitEvent(set.copy_stream, set.received[i & 1], 0), "wait received");
-            cuda_throw(cudaMemcpyAsync(blk + off, scr, c, cudaMemcpyDeviceToDevice, set.copy_stream), "exchange copy");
-            cuda_throw(cudaEventRecord(set.copied[i & 1], set.copy_stream), "record copied");
-        }
-    }
-    for (int b = 0; b < 2 && (uint64_t)b < i; ++b)  // later work on the state stream sees every copy
-        cuda_throw(cudaStreamWaitEvent(st, set.copied[b], 0), "wait copies");
-    stats.exchanges += 1;
-    stats.exchange_bytes += half_bytes;
-    return false;
-}
-
-// Bits of r at the set bits of mask, packed (pext) / spread back (pdep).
-inline uint32_t bits_pext(uint32_t r, uint32_t mask) {
-    uint32_t out = 0, i = 0;
-    for (uint32_t b = 0; b < 32; ++b)
-        if ((mask >> b) & 1u) out |= ((r >> b) & 1u) << i++;
-    return out;
-}
-inline uint32_t bits_pdep(uint32_t v, uint32_t mask) {
-    uint32_t out = 0, i = 0;
-    for (uint32_t b = 0; b < 32; ++b)
-        if ((mask >> b) & 1u) out |= ((v >> i++) & 1u) << b;
-    return out;
+    throw std::runtime_error("internal: exchange without a transport");
 }
 
 // Batched exchange (STEP_MULTI_EXCHANGE): the 2^k ranks that differ only in
@@ -418,7 +455,7 @@ inline void run_multi_exchange(qvg_state &s, ShardSet &set, const ShardStep &st)
         else launch(float{}, self, peer_of, w, fence);
     };
     const uint32_t gmask = mask;  // rank bits
-    if (set.is_virtual || kernel) {
+    if (kernel) {
         if (set.is_virtual) {
             for (size_t b = 0; b < set.bufs.size(); ++b) {
                 const uint32_t r = set.ranks[b];
@@ -441,44 +478,11 @@ inline void run_multi_exchange(qvg_state &s, ShardSet &set, const ShardStep &st)
         stats.exchanges += 1;
         return;
     }
-    // NCCL copy transport: round t is a pairwise exchange of the region whose
-    // local bits read the partner's value, in runs of 2^min(pos) amplitudes.
-    const uint32_t r = set.rank, w = bits_pext(r, gmask);
-    const int pmin = pos[idx[0]];
-    const uint64_t run_bytes = (uint64_t)S << pmin;
-    const uint64_t nruns = 1ull << (set.L - k - pmin);
-    char *base = static_cast<char *>(set.bufs[0]);
-    uint64_t i = 0;
-    for (uint32_t t = 1; t <= rounds; ++t) {
-        const int partner = (int)(r ^ bits_pdep(t, gmask));
-        const uint32_t v = w ^ t;  // region I send and receive into
-        for (uint64_t run = 0; run < nruns; ++run) {
-            uint64_t x = run << pmin;
-            for (uint32_t j = 0; j < k; ++j) {
-                const uint64_t low = (1ull << pos[idx[j]]) - 1;
-                x = ((x & ~low) << 1) | (x & low) | ((uint64_t)((v >> idx[j]) & 1u) << pos[idx[j]]);
-            }
-            char *blk = base + x * S;
-            for (uint64_t off = 0; off < run_bytes; off += set.chunk_bytes, ++i) {
-                const uint64_t c = std::min<uint64_t>(set.chunk_bytes, run_bytes - off);
-                char *scr = static_cast<char *>(set.scratch) + (i & 1) * set.chunk_bytes;
-                if (i >= 2) cuda_throw(cudaStreamWaitEvent(stream, set.copied[i & 1], 0), "wait scratch");
-                nccl_check(ncclGroupStart(), "ncclGroupStart");
-                nccl_check(ncclSend(blk + off, c, ncclChar, partner, set.comm, stream), "ncclSend");
-                nccl_check(ncclRecv(scr, c, ncclChar, partner, set.comm, stream), "ncclRecv");
-                nccl_check(ncclGroupEnd(), "ncclGroupEnd");
-                cuda_throw(cudaEventRecord(set.received[i & 1], stream), "record received");
-                cuda_throw(cudaStreamWaitEvent(set.copy_stream, set.received[i & 1], 0), "wait received");
-                cuda_throw(cudaMemcpyAsync(blk + off, scr, c, cudaMemcpyDeviceToDevice, set.copy_stream),
-                           "exchange copy");
-                cuda_throw(cudaEventRecord(set.copied[i & 1], set.copy_stream), "record copied");
-            }
-        }
-    }
-    for (int b = 0; b < 2 && (uint64_t)b < i; ++b)
-        cuda_throw(cudaStreamWaitEvent(stream, set.copied[b], 0), "wait copies");
+    // copy transport: round t is a pairwise exchange of the region whose
+    // local bits read the partner's value (exchange_chunks)
+    copy_exchange(s, set, st);
     stats.exchanges += 1;
-    stats.exchange_bytes += (uint64_t)rounds * region * S;
+    stats.exchange_bytes += (set.is_virtual ? set.world : 1) * (uint64_t)rounds * region * S;
 }
 
 // Execute a step list: consecutive local steps are batched per shard (each
@@ -488,11 +492,49 @@ inline void run_multi_exchange(qvg_state &s, ShardSet &set, const ShardStep &st)
 // to the exchange kernel.
 inline void run_steps(qvg_state &s, ShardSet &set, const std::vector<ShardStep> &steps) {
     std::vector<std::vector<qvg_gate>> batch(set.bufs.size());
-    auto flush = [&] {
-        for (size_t b = 0; b < set.bufs.size(); ++b) {
-            if (!batch[b].empty()) shard_run_local(s, set.bufs[b], batch[b].data(), batch[b].size());
-            batch[b].clear();
+    uint64_t segment = 0;
+    // One executed segment: hooks before (phase 0) and after its device work
+    // completed (phase 1; the stream is synchronised only when a hook is
+    // installed), CUDA events around it when timing. A nonzero hook value is
+    // an injected fault: IoError, and no later segment runs (the reference's
+    // rethrow after join, parallel.cpp:128-132).
+    auto run_segment = [&](uint32_t type, auto &&work) {
+        const bool hooked = shard_has_hook(s);
+        auto call_hooks = [&](uint32_t phase) {
+            for (uint32_t r : set.ranks)
+                if (shard_step_hook(s, r, segment, type, phase))
+                    throw std::runtime_error("injected fault on rank " + std::to_string(r) + " at segment " +
+                                             std::to_string(segment) + (phase ? " (end)" : " (start)"));
+        };
+        if (hooked) call_hooks(0);
+        cudaEvent_t ev[2] = {nullptr, nullptr};
+        const bool timed = shard_timing(s);
+        cudaStream_t st = shard_stream(s);
+        if (timed) {
+            for (auto &e : ev) cuda_throw(cudaEventCreate(&e), "cudaEventCreate");
+            cuda_throw(cudaEventRecord(ev[0], st), "cudaEventRecord");
         }
+        work();
+        if (timed) {
+            cuda_throw(cudaEventRecord(ev[1], st), "cudaEventRecord");
+            shard_time_push(s, ev[0], ev[1], type == STEP_LOCAL ? 0 : 1);
+        }
+        if (hooked) {
+            cuda_throw(cudaStreamSynchronize(st), "hooked segment sync");
+            call_hooks(1);
+        }
+        ++segment;
+    };
+    auto flush = [&] {
+        bool any = false;
+        for (auto &b : batch) any = any || !b.empty();
+        if (!any) return;
+        run_segment(STEP_LOCAL, [&] {
+            for (size_t b = 0; b < set.bufs.size(); ++b) {
+                if (!batch[b].empty()) shard_run_local(s, set.bufs[b], batch[b].data(), batch[b].size());
+                batch[b].clear();
+            }
+        });
     };
     for (size_t i = 0; i < steps.size(); ++i) {
         const ShardStep &st = steps[i];
@@ -506,11 +548,13 @@ inline void run_steps(qvg_state &s, ShardSet &set, const std::vector<ShardStep> 
             const ShardStep *next = i + 1 < steps.size() ? &steps[i + 1] : nullptr;
             const bool candidate = next && next->type == STEP_LOCAL && next->op.target == st.lpos &&
                                    !op_is_diag(next->op);
-            if (run_exchange(s, set, st.gpos, st.lpos, candidate ? next : nullptr)) ++i;
+            bool fused = false;
+            run_segment(STEP_EXCHANGE, [&] { fused = run_exchange(s, set, st.gpos, st.lpos, candidate ? next : nullptr); });
+            if (fused) ++i;
         } else if (st.type == STEP_MULTI_EXCHANGE) {
-            run_multi_exchange(s, set, st);
+            run_segment(STEP_MULTI_EXCHANGE, [&] { run_multi_exchange(s, set, st); });
         } else {
-            run_local_swap(s, set, st.lpos, st.lpos2);
+            run_segment(STEP_LOCAL_SWAP, [&] { run_local_swap(s, set, st.lpos, st.lpos2); });
         }
     }
     flush();
@@ -598,10 +642,11 @@ inline void shard_top_amplitudes(qvg_state &s, ShardSet &set, uint32_t k, uint64
     const uint32_t kk = (uint32_t)std::min<uint64_t>(k, total);
     const bool dbl = S == 16;
     const unsigned grid = (unsigned)std::min<uint64_t>((local + 255) / 256, 4096);
-    // device scratch: histogram, candidate list, counters
-    unsigned int *d_hist = nullptr, *d_n = nullptr;
+    // device scratch: histogram (64-bit bins), candidate list, counters
+    unsigned long long *d_hist = nullptr;
+    unsigned int *d_n = nullptr;
     TopkEntry *d_out = nullptr;
-    cuda_throw(cudaMalloc(&d_hist, kTopkBins * sizeof(unsigned int)), "cudaMalloc(top-k hist)");
+    cuda_throw(cudaMalloc(&d_hist, kTopkBins * sizeof(unsigned long long)), "cudaMalloc(top-k hist)");
     cuda_throw(cudaMalloc(&d_n, sizeof(unsigned int)), "cudaMalloc(top-k count)");
     cuda_throw(cudaMalloc(&d_out, (size_t)kk * sizeof(TopkEntry)), "cudaMalloc(top-k out)");
     struct Free {
@@ -610,23 +655,23 @@ inline void shard_top_amplitudes(qvg_state &s, ShardSet &set, uint32_t k, uint64
             for (void *q : p) cudaFree(q);
         }
     } guard{{d_hist, d_n, d_out}};
-    std::vector<unsigned int> h(kTopkBins);
+    std::vector<unsigned long long> h(kTopkBins);
     static const int widths[6] = {11, 11, 11, 11, 11, 9};
-    uint64_t prefix = 0, needed = kk, tau = 0;
+    uint64_t prefix = 0, needed = kk;
     bool all_above = false;  // every key >= the selected bin's low edge is in
     int shift = 64;
     for (int level = 0; level < 6; ++level) {
         const int w = widths[level];
         shift -= w;
-        cuda_throw(cudaMemsetAsync(d_hist, 0, kTopkBins * sizeof(unsigned int), st), "memset hist");
+        cuda_throw(cudaMemsetAsync(d_hist, 0, kTopkBins * sizeof(unsigned long long), st), "memset hist");
         for (void *psi : set.bufs) {
             if (dbl) k_topk_hist<double><<<grid, 256, 0, st>>>(static_cast<const double2 *>(psi), local, prefix, shift, w, d_hist);
             else k_topk_hist<float><<<grid, 256, 0, st>>>(static_cast<const float2 *>(psi), local, prefix, shift, w, d_hist);
         }
         cuda_throw(cudaGetLastError(), "top-k hist launch");
         if (set.comm)
-            nccl_check(ncclAllReduce(d_hist, d_hist, kTopkBins, ncclUint32, ncclSum, set.comm, st), "ncclAllReduce(hist)");
-        cuda_throw(cudaMemcpyAsync(h.data(), d_hist, kTopkBins * sizeof(unsigned int), cudaMemcpyDeviceToHost, st),
+            nccl_check(ncclAllReduce(d_hist, d_hist, kTopkBins, ncclUint64, ncclSum, set.comm, st), "ncclAllReduce(hist)");
+        cuda_throw(cudaMemcpyAsync(h.data(), d_hist, kTopkBins * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st),
                    "D2H hist");
         cuda_throw(cudaStreamSynchronize(st), "top-k sync");
         uint64_t cum = 0;
@@ -642,19 +687,18 @@ inline void shard_top_amplitudes(qvg_state &s, ShardSet &set, uint32_t k, uint64
         prefix = (prefix << w) | (uint64_t)sel;
         if (h[sel] == needed) {  // the whole bin is in: no ties to break
             all_above = true;
-            needed = 0;
             break;
         }
     }
-    // keys strictly above tau are all in; `needed` keys equal to tau follow
-    if (all_above) {
-        const uint64_t low_edge = prefix << shift;
-        tau = low_edge == 0 ? 0 : low_edge - 1;
-        if (low_edge == 0) needed = 0;  // every key qualifies: handled by the tie path below
-    } else {
-        tau = prefix;
-    }
-    const bool take_all_zero = all_above && (prefix << shift) == 0;
+    // Collect every key > tau, then fill the remaining kk - |collected| slots
+    // with the keys == tie_key in ascending global index.
+    //   whole bin in, low edge e > 0: tau = e - 1 (keys >= e), no ties left;
+    //   whole bin in, low edge 0 (every key qualifies, e.g. k >= 2^n):
+    //     tau = 0 collects the nonzero keys, ties at key 0 fill the rest;
+    //   otherwise the full 64-bit key was selected: tau = prefix, ties at tau.
+    const uint64_t low_edge = all_above ? prefix << shift : prefix;
+    const uint64_t tau = all_above ? (low_edge == 0 ? 0 : low_edge - 1) : prefix;
+    const uint64_t tie_key = all_above ? 0 : prefix;
     std::vector<TopkEntry> cand;
     auto gather_rank_lists = [&](std::vector<TopkEntry> &mine) {
         if (!set.comm) return mine;
@@ -675,7 +719,7 @@ inline void shard_top_amplitudes(qvg_state &s, ShardSet &set, uint32_t k, uint64
             if (e.index != ~0ull) out.push_back(e);
         return out;
     };
-    if (!take_all_zero) {
+    {
         cuda_throw(cudaMemsetAsync(d_n, 0, sizeof(unsigned int), st), "memset count");
         for (size_t b = 0; b < set.bufs.size(); ++b) {
             const uint64_t base = (uint64_t)set.ranks[b] * local;
@@ -690,21 +734,22 @@ inline void shard_top_amplitudes(qvg_state &s, ShardSet &set, uint32_t k, uint64
         if (!mine.empty())
             cuda_throw(cudaMemcpy(mine.data(), d_out, mine.size() * sizeof(TopkEntry), cudaMemcpyDeviceToHost), "D2H");
         cand = gather_rank_lists(mine);
-    } else {
-        needed = kk;  // all keys are 0: the first kk indices
-        tau = 0;
     }
-    if (needed > 0) {  // ties at tau, by ascending global index
+    needed = cand.size() < kk ? kk - cand.size() : 0;
+    if (needed > 0) {  // ties at tie_key, by ascending global index
         constexpr uint64_t chunk = 1ull << 16;
         const uint64_t nchunks = (local + chunk - 1) / chunk;
         unsigned int *d_cnt = nullptr;
+        unsigned char *d_flags = nullptr;
         cuda_throw(cudaMalloc(&d_cnt, nchunks * sizeof(unsigned int)), "cudaMalloc(tie counts)");
+        cuda_throw(cudaMalloc(&d_flags, chunk), "cudaMalloc(tie flags)");
         std::vector<TopkEntry> ties;
         std::vector<unsigned int> cnt(nchunks);
+        std::vector<unsigned char> flags(chunk);
         std::vector<char> host((size_t)chunk * S);
         for (size_t b = 0; b < set.bufs.size() && ties.size() < needed; ++b) {
-            if (dbl) k_topk_tie_counts<double><<<(unsigned)nchunks, 256, 0, st>>>(static_cast<const double2 *>(set.bufs[b]), local, chunk, tau, d_cnt);
-            else k_topk_tie_counts<float><<<(unsigned)nchunks, 256, 0, st>>>(static_cast<const float2 *>(set.bufs[b]), local, chunk, tau, d_cnt);
+            if (dbl) k_topk_tie_counts<double><<<(unsigned)nchunks, 256, 0, st>>>(static_cast<const double2 *>(set.bufs[b]), local, chunk, tie_key, d_cnt);
+            else k_topk_tie_counts<float><<<(unsigned)nchunks, 256, 0, st>>>(static_cast<const float2 *>(set.bufs[b]), local, chunk, tie_key, d_cnt);
             cuda_throw(cudaGetLastError(), "tie count launch");
             cuda_throw(cudaMemcpyAsync(cnt.data(), d_cnt, nchunks * sizeof(unsigned int), cudaMemcpyDeviceToHost, st), "D2H");
             cuda_throw(cudaStreamSynchronize(st), "tie sync");
@@ -712,9 +757,15 @@ inline void shard_top_amplitudes(qvg_state &s, ShardSet &set, uint32_t k, uint64
             for (uint64_t c = 0; c < nchunks && ties.size() < needed; ++c) {
                 if (!cnt[c]) continue;
                 const uint64_t len = std::min(chunk, local - c * chunk);
-                cuda_throw(cudaMemcpy(host.data(), static_cast<char *>(set.bufs[b]) + c * chunk * S, len * S,
-                                      cudaMemcpyDeviceToHost), "D2H tie chunk");
+                if (dbl) k_topk_tie_flags<double><<<64, 256, 0, st>>>(static_cast<const double2 *>(set.bufs[b]), c * chunk, len, tie_key, d_flags);
+                else k_topk_tie_flags<float><<<64, 256, 0, st>>>(static_cast<const float2 *>(set.bufs[b]), c * chunk, len, tie_key, d_flags);
+                cuda_throw(cudaGetLastError(), "tie flags launch");
+                cuda_throw(cudaMemcpyAsync(flags.data(), d_flags, len, cudaMemcpyDeviceToHost, st), "D2H tie flags");
+                cuda_throw(cudaMemcpyAsync(host.data(), static_cast<char *>(set.bufs[b]) + c * chunk * S, len * S,
+                                           cudaMemcpyDeviceToHost, st), "D2H tie chunk");
+                cuda_throw(cudaStreamSynchronize(st), "tie chunk sync");
                 for (uint64_t j = 0; j < len && ties.size() < needed; ++j) {
+                    if (!flags[j]) continue;
                     double re, im;
                     if (dbl) {
                         re = reinterpret_cast<const double *>(host.data())[2 * j];
@@ -723,19 +774,22 @@ inline void shard_top_amplitudes(qvg_state &s, ShardSet &set, uint32_t k, uint64
                         re = reinterpret_cast<const float *>(host.data())[2 * j];
                         im = reinterpret_cast<const float *>(host.data())[2 * j + 1];
                     }
-                    const double p = re * re + im * im;
-                    uint64_t key;
-                    std::memcpy(&key, &p, sizeof(key));
-                    if (key == tau) ties.push_back(TopkEntry{base + c * chunk + j, re, im});
+                    ties.push_back(TopkEntry{base + c * chunk + j, re, im});
                 }
             }
         }
         cudaFree(d_cnt);
+        cudaFree(d_flags);
         // sharded: every rank offers its first ties; the lowest indices win below
         std::vector<TopkEntry> all_ties = gather_rank_lists(ties);
         cand.insert(cand.end(), all_ties.begin(), all_ties.end());
     }
-    auto prob = [](const TopkEntry &e) { return e.re * e.re + e.im * e.im; };
+    // |a|^2 without FMA contraction (volatile products), so the host orders
+    // candidates by the same rounded keys the device selected on
+    auto prob = [](const TopkEntry &e) {
+        volatile double rr = e.re * e.re, ii = e.im * e.im;
+        return rr + ii;
+    };
     std::sort(cand.begin(), cand.end(), [&](const TopkEntry &a, const TopkEntry &b) {
         const double pa = prob(a), pb = prob(b);
         return pa != pb ? pa > pb : a.index < b.index;

@@ -113,7 +113,7 @@ def test_virtual_shards_bit_identical(qv, oracle, world):
 
 @pytest.mark.parametrize("world", [2, 4, 8])
 def test_exchange_transports_bit_identical(qv, oracle, world):
-    """QVG_OPT_EXCHANGE 0 (swap kernel), 1 (k_xchg, split in two rank-role
+    """QVG_OPT_EXCHANGE 0 (copy transport: libqvg's chunk plan, D2D copies), 1 (k_xchg, split in two rank-role
     launches like the peer transport) and 2 (k_xchg fused with the gate that
     triggered the exchange, incl. local and global controls), with pairwise
     exchanges only (QVG_OPT_BATCH_EXCHANGE 1) or batched ones (k_mxchg, up to
@@ -134,6 +134,105 @@ def test_exchange_transports_bit_identical(qv, oracle, world):
                     assert s["exchanges"] > 0
                     if batch == 1:
                         assert (s["fused_exchanges"] > 0) == (mode == 2), (mode, s)
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_copy_transport_chunk_plan_on_device(qv, oracle, world):
+    """Exchange mode 0 on virtual shards runs the NCCL copy transport's chunk
+    plan (qvg_exchange_plan) with one D2D copy per chunk and side; chunks of
+    48 B / 4 KiB split every run, the default 256 MiB keeps them whole. Both
+    pairwise and batched exchanges stay bit-exact with the oracle."""
+    c = qv.u3_ladder_circuit(13, 4, 8)
+    want = oracle.simulate(13, gate_array(c))
+    for chunk in (48, 4096, 0):
+        for batch in (1, 4):
+            st = qv.StateVector.create_sharded(13, 128, 0, 0, world, None)
+            st.set_option(qv.OPT_EXCHANGE, 0)
+            st.set_option(qv.OPT_XCHG_CHUNK, chunk)
+            st.set_option(qv.OPT_BATCH_EXCHANGE, batch)
+            qv.apply_circuit(st, c)
+            assert st.stats()["exchanges"] > 0
+            assert np.array_equal(st.read_state(), want), (world, chunk, batch)
+    with pytest.raises(qv.ValidationError):
+        st.set_option(qv.OPT_XCHG_CHUNK, 40)
+
+
+def test_sharded_timing_splits_passes_and_exchanges(qv):
+    """QVG_OPT_TIMING on a sharded state times every segment with CUDA events:
+    local pass batches -> kernel_ms, exchanges -> exchange_ms."""
+    c = qv.u3_ladder_circuit(20, 3, 2)
+    st = qv.StateVector.create_sharded(20, 128, 0, 0, 4, None)
+    st.set_option(qv.OPT_TIMING, 1)
+    qv.apply_circuit(st, c)
+    s = st.stats()
+    assert s["exchanges"] > 0 and s["kernel_ms"] > 0 and s["exchange_ms"] > 0
+    u = qv.StateVector.create(20, 128, 0)
+    u.set_option(qv.OPT_TIMING, 1)
+    qv.apply_circuit(u, c)
+    assert u.stats()["kernel_ms"] > 0 and u.stats()["exchange_ms"] == 0
+
+
+def _hook_lib(qv):
+    import ctypes
+
+    lib = ctypes.CDLL(qv.LIBQVG)
+    fn_t = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint32,
+                            ctypes.c_uint32)
+    lib.qvg_set_step_hook.argtypes = [ctypes.c_void_p, fn_t, ctypes.c_void_p]
+    return lib, fn_t
+
+
+def test_step_hooks_barrier_stagger_and_fault(qv, oracle):
+    """The reference's ExecHooks tests (test_parallel.cpp:178-235) on the
+    sharded executor: (1) every rank's segment s ends before any rank's
+    segment s+1 starts, with rank 0 staggered by a sleep, and the result stays
+    bit-exact; (2) an injected fault on rank 1 at segment 2 fails the apply
+    with IoError and no later segment starts."""
+    import time
+
+    lib, fn_t = _hook_lib(qv)
+    c = qv.u3_ladder_circuit(12, 3, 4)
+    want = oracle.simulate(12, gate_array(c))
+    st = qv.StateVector.create_sharded(12, 128, 0, 0, 4, None)
+    start, end = {}, {}
+
+    def hook(user, rank, seg, typ, phase):
+        now = time.perf_counter()
+        if phase == 1 and rank == 0:
+            time.sleep(0.003)
+            now = time.perf_counter()
+        book = start if phase == 0 else end
+        if phase == 0:
+            book[seg] = min(book.get(seg, now), now)
+        else:
+            book[seg] = max(book.get(seg, now), now)
+        return 0
+
+    cb = fn_t(hook)
+    assert lib.qvg_set_step_hook(st.handle(), cb, None) == 0
+    qv.apply_circuit(st, c)
+    assert np.array_equal(st.read_state(), want)
+    assert len(start) == len(end) >= 3 and st.stats()["exchanges"] > 0
+    for k in range(len(start) - 1):
+        assert end[k] <= start[k + 1]
+
+    seen = []
+
+    def faulty(user, rank, seg, typ, phase):
+        seen.append((seg, rank, phase))
+        return 1 if (rank == 1 and seg == 2 and phase == 0) else 0
+
+    st2 = qv.StateVector.create_sharded(12, 128, 0, 0, 4, None)
+    cb2 = fn_t(faulty)
+    lib.qvg_set_step_hook(st2.handle(), cb2, None)
+    with pytest.raises(qv.IoError, match="injected fault"):
+        qv.apply_circuit(st2, c)
+    assert max(s for s, _, _ in seen) == 2
+    assert not any(s == 2 and p == 1 for s, _, p in seen)
+    assert lib.qvg_set_step_hook(st2.handle(), None, None) == 0  # removed: runs again
+    st2.init_basis(0)
+    qv.apply_circuit(st2, c)
+    assert np.array_equal(st2.read_state(), want)
 
 
 def test_exchange_fused_complex64(qv, oracle):

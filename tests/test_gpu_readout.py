@@ -71,3 +71,23 @@ def test_sharded_inner_equals_unsharded(qv):
         qv.apply_circuit(s, c)
     assert abs(sa.inner(sb) - ua.inner(ub)) <= 1e-13
     assert sa.max_deviation(sb) == ua.max_deviation(ub)
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_topk_whole_state_with_zero_amplitudes(qv, world):
+    """k >= 2^n on states with zero amplitudes: a basis state and a
+    GHZ state return every index, the nonzero ones first, then the zeros by
+    ascending index."""
+    st = (qv.StateVector.create(3, 128, 0) if world == 1
+          else qv.StateVector.create_sharded(3, 128, 0, 0, world, None))
+    assert [i for i, _ in st.top_amplitudes(8)] == list(range(8))
+    ghz = qv.parse_circuit("qubits 4\nh 0\ncx 0 1\ncx 1 2\ncx 2 3\n")
+    st = (qv.StateVector.create(4, 128, 0) if world == 1
+          else qv.StateVector.create_sharded(4, 128, 0, 0, world, None))
+    qv.apply_circuit(st, ghz)
+    for k in (16, 20):
+        got = st.top_amplitudes(k)
+        assert [i for i, _ in got] == [0, 15] + list(range(1, 15)), k
+        assert abs(got[0][1] - 2 ** -0.5) <= 1e-15 and got[2][1] == 0
+    st.init_basis(5)
+    assert [i for i, _ in st.top_amplitudes(16)] == [5] + [i for i in range(16) if i != 5]

@@ -152,6 +152,18 @@ def test_planner_bytes_and_fusion(qv):
     assert f == p and p < len(c3) / 8
 
 
+def test_planner_uses_engine_shape(qv):
+    """plan_passes plans with the engine's own defaults: complex64
+    tiles are 12 qubits, complex128 11, and complex128 states of <= 17 qubits
+    use 10-qubit tiles unless the caller picks a shape."""
+    h = lambda n, k: qv.parse_circuit(f"qubits {n}\n" + "\n".join(f"h {q}" for q in range(k)) + "\n").gates()
+    assert qv.plan_passes(20, h(20, 12), precision=64)[:2] == (1, 1)
+    assert qv.plan_passes(20, h(20, 12), precision=128)[:2] == (2, 1)
+    assert qv.plan_passes(16, h(16, 11))[:2] == (2, 1)                    # small state: 10-qubit tiles
+    assert qv.plan_passes(16, h(16, 11), tile_qubits=11)[:2] == (1, 1)    # caller's shape wins
+    assert qv.plan_passes(18, h(18, 11))[:2] == (1, 1)
+
+
 def test_planner_bit_exact_reorder(qv):
     # The default plan lets X/CX permutations and Z/CZ sign flips move past
     # ops on other qubits (bit-exact, qvg_plan.hpp reorder_for_tiles); the
@@ -180,7 +192,9 @@ def test_capi_exports_every_declared_symbol(qv):
     for name in names:
         assert hasattr(lib, name), name
     lib.qvg_abi_version.restype = ctypes.c_int
-    assert lib.qvg_abi_version() == qv.QVG_ABI_VERSION == 2
+    assert lib.qvg_abi_version() == qv.QVG_ABI_VERSION == 3
+    for name in ("qvg_exchange_plan", "qvg_set_step_hook"):
+        assert name in names
 
 
 @pytest.mark.skipif(cuda_present(), reason="checks the no-device error path")

@@ -21,6 +21,53 @@ STEP_DTYPE = np.dtype([("type", "<u4"), ("rank_mask", "<u4"), ("rank_value", "<u
 assert STEP_DTYPE.itemsize == 104
 
 
+XCHUNK_DTYPE = np.dtype([("round", "<u4"), ("partner", "<u4"), ("offset", "<u8"), ("bytes", "<u8")])
+assert XCHUNK_DTYPE.itemsize == 24
+
+
+def exchange_plan(n, world, rank, step, chunk_bytes, precision=128):
+    """libqvg's copy-transport chunk plan for one exchange step on one rank
+    (qvg_exchange_plan, the plan the NCCL and virtual-shard transports run)."""
+    import ctypes
+
+    import paper_2508_15545_b200 as qv
+
+    lib = ctypes.CDLL(qv.LIBQVG)
+    st = np.ascontiguousarray(np.asarray(step).reshape(1), STEP_DTYPE)
+    cnt = ctypes.c_uint64(0)
+    vp = ctypes.c_void_p
+    args = [ctypes.c_uint32(n), ctypes.c_uint32(world), ctypes.c_uint32(rank), ctypes.c_uint32(precision),
+            vp(st.ctypes.data), ctypes.c_uint64(chunk_bytes)]
+    rc = lib.qvg_exchange_plan(*args, None, ctypes.c_uint64(0), ctypes.byref(cnt))
+    if rc:
+        lib.qvg_last_error.restype = ctypes.c_char_p
+        raise ValueError(lib.qvg_last_error().decode())
+    out = np.zeros(cnt.value, XCHUNK_DTYPE)
+    rc = lib.qvg_exchange_plan(*args, vp(out.ctypes.data), ctypes.c_uint64(out.size), ctypes.byref(cnt))
+    assert rc == 0
+    return out
+
+
+def plan_exchange(n, world, shards, st, chunk_bytes):
+    """Execute one exchange step on in-process shards through libqvg's chunk
+    plans: chunk i of rank r and chunk i of its partner trade places (what the
+    NCCL transport's grouped send/recv does, and the virtual-shard copies)."""
+    raw = [s.view(np.uint8) for s in shards]
+    plans = [exchange_plan(n, world, r, st, chunk_bytes) for r in range(world)]
+    for r in range(world):
+        for i, c in enumerate(plans[r]):
+            p = int(c["partner"])
+            if p < r:
+                continue
+            d = plans[p][i]
+            assert int(d["partner"]) == r and d["bytes"] == c["bytes"] and d["round"] == c["round"]
+            a = slice(int(c["offset"]), int(c["offset"] + c["bytes"]))
+            b = slice(int(d["offset"]), int(d["offset"] + d["bytes"]))
+            tmp = raw[r][a].copy()
+            raw[r][a] = raw[p][b]
+            raw[p][b] = tmp
+
+
 def schedule(qv, circuit, world, canonicalize=True, batch=1):
     raw = qv.shard_schedule(circuit.n_qubits, world, circuit.gates(), canonicalize, batch)
     return np.frombuffer(raw.tobytes(), STEP_DTYPE)
@@ -83,15 +130,18 @@ def run_local_steps(oracle, L, shard, rank, steps):
             shard[:] = swap_local_bits(shard, int(st["lpos"]), int(st["lpos2"]))
 
 
-def emulate(oracle, n, world, steps):
-    """All shards in one process; exchange = swap of half-shards."""
+def emulate(oracle, n, world, steps, chunk_bytes=None):
+    """All shards in one process; exchange = swap of half-shards (or, with
+    chunk_bytes, libqvg's copy-transport chunk plan)."""
     g = int(np.log2(world))
     L = n - g
     shards = [np.zeros(1 << L, np.complex128) for _ in range(world)]
     shards[0][0] = 1.0
     half = 1 << (L - 1)
     for st in steps:
-        if st["type"] == 1:
+        if chunk_bytes is not None and st["type"] in (1, 3):
+            plan_exchange(n, world, shards, st, chunk_bytes)
+        elif st["type"] == 1:
             bit = 1 << (int(st["gpos"]) - L)
             lpos = int(st["lpos"])
             base = half_indices(L, lpos)
@@ -147,6 +197,57 @@ def test_schedule_emulated_bit_identical(qv, oracle, world, fn, args, batch):
     want = oracle.simulate(c.n_qubits, gate_array(c))
     got = emulate(oracle, c.n_qubits, world, steps)
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("chunk", [16, 48, 1 << 20])
+@pytest.mark.parametrize("batch", [1, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_copy_transport_plan_emulated_bit_identical(qv, oracle, world, batch, chunk):
+    """Every exchange executed through libqvg's chunk plan (qvg_exchange_plan,
+    the NCCL copy transport's send/recv list), with chunks that split runs
+    (16 / 48 B) or hold whole runs, reproduces the oracle bit for bit."""
+    for fn, args in [("u3_ladder_circuit", (10, 3, 5)), ("random_circuit", (9, 150, 2))]:
+        c = build(qv, fn, args)
+        steps = schedule(qv, c, world, batch=batch)
+        assert (steps["type"] == 1).any() or (steps["type"] == 3).any()
+        got = emulate(oracle, c.n_qubits, world, steps, chunk_bytes=chunk)
+        assert np.array_equal(got, oracle.simulate(c.n_qubits, gate_array(c))), (fn, world, batch, chunk)
+
+
+def test_copy_transport_plan_geometry(qv):
+    """The plan of one exchange: a pairwise step sends exactly the amplitudes
+    whose local bit lpos differs from the rank's gpos bit (2^(L-1) amplitudes,
+    runs of 2^lpos, split at chunk_bytes); a k-qubit batched step sends
+    (1 - 2^-k) of the shard in 2^k - 1 rounds, round t with rank ^ pdep(t)."""
+    n, world = 12, 4
+    L = 10
+    st = np.zeros(1, STEP_DTYPE)[0]
+    st["type"], st["gpos"], st["lpos"] = 1, 11, 7
+    for rank in range(world):
+        for chunk in (16, 1000 * 16, 1 << 20):
+            plan = exchange_plan(n, world, rank, st, chunk)
+            assert set(plan["partner"]) == {rank ^ 2} and set(plan["round"]) == {1}
+            assert plan["bytes"].max() <= chunk and plan["bytes"].sum() == (1 << (L - 1)) * 16
+            amps = np.concatenate([np.arange(o, o + b, 16) // 16 for o, b in zip(plan["offset"], plan["bytes"])])
+            sendbit = 0 if rank & 2 else 1
+            assert np.array_equal(amps, half_indices(L, 7) | (sendbit << 7))
+    mt = np.zeros(1, STEP_DTYPE)[0]
+    mt["type"], mt["gpos"], mt["lpos"], mt["lpos2"] = 3, 0b11, 9 | (8 << 8), 2
+    for rank in range(world):
+        plan = exchange_plan(n, world, rank, mt, 1 << 20)
+        assert list(np.unique(plan["round"])) == [1, 2, 3]
+        for t in (1, 2, 3):
+            part = plan[plan["round"] == t]
+            assert set(part["partner"]) == {rank ^ pdep(t, 0b11)}
+            amps = np.concatenate([np.arange(o, o + b, 16) // 16 for o, b in zip(part["offset"], part["bytes"])])
+            assert np.array_equal(amps, region(L, [9, 8], pext(rank, 0b11) ^ t))
+        assert plan["bytes"].sum() == (1 - 2 ** -2) * (1 << L) * 16
+    with pytest.raises(ValueError):
+        exchange_plan(n, world, 0, st, 8)            # chunk not a multiple of 16
+    bad = st.copy()
+    bad["gpos"] = 3                                  # a local qubit is not an exchange
+    with pytest.raises(ValueError):
+        exchange_plan(n, world, 0, bad, 1 << 20)
 
 
 def test_batched_exchange_moves_fewer_bytes(qv):
@@ -209,6 +310,81 @@ def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         return s.getsockname()[1]
+
+
+def _plan_worker(rank, world, port, fn, args, q, batch, chunk):
+    """One rank of the NCCL copy transport over gloo: every exchange step runs
+    libqvg's chunk plan for this rank (qvg_exchange_plan) — per chunk a
+    grouped isend of the chunk and irecv into a scratch buffer, then the
+    scratch copied into place, exactly the qvg_shard.hpp copy_exchange
+    sequence with NCCL replaced by gloo."""
+    import sys
+
+    import torch
+    import torch.distributed as dist
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    sys.path.insert(0, os.path.join(root, "tests"))
+    import paper_2508_15545_b200 as qv
+    from oracle.oracle import Oracle
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        oracle = Oracle()
+        c = build(qv, fn, args)
+        n = c.n_qubits
+        L = n - int(np.log2(world))
+        steps = schedule(qv, c, world, batch=batch)
+        shard = np.zeros(1 << L, np.complex128)
+        if rank == 0:
+            shard[0] = 1.0
+        raw = shard.view(np.uint8)
+        chunks = 0
+        for st in steps:
+            if st["type"] in (1, 3):
+                for ch in exchange_plan(n, world, rank, st, chunk):
+                    a, b = int(ch["offset"]), int(ch["offset"] + ch["bytes"])
+                    send = torch.from_numpy(raw[a:b].copy())
+                    scratch = torch.empty_like(send)
+                    reqs = [dist.isend(send, int(ch["partner"])), dist.irecv(scratch, int(ch["partner"]))]
+                    for r in reqs:
+                        r.wait()
+                    raw[a:b] = scratch.numpy()
+                    chunks += 1
+            else:
+                run_local_steps(oracle, L, shard, rank, [st])
+        parts = [torch.empty(2 << L, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(parts, torch.from_numpy(shard.view(np.float64).copy()))
+        if rank == 0:
+            got = np.concatenate([p.numpy().view(np.complex128) for p in parts])
+            want = oracle.simulate(n, gate_array(c))
+            q.put((bool(np.array_equal(got, want)), chunks))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,batch,chunk", [(2, 1, 48), (4, 1, 1 << 20), (4, 4, 64)])
+def test_gloo_copy_transport_plan_bit_identical(world, batch, chunk):
+    """The copy transport's libqvg chunk plan executed by real processes over
+    gloo (world 2 / 4, pairwise and batched exchanges) equals the oracle."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    for fn, args in [("u3_ladder_circuit", (10, 3, 5)), ("random_circuit", (8, 120, 4))]:
+        port = _free_port()
+        procs = [ctx.Process(target=_plan_worker, args=(r, world, port, fn, args, q, batch, chunk))
+                 for r in range(world)]
+        for p in procs:
+            p.start()
+        for p in procs:
+            p.join(180)
+            assert p.exitcode == 0
+        ok, chunks = q.get(timeout=10)
+        assert ok and chunks > 0, (fn, world, batch, chunk)
 
 
 def _worker(rank, world, port, fn, args, q, batch=1):
