@@ -45,11 +45,15 @@ def chunk_hashes(st, chunk=CHUNK):
     """sha256 of every `chunk`-amplitude slice of the state (complex128 host
     bytes), D2H of the next chunk overlapping the hashing of the previous."""
     total = 1 << st.n_qubits
-    offs = list(range(0, total, chunk))
-    with ThreadPoolExecutor(8) as pool:
-        futs = [pool.submit(lambda a: hashlib.sha256(a.tobytes()).hexdigest(), st.read_state(o, min(chunk, total - o)))
-                for o in offs]
-        return [f.result() for f in futs]
+    out, futs = [], []
+    with ThreadPoolExecutor(6) as pool:
+        for o in range(0, total, chunk):
+            if len(futs) >= 6:  # bound the host memory held by chunks in flight
+                out.append(futs.pop(0).result())
+            a = st.read_state(o, min(chunk, total - o))
+            futs.append(pool.submit(lambda a: hashlib.sha256(a.data).hexdigest(), a))
+        out += [f.result() for f in futs]
+    return out
 
 
 def circuit_of(qv, fx):
