@@ -15,7 +15,19 @@ top log2 N qubits trigger NVLink half-shard exchanges.
   --impl ours (default)  libqvg.so kernels
   --impl reference       the reference's own CPU engine (oracle/_ref, compiled
                          from /root/reference by oracle/Makefile) on the host
-                         cores, on a bounded sample of the same sweep.
+                         cores, on a bounded sample of the same sweep: one
+                         sweep gate per step in a fixed stratified order
+                         (U q, then 3 CX) that keeps the sweep's 1:3 mix
+                         exactly every 4 steps. It never imports the package:
+                         the 120 gate records come from the committed
+                         tests/golden/config2_haar_sweep_n30_ops.npy (sha256
+                         pinned in tests/golden/ref_full.json and checked
+                         against the package's builder by a CPU test).
+
+  --gpus N               N > 1 needs torchrun (one rank per GPU); without
+                         WORLD_SIZE the script re-launches itself under
+                         torch.distributed.run when N GPUs are visible, and
+                         fails (exit 2) when they are not.
 
 Inputs are synthetic and seeded (no dataset exists for this path); the state
 (16 GiB) is larger than L2 (126 MB), so no flush is needed between passes.
@@ -145,6 +157,22 @@ def algorithmic_bytes(n, rec, S=16):
     return min(b * max(1, 32 // run) if run < 32 else b, 2 * (1 << n) * S)
 
 
+def granule_bytes(n, rec, S=16):
+    """DRAM bytes a pass costs at the HBM3e access granularity measured with
+    ncu (profiles/r01_ncu_summary.md, per-gate rows): reads move whole 128-B
+    granules, writes 32-B sectors. A CX whose control-1 runs are 32 or 64 B
+    (control qubit 1 or 2 in complex128) therefore reads the whole state while
+    writing half; SURVEY §8d's sector rounding charges only half the reads."""
+    total = (1 << n) * S
+    kind = int(np.frombuffer(rec[:4].tobytes(), np.uint32)[0])
+    if kind == 0:
+        return 2 * total
+    run = (1 << int(np.frombuffer(rec[8:12].tobytes(), np.int32)[0])) * S
+    read = total if run < 128 else total // 2
+    write = total if run < 32 else total // 2
+    return read + write
+
+
 def gate_label(rec):
     """'U q' for a single-qubit op, 'CX c->t' style for a controlled one."""
     kind, target = (int(x) for x in np.frombuffer(rec[:8].tobytes(), np.uint32))
@@ -182,6 +210,8 @@ def run_ours(args, rank, world, dist):
         dist.broadcast_object_list(box, src=0)
         st = qv.StateVector.create_sharded(n, 128, dev, rank, world, box[0])
     st.set_option(qv.OPT_FUSE, 0)
+    if world > 1:  # CUDA events around every local-pass batch and every exchange (per rank)
+        st.set_option(qv.OPT_TIMING, 1)
     stream = torch.cuda.ExternalStream(st.stream(), device=dev)
     L = n - g
     # uniform start state with |a|^2 = 2^-n so no pass sees denormals/zeros
@@ -225,43 +255,22 @@ def run_ours(args, rank, world, dist):
         dist.barrier()
     total_ms = t_start.elapsed_time(t_end)
     stats = st.stats()
-    # per-launch durations from the interleaved events (same stream); N > 1
-    # records none (one call per step): the step's pass time is spread over
-    # the ops in proportion to their algorithmic bytes
+    # N = 1: per-launch durations from the interleaved events (same stream).
+    # N > 1: one call per step, timed per segment by the engine (local pass
+    # batches -> kernel_ms, exchanges -> exchange_ms); no per-gate times.
     per_op = np.zeros((args.steps, nops))
     if world == 1:
         for k in range(args.steps):
             for i in range(nops):
                 per_op[k, i] = evs[k][i].elapsed_time(evs[k][i + 1])
-    else:
-        lb = np.array([algorithmic_bytes(n - g, recs[i]) for i in range(nops)], dtype=np.float64)
-        per_op[:] = (total_ms / args.steps) * lb / lb.sum()
     if dist is not None:
         t = torch.tensor([total_ms], device=f"cuda:{dev}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_step = total_ms / args.steps
-    amps_per_gpu = 1 << L
     value = nops * (1 << n) / (ms_step / 1e3)
-    # roofline of the dominant kernel (largest share of the step's device time)
-    local_bytes = [algorithmic_bytes(L, recs[i]) for i in range(nops)]
-    kernels = [kernel_of(L, recs[i]) for i in range(nops)]
-    mean_op = per_op.mean(axis=0)
-    share = {}
-    for i in range(nops):
-        share.setdefault(kernels[i], [0.0, 0, 0])
-        share[kernels[i]][0] += mean_op[i]
-        share[kernels[i]][1] += local_bytes[i]
-        share[kernels[i]][2] += 1
-    dom = max(share, key=lambda k: share[k][0])
-    dom_ms, dom_bytes, dom_n = share[dom]
     hbm_peak, peak_kind = peaks()
-    achieved = (dom_bytes / dom_n) / ((dom_ms / dom_n) / 1e3) / 1e9
-    traffic, traffic_src = measured_traffic(dom)
-    for i in range(nops):  # per-op diagnostics (stderr): ms and algorithmic GB/s
-        print(f"op {i:3d} {kernels[i]:24s} {mean_op[i]:8.3f} ms {local_bytes[i] / (mean_op[i] / 1e3) / 1e9:8.1f} GB/s",
-              file=sys.stderr)
-    all_gbs = sum(local_bytes) / (mean_op.sum() / 1e3) / 1e9
+    local_bytes = [algorithmic_bytes(L, recs[i]) for i in range(nops)]
     line = {
         "metric": METRIC,
         "value": value,
@@ -275,35 +284,90 @@ def run_ours(args, rank, world, dist):
         "vs_baseline": None,
         "dtype": "c128 (f64)",
         "data": "synthetic (seeded Haar-random unitaries, mt19937_64 seed 2508)",
-        "config": {"workload": WORKLOAD, "n_qubits": n, "local_qubits": L, "precision": "complex128",
-                   "gate_passes_per_step": nops, "fusion": "off (one HBM pass per gate)",
-                   "l2": "state 16 GiB/GPU >> 126 MB L2; no flush needed", "parallelism": f"shard{world}"},
-        "hbm_gbs_step": all_gbs,
-        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak,
-                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm_peak,
-                     "traffic": traffic, "traffic_source": traffic_src,
-                     "algorithmic_bytes_per_launch": dom_bytes / dom_n,
-                     "launch_ms": dom_ms / dom_n, "share_of_step": dom_ms / mean_op.sum()},
-        "per_kernel": {k: {"launches_per_step": v[2], "ms_per_launch": v[0] / v[2],
-                           "gbs": (v[1] / v[2]) / ((v[0] / v[2]) / 1e3) / 1e9} for k, v in share.items()},
-        # per-gate time and HBM GB/s, individually
-        "per_gate": [{"op": i, "gate": gate_label(recs[i]), "ms": round(float(mean_op[i]), 4),
-                      "gbs": round(local_bytes[i] / (mean_op[i] / 1e3) / 1e9, 1)} for i in range(nops)],
-        "per_gate_timing": "CUDA events between launches" if world == 1 else
-                           "apportioned: N > 1 applies the whole sweep per call (exchange schedule with lookahead); "
-                           "the step time, exchanges included, is spread over the ops by algorithmic bytes",
+        "config": bench_config(n, L, world),
         "gpu_launches": int(stats["kernel_launches"]),
-        "exchanges_per_step": stats["exchanges"] / args.steps,
-        # N > 1: the exchange traffic's NVLink floor (per-GPU bytes sent at the
-        # measured 770 GB/s peer copy, B200_PROFILING.md) against the step
-        "exchange_roofline": None if world == 1 else {
-            "bound": "nvlink", "bytes_per_step_per_gpu": stats["exchange_bytes"] / args.steps,
-            "peak_gbs": 770.0, "peak_kind": "measured peer copy per direction (B200_PROFILING.md)",
-            "floor_ms": stats["exchange_bytes"] / args.steps / 770e9 * 1e3,
-            "floor_frac_of_step": (stats["exchange_bytes"] / args.steps / 770e9 * 1e3) / ms_step},
         "clocks": sampler.summary(),
     }
+    if world == 1:
+        kernels = [kernel_of(L, recs[i]) for i in range(nops)]
+        mean_op = per_op.mean(axis=0)
+        share = {}
+        for i in range(nops):
+            share.setdefault(kernels[i], [0.0, 0, 0])
+            share[kernels[i]][0] += mean_op[i]
+            share[kernels[i]][1] += local_bytes[i]
+            share[kernels[i]][2] += 1
+        dom = max(share, key=lambda k: share[k][0])
+        dom_ms, dom_bytes, dom_n = share[dom]
+        achieved = (dom_bytes / dom_n) / ((dom_ms / dom_n) / 1e3) / 1e9
+        traffic, traffic_src = measured_traffic(dom)
+        for i in range(nops):  # per-op diagnostics (stderr): ms and algorithmic GB/s
+            print(f"op {i:3d} {kernels[i]:24s} {mean_op[i]:8.3f} ms {local_bytes[i] / (mean_op[i] / 1e3) / 1e9:8.1f} GB/s",
+                  file=sys.stderr)
+        gran = [granule_bytes(L, recs[i]) for i in range(nops)]
+        dense = [i for i in range(nops) if kernels[i].endswith("/dense")]
+        t_dense = float(np.mean([mean_op[i] for i in dense]))
+        line.update({
+            "hbm_gbs_step": sum(local_bytes) / (mean_op.sum() / 1e3) / 1e9,
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak,
+                         "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm_peak,
+                         "traffic": traffic, "traffic_source": traffic_src,
+                         "algorithmic_bytes_per_launch": dom_bytes / dom_n,
+                         "launch_ms": dom_ms / dom_n, "share_of_step": dom_ms / mean_op.sum()},
+            # "quote the headline on dense 1q gates, where every
+            # definition coincides" (2^n amp-updates and 2*2^n*S bytes per pass)
+            "dense_1q": {"value": (1 << n) / (t_dense / 1e3), "unit": UNIT, "passes": len(dense),
+                         "ms_per_pass": t_dense, "gbs": 2 * (1 << n) * 16 / (t_dense / 1e3) / 1e9,
+                         "frac": 2 * (1 << n) * 16 / (t_dense / 1e3) / 1e9 / hbm_peak},
+            "per_kernel": {k: {"launches_per_step": v[2], "ms_per_launch": v[0] / v[2],
+                               "gbs": (v[1] / v[2]) / ((v[0] / v[2]) / 1e3) / 1e9} for k, v in share.items()},
+            # per-gate time and HBM GB/s, individually;
+            # granule-rounded bytes beside the sector-rounded ones where they differ
+            "per_gate": [dict({"op": i, "gate": gate_label(recs[i]), "ms": round(float(mean_op[i]), 4),
+                               "gbs": round(local_bytes[i] / (mean_op[i] / 1e3) / 1e9, 1)},
+                              **({"granule_gbs": round(gran[i] / (mean_op[i] / 1e3) / 1e9, 1),
+                                  "granule_frac": round(gran[i] / (mean_op[i] / 1e3) / 1e9 / hbm_peak, 3)}
+                                 if gran[i] != local_bytes[i] else {})) for i in range(nops)],
+            "per_gate_timing": "CUDA events between launches on the state's stream",
+            "granule_note": "granule_gbs: DRAM bytes at the measured access granularity (128-B reads, 32-B "
+                            "writes): CX with control qubit 1/2 (32/64-B runs) read the whole state",
+        })
+    else:
+        t = torch.tensor([stats["kernel_ms"] / args.steps, stats["exchange_ms"] / args.steps,
+                          stats["exchange_bytes"] / args.steps, stats["bytes_moved"] / args.steps],
+                         dtype=torch.float64, device=f"cuda:{dev}")
+        if dist is not None:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        k_ms, x_ms, x_bytes, hbm_bytes = (float(v) for v in t.tolist())
+        local_gbs = hbm_bytes / (k_ms / 1e3) / 1e9 if k_ms else None
+        x_gbs = x_bytes / (x_ms / 1e3) / 1e9 if x_ms else None
+        line.update({
+            # measured per rank with CUDA events around every local-pass batch
+            # (max over ranks); no per-gate split at N > 1
+            "roofline": {"bound": "hbm", "kernel": "local gate passes (all k_pairs classes, per rank)",
+                         "achieved": local_gbs, "peak": hbm_peak, "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": local_gbs / hbm_peak if local_gbs else None, "traffic": None,
+                         "local_ms_per_step": k_ms, "share_of_step": k_ms / ms_step if ms_step else None},
+            "per_gate": None,
+            "per_gate_timing": "N > 1: the whole sweep per call (exchange lookahead); segments timed by the "
+                               "engine (QVG_OPT_TIMING), not per gate",
+            "exchanges_per_step": stats["exchanges"] / args.steps,
+            "exchange": {"bound": "nvlink", "bytes_per_step_per_gpu": x_bytes, "ms_per_step": x_ms,
+                         "gbs_per_gpu": x_gbs, "peak_gbs": 900.0,
+                         "peak_kind": "NVLink 5 per direction per GPU (north_star)",
+                         "frac": x_gbs / 900.0 if x_gbs else None,
+                         "frac_of_measured_peer_copy": x_gbs / 770.0 if x_gbs else None,
+                         "transport": "peer-memory kernel (CUDA IPC) when peers map, else NCCL copy"},
+        })
     return st, circ, recs, line, n
+
+
+def bench_config(n, L, world):
+    """The `config` object both arms print (same keys, same values)."""
+    return {"workload": WORKLOAD if world == 1 else WORKLOAD.replace("n=30", f"n={n}"),
+            "n_qubits": n, "local_qubits": L, "precision": "complex128", "gate_passes_per_step": 120,
+            "fusion": "off (one HBM pass per gate)", "l2": "state 16 GiB/GPU >> 126 MB L2; no flush needed",
+            "parallelism": f"shard{world}"}
 
 
 def fused_leg(qv, st, circ, line, args):
@@ -398,10 +462,12 @@ def c64_leg(qv, circ, recs, line, args):
     del st
 
 
-def pcie_bidir_gbs(host, host2):
+def pcie_bidir_gbs(host, host2, chunks=E2E_CHUNKS):
     """The e2e roofline: pinned host<->device bandwidth with both directions
-    busy at once (what a pipelined e2e step needs), measured here with a
-    state-sized (16 GiB) copy each way on two streams."""
+    busy at once, measured the way the e2e step moves data — the state-sized
+    buffer in `chunks` cudaMemcpyAsync pieces per direction on two streams,
+    timed with CUDA events (start on one stream, the other waits on it; end =
+    the later of the two streams' end events). Best of 3."""
     import torch
 
     nbytes = host.numel() * host.element_size()
@@ -410,16 +476,25 @@ def pcie_bidir_gbs(host, host2):
     d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
     d2 = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
     s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    per = nbytes // chunks
     best = 0.0
-    for _ in range(2):
+    for _ in range(3):
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        with torch.cuda.stream(s1):
-            d.copy_(h, non_blocking=True)
-        with torch.cuda.stream(s2):
-            h2.copy_(d2, non_blocking=True)
+        t0 = torch.cuda.Event(enable_timing=True)
+        e1, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(s1)
+        s2.wait_event(t0)
+        for c in range(chunks):
+            sl = slice(c * per, (c + 1) * per if c + 1 < chunks else nbytes)
+            with torch.cuda.stream(s1):
+                d[sl].copy_(h[sl], non_blocking=True)
+            with torch.cuda.stream(s2):
+                h2[sl].copy_(d2[sl], non_blocking=True)
+        e1.record(s1)
+        e2.record(s2)
         torch.cuda.synchronize()
-        best = max(best, 2 * nbytes / (time.perf_counter() - t0) / 1e9)
+        ms = max(t0.elapsed_time(e1), t0.elapsed_time(e2))
+        best = max(best, 2 * nbytes / (ms / 1e3) / 1e9)
     del d, d2
     return best
 
@@ -445,13 +520,15 @@ def e2e_leg(qv, st, circ, recs, line, args):
         a = h.numpy().view(np.complex128)
         a[:] = 1.0 / math.sqrt(count)
         bufs.append((h, a))
-    # serial latency of one step
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    st.load_state(bufs[0][1])
-    m = qv.apply_circuit(st, circ)
-    st.read_into(bufs[0][1])
-    latency = (time.perf_counter() - t0) * 1e3
+    # serial latency of one step (best of 2)
+    latency = float("inf")
+    for _ in range(2):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        st.load_state(bufs[0][1])
+        m = qv.apply_circuit(st, circ)
+        st.read_into(bufs[0][1])
+        latency = min(latency, (time.perf_counter() - t0) * 1e3)
     # pipelined stream of steps over E2E_STATES device states, each copy in
     # E2E_CHUNKS pieces so the copy engines interleave H2D and D2H
     # (profiles/r01_e2e_ab.json: 3 states x 8 chunks 416 ms/step, 2 x 1 472)
@@ -474,12 +551,13 @@ def e2e_leg(qv, st, circ, recs, line, args):
     pcie = pcie_bidir_gbs(bufs[0][0], bufs[1][0])
     line["e2e"] = {"value": len(circ) * count / (ms / 1e3), "unit": UNIT, "ms_per_step": ms,
                    "pcie_bidir_gbs": pcie, "pcie_frac": (2 * count * 16 / (ms / 1e3) / 1e9) / pcie,
-                   "latency_ms": latency, "latency_value": len(circ) * count / (latency / 1e3),
+                   # one request alone, synchronous: load -> apply -> read
+                   "serial": {"value": len(circ) * count / (latency / 1e3), "unit": UNIT, "ms": latency},
                    "steps": steps, "h2d_bytes_per_step": count * 16, "d2h_bytes_per_step": count * 16,
                    "hbm_passes_per_step": m["traversals"],
                    "path": "per step: StateVector.load_async(pinned) -> apply_circuit(state, circuit) [API defaults: "
-                           f"gpu, fused] -> read_async(pinned); {E2E_STATES} states rotate, copies in "
-                           f"{E2E_CHUNKS} chunks, host wall clock"}
+                           f"gpu, fused] -> read_async(pinned); {E2E_STATES} states rotate (pipelined throughput), "
+                           f"copies in {E2E_CHUNKS} chunks, host wall clock; `serial` = one step alone"}
 
 
 def e2e_leg_sharded(qv, st, circ, line, args, rank, world, dist):
@@ -521,14 +599,54 @@ def e2e_leg_sharded(qv, st, circ, line, args, rank, world, dist):
                            "wall clock, max over ranks; bytes are whole-job totals"}
 
 
-def cpu_baseline(args, nops_hint=120):
-    """The reference engine (oracle/_ref) on the host cores: a bounded sample of
-    the same n=30 sweep (2 gate passes: a Haar U on q=0 and a CX), strategy
-    paired-cached-parallel, workers = host cores, block 65536, cache
-    workers x 64 MiB, store on /dev/shm (reference's RAM-disk setup)."""
-    from oracle.oracle import GATE_DTYPE, RefEngine, default_scratch
+SWEEP_OPS = os.path.join(ROOT, "tests", "golden", "config2_haar_sweep_n30_ops.npy")
+SWEEP_FIXTURE = os.path.join(ROOT, "tests", "golden", "ref_full.json")
 
-    import paper_2508_15545_b200 as qv
+
+def sweep_ops():
+    """The config-2 sweep's 120 qvg_gate records (Haar U on q = 0..29, then 90
+    CX) from the committed fixture — the reference arm and the cpu_baseline
+    leg never import the package. sha256 pinned in ref_full.json (and
+    tests/test_oracle.py checks the package's builder emits the same bytes)."""
+    import hashlib
+
+    from oracle.oracle import GATE_DTYPE
+
+    ops = np.load(SWEEP_OPS)
+    with open(SWEEP_FIXTURE) as f:
+        want = json.load(f)["config2_haar_sweep_n30"]["ops_sha256"]
+    if hashlib.sha256(ops.tobytes()).hexdigest() != want:
+        raise RuntimeError(f"{SWEEP_OPS} does not match its pinned sha256")
+    return np.ascontiguousarray(ops, GATE_DTYPE)
+
+
+def stratified_order(n_u=30, n_cx=90):
+    """Gate order for one-gate steps that keeps the sweep's 1 U : 3 CX mix
+    exactly in every 4 consecutive steps: U0, CX0, CX1, CX2, U1, CX3, ...
+    (indices into the sweep; a full cycle is the whole sweep once)."""
+    per = n_cx // n_u
+    order = []
+    for q in range(n_u):
+        order.append(q)
+        order += [n_u + per * q + j for j in range(per)]
+    return order
+
+
+def ref_store_ok(scratch, n):
+    try:
+        st_ = os.statvfs(scratch)
+        return st_.f_bavail * st_.f_frsize >= (16 << n) * 1.1
+    except OSError:
+        return True
+
+
+def cpu_baseline(args):
+    """The reference engine (oracle/_ref) on the host cores: a bounded sample of
+    the same n=30 sweep — its first 4 gates in the stratified order (Haar U on
+    q=0 and the CX 0->1, 0->15, 0->29: the sweep's 1:3 mix), strategy
+    paired-cached-parallel, workers = host cores, block 65536, cache
+    workers x 64 MiB, store on /dev/shm (the reference's RAM-disk setup)."""
+    from oracle.oracle import RefEngine, default_scratch
 
     if not RefEngine.available():
         return None
@@ -536,38 +654,34 @@ def cpu_baseline(args, nops_hint=120):
     n = N_QUBITS
     cores = os.cpu_count() or 1
     scratch = default_scratch()
-    try:
-        st_ = os.statvfs(scratch)
-        if st_.f_bavail * st_.f_frsize < (16 << 30) * 1.1:
-            return {"value": None, "unit": UNIT, "cores": cores, "kind": "reference",
-                    "sample": f"skipped: {scratch} has < 17.6 GB free for the n=30 store"}
-    except OSError:
-        pass
-    circ = qv.haar_sweep_circuit(n, SEED)
-    ops = np.frombuffer(circ.gates().tobytes(), dtype=GATE_DTYPE)
-    sample = np.concatenate([ops[0:1], ops[30:31]])
-    best = float("inf")
+    if not ref_store_ok(scratch, n):
+        return {"value": None, "unit": UNIT, "cores": cores, "kind": "reference",
+                "sample": f"skipped: {scratch} has < 17.6 GB free for the n=30 store"}
+    ops = sweep_ops()
+    sample = ops[stratified_order()[:4]]
     with eng.store(n, 65536, 0, scratch) as store:
         store.apply(sample[:1], "paired-cached-parallel", cores, cores * (64 << 20))  # touch every page
-        for _ in range(2):
-            wall = store.apply(sample, "paired-cached-parallel", cores, cores * (64 << 20))
-            best = min(best, wall)
+        wall = store.apply(sample, "paired-cached-parallel", cores, cores * (64 << 20))
         # also the single-threaded column (the paper's 1-worker
         # paired_cached with a 64 MiB window), one gate pass
         single = store.apply(sample[:1], "paired-cached", 1, 64 << 20)
-    return {"value": len(sample) * (1 << n) / (best / 1e3), "unit": UNIT, "cores": cores, "kind": "reference",
-            "ms_per_gate": best / len(sample),
-            "sample": "2 gate passes of the n=30 sweep (Haar U q=0, CX 0->1), paired-cached-parallel, "
-                      f"workers={cores}, block_amps=65536, store on {scratch}, min of 2",
+    return {"value": len(sample) * (1 << n) / (wall / 1e3), "unit": UNIT, "cores": cores, "kind": "reference",
+            "ms_per_gate": wall / len(sample),
+            "sample": "4 gate passes of the n=30 sweep (Haar U q=0, CX 0->1, 0->15, 0->29: the sweep's 1:3 mix), "
+                      f"paired-cached-parallel, workers={cores}, block_amps=65536, store on {scratch}",
             "single_thread": {"value": (1 << n) / (single / 1e3), "unit": UNIT, "cores": 1, "ms_per_gate": single,
                               "sample": "1 gate pass (Haar U q=0), paired-cached, 1 worker, 64 MiB window"}}
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the reference's CPU path on the host cores."""
-    from oracle.oracle import GATE_DTYPE, RefEngine, default_scratch
-
-    import paper_2508_15545_b200 as qv
+    """--impl reference: the reference's own CPU engine (oracle/_ref) on the
+    host cores, through its public apply_circuit with a QVSV store on
+    /dev/shm. One sweep gate per step in stratified_order (the sweep's exact
+    1:3 U:CX mix every 4 steps; the timed steps start at the cycle's start),
+    value = amp-updates per gate pass / time, the same metric, unit and config
+    object as our arm. Rank 0 only under torchrun; the state is n = 30 for
+    every N (the CPU holds one 16 GiB store)."""
+    from oracle.oracle import RefEngine, default_scratch
 
     if rank != 0:
         return None
@@ -577,25 +691,92 @@ def run_reference(args, rank, world):
     n = N_QUBITS
     cores = os.cpu_count() or 1
     scratch = default_scratch()
-    circ = qv.haar_sweep_circuit(n, SEED)
-    ops = np.frombuffer(circ.gates().tobytes(), dtype=GATE_DTYPE)
+    if not ref_store_ok(scratch, n):
+        return {"impl": "reference", "unavailable": f"{scratch} has < 17.6 GB free for the n=30 reference store"}
+    ops = sweep_ops()
+    order = stratified_order()
     walls = []
     with eng.store(n, 65536, 0, scratch) as store:
-        for k in range(args.warmup + args.steps):
-            op = ops[(k * 7) % len(ops):(k * 7) % len(ops) + 1]  # one sweep gate per step, rotating
-            w = store.apply(op, "paired-cached-parallel", cores, cores * (64 << 20))
-            if k >= args.warmup:
-                walls.append(w)
+        for k in range(args.warmup):
+            store.apply(ops[[order[(len(order) - args.warmup + k) % len(order)]]], "paired-cached-parallel", cores,
+                        cores * (64 << 20))
+        for k in range(args.steps):
+            walls.append(store.apply(ops[[order[k % len(order)]]], "paired-cached-parallel", cores,
+                                     cores * (64 << 20)))
     ms = sum(walls) / len(walls)
     value = (1 << n) / (ms / 1e3)
+    sample = (f"{args.steps} steps of 1 sweep gate each (order U0,CX,CX,CX,U1,...: the sweep's 1:3 mix"
+              f"{' exactly' if args.steps % 4 == 0 else ''}), reference apply_circuit paired-cached-parallel, "
+              f"workers={cores}, block_amps=65536, store on {scratch}; Metrics.wall_ms per step; the CPU runs "
+              f"the n=30 sweep (2^30 amplitudes, the per-GPU shard size) at every N")
     return {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "n_qubits": n, "precision": "complex128"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
-                             "sample": f"1 gate pass of the n=30 sweep per step (rotating), reference "
-                                       f"paired-cached-parallel, workers={cores}, store on {scratch}"},
+            "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)",
+            "data": "synthetic (seeded Haar-random unitaries, mt19937_64 seed 2508; committed gate records)",
+            "config": bench_config(n + int(math.log2(world)), n, world),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def config4_leg(qv, line, args, rank, world, dist):
+    """BASELINE config 4 (weak scaling): the U3 + CX-ladder layer circuit (20
+    layers) at n = 32 + log2 N, a 64 GiB complex128 shard per GPU, through the
+    API defaults (fused passes; global-qubit gates trigger exchanges over
+    peer memory / NCCL). value = ops * 2^n / t_step (whole job), CUDA events on
+    the state's stream, max over ranks. At N > 1 the engine times every
+    local-pass batch and exchange (QVG_OPT_TIMING)."""
+    import torch
+
+    g = int(math.log2(world))
+    n = 32 + g
+    dev = torch.cuda.current_device()
+    free, _ = torch.cuda.mem_get_info(dev)
+    if free < (16 << (n - g)) * 1.05:
+        line["config4"] = {"skipped": f"needs {(16 << (n - g)) / 2**30:.0f} GiB free, {free / 2**30:.0f} GiB free"}
+        return
+    c = qv.u3_ladder_circuit(n, 20, 1)
+    if world == 1:
+        st = qv.StateVector.create(n, 128, dev)
+    else:
+        box = [qv.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        st = qv.StateVector.create_sharded(n, 128, dev, rank, world, box[0])
+        st.set_option(qv.OPT_TIMING, 1)
+    stream = torch.cuda.ExternalStream(st.stream(), device=dev)
+    qv.apply_circuit(st, c)  # warm-up (plans, exchange mappings)
+    st.sync()
+    st.reset_stats()
+    steps = max(1, min(args.steps, 3))
+    if dist is not None:
+        dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        qv.apply_circuit(st, c, sync=False)
+    b.record(stream)
+    st.sync()
+    ms = a.elapsed_time(b) / steps
+    s = st.stats()
+    vals = [ms, s["kernel_ms"] / steps, s["exchange_ms"] / steps, s["exchange_bytes"] / steps]
+    if dist is not None:
+        t = torch.tensor(vals, dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        vals = [float(v) for v in t.tolist()]
+    ms, k_ms, x_ms, x_bytes = vals
+    out = {"workload": f"config4: U3 layers + CX ladder, 20 layers, n={n} ({world} x 64 GiB c128 shards), "
+                       "API defaults (fused, exchanges)",
+           "value": len(c) * (1 << n) / (ms / 1e3), "unit": UNIT, "ms_per_step": ms, "steps": steps,
+           "ops": len(c), "passes_per_step": s["passes"] / steps, "exchanges_per_step": s["exchanges"] / steps,
+           "hbm_gbs_per_gpu": s["bytes_moved"] / steps / (ms / 1e3) / 1e9,
+           "timing": "CUDA events on the state's stream around the steps (the circuit applied again to the "
+                     "evolving state each step), max over ranks"}
+    if world > 1:
+        out["exchange"] = {"bytes_per_step_per_gpu": x_bytes, "ms_per_step": x_ms,
+                           "gbs_per_gpu": x_bytes / (x_ms / 1e3) / 1e9 if x_ms else None, "peak_gbs": 900.0,
+                           "frac": x_bytes / (x_ms / 1e3) / 1e9 / 900.0 if x_ms else None,
+                           "local_pass_ms_per_step": k_ms}
+    line["config4"] = out
+    del st
 
 
 def configs_mode(args):
@@ -666,6 +847,31 @@ def configs_mode(args):
                           "cpu_reference": cpu}), flush=True)
 
 
+def relaunch_or_fail(args):
+    """--gpus N > 1 without torchrun: re-launch under torch.distributed.run
+    with N ranks when N GPUs are visible; otherwise fail loudly (a one-GPU run
+    must never print n_gpus: 1 for --gpus N)."""
+    try:
+        import torch
+
+        have = torch.cuda.device_count()
+    except Exception:
+        have = 0
+    if have < args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} requested but {have} CUDA device(s) visible"}), flush=True)
+        sys.exit(2)
+    import socket
+    import subprocess
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ, NCCL_DEBUG=os.environ.get("NCCL_DEBUG", "INFO"))
+    sys.exit(subprocess.call(cmd, env=env))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -674,6 +880,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-config4", action="store_true")
     ap.add_argument("--configs", action="store_true", help="per-config lines (C0..C4) instead of the headline")
     args = ap.parse_args()
     if args.configs:
@@ -681,8 +888,16 @@ def main():
         return
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus < 1 or args.gpus & (args.gpus - 1):
+        ap.error("--gpus must be a power of two")
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is None and args.gpus > 1 and args.impl == "ours":
+        relaunch_or_fail(args)
+    world = int(env_world or "1")
     rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus and args.impl == "ours":
+        print(json.dumps({"error": f"WORLD_SIZE={world} but --gpus {args.gpus}"}), flush=True)
+        sys.exit(2)
     dist = None
     if args.impl == "reference":
         line = run_reference(args, rank, world)
@@ -693,6 +908,7 @@ def main():
         import torch
         import torch.distributed as tdist
 
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # the communicator lines show the N ranks
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
         tdist.init_process_group("nccl")
         dist = tdist
@@ -706,6 +922,12 @@ def main():
         c64_leg(qv, circ, recs, line, args)
     elif not args.no_e2e:
         e2e_leg_sharded(qv, st, circ, line, args, rank, world, dist)
+    del st
+    if not args.no_config4:
+        try:
+            config4_leg(qv, line, args, rank, world, dist)
+        except Exception as exc:  # keep the headline line if the 64 GiB leg cannot run
+            line["config4"] = {"error": str(exc)[:200]}
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
             try:

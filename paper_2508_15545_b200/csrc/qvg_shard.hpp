@@ -517,7 +517,7 @@ inline void run_steps(qvg_state &s, ShardSet &set, const std::vector<ShardStep> 
         work();
         if (timed) {
             cuda_throw(cudaEventRecord(ev[1], st), "cudaEventRecord");
-            shard_time_push(s, ev[0], ev[1], type == STEP_LOCAL ? 0 : 1);
+            shard_time_push(s, ev[0], ev[1], (type == STEP_EXCHANGE || type == STEP_MULTI_EXCHANGE) ? 1 : 0);
         }
         if (hooked) {
             cuda_throw(cudaStreamSynchronize(st), "hooked segment sync");
