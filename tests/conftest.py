@@ -6,6 +6,14 @@ import sys
 import numpy as np
 import pytest
 
+try:
+    # torch first: once libqvg.so has mapped libcudart, `import torch` preloads
+    # every CUDA wheel library, and on a host without a driver one of those
+    # crashes the process (the GPU box is unaffected). Tests import torch lazily.
+    import torch  # noqa: F401
+except Exception:  # pragma: no cover
+    pass
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)

@@ -27,6 +27,10 @@ def run_isolated(body, tmp_path):
         pytest.fail("reference drop-in not built: make -C oracle dropin (needs /root/reference once)")
     code = textwrap.dedent("""
         import math, os, sys
+        try:  # torch before any CUDA library of ours: on a box without a driver, torch's import
+            import torch  # noqa: F401  segfaults once libcudart is already mapped
+        except Exception:
+            pass
         sys.path.insert(0, {dropin!r})
         import qvsim
         assert qvsim.__file__.startswith({dropin!r}), qvsim.__file__
