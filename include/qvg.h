@@ -96,8 +96,10 @@ enum qvg_option {
                                 NOT bit-identical to the reference), 0 = circuit order */
     QVG_OPT_CLASSES = 16,    /* fused tile: 1 = structured-matrix op bodies (real, X, entries +-1/2, Z),
                                 same values with fewer FP64 instructions (default); 0 = general bodies */
-    QVG_OPT_XCHG_CHUNK = 17  /* sharded: copy-transport chunk bytes (multiple of 16; 0 = default 256 MiB,
+    QVG_OPT_XCHG_CHUNK = 17, /* sharded: copy-transport chunk bytes (multiple of 16; 0 = default 256 MiB,
                                 capped by the NCCL scratch); tests use small chunks to split runs */
+    QVG_OPT_PIPE = 18        /* fused tiles: 2 or 3 = warp-specialised bulk-copy pipeline (k_tile_pipe) with
+                                that many shared-memory ring stages (default 2); 0 = k_tile (per-thread loads) */
 };
 
 /* Counters (the reference's Metrics, metrics.hpp:14-30, plus the GPU pass

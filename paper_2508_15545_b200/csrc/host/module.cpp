@@ -463,4 +463,5 @@ PYBIND11_MODULE(_core, m) {
     m.attr("OPT_REORDER") = (int)QVG_OPT_REORDER;
     m.attr("OPT_CLASSES") = (int)QVG_OPT_CLASSES;
     m.attr("OPT_XCHG_CHUNK") = (int)QVG_OPT_XCHG_CHUNK;
+    m.attr("OPT_PIPE") = (int)QVG_OPT_PIPE;
 }

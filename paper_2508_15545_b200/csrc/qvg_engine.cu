@@ -107,6 +107,7 @@ struct qvg_state {
     bool graph = false;        // QVG_OPT_GRAPH: replay repeated op lists as captured CUDA graphs
     uint32_t reorder = REORDER_EXACT;  // QVG_OPT_REORDER: commutation-aware fusion order (qvg_plan.hpp)
     bool classes = true;       // QVG_OPT_CLASSES: structured-matrix op bodies in fused tiles
+    uint32_t pipe_stages = 2;  // QVG_OPT_PIPE: fused tiles through the bulk-copy pipeline (k_tile_pipe), ring stages; 0 = k_tile
     bool shape_set = false;    // tile_qubits / sub_bits set by the caller (no small-state default)
     struct GraphEntry {
         uint64_t key = 0;
@@ -227,22 +228,28 @@ void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *recs) {
     thread_local TileParams prm;  // 25 KB; the launch copies it into the parameter block (per host thread: states on different threads may launch concurrently)
     prm.g = g;
     std::memcpy(prm.ops, recs + p.op_begin, sizeof(TileOp) * g.nrec);
-    const unsigned threads = 1u << (g.k - g.sub);  // one 2^sub-amplitude subcube per thread
+    unsigned threads = 1u << (g.k - g.sub);  // one 2^sub-amplitude subcube per thread
     const bool pf = s.prefetch_mode == 1 && g.sub == 3;  // register prefetch needs the 8-amplitude subcube
-    const size_t smem = (((sizeof(uint64_t) << g.nhi) + 15) & ~size_t(15)) +
-                        (g.ngroups > 1 || g.stage ? (sizeof(T) << g.k) : 0);
+    size_t smem = (((sizeof(uint64_t) << g.nhi) + 15) & ~size_t(15)) +
+                  (g.ngroups > 1 || g.stage ? (sizeof(T) << g.k) : 0);
     const bool fma = s.fma && sizeof(R) == 8;  // complex64 always contracts
     const bool small = threads <= 256;
     const bool tiny = threads <= 128;  // sub 4 at k <= 11: 128-thread CTAs
+    // the bulk-copy pipeline serves 128-thread tiles (every default shape)
+    const int pipe = (s.pipe_stages > 0 && threads == (unsigned)kPipeConsumers && !pf) ? (int)s.pipe_stages : 0;
+    if (pipe) {
+        threads = kPipeThreads;
+        smem = pipe_smem_bytes(g.nhi, g.k, (int)sizeof(T), pipe >= 3 ? 3 : 2);
+    }
     // Passes without structured ops (classes off) use the REAL-set kernel:
     // their records only name general bodies, which every set compiles.
     const int set_idx = class_set_index(g.cls_set);
-    const TileKernel<R> kern = tile_kernel<R>(set_idx, TileVariant{g.sub, tiny, small, fma, pf});
+    const TileKernel<R> kern = tile_kernel<R>(set_idx, TileVariant{g.sub, tiny, small, fma, pf, pipe});
     // The shared-memory opt-in is a per-device function attribute: set it once
     // per (device, variant).
-    static std::atomic<uint64_t> attr_set[64][4][2];  // [device][class set][variant / 64]: a bit per variant
+    static std::atomic<uint64_t> attr_set[64][4][4];  // [device][class set][variant / 64]: a bit per variant
     const int variant = (sizeof(R) == 8 ? 1 : 0) | (g.sub == 4 ? 2 : 0) | (fma ? 4 : 0) | (small ? 8 : 0) |
-                        (pf ? 16 : 0) | (tiny ? 32 : 0) | (g.sub == 5 ? 64 : 0);
+                        (pf ? 16 : 0) | (tiny ? 32 : 0) | (g.sub == 5 ? 64 : 0) | (pipe ? (pipe >= 3 ? 256 : 128) : 0);
     std::atomic<uint64_t> &set = attr_set[s.device & 63][set_idx][variant >> 6];
     const uint64_t bit = 1ull << (variant & 63);
     if (!(set.load(std::memory_order_acquire) & bit)) {
@@ -336,7 +343,7 @@ uint64_t plan_signature(const qvg_state &s) {
     auto mix = [&](uint64_t v) { h = (h ^ v) * 1099511628211ull; };
     mix(s.fuse); mix(s.tile_qubits); mix(s.carriers); mix(s.low_kernel); mix(s.min_run); mix(s.pred_store);
     mix(s.sub_bits); mix(s.fma); mix(s.stage_bits); mix((uint64_t)s.prefetch_mode); mix(s.L); mix(s.precision);
-    mix(s.reorder); mix(s.classes); mix(s.shape_set);
+    mix(s.reorder); mix(s.classes); mix(s.shape_set); mix(s.pipe_stages);
     return h;
 }
 
@@ -596,6 +603,10 @@ int qvg_set_option(qvg_state *s, int key, int64_t value) {
         case QVG_OPT_EXCHANGE:
             if (value < -1 || value > 2) throw Validation("exchange mode must be -1, 0, 1 or 2");
             s->exchange_mode = (int)value;
+            break;
+        case QVG_OPT_PIPE:
+            if (value < 0 || value > 3 || value == 1) throw Validation("pipe must be 0 (k_tile), 2 or 3 ring stages");
+            s->pipe_stages = (uint32_t)value;
             break;
         case QVG_OPT_XCHG_CHUNK:
             if (value < 0 || (value % 16) != 0) throw Validation("exchange chunk must be a multiple of 16 bytes (0 = default)");
