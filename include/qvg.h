@@ -88,8 +88,9 @@ enum qvg_option {
                                     pairwise exchanges only) */
     QVG_OPT_STAGE = 13,      /* fused tile: a first/last register group holding tile bits 0..b-1 moves
                                 its HBM data through shared memory, coalesced (default b = 3; 0 never) */
-    QVG_OPT_GRAPH = 14,      /* 1: unsharded states replay a repeated op list as a captured CUDA graph
-                                (no per-pass host planning/launch cost; default 0) */
+    QVG_OPT_GRAPH = 14,      /* unsharded states: replay an op list as a captured CUDA graph (no per-pass host
+                                planning / launch cost): 2 = auto (default; lists of >= 8 ops, from their second
+                                apply on this state), 1 = every list, 0 = never */
     QVG_OPT_REORDER = 15,    /* fusion may move an op ahead of ops on disjoint qubits (fewer passes):
                                 2 = only moves that keep every bit (an X/CX permutation or a Z/CZ sign
                                 flip on either side; default), 1 = any such move (mathematically equal,
@@ -115,6 +116,7 @@ typedef struct qvg_stats {
     double kernel_ms;        /* device time of gate passes (QVG_OPT_TIMING states only) */
     double exchange_ms;      /* device time of exchanges (QVG_OPT_TIMING, sharded states) */
     uint64_t fused_exchanges; /* exchanges that also applied the gate that caused them (k_xchg) */
+    uint64_t graph_replays;   /* applies that ran as a captured CUDA graph (QVG_OPT_GRAPH) */
 } qvg_stats;
 
 typedef struct qvg_state qvg_state;

@@ -64,6 +64,7 @@ py::dict stats_dict(const qvg_stats &s) {
     d["kernel_ms"] = s.kernel_ms;
     d["exchange_ms"] = s.exchange_ms;
     d["fused_exchanges"] = s.fused_exchanges;
+    d["graph_replays"] = s.graph_replays;
     return d;
 }
 

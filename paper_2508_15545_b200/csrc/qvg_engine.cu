@@ -104,7 +104,9 @@ struct qvg_state {
     int prefetch_mode = 0;     // fused tile next-tile prefetch (QVG_OPT_PREFETCH): 1 = into registers
     uint32_t batch_max = 4;    // sharded: most global qubits one exchange swaps (QVG_OPT_BATCH_EXCHANGE)
     uint32_t stage_bits = 3;   // fused tile: stage first/last group HBM access through shared memory (QVG_OPT_STAGE)
-    bool graph = false;        // QVG_OPT_GRAPH: replay repeated op lists as captured CUDA graphs
+    uint32_t graph_mode = 2;   // QVG_OPT_GRAPH: 0 never, 1 capture every op list, 2 auto (default):
+                               // capture an op list of >= kGraphMinOps ops the second time it is applied
+    std::vector<uint64_t> graph_seen;  // auto mode: keys applied once (ring)
     uint32_t reorder = REORDER_EXACT;  // QVG_OPT_REORDER: commutation-aware fusion order (qvg_plan.hpp)
     bool classes = true;       // QVG_OPT_CLASSES: structured-matrix op bodies in fused tiles
     uint32_t pipe_stages = 2;  // QVG_OPT_PIPE: fused tiles through the bulk-copy pipeline (k_tile_pipe), ring stages; 0 = k_tile
@@ -247,7 +249,7 @@ void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *recs) {
     const TileKernel<R> kern = tile_kernel<R>(set_idx, TileVariant{g.sub, tiny, small, fma, pf, pipe});
     // The shared-memory opt-in is a per-device function attribute: set it once
     // per (device, variant).
-    static std::atomic<uint64_t> attr_set[64][4][4];  // [device][class set][variant / 64]: a bit per variant
+    static std::atomic<uint64_t> attr_set[64][4][8];  // [device][class set][variant / 64]: a bit per variant
     const int variant = (sizeof(R) == 8 ? 1 : 0) | (g.sub == 4 ? 2 : 0) | (fma ? 4 : 0) | (small ? 8 : 0) |
                         (pf ? 16 : 0) | (tiny ? 32 : 0) | (g.sub == 5 ? 64 : 0) | (pipe ? (pipe >= 3 ? 256 : 128) : 0);
     std::atomic<uint64_t> &set = attr_set[s.device & 63][set_idx][variant >> 6];
@@ -348,11 +350,19 @@ uint64_t plan_signature(const qvg_state &s) {
 }
 
 uint64_t ops_hash(const qvg_gate *ops, uint64_t count, uint64_t seed) {
+    // 8 bytes per step (an op is 80 B): a lookup key; entries also compare the bytes
     uint64_t h = seed;
-    const auto *b = reinterpret_cast<const unsigned char *>(ops);
-    for (uint64_t i = 0; i < count * sizeof(qvg_gate); ++i) h = (h ^ b[i]) * 1099511628211ull;
+    const auto *w = reinterpret_cast<const unsigned char *>(ops);
+    for (uint64_t i = 0; i < count * sizeof(qvg_gate); i += 8) {
+        uint64_t x;
+        std::memcpy(&x, w + i, 8);
+        h = (h ^ x) * 0x9e3779b97f4a7c15ull;
+        h ^= h >> 29;
+    }
     return h;
 }
+
+constexpr uint64_t kGraphMinOps = 8;  // auto mode: shorter lists launch a pass or two, nothing to save
 
 qvg_stats stats_diff(const qvg_stats &a, const qvg_stats &b) {
     qvg_stats d{};
@@ -367,8 +377,27 @@ qvg_stats stats_diff(const qvg_stats &a, const qvg_stats &b) {
 // same plan options) replays as one captured CUDA graph; a new one is
 // captured while it runs. Removes the per-pass host planning and launch
 // cost that bounds small states.
-void apply_graph(qvg_state &s, const qvg_gate *ops, uint64_t count) {
-    const uint64_t key = ops_hash(ops, count, plan_signature(s));
+bool graph_cached(const qvg_state &s, uint64_t key) {
+    for (const auto &g : s.graphs)
+        if (g.key == key) return true;
+    return false;
+}
+
+// QVG_OPT_GRAPH auto: replay when this op list was applied before on this
+// state (a repeated circuit: the bench's steps, a parameter sweep), so a
+// one-shot apply never pays the capture and instantiation.
+bool graph_wanted(qvg_state &s, uint64_t key, uint64_t count) {
+    if (s.graph_mode == 1) return true;
+    if (s.graph_mode != 2 || count < kGraphMinOps) return false;
+    if (graph_cached(s, key)) return true;
+    if (std::find(s.graph_seen.begin(), s.graph_seen.end(), key) != s.graph_seen.end()) return true;
+    constexpr size_t kSeen = 32;
+    if (s.graph_seen.size() >= kSeen) s.graph_seen.erase(s.graph_seen.begin());
+    s.graph_seen.push_back(key);
+    return false;
+}
+
+void apply_graph(qvg_state &s, const qvg_gate *ops, uint64_t count, uint64_t key) {
     for (auto &g : s.graphs) {
         if (g.key == key && g.ops.size() == count &&
             std::memcmp(g.ops.data(), ops, count * sizeof(qvg_gate)) == 0) {
@@ -377,6 +406,7 @@ void apply_graph(qvg_state &s, const qvg_gate *ops, uint64_t count) {
             s.stats.fused_passes += g.delta.fused_passes;
             s.stats.kernel_launches += g.delta.kernel_launches;
             s.stats.bytes_moved += g.delta.bytes_moved;
+            s.stats.graph_replays += 1;
             g.last_use = ++s.graph_clock;
             return;
         }
@@ -402,6 +432,7 @@ void apply_graph(qvg_state &s, const qvg_gate *ops, uint64_t count) {
     cudaGraphDestroy(graph);
     cuda_check(inst, "cudaGraphInstantiate");
     cuda_check(cudaGraphLaunch(e.exec, s.stream), "cudaGraphLaunch");
+    s.stats.graph_replays += 1;
     constexpr size_t kMaxGraphs = 8;
     if (s.graphs.size() >= kMaxGraphs) {
         auto lru = std::min_element(s.graphs.begin(), s.graphs.end(),
@@ -589,8 +620,10 @@ int qvg_set_option(qvg_state *s, int key, int64_t value) {
             break;
         case QVG_OPT_CLASSES: s->classes = value != 0; break;
         case QVG_OPT_GRAPH:
-            s->graph = value != 0;
-            if (!s->graph) drop_graphs(*s);
+            if (value < 0 || value > 2) throw Validation("graph must be 0 (never), 1 (always) or 2 (auto)");
+            s->graph_mode = (uint32_t)value;
+            if (!s->graph_mode) drop_graphs(*s);
+            s->graph_seen.clear();
             break;
         case QVG_OPT_STAGE:
             if (value < 0 || value > 12) throw Validation("stage must be 0 (never) .. 12");
@@ -697,7 +730,10 @@ int qvg_apply(qvg_state *s, const qvg_gate *ops, uint64_t count) {
             for (auto &e : ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
             cuda_check(cudaEventRecord(ev[0], s->stream), "cudaEventRecord");
         }
-        if (s->graph && s->world == 1 && count > 0) apply_graph(*s, ops, count);
+        uint64_t key = 0;
+        const bool graph = s->world == 1 && count > 0 && s->graph_mode &&
+                           graph_wanted(*s, key = ops_hash(ops, count, plan_signature(*s)), count);
+        if (graph) apply_graph(*s, ops, count, key);
         else shard_apply(*s, s->shards, ops, count);
         if (whole) {
             cuda_check(cudaEventRecord(ev[1], s->stream), "cudaEventRecord");

@@ -169,6 +169,27 @@ def test_states_on_concurrent_host_threads(qv, oracle):
         assert np.array_equal(got[i], wants[i]), i
 
 
+def test_graph_auto_mode_replays_repeated_circuits(qv, oracle):
+    """QVG_OPT_GRAPH 2 (default): a circuit applied once runs eagerly; from its
+    second apply on the same state it replays as a captured graph, bit-exact.
+    Single-gate calls (the per-gate bench) never capture."""
+    n = 16
+    c = qv.u3_ladder_circuit(n, 4, 2)
+    want = oracle.simulate(n, gate_array(c))
+    st = qv.StateVector.create(n, 128, 0)
+    for rep in range(3):
+        st.init_basis(0)
+        qv.apply_circuit(st, c)
+        assert np.array_equal(st.read_state(), want), rep
+        assert st.stats()["graph_replays"] == rep
+    g = gate_array(c)
+    for _ in range(3):
+        st.apply_gates(g[:1].tobytes())
+    assert st.stats()["graph_replays"] == 2
+    with pytest.raises(qv.ValidationError):
+        st.set_option(qv.OPT_GRAPH, 3)
+
+
 def test_graph_replay_bit_identical(qv, oracle):
     """QVG_OPT_GRAPH: a repeated op list replays as a captured CUDA graph with
     the same results and pass accounting; a changed option or op list

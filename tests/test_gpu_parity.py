@@ -230,7 +230,7 @@ def test_step_hooks_barrier_stagger_and_fault(qv, oracle):
         qv.apply_circuit(st2, c)
     assert max(s for s, _, _ in seen) == 2
     assert not any(s == 2 and p == 1 for s, _, p in seen)
-    assert lib.qvg_set_step_hook(st2.handle(), None, None) == 0  # removed: runs again
+    assert lib.qvg_set_step_hook(st2.handle(), fn_t(), None) == 0  # a NULL hook: removed, runs again
     st2.init_basis(0)
     qv.apply_circuit(st2, c)
     assert np.array_equal(st2.read_state(), want)
