@@ -100,7 +100,8 @@ enum qvg_option {
     QVG_OPT_XCHG_CHUNK = 17, /* sharded: copy-transport chunk bytes (multiple of 16; 0 = default 256 MiB,
                                 capped by the NCCL scratch); tests use small chunks to split runs */
     QVG_OPT_PIPE = 18        /* fused tiles: 2 or 3 = warp-specialised bulk-copy pipeline (k_tile_pipe) with
-                                that many shared-memory ring stages (default 2); 0 = k_tile (per-thread loads) */
+                                that many shared-memory ring stages; 0 = k_tile, per-thread loads (default:
+                                measured 1.5-2x faster, profiles/r02_pipe_ab.json) */
 };
 
 /* Counters (the reference's Metrics, metrics.hpp:14-30, plus the GPU pass

@@ -109,7 +109,7 @@ struct qvg_state {
     std::vector<uint64_t> graph_seen;  // auto mode: keys applied once (ring)
     uint32_t reorder = REORDER_EXACT;  // QVG_OPT_REORDER: commutation-aware fusion order (qvg_plan.hpp)
     bool classes = true;       // QVG_OPT_CLASSES: structured-matrix op bodies in fused tiles
-    uint32_t pipe_stages = 2;  // QVG_OPT_PIPE: fused tiles through the bulk-copy pipeline (k_tile_pipe), ring stages; 0 = k_tile
+    uint32_t pipe_stages = 0;  // QVG_OPT_PIPE: fused tiles through the bulk-copy pipeline (k_tile_pipe) with this many ring stages; 0 = k_tile (default: measured faster, profiles/r02_pipe_ab.json)
     bool shape_set = false;    // tile_qubits / sub_bits set by the caller (no small-state default)
     struct GraphEntry {
         uint64_t key = 0;

@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--prefetch", type=int, default=0)
     ap.add_argument("--tile", type=int, default=0, help="tile qubits (0: the precision's default)")
     ap.add_argument("--precision", type=int, default=128)
+    ap.add_argument("--pipe", type=int, default=-1, help="QVG_OPT_PIPE (-1: the engine's default)")
     a = ap.parse_args()
     n = a.n
     c = {"sweep": lambda: qv.haar_sweep_circuit(n, 2508),
@@ -39,6 +40,8 @@ def main():
     st.set_option(qv.OPT_PREFETCH, a.prefetch)
     if a.tile:
         st.set_option(qv.OPT_TILE_QUBITS, a.tile)
+    if a.pipe >= 0:
+        st.set_option(qv.OPT_PIPE, a.pipe)
     st.apply_gates(c.gates())
     st.sync()
     print("ok", st.stats())
