@@ -215,6 +215,15 @@ int qvg_inner_product(qvg_state *a, qvg_state *b, double *re, double *im);
 /* max_i |a_i - b_i| (max_deviation, reference dense.cpp:174-183). */
 int qvg_max_deviation(qvg_state *a, qvg_state *b, double *out);
 
+/* Chunk checksums of the state in canonical order: for every chunk of
+ * `chunk_amps` amplitudes (a power of two >= 4096), two 64-bit words of
+ * order-independent sums of mixed amplitude bit patterns (qvg_readout.cuh
+ * k_checksum; numpy restatement in tests/conftest.py). out[2c], out[2c+1]
+ * for chunk c; `cap` counts chunks; *count = 2^n / chunk_amps (call with
+ * out = NULL to size). A size-independent parity property: equal states
+ * have equal words, and any bit change shows with probability ~1 - 2^-128. */
+int qvg_checksums(qvg_state *s, uint64_t chunk_amps, uint64_t *out, uint64_t cap, uint64_t *count);
+
 /* ---- instrumentation --------------------------------------------------------- */
 int qvg_stats_get(const qvg_state *s, qvg_stats *out);
 int qvg_stats_reset(qvg_state *s);

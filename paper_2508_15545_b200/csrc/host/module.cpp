@@ -230,6 +230,19 @@ PYBIND11_MODULE(_core, m) {
         }, py::arg("other"), "max_i |a_i - b_i| on the device")
         .def("set_option", &StateVector::set_option, py::arg("key"), py::arg("value"))
         .def("stats", [](const StateVector &s) { return stats_dict(s.stats()); })
+        .def("checksums",
+             [](StateVector &s, std::uint64_t chunk_amps) {
+                 std::uint64_t n = 0;
+                 check_status(qvg_checksums(s.handle(), chunk_amps, nullptr, 0, &n));
+                 py::array_t<std::uint64_t> out({(py::ssize_t)n, (py::ssize_t)2});
+                 {
+                     py::gil_scoped_release nogil;
+                     check_status(qvg_checksums(s.handle(), chunk_amps, out.mutable_data(), n, &n));
+                 }
+                 return out;
+             },
+             py::arg("chunk_amps") = std::uint64_t{1} << 26,
+             "(chunks, 2) uint64 checksum words of the state in canonical order (qvg_checksums)")
         .def("handle", [](const StateVector &s) { return reinterpret_cast<std::uintptr_t>(s.handle()); },
              "the qvg_state* of this state (for C-ABI calls through ctypes, e.g. qvg_set_step_hook)")
         .def("reset_stats", [](StateVector &s) { check_status(qvg_stats_reset(s.handle())); })

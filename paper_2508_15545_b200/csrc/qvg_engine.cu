@@ -913,6 +913,47 @@ int qvg_max_deviation(qvg_state *a, qvg_state *b, double *out) {
     });
 }
 
+int qvg_checksums(qvg_state *s, uint64_t chunk_amps, uint64_t *out, uint64_t cap, uint64_t *count) {
+    return guarded([&] {
+        check_state(s);
+        const uint64_t dim = 1ull << s->n;
+        if (chunk_amps < 4096 || (chunk_amps & (chunk_amps - 1)) || chunk_amps > dim)
+            throw Validation("chunk_amps must be a power of two in [4096, 2^n]");
+        const uint64_t nchunks = dim / chunk_amps;
+        if (count) *count = nchunks;
+        if (!out) return;
+        if (cap < nchunks) throw Validation("output too small: need 2 words per chunk");
+        set_device(s);
+        shard_canonicalize(*s, s->shards);
+        int cbits = 0;
+        while ((1ull << cbits) < chunk_amps) ++cbits;
+        unsigned long long *d = nullptr;
+        cuda_check(cudaMalloc(&d, nchunks * 2 * sizeof(uint64_t)), "cudaMalloc(checksums)");
+        std::unique_ptr<void, cudaError_t (*)(void *)> guard(d, cudaFree);
+        cuda_check(cudaMemsetAsync(d, 0, nchunks * 2 * sizeof(uint64_t), s->stream), "memset checksums");
+        const uint64_t local = 1ull << s->L;
+        const std::vector<void *> bufs = s->shards.local_buffers();
+        const std::vector<uint32_t> ranks = s->shards.local_ranks();
+        for (size_t b = 0; b < bufs.size(); ++b) {
+            const unsigned blocks = (unsigned)((local + 4095) / 4096);
+            const uint64_t base = (uint64_t)ranks[b] * local;
+            if (s->precision == QVG_C128)
+                k_checksum<double><<<blocks, 256, 0, s->stream>>>(static_cast<const double2 *>(bufs[b]), local, base,
+                                                                 cbits, d);
+            else
+                k_checksum<float><<<blocks, 256, 0, s->stream>>>(static_cast<const float2 *>(bufs[b]), local, base,
+                                                                cbits, d);
+            cuda_check(cudaGetLastError(), "checksum launch");
+        }
+        if (s->shards.comm)
+            nccl_check(ncclAllReduce(d, d, nchunks * 2, ncclUint64, ncclSum, s->shards.comm, s->stream),
+                       "ncclAllReduce(checksums)");
+        cuda_check(cudaMemcpyAsync(out, d, nchunks * 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s->stream),
+                   "D2H checksums");
+        cuda_check(cudaStreamSynchronize(s->stream), "checksum sync");
+    });
+}
+
 int qvg_stats_get(const qvg_state *s, qvg_stats *out) {
     return guarded([&] {
         check_state(s);

@@ -68,6 +68,70 @@ k_maxdiff_partials(const typename Cplx<R>::T *__restrict__ a, const typename Cpl
     if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
 }
 
+// ---- chunk checksums (qvg_checksums) ------------------------------------------
+// Per chunk of C = 2^cbits amplitudes (global index order), two 64-bit sums
+// mod 2^64 of mixed amplitude bit patterns:
+//   w0 += mix(re_bits ^ i*K0) + mix(im_bits ^ (i*K1 + K2))
+//   w1 += mix(re_bits ^ (i*K3 + K4)) + mix(im_bits ^ i*K5)
+// (mix = splitmix64's finaliser; re/im bits of the stored precision,
+// complex64 zero-extended). Integer sums are order-independent, so any grid
+// gives the same words, and every bit of every amplitude, including the sign
+// of a zero, reaches both. A size-independent property for full-size parity:
+// G-invariance at n = 32/33 compares 2 x 64 bits per chunk on the device
+// instead of hashing 64-128 GiB on the host (tests/test_gpu_fullsize.py;
+// numpy restatement in tests/conftest.py).
+__host__ __device__ __forceinline__ uint64_t ck_mix(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+constexpr uint64_t kCkK0 = 0x9e3779b97f4a7c15ull, kCkK1 = 0xc2b2ae3d27d4eb4full, kCkK2 = 0x165667b19e3779f9ull,
+                   kCkK3 = 0x27d4eb2f165667c5ull, kCkK4 = 0xd6e8feb86659fd93ull, kCkK5 = 0xff51afd7ed558ccdull;
+__device__ __forceinline__ void ck_bits(double2 v, uint64_t &re, uint64_t &im) {
+    re = (uint64_t)__double_as_longlong(v.x);
+    im = (uint64_t)__double_as_longlong(v.y);
+}
+__device__ __forceinline__ void ck_bits(float2 v, uint64_t &re, uint64_t &im) {
+    re = (uint64_t)(uint32_t)__float_as_int(v.x);
+    im = (uint64_t)(uint32_t)__float_as_int(v.y);
+}
+
+// One block: 4096 consecutive amplitudes (inside one chunk, C >= 4096);
+// its two partial words are added to out[2*chunk], out[2*chunk+1].
+template <class R>
+__global__ void __launch_bounds__(256)
+k_checksum(const typename Cplx<R>::T *__restrict__ psi, uint64_t count, uint64_t base_index, int cbits,
+           unsigned long long *__restrict__ out) {
+    __shared__ unsigned long long r0[256], r1[256];
+    const uint64_t start = (uint64_t)blockIdx.x * 4096;
+    uint64_t w0 = 0, w1 = 0;
+#pragma unroll 4
+    for (int k = 0; k < 16; ++k) {
+        const uint64_t li = start + (uint64_t)k * 256 + threadIdx.x;
+        if (li >= count) break;
+        uint64_t re, im;
+        ck_bits(psi[li], re, im);
+        const uint64_t i = base_index + li;
+        w0 += ck_mix(re ^ (i * kCkK0)) + ck_mix(im ^ (i * kCkK1 + kCkK2));
+        w1 += ck_mix(re ^ (i * kCkK3 + kCkK4)) + ck_mix(im ^ (i * kCkK5));
+    }
+    r0[threadIdx.x] = w0;
+    r1[threadIdx.x] = w1;
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+        if (threadIdx.x < s) {
+            r0[threadIdx.x] += r0[threadIdx.x + s];
+            r1[threadIdx.x] += r1[threadIdx.x + s];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const uint64_t c = (base_index + start) >> cbits;
+        atomicAdd(out + 2 * c, r0[0]);
+        atomicAdd(out + 2 * c + 1, r1[0]);
+    }
+}
+
 // ---- top-k by exact radix select over the IEEE bits of |a|^2 ------------------
 // For p >= 0 the bit pattern of p, read as uint64, orders like p. One digit of
 // `width` bits (starting at bit `shift`) is histogrammed per pass among the

@@ -42,3 +42,34 @@ def gate_array(circuit):
     from oracle.oracle import GATE_DTYPE
 
     return np.frombuffer(circuit.gates().tobytes(), dtype=GATE_DTYPE).copy()
+
+
+_CK = [0x9e3779b97f4a7c15, 0xc2b2ae3d27d4eb4f, 0x165667b19e3779f9, 0x27d4eb2f165667c5, 0xd6e8feb86659fd93,
+       0xff51afd7ed558ccd]
+
+
+def _ck_mix(z):
+    z = (z ^ (z >> np.uint64(30))) * np.uint64(0xbf58476d1ce4e5b9)
+    z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94d049bb133111eb)
+    return z ^ (z >> np.uint64(31))
+
+
+def checksums_numpy(amps, chunk_amps, base_index=0):
+    """numpy restatement of the device chunk checksums (qvg_readout.cuh
+    k_checksum, qvg_checksums): per chunk, two uint64 sums (mod 2^64) of
+    splitmix-mixed amplitude bit patterns, salted with the global index."""
+    K = [np.uint64(k) for k in _CK]
+    if amps.dtype == np.complex128:
+        bits = amps.view(np.uint64).reshape(-1, 2)
+        re, im = bits[:, 0], bits[:, 1]
+    else:
+        bits = amps.view(np.uint32).reshape(-1, 2).astype(np.uint64)
+        re, im = bits[:, 0], bits[:, 1]
+    with np.errstate(over="ignore"):
+        i = np.arange(base_index, base_index + amps.size, dtype=np.uint64)
+        w0 = _ck_mix(re ^ (i * K[0])) + _ck_mix(im ^ (i * K[1] + K[2]))
+        w1 = _ck_mix(re ^ (i * K[3] + K[4])) + _ck_mix(im ^ (i * K[5]))
+        out = np.zeros((amps.size // chunk_amps, 2), np.uint64)
+        out[:, 0] = w0.reshape(-1, chunk_amps).sum(axis=1, dtype=np.uint64)
+        out[:, 1] = w1.reshape(-1, chunk_amps).sum(axis=1, dtype=np.uint64)
+    return out

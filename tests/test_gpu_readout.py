@@ -91,3 +91,32 @@ def test_topk_whole_state_with_zero_amplitudes(qv, world):
         assert abs(got[0][1] - 2 ** -0.5) <= 1e-15 and got[2][1] == 0
     st.init_basis(5)
     assert [i for i, _ in st.top_amplitudes(16)] == [5] + [i for i in range(16) if i != 5]
+
+
+@pytest.mark.parametrize("world", [1, 4])
+@pytest.mark.parametrize("prec", [128, 64])
+def test_device_checksums_match_numpy(qv, world, prec):
+    """qvg_checksums equals its numpy restatement on the state read back, for
+    sharded (canonicalised first) and unsharded states, both precisions; a
+    single flipped bit (the sign of one zero) changes its chunk's words."""
+    from conftest import checksums_numpy
+
+    n = 16
+    st = (qv.StateVector.create(n, prec, 0) if world == 1
+          else qv.StateVector.create_sharded(n, prec, 0, 0, world, None))
+    qv.apply_circuit(st, qv.random_circuit(n, 300, 8))
+    host = st.read_state()
+    if prec == 64:
+        host = host.astype(np.complex64)
+    for chunk in (4096, 1 << 14, 1 << n):
+        assert np.array_equal(st.checksums(chunk), checksums_numpy(host, chunk)), chunk
+    z = qv.StateVector.create(n, 128, 0)
+    a = z.checksums(4096)
+    neg = np.zeros(1 << n, np.complex128)
+    neg[0] = 1.0
+    neg[5000] = complex(-0.0, 0.0)
+    z.load_state(neg)
+    b = z.checksums(4096)
+    assert (a[1] != b[1]).all() and np.array_equal(np.delete(a, 1, 0), np.delete(b, 1, 0))
+    with pytest.raises(qv.ValidationError):
+        z.checksums(1000)
