@@ -140,9 +140,9 @@ def test_config4_worker_count_law_full_size(qv, n):
         if world == 1 and n == 32:  # the device words agree with the host's view of the bytes
             from conftest import checksums_numpy
 
-            for c in (0, 17, 63):
-                assert np.array_equal(checksums_numpy(st.read_state(c * CHUNK, CHUNK), CHUNK, c * CHUNK)[0],
-                                      hashes[1][c])
+            for k in (0, 17, 63):
+                assert np.array_equal(checksums_numpy(st.read_state(k * CHUNK, CHUNK), CHUNK, k * CHUNK)[0],
+                                      hashes[1][k])
         del st
     for world in (2, 4, 8):
         assert np.array_equal(hashes[world], hashes[1]), world
