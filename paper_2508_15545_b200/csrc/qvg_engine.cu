@@ -5,6 +5,8 @@
 // paired kernel + thread pool (reference store.cpp, cache.cpp, kernel.cpp,
 // parallel.cpp): the state stays resident in HBM for the whole circuit and
 // each planned pass is one kernel launch on the state's stream.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <nvtx3/nvToolsExt.h>
 
@@ -222,6 +224,76 @@ void launch_phase(const qvg_state &s, void *psi, uint32_t L, const qvg_gate &g, 
     }
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        (void)cudaGetLastError();
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }();
+    return fn;
+}
+
+// The tile of a pass as one box of a <= 5-D tensor map over the state (TileTma,
+// qvg_tile.cuh): dim 0 = a 128-B row (amplitude bits 0..rb-1), then the runs
+// of tile / non-tile qubits above it. False when the pass needs more than 5
+// dims (it then runs k_tile).
+bool tma_tile_map(const TileGeom &g, int amp_bytes, void *psi, TileTma &out) {
+    const int rb = amp_bytes == 16 ? 3 : 4;
+    if (g.lowc < rb) return false;
+    struct Seg { int start, len, gap; };
+    std::vector<Seg> segs;
+    if (g.lowc > rb) segs.push_back({rb, g.lowc - rb, 0});
+    int cur = g.lowc;
+    for (int i = 0; i < g.nhi;) {
+        int j = i;
+        while (j + 1 < g.nhi && g.hiq[j + 1] == g.hiq[j] + 1) ++j;
+        const int start = g.hiq[i], len = j - i + 1;
+        if (start > cur) segs.push_back({cur, start - cur, 1});
+        segs.push_back({start, len, 0});
+        cur = start + len;
+        i = j + 1;
+    }
+    if (cur < g.n) segs.push_back({cur, g.n - cur, 1});
+    if (segs.size() > 4) return false;
+    for (const Seg &sg : segs)
+        if ((!sg.gap && sg.len > 8) || sg.len > 32) return false;
+    const auto encode = tensor_map_encoder();
+    if (!encode) return false;
+    cuuint64_t dim[5], stride[4];
+    cuuint32_t box[5], estr[5] = {1, 1, 1, 1, 1};
+    dim[0] = 16;  // 8-byte elements: one 128-B row
+    box[0] = 16;
+    for (int d = 1; d < 5; ++d) {
+        if (d - 1 < (int)segs.size()) {
+            const Seg &sg = segs[d - 1];
+            dim[d] = 1ull << sg.len;
+            stride[d - 1] = (cuuint64_t)amp_bytes << sg.start;
+            box[d] = sg.gap ? 1u : (1u << sg.len);
+            out.shift[d] = sg.start;
+            out.len[d] = sg.len;
+            out.gap[d] = sg.gap;
+        } else {
+            dim[d] = 1;
+            stride[d - 1] = (cuuint64_t)amp_bytes << g.n;
+            box[d] = 1;
+            out.shift[d] = 0;
+            out.len[d] = 0;
+            out.gap[d] = 0;
+        }
+    }
+    out.shift[0] = out.len[0] = out.gap[0] = 0;
+    const CUresult r = encode(&out.map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 5, psi, dim, stride, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return true;
+}
+
 template <class R>
 void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *recs) {
     using T = typename Cplx<R>::T;
@@ -237,21 +309,27 @@ void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *recs) {
     const bool fma = s.fma && sizeof(R) == 8;  // complex64 always contracts
     const bool small = threads <= 256;
     const bool tiny = threads <= 128;  // sub 4 at k <= 11: 128-thread CTAs
-    // the bulk-copy pipeline serves 128-thread tiles (every default shape)
-    const int pipe = (s.pipe_stages > 0 && threads == (unsigned)kPipeConsumers && !pf) ? (int)s.pipe_stages : 0;
-    if (pipe) {
+    // the bulk-copy pipelines serve 128-thread tiles (every default shape)
+    const bool pipe_ok = threads == (unsigned)kPipeConsumers && !pf;
+    const bool tma = pipe_ok && s.pipe_stages == 4 && tma_tile_map(g, (int)sizeof(T), psi, prm.tma);
+    const int pipe = (!tma && pipe_ok && (s.pipe_stages == 2 || s.pipe_stages == 3)) ? (int)s.pipe_stages : 0;
+    if (tma) {
+        threads = kPipeThreads;
+        smem = tma_smem_bytes(g.k, (int)sizeof(T), 2);
+    } else if (pipe) {
         threads = kPipeThreads;
         smem = pipe_smem_bytes(g.nhi, g.k, (int)sizeof(T), pipe >= 3 ? 3 : 2);
     }
     // Passes without structured ops (classes off) use the REAL-set kernel:
     // their records only name general bodies, which every set compiles.
     const int set_idx = class_set_index(g.cls_set);
-    const TileKernel<R> kern = tile_kernel<R>(set_idx, TileVariant{g.sub, tiny, small, fma, pf, pipe});
+    const TileKernel<R> kern = tile_kernel<R>(set_idx, TileVariant{g.sub, tiny, small, fma, pf, pipe, tma});
     // The shared-memory opt-in is a per-device function attribute: set it once
     // per (device, variant).
     static std::atomic<uint64_t> attr_set[64][4][8];  // [device][class set][variant / 64]: a bit per variant
     const int variant = (sizeof(R) == 8 ? 1 : 0) | (g.sub == 4 ? 2 : 0) | (fma ? 4 : 0) | (small ? 8 : 0) |
-                        (pf ? 16 : 0) | (tiny ? 32 : 0) | (g.sub == 5 ? 64 : 0) | (pipe ? (pipe >= 3 ? 256 : 128) : 0);
+                        (pf ? 16 : 0) | (tiny ? 32 : 0) | (g.sub == 5 ? 64 : 0) | (pipe ? (pipe >= 3 ? 256 : 128) : 0) |
+                        (tma ? 384 : 0);
     std::atomic<uint64_t> &set = attr_set[s.device & 63][set_idx][variant >> 6];
     const uint64_t bit = 1ull << (variant & 63);
     if (!(set.load(std::memory_order_acquire) & bit)) {
@@ -638,7 +716,8 @@ int qvg_set_option(qvg_state *s, int key, int64_t value) {
             s->exchange_mode = (int)value;
             break;
         case QVG_OPT_PIPE:
-            if (value < 0 || value > 3 || value == 1) throw Validation("pipe must be 0 (k_tile), 2 or 3 ring stages");
+            if (value < 0 || value > 4 || value == 1)
+                throw Validation("pipe must be 0 (k_tile), 2 or 3 (bulk-copy ring stages) or 4 (tensor-map TMA)");
             s->pipe_stages = (uint32_t)value;
             break;
         case QVG_OPT_XCHG_CHUNK:

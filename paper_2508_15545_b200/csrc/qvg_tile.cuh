@@ -28,6 +28,7 @@
 // 16 register amplitudes per thread.
 #pragma once
 
+#include <cuda.h>  // CUtensorMap (k_tile_tma's tensor-map descriptor; types only, no driver link)
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -72,8 +73,21 @@ struct TileGeom {
 // (A 32-record block, 3 KB instead of 25 KB, measured no faster to launch at
 // n = 12..22.)
 constexpr int kMaxTileRecs = 256;
+// k_tile_tma (qvg_tile_pipe.cuh): the tile as ONE box of a <= 5-D tensor map
+// over the state. Dim 0 is a 128-B row (the lowest rb = log2(128 / S)
+// amplitude bits); dims 1.. are the alternating runs of tile and non-tile
+// qubits above it, from bit rb up. A tile dim's box spans the run (its
+// coordinate is 0); a non-tile ("gap") dim's box is 1 and its coordinate is
+// the tile base's bits in that run. Unused dims have size 1.
+struct TileTma {
+    CUtensorMap map;  // cuTensorMapEncodeTiled, UINT64 elements, SWIZZLE_128B
+    int shift[5];     // first amplitude-index bit of dim d (d >= 1)
+    int len[5];       // bits of dim d
+    int gap[5];       // 1: coordinate = (base >> shift) & (2^len - 1)
+};
 struct TileParams {
     TileGeom g;
+    TileTma tma;  // k_tile_tma only
     TileOp ops[kMaxTileRecs];
 };
 static_assert(sizeof(TileParams) < 32000, "kernel parameter block limit");

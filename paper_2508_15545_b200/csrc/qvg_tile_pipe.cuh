@@ -261,4 +261,154 @@ k_tile_pipe(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileP
     }
 }
 
+// ---- K4c: the same pipeline with ONE tensor-map TMA per tile -------------------
+// k_tile_pipe issues a bulk copy per contiguous segment, and cp.async.bulk takes
+// uniform operands, so the producer walks its lanes' segments through an R2UR
+// waterfall: 512 serialised trips per tile of 256 x 128-B segments
+// (profiles/r02_pipe_sass.txt). Here the tile is one box of a <= 5-D tensor
+// map (TileTma, built per pass on the host): one cp.async.bulk.tensor load and
+// one store per tile. The map uses SWIZZLE_128B, whose layout in a 1024-B
+// aligned slot is exactly k_tile's swizzled layout swz(l) (16-B column ^=
+// 128-B row index & 7), so consumers read and write every group through
+// swz(lidx) with no staging transposes and no bank conflicts, and the TMA
+// store un-swizzles on the way out.
+__device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap *map, const int (&c)[5], uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
+        "%6}], [%7];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_5d(const CUtensorMap *map, const int (&c)[5], uint32_t src) {
+    asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(src)
+                 : "memory");
+}
+
+__host__ __device__ constexpr uint32_t tma_ring_offset(int stages) { return (16u * (uint32_t)stages + 1023u) & ~1023u; }
+__host__ __device__ constexpr uint32_t tma_smem_bytes(int k, int amp_bytes, int stages) {
+    return tma_ring_offset(stages) + (uint32_t)stages * ((uint32_t)amp_bytes << k) + 1024u;  // + slack to 1024-align
+}
+
+template <class R, int SUB, bool FMA, int CM, int STAGES>
+__global__ void __launch_bounds__(kPipeThreads, QVG_PIPE_MINB)
+k_tile_tma(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams prm) {
+    using T = typename Cplx<R>::T;
+    constexpr int E = 1 << SUB;
+    constexpr uint32_t NC = kPipeConsumers;
+    const TileGeom &g = prm.g;
+    const TileOp *ops = prm.ops;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    // 1024-B aligned ring (SWIZZLE_128B atoms), mbarriers below it
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t pad = ((raw + 1023u) & ~1023u) - raw;
+    unsigned char *base_ptr = smem_raw + pad;
+    const uint32_t bar0 = smem_u32(base_ptr);  // full[s] at bar0 + 8s, done[s] at bar0 + 8(STAGES+s)
+    T *ring = reinterpret_cast<T *>(base_ptr + tma_ring_offset(STAGES));
+    const uint32_t tile_amps = 1u << g.k;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(bar0 + 8u * s, 1);
+            mbar_init(bar0 + 8u * (STAGES + s), NC);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    auto tile_base = [&](uint64_t tile) {
+        uint64_t base = tile << g.lowc;
+#pragma unroll
+        for (int i = 0; i < 24; ++i)
+            if (i < g.nhi) base = ins0(base, g.hiq[i]);
+        return base;
+    };
+    const uint64_t first = blockIdx.x;
+    const uint64_t cnt = first < g.ntiles ? (g.ntiles - first + gridDim.x - 1) / gridDim.x : 0;
+
+    if (threadIdx.x >= NC) {  // ---------------- producer warp (one lane) ----------------
+        if ((threadIdx.x & 31u) != 0) return;
+        const CUtensorMap *map = &prm.tma.map;
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+        auto coords = [&](uint64_t tile, int(&c)[5]) {
+            const uint64_t base = tile_base(tile);
+            c[0] = 0;
+#pragma unroll
+            for (int d = 1; d < 5; ++d)
+                c[d] = prm.tma.gap[d] ? (int)((base >> prm.tma.shift[d]) & ((1ull << prm.tma.len[d]) - 1)) : 0;
+        };
+        auto store_tile = [&](uint64_t i) {
+            const uint32_t s = (uint32_t)(i % STAGES);
+            mbar_wait(bar0 + 8u * (STAGES + s), (uint32_t)((i / STAGES) & 1));
+            int c[5];
+            coords(first + i * gridDim.x, c);
+            tma_store_5d(map, c, smem_u32(ring + (size_t)s * tile_amps));
+            bulk_commit();
+        };
+        for (uint64_t i = 0; i < cnt; ++i) {
+            const uint32_t s = (uint32_t)(i % STAGES);
+            if (i >= STAGES) {
+                store_tile(i - STAGES);
+                bulk_wait_read0();
+            }
+            const uint32_t full = bar0 + 8u * s;
+            mbar_expect_tx(full, (uint32_t)sizeof(T) * tile_amps);
+            int c[5];
+            coords(first + i * gridDim.x, c);
+            tma_load_5d(smem_u32(ring + (size_t)s * tile_amps), map, c, full);
+        }
+        for (uint64_t i = cnt > STAGES ? cnt - STAGES : 0; i < cnt; ++i) store_tile(i);
+        bulk_wait0();
+        return;
+    }
+
+    // ---------------- consumer warps: every group through swz(lidx) ----------------
+    const uint32_t t = threadIdx.x;
+    for (uint64_t i = 0; i < cnt; ++i) {
+        const uint32_t s = (uint32_t)(i % STAGES);
+        const uint64_t base = tile_base(first + i * gridDim.x);
+        T *sm = ring + (size_t)s * tile_amps;
+        mbar_wait(bar0 + 8u * s, (uint32_t)((i / STAGES) & 1));
+        int rec = 0;
+        for (int gi = 0; gi < g.ngroups; ++gi) {
+            const int nops = ops[rec].tbit;
+            const uint64_t packed = ops[rec].gtgt;
+            ++rec;
+            int b[SUB];
+#pragma unroll
+            for (int j = 0; j < SUB; ++j) b[j] = (int)((packed >> (8 * j)) & 0xff);
+            uint32_t l0 = t;
+#pragma unroll
+            for (int j = 0; j < SUB; ++j) l0 = (uint32_t)ins0(l0, b[j]);
+            auto lidx = [&](int r) {
+                uint32_t l = l0;
+#pragma unroll
+                for (int j = 0; j < SUB; ++j) l |= ((r >> j) & 1) ? (1u << b[j]) : 0u;
+                return l;
+            };
+            T v[E];
+#pragma unroll
+            for (int r = 0; r < E; ++r) v[r] = sm[swz(lidx(r))];
+            for (int k = 0; k < nops; ++k) {
+                const TileOp &op = ops[rec + k];
+                if ((base & op.greq) != op.greq) continue;
+                const int sl = op.slot;
+                if ((sl & kSlotCtlTest) && !((t >> op.cbit) & 1u)) continue;
+                bool t1 = false;
+                if (sl & kSlotT1) t1 = op.tbit >= 0 ? ((t >> op.tbit) & 1u) != 0 : (base & op.gtgt) != 0;
+                op_dispatch<R, SUB, FMA, CM>(sl & 0xff, v, reinterpret_cast<const R *>(op.u), t1, (sl & kSlotD0) != 0);
+            }
+            rec += nops;
+            // each thread rewrites exactly the slots it read: no barrier before
+#pragma unroll
+            for (int r = 0; r < E; ++r) sm[swz(lidx(r))] = v[r];
+            if (gi == g.ngroups - 1) {
+                fence_proxy_async();
+                mbar_arrive(bar0 + 8u * (STAGES + s));
+            } else {
+                cbar();
+            }
+        }
+    }
+}
+
 }  // namespace qvg

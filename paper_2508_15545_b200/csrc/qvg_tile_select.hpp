@@ -19,6 +19,7 @@ struct TileVariant {
     bool fma;    // complex128 DFMA arithmetic (QVG_OPT_FMA)
     bool pf;     // next-tile register prefetch (QVG_OPT_PREFETCH)
     int pipe;    // > 0: k_tile_pipe with this many ring stages (QVG_OPT_PIPE; 128-thread tiles only)
+    bool tma;    // k_tile_tma: one tensor-map TMA per tile (QVG_OPT_PIPE 4)
 };
 
 // Class-set index: 0 {gen, real, X}, 1 {gen, +-1/2, X}, 2 {gen, +-1/2, sqrt(W)},
@@ -62,6 +63,13 @@ inline TileKernel<R> tile_kernel(int set_idx, const TileVariant &v) {
 // qvg_tile_inst.cu only.
 template <class R, int CM>
 TileKernel<R> tile_kernel_pick(const TileVariant &v) {
+    if (v.tma && v.tiny && !v.pf) {  // tensor-map pipeline (qvg_tile_pipe.cuh)
+        if constexpr (sizeof(R) == 4) {
+            if (v.sub == 5) return k_tile_tma<R, 5, false, CM, 2>;
+        }
+        if (v.sub == 4) return v.fma ? k_tile_tma<R, 4, true, CM, 2> : k_tile_tma<R, 4, false, CM, 2>;
+        if (v.sub == 3) return v.fma ? k_tile_tma<R, 3, true, CM, 2> : k_tile_tma<R, 3, false, CM, 2>;
+    }
     if (v.pipe > 0 && v.tiny && !v.pf) {  // bulk-copy pipeline (qvg_tile_pipe.cuh)
         if constexpr (sizeof(R) == 4) {
             if (v.sub == 5) return v.pipe >= 3 ? k_tile_pipe<R, 5, false, CM, 3> : k_tile_pipe<R, 5, false, CM, 2>;
