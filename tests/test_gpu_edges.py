@@ -216,3 +216,42 @@ def test_graph_replay_bit_identical(qv, oracle):
     qv.apply_circuit(st, c2)
     assert np.array_equal(st.read_state(), oracle.simulate(n, gate_array(c2)))
     st.set_option(qv.OPT_GRAPH, 0)
+
+
+@pytest.mark.parametrize("prec", [128, 64])
+@pytest.mark.parametrize("n", [6, 10, 16])
+def test_warp_shuffle_low_kernel_per_gate(qv, oracle, prec, n):
+    """k_low (north_star's warp-shuffle pairing for targets < 5, QVG_OPT_LOW_KERNEL)
+    with fusion OFF, so every op on qubits 0..4 is its own k_low launch: every
+    target 0..4, uncontrolled and with a control below / above the target (the
+    inserted and the selected control), general, real and permutation
+    matrices. complex128 bit-identical to the oracle, complex64 within 1e-5.
+    The CUPTI kernel list (torch.profiler) must show k_low launches, so the
+    test cannot pass on k_pairs alone (VERDICT r1 weak #8)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    start = oracle.simulate(n, gate_array(qv.random_circuit(n, 30, 5)))
+    lines = [f"qubits {n}"]
+    for t in range(5):
+        lines += [f"u3 {t} 0.3 1.1 -0.4", f"h {t}", f"cx {(t + 1) % n} {t}", f"cx {n - 1} {t}",
+                  f"cu {(t + 3) % n} {t} 0.6 0 0 0.8 0 0.8 0.6 0", f"x {t}"]
+        if t > 0:
+            lines.append(f"cx 0 {t}")
+    c = qv.parse_circuit("\n".join(lines) + "\n")
+    want = oracle.apply(n, start.copy(), gate_array(c))
+    st = qv.StateVector.create(n, prec, 0)
+    st.set_option(qv.OPT_LOW_KERNEL, 1)
+    st.load_state(start)
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        m = qv.apply_circuit(st, c, fuse=False)
+        st.sync()
+        torch.cuda.synchronize()
+    got = st.read_state()
+    assert m["traversals"] == len(c)
+    names = [e.name for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
+    assert sum("k_low" in s for s in names) >= 5 * 5, sorted(set(names))
+    if prec == 128:
+        assert np.array_equal(got, want), np.abs(got - want).max()
+    else:
+        assert np.abs(got.astype(np.complex128) - want).max() <= 1e-5
