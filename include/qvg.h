@@ -99,6 +99,11 @@ enum qvg_option {
                                 same values with fewer FP64 instructions (default); 0 = general bodies */
     QVG_OPT_XCHG_CHUNK = 17, /* sharded: copy-transport chunk bytes (multiple of 16; 0 = default 256 MiB,
                                 capped by the NCCL scratch); tests use small chunks to split runs */
+    QVG_OPT_JIT = 19,        /* fused tiles: run a pass as a kernel specialised to its op list (NVRTC,
+                                cached per pass structure; bit-identical to k_tile) where that measured
+                                faster (every complex64 pass; complex128 passes of X / real / diagonal ops):
+                                1 = compile on worker threads, k_tile until ready (default), 2 = compile
+                                before the first launch, 3 = every pass, compiled first; 0 = never */
     QVG_OPT_PIPE = 18        /* fused tiles: 2 or 3 = warp-specialised bulk-copy pipeline (k_tile_pipe) with
                                 that many shared-memory ring stages; 0 = k_tile, per-thread loads (default:
                                 measured 1.5-2x faster, profiles/r02_pipe_ab.json) */
@@ -118,6 +123,7 @@ typedef struct qvg_stats {
     double exchange_ms;      /* device time of exchanges (QVG_OPT_TIMING, sharded states) */
     uint64_t fused_exchanges; /* exchanges that also applied the gate that caused them (k_xchg) */
     uint64_t graph_replays;   /* applies that ran as a captured CUDA graph (QVG_OPT_GRAPH) */
+    uint64_t jit_passes;      /* fused passes that ran as a JIT-specialised kernel (QVG_OPT_JIT) */
 } qvg_stats;
 
 typedef struct qvg_state qvg_state;
@@ -231,6 +237,19 @@ int qvg_stats_reset(qvg_state *s);
 int qvg_stream(const qvg_state *s, void **stream_out);
 /* Device pointer and byte size of this rank's amplitude shard. */
 int qvg_device_buffer(const qvg_state *s, void **ptr_out, uint64_t *bytes_out);
+/* JIT-specialised tile passes (QVG_OPT_JIT, paper_2508_15545_b200/csrc/qvg_jit.hpp):
+ * process-wide counters (kernels compiled / failed / queued, summed compile
+ * ms); drain != 0 first waits for every queued compile. available = NVRTC and
+ * the driver entry points loaded. */
+int qvg_jit_info(int drain, uint64_t *compiled, uint64_t *failed, uint64_t *queued, double *compile_ms,
+                 int *available);
+/* Host-only check of the JIT source path (no GPU needed): plans the ops as
+ * qvg_apply would on an unsharded state of this width/precision (defaults,
+ * fusion on), generates every fused pass's specialised source and compiles
+ * it with NVRTC for sm_100a. *passes_out = fused passes, *compiled_out = those
+ * that compiled; the first error log goes to err (NUL-terminated, cap bytes). */
+int qvg_jit_check(uint32_t n_qubits, uint32_t precision, const qvg_gate *ops, uint64_t count,
+                  uint64_t *passes_out, uint64_t *compiled_out, char *err, uint64_t err_cap);
 /* Number of gate passes qvg_apply would launch for these ops (planner only,
  * no device work; usable without a GPU). */
 int qvg_plan_passes(uint32_t n_qubits, uint32_t precision, int fuse,

@@ -65,6 +65,7 @@ py::dict stats_dict(const qvg_stats &s) {
     d["exchange_ms"] = s.exchange_ms;
     d["fused_exchanges"] = s.fused_exchanges;
     d["graph_replays"] = s.graph_replays;
+    d["jit_passes"] = s.jit_passes;
     return d;
 }
 
@@ -425,6 +426,43 @@ PYBIND11_MODULE(_core, m) {
         return py::bytes(id);
     });
 
+    m.def("jit_info",
+          [](bool drain) {
+              std::uint64_t compiled = 0, failed = 0, queued = 0;
+              double ms = 0;
+              int avail = 0;
+              {
+                  py::gil_scoped_release nogil;
+                  check_status(qvg_jit_info(drain ? 1 : 0, &compiled, &failed, &queued, &ms, &avail));
+              }
+              py::dict d;
+              d["compiled"] = compiled;
+              d["failed"] = failed;
+              d["queued"] = queued;
+              d["compile_ms"] = ms;
+              d["available"] = avail != 0;
+              return d;
+          },
+          py::arg("drain") = false,
+          "JIT tile-pass counters (process-wide); drain=True waits for queued compiles first");
+    m.def("jit_check",
+          [](std::uint32_t n, py::buffer buf, std::uint32_t precision) {
+              const py::buffer_info b = buf.request();
+              std::size_t count = 0;
+              const qvg_gate *g = gate_ptr(b, count);
+              std::uint64_t passes = 0, compiled = 0;
+              std::string err(4096, '\0');
+              {
+                  py::gil_scoped_release nogil;
+                  check_status(qvg_jit_check(n, precision, g, count, &passes, &compiled, &err[0], err.size()));
+              }
+              err.resize(std::strlen(err.c_str()));
+              return py::make_tuple(passes, compiled, err);
+          },
+          py::arg("n_qubits"), py::arg("gates"), py::arg("precision") = 128,
+          "(fused passes, compiled, first error): generate and NVRTC-compile every fused pass's "
+          "JIT-specialised kernel (host-only, no GPU)");
+
     m.def("plan_passes",
           [](std::uint32_t n, py::buffer buf, std::uint32_t precision, bool fuse, std::uint32_t tile_qubits,
              std::uint32_t carriers) {
@@ -478,4 +516,5 @@ PYBIND11_MODULE(_core, m) {
     m.attr("OPT_CLASSES") = (int)QVG_OPT_CLASSES;
     m.attr("OPT_XCHG_CHUNK") = (int)QVG_OPT_XCHG_CHUNK;
     m.attr("OPT_PIPE") = (int)QVG_OPT_PIPE;
+    m.attr("OPT_JIT") = (int)QVG_OPT_JIT;
 }

@@ -28,6 +28,7 @@
 #include "qvg_plan.hpp"
 #include "qvg_shard.hpp"
 #include "qvg_tile_select.hpp"
+#include "qvg_jit.hpp"
 
 using namespace qvg;
 
@@ -111,6 +112,9 @@ struct qvg_state {
     std::vector<uint64_t> graph_seen;  // auto mode: keys applied once (ring)
     uint32_t reorder = REORDER_EXACT;  // QVG_OPT_REORDER: commutation-aware fusion order (qvg_plan.hpp)
     bool classes = true;       // QVG_OPT_CLASSES: structured-matrix op bodies in fused tiles
+    uint32_t jit_mode = 1;     // QVG_OPT_JIT: fused passes as specialised kernels (qvg_jit.hpp); 1 async, 2 sync, 0 off
+    bool jit_pending = false;  // a pass of the current apply ran k_tile while its JIT kernel was compiling
+    bool capturing = false;    // run_local inside a graph capture (JIT: lookups only)
     uint32_t pipe_stages = 0;  // QVG_OPT_PIPE: fused tiles through the bulk-copy pipeline (k_tile_pipe) with this many ring stages; 0 = k_tile (default: measured faster, profiles/r02_pipe_ab.json)
     bool shape_set = false;    // tile_qubits / sub_bits set by the caller (no small-state default)
     struct GraphEntry {
@@ -294,6 +298,25 @@ bool tma_tile_map(const TileGeom &g, int amp_bytes, void *psi, TileTma &out) {
     return true;
 }
 
+// Which fused passes run as JIT kernels by default (QVG_OPT_JIT 1/2), from
+// the per-pass A/B in profiles/r02_jit_ab.json (n = 30, CUPTI per-pass times):
+// complex64 passes were faster as JIT kernels on every BASELINE circuit
+// (3-11%); complex128 passes were faster only when their pair ops are the
+// cheap classes (X, real: the CX and QFT passes, 6-7%), and slower (up to
+// 20%) with general, U3 (real u00) or +-1/2 / sqrt(W) bodies, whose straight-
+// line code spills and misses the instruction cache where k_tile's shared
+// op bodies do not.
+bool jit_pays(const TileGeom &g, const TileOp *recs, size_t amp_bytes) {
+    if (amp_bytes == 8) return true;
+    for (int i = 0; i < g.nrec; ++i) {
+        const TileOp &o = recs[i];
+        if (o.kind != TILE_PAIR) continue;
+        const int cls = (o.slot & 0xff) / 30;
+        if (cls != TILE_CLS_REAL && cls != TILE_CLS_SWAP) return false;
+    }
+    return true;
+}
+
 template <class R>
 void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *recs) {
     using T = typename Cplx<R>::T;
@@ -319,6 +342,22 @@ void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *recs) {
     } else if (pipe) {
         threads = kPipeThreads;
         smem = pipe_smem_bytes(g.nhi, g.k, (int)sizeof(T), pipe >= 3 ? 3 : 2);
+    }
+    // A JIT-specialised kernel for this pass (qvg_jit.hpp): the plain k_tile
+    // variants only (no register prefetch, no bulk-copy pipelines).
+    if (s.jit_mode && !tma && !pipe && !pf && (s.jit_mode == 3 || jit_pays(g, prm.ops, sizeof(T)))) {
+        const JitVariant jv{(int)sizeof(T), g.sub, fma, tiny ? 128 : small ? 256 : 512,
+                            kClsSets[class_set_index(g.cls_set)]};
+        bool pending = false;
+        const int mode = s.capturing ? -1 : s.jit_mode == 1 ? 1 : 2;
+        if (void *fn = jit_tile_function(g, prm.ops, jv, mode, &pending)) {
+            const int per_sm = jit_occupancy(fn, threads, smem);
+            const uint64_t grid = std::min<uint64_t>(g.ntiles, (uint64_t)per_sm * s.sm_count);
+            cuda_check(jit_launch(fn, (unsigned)grid, threads, smem, s.stream, psi, &prm), "JIT tile launch");
+            s.stats.jit_passes += 1;
+            return;
+        }
+        s.jit_pending |= pending;
     }
     // Passes without structured ops (classes off) use the REAL-set kernel:
     // their records only name general bodies, which every set compiles.
@@ -448,6 +487,7 @@ qvg_stats stats_diff(const qvg_stats &a, const qvg_stats &b) {
     d.fused_passes = a.fused_passes - b.fused_passes;
     d.kernel_launches = a.kernel_launches - b.kernel_launches;
     d.bytes_moved = a.bytes_moved - b.bytes_moved;
+    d.jit_passes = a.jit_passes - b.jit_passes;
     return d;
 }
 
@@ -484,6 +524,7 @@ void apply_graph(qvg_state &s, const qvg_gate *ops, uint64_t count, uint64_t key
             s.stats.fused_passes += g.delta.fused_passes;
             s.stats.kernel_launches += g.delta.kernel_launches;
             s.stats.bytes_moved += g.delta.bytes_moved;
+            s.stats.jit_passes += g.delta.jit_passes;
             s.stats.graph_replays += 1;
             g.last_use = ++s.graph_clock;
             return;
@@ -492,14 +533,21 @@ void apply_graph(qvg_state &s, const qvg_gate *ops, uint64_t count, uint64_t key
     const qvg_stats before = s.stats;
     cudaGraph_t graph = nullptr;
     cuda_check(cudaStreamBeginCapture(s.stream, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+    // inside the capture JIT kernels are only looked up (no compiles, no
+    // module loads); a pass whose kernel is still compiling runs k_tile and
+    // the graph is then used once, not cached (the next apply captures again)
+    s.capturing = true;
+    s.jit_pending = false;
     try {
         run_local(s, s.shards.bufs[0], ops, count);
     } catch (...) {
+        s.capturing = false;
         cudaStreamEndCapture(s.stream, &graph);
         if (graph) cudaGraphDestroy(graph);
         s.stats = before;
         throw;
     }
+    s.capturing = false;
     cuda_check(cudaStreamEndCapture(s.stream, &graph), "cudaStreamEndCapture");
     qvg_state::GraphEntry e;
     e.key = key;
@@ -511,6 +559,10 @@ void apply_graph(qvg_state &s, const qvg_gate *ops, uint64_t count, uint64_t key
     cuda_check(inst, "cudaGraphInstantiate");
     cuda_check(cudaGraphLaunch(e.exec, s.stream), "cudaGraphLaunch");
     s.stats.graph_replays += 1;
+    if (s.jit_pending) {  // k_tile stood in for a kernel still compiling: do not keep this graph
+        cudaGraphExecDestroy(e.exec);
+        return;
+    }
     constexpr size_t kMaxGraphs = 8;
     if (s.graphs.size() >= kMaxGraphs) {
         auto lru = std::min_element(s.graphs.begin(), s.graphs.end(),
@@ -714,6 +766,11 @@ int qvg_set_option(qvg_state *s, int key, int64_t value) {
         case QVG_OPT_EXCHANGE:
             if (value < -1 || value > 2) throw Validation("exchange mode must be -1, 0, 1 or 2");
             s->exchange_mode = (int)value;
+            break;
+        case QVG_OPT_JIT:
+            if (value < 0 || value > 3)
+                throw Validation("jit must be 0 (never), 1 (async), 2 (compile before launch) or 3 (every pass, compiled first)");
+            s->jit_mode = (uint32_t)value;
             break;
         case QVG_OPT_PIPE:
             if (value < 0 || value > 4 || value == 1)
@@ -1300,6 +1357,58 @@ int qvg_plan_passes(uint32_t n_qubits, uint32_t precision, int fuse, uint32_t ti
         if (passes_out) *passes_out = plan.passes.size();
         if (fused_out) *fused_out = fused;
         if (bytes_out) *bytes_out = bytes;
+    });
+}
+
+int qvg_jit_info(int drain, uint64_t *compiled, uint64_t *failed, uint64_t *queued, double *compile_ms,
+                 int *available) {
+    return guarded([&] {
+        if (drain) jit_drain();
+        const JitCounters c = jit_counters();
+        if (compiled) *compiled = c.compiled;
+        if (failed) *failed = c.failed;
+        if (queued) *queued = c.queued;
+        if (compile_ms) *compile_ms = c.compile_ms;
+        if (available) *available = jit_available() ? 1 : 0;
+    });
+}
+
+int qvg_jit_check(uint32_t n_qubits, uint32_t precision, const qvg_gate *ops, uint64_t count, uint64_t *passes_out,
+                  uint64_t *compiled_out, char *err, uint64_t err_cap) {
+    return guarded([&] {
+        if (precision != QVG_C64 && precision != QVG_C128) throw Validation("precision must be 64 or 128");
+        if (n_qubits < 1 || n_qubits > 40) throw Validation("n_qubits must be in [1, 40]");
+        if (count && !ops) throw Validation("null op array");
+        for (uint64_t i = 0; i < count; ++i) validate_op(ops[i], n_qubits, i);
+        const TileShape shape = default_shape(precision);
+        PlanOptions po;
+        po.n = n_qubits;
+        po.amp_bytes = precision == QVG_C128 ? 16 : 8;
+        po.tile_qubits = shape.tile_qubits;
+        po.carriers = shape.carriers;
+        po.sub_bits = shape.sub_bits;
+        small_state_shape(po, precision, n_qubits, false);
+        const Plan plan = plan_ops(ops, count, po);
+        uint64_t passes = 0, compiled = 0;
+        std::string first;
+        for (const Pass &p : plan.passes) {
+            if (p.kind != PASS_TILE) continue;
+            ++passes;
+            const TileGeom &g = p.geom;
+            const unsigned threads = 1u << (g.k - g.sub);
+            const JitVariant jv{(int)po.amp_bytes, g.sub, false, threads <= 128 ? 128 : threads <= 256 ? 256 : 512,
+                                kClsSets[class_set_index(g.cls_set)]};
+            const std::string e = jit_compile(jit_source(g, plan.tile_ops.data() + p.op_begin, jv), nullptr);
+            if (e.empty()) ++compiled;
+            else if (first.empty()) first = e;
+        }
+        if (passes_out) *passes_out = passes;
+        if (compiled_out) *compiled_out = compiled;
+        if (err && err_cap) {
+            const size_t n = std::min<size_t>(first.size(), err_cap - 1);
+            std::memcpy(err, first.data(), n);
+            err[n] = 0;
+        }
     });
 }
 

@@ -13,8 +13,16 @@
 // reference. Complex64 (not in the reference) lets the compiler use FFMA.
 #pragma once
 
+#ifndef __CUDACC_RTC__
 #include <cuda_runtime.h>
 #include <stdint.h>
+#else  // NVRTC (the JIT-specialised tile passes, qvg_jit.hpp): no system headers
+typedef unsigned long long uint64_t;
+typedef long long int64_t;
+typedef unsigned int uint32_t;
+typedef int int32_t;
+typedef unsigned char uint8_t;
+#endif
 
 namespace qvg {
 

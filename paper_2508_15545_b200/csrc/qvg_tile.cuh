@@ -28,9 +28,13 @@
 // 16 register amplitudes per thread.
 #pragma once
 
+#ifndef __CUDACC_RTC__
 #include <cuda.h>  // CUtensorMap (k_tile_tma's tensor-map descriptor; types only, no driver link)
 #include <cuda_runtime.h>
 #include <stdint.h>
+#else  // NVRTC (qvg_jit.hpp): the descriptor's layout only (128 B, 64-B aligned)
+typedef struct alignas(64) { unsigned long long opaque[16]; } CUtensorMap;
+#endif
 
 #include "qvg_kernels.cuh"
 
@@ -451,14 +455,42 @@ __device__ __forceinline__ void op_dispatch(int d, typename Cplx<R>::T (&v)[1 <<
 #define QVG_SUB5_MINB 5  // complex64 32-amplitude subcubes, 128 threads: 96 registers
                          // (vs 4 CTAs at 128: C1 -5%, C3 -4%; profiles/r01_sub5_ab.json)
 #endif
-template <class R, int SUB, bool FMA, int MAXT, bool PF, int CM>
-__global__ void __launch_bounds__(MAXT, PF                         ? 2
-                                        : (SUB == 5) ? (MAXT <= 128 ? QVG_SUB5_MINB : 2)
-                                        : (MAXT <= 128 && SUB == 4) ? QVG_SUB4_MINB
-                                        : (MAXT <= 256 && SUB == 4) ? (sizeof(R) == 4 ? QVG_C64_SUB4_256_MINB : QVG_SUB4_256_MINB)
-                                        : (MAXT <= 256 && SUB == 3) ? 4
-                                                                    : 2)
-k_tile(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams prm) {
+template <class R, int SUB, int MAXT, bool PF>
+constexpr int tile_min_blocks() {
+    return PF                           ? 2
+           : (SUB == 5)                 ? (MAXT <= 128 ? QVG_SUB5_MINB : 2)
+           : (MAXT <= 128 && SUB == 4)  ? QVG_SUB4_MINB
+           : (MAXT <= 256 && SUB == 4)  ? (sizeof(R) == 4 ? QVG_C64_SUB4_256_MINB : QVG_SUB4_256_MINB)
+           : (MAXT <= 256 && SUB == 3)  ? 4
+                                        : 2;
+}
+
+// The op program of a register group, run by k_tile_body between the group's
+// load and store. TileOpsRuntime interprets the pass's records (one jump-table
+// dispatch per op); a JIT-specialised pass (qvg_jit.hpp) supplies a program
+// with every op's body, bits and tests fixed at compile time and its matrix
+// read from the same parameter-bank record.
+struct TileOpsRuntime {
+    template <class R, int SUB, bool FMA, int CM>
+    static __device__ __forceinline__ void apply(int /*gi*/, typename Cplx<R>::T (&v)[1 << SUB], uint64_t base,
+                                                 const TileOp *ops, int rec, int nops) {
+        for (int i = 0; i < nops; ++i) {
+            const TileOp &op = ops[rec + i];
+            if ((base & op.greq) != op.greq) continue;  // control outside the tile is 0
+            const int sl = op.slot;
+            // tile bits outside the group are bits of the thread index
+            // (the planner stores their thread-bit positions)
+            if ((sl & kSlotCtlTest) && !((threadIdx.x >> op.cbit) & 1u)) continue;
+            bool t1 = false;
+            if (sl & kSlotT1) t1 = op.tbit >= 0 ? ((threadIdx.x >> op.tbit) & 1u) != 0 : (base & op.gtgt) != 0;
+            // complex64 records carry the matrix as 8 floats (tile_record_precision)
+            op_dispatch<R, SUB, FMA, CM>(sl & 0xff, v, reinterpret_cast<const R *>(op.u), t1, (sl & kSlotD0) != 0);
+        }
+    }
+};
+
+template <class R, int SUB, bool FMA, int MAXT, bool PF, int CM, class Ops>
+__device__ __forceinline__ void k_tile_body(typename Cplx<R>::T *__restrict__ psi, const TileParams &prm) {
     using T = typename Cplx<R>::T;
     constexpr int E = 1 << SUB;
     const TileGeom &g = prm.g;
@@ -610,18 +642,7 @@ k_tile(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams
 #pragma unroll
                 for (int r = 0; r < E; ++r) v[r] = sm[swz(lidx(r))];
             }
-            for (int i = 0; i < nops; ++i) {
-                const TileOp &op = ops[rec + i];
-                if ((base & op.greq) != op.greq) continue;  // control outside the tile is 0
-                const int sl = op.slot;
-                // tile bits outside the group are bits of the thread index
-                // (the planner stores their thread-bit positions)
-                if ((sl & kSlotCtlTest) && !((threadIdx.x >> op.cbit) & 1u)) continue;
-                bool t1 = false;
-                if (sl & kSlotT1) t1 = op.tbit >= 0 ? ((threadIdx.x >> op.tbit) & 1u) != 0 : (base & op.gtgt) != 0;
-                // complex64 records carry the matrix as 8 floats (tile_record_precision)
-                op_dispatch<R, SUB, FMA, CM>(sl & 0xff, v, reinterpret_cast<const R *>(op.u), t1, (sl & kSlotD0) != 0);
-            }
+            Ops::template apply<R, SUB, FMA, CM>(gi, v, base, ops, rec, nops);
             rec += nops;
             if (gi == g.ngroups - 1 && (g.stage & 2)) {
                 // each thread rewrites only the slots it read, then the tile
@@ -648,6 +669,12 @@ k_tile(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams
         }
         if (use_sm) __syncthreads();  // sm was read this tile; the next tile writes it
     }
+}
+
+template <class R, int SUB, bool FMA, int MAXT, bool PF, int CM>
+__global__ void __launch_bounds__(MAXT, (tile_min_blocks<R, SUB, MAXT, PF>()))
+k_tile(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams prm) {
+    k_tile_body<R, SUB, FMA, MAXT, PF, CM, TileOpsRuntime>(psi, prm);
 }
 
 }  // namespace qvg

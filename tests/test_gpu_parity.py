@@ -494,3 +494,59 @@ def test_subcube_option_bounds(qv, oracle):
         assert np.abs(st.read_state() - want).max() <= 1e-5, sub
     with pytest.raises(qv.ValidationError):
         qv.StateVector.create(10, 64, 0).set_option(qv.OPT_SUB_BITS, 6)
+
+
+# --- JIT-specialised fused passes (QVG_OPT_JIT, csrc/qvg_jit.hpp) -------------------
+@pytest.mark.parametrize("prec", [128, 64])
+def test_jit_passes_bit_exact(qv, oracle, prec):
+    """Every fused pass compiled before launch (mode 3) as a kernel specialised
+    to its op list: complex128 bit-identical to the oracle, complex64 within
+    1e-5 and bit-identical to k_tile; the passes did run as JIT kernels."""
+    rng = np.random.default_rng(5)
+    for trial in range(12):
+        n = int(rng.integers(6, 15))
+        c = qv.random_circuit(n, int(rng.integers(20, 120)), 7000 + trial)
+        want = oracle.simulate(n, gate_array(c))
+        st = qv.StateVector.create(n, prec, 0)
+        st.set_option(qv.OPT_JIT, 3)
+        m = qv.apply_circuit(st, c, fuse=True)
+        got = st.read_state()
+        if m["fused_passes"]:
+            assert st.stats()["jit_passes"] == m["fused_passes"], (trial, st.stats())
+        if prec == 128:
+            assert np.array_equal(got, want), (trial, n, np.abs(got - want).max())
+        else:
+            assert np.abs(got.astype(np.complex128) - want).max() <= 1e-5
+            ref = qv.StateVector.create(n, prec, 0)
+            ref.set_option(qv.OPT_JIT, 0)
+            qv.apply_circuit(ref, c, fuse=True)
+            assert st.max_deviation(ref) <= 1e-6
+
+
+def test_jit_config_circuits_and_graphs(qv, oracle):
+    """The BASELINE circuit shapes (QFT, grid, U3 ladder, Haar sweep) at n = 16
+    through JIT kernels on every pass (mode 3) and through the default mode
+    (async, the passes jit_pays picks) with graph replay: bit-identical to the
+    oracle on every apply; once compiled, the replayed graph holds the JIT
+    kernels (QFT: every pass is real / diagonal, so JIT by default)."""
+    n = 16
+    circs = [qv.qft_circuit(n, 3)[0], qv.grid_circuit(4, 4, 8, 2), qv.u3_ladder_circuit(n, 3, 4),
+             qv.haar_sweep_circuit(n, 9)]
+    for ci, c in enumerate(circs):
+        want = oracle.simulate(n, gate_array(c))
+        st = qv.StateVector.create(n, 128, 0)
+        st.set_option(qv.OPT_JIT, 3)
+        qv.apply_circuit(st, c)
+        assert np.array_equal(st.read_state(), want)
+        assert st.stats()["jit_passes"] > 0
+        st2 = qv.StateVector.create(n, 128, 0)  # defaults: JIT async, graphs auto
+        g = c.gates()
+        for rep in range(5):
+            st2.init_basis(0)
+            st2.apply_gates(g)
+            assert np.array_equal(st2.read_state(), want), rep
+            if rep == 2:
+                qv.jit_info(True)  # drain the compile queue
+        if ci == 0:
+            assert st2.stats()["jit_passes"] > 0
+            assert st2.stats()["graph_replays"] > 0

@@ -219,3 +219,17 @@ def test_capi_validation_codes(qv):
     assert rc == 1 and b"target 5" in lib.qvg_last_error()
     rc = lib.qvg_create(4, 96, 0, ctypes.byref(ctypes.c_void_p()))
     assert rc == 1
+
+
+def test_jit_sources_compile_without_gpu(qv):
+    """The JIT path's generated sources (one per fused pass, csrc/qvg_jit.cu)
+    compile with NVRTC for sm_100a on a host without a GPU: config-shaped
+    circuits in both precisions (c64 uses 32-amplitude subcubes)."""
+    import shutil
+    if not (os.path.exists("/usr/local/cuda/lib64/libnvrtc.so.12") or shutil.which("nvcc")):
+        pytest.skip("no NVRTC in this image")
+    for c in (qv.qft_circuit(14, 1)[0], qv.grid_circuit(3, 4, 4, 1), qv.u3_ladder_circuit(13, 2, 1)):
+        for prec in (128, 64):
+            passes, compiled, err = qv.jit_check(c.n_qubits, c.gates(), prec)
+            assert passes > 0
+            assert compiled == passes, err

@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--tile", type=int, default=0, help="tile qubits (0: the precision's default)")
     ap.add_argument("--precision", type=int, default=128)
     ap.add_argument("--pipe", type=int, default=-1, help="QVG_OPT_PIPE (-1: the engine's default)")
+    ap.add_argument("--jit", type=int, default=-1, help="QVG_OPT_JIT (-1: the engine's default; 2 = compile first)")
     a = ap.parse_args()
     n = a.n
     c = {"sweep": lambda: qv.haar_sweep_circuit(n, 2508),
@@ -42,6 +43,8 @@ def main():
         st.set_option(qv.OPT_TILE_QUBITS, a.tile)
     if a.pipe >= 0:
         st.set_option(qv.OPT_PIPE, a.pipe)
+    if a.jit >= 0:
+        st.set_option(qv.OPT_JIT, a.jit)
     st.apply_gates(c.gates())
     st.sync()
     print("ok", st.stats())

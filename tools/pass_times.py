@@ -5,7 +5,10 @@ circuit and variant: every k_tile* launch's duration (median over reps),
 the total, and per pass which variant is fastest ("best" = the sum of
 per-pass minima, i.e. what a per-pass selection would give).
 
-    python tools/pass_times.py [--n 30] [--precision 128] [--pipes 0,4] [--reps 3] > out.json
+    python tools/pass_times.py [--n 30] [--precision 128] [--variants "jit=0;jit=2"] [--reps 3] > out.json
+
+A variant is a ","-separated list of option=value (option = a qv.OPT_* name
+without the prefix, lower case); JIT variants compile before timing.
 """
 import argparse
 import json
@@ -38,7 +41,8 @@ def kernel_times(st, g, reps):
             st.apply_gates(g)
             st.sync()
             torch.cuda.synchronize()
-        ev = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA and "k_" in e.name]
+        ev = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA
+              and ("k_" in e.name or "qvg_jit" in e.name)]
         ev.sort(key=lambda e: e.time_range.start)
         runs.append([(e.name, (e.time_range.end - e.time_range.start) / 1e3) for e in ev])
     return runs
@@ -48,14 +52,18 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=30)
     ap.add_argument("--precision", type=int, default=128)
-    ap.add_argument("--pipes", default="0,4")
+    ap.add_argument("--variants", default="jit=0;jit=2")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--only", default="")
     a = ap.parse_args()
-    pipes = [int(x) for x in a.pipes.split(",")]
+    variants = [v.strip() for v in a.variants.split(";") if v.strip()]
     only = set(filter(None, a.only.split(",")))
     st = qv.StateVector.create(a.n, a.precision, 0)
+    ref = qv.StateVector.create(a.n, a.precision, 0)  # k_tile's result (JIT off), for the bitwise check
+    ref.set_option(qv.OPT_JIT, 0)
+    ref.set_option(qv.OPT_GRAPH, 0)
     st.set_option(qv.OPT_GRAPH, 0)
+    st.set_option(qv.OPT_TIMING, 0)
     rows = []
     for name, c in circuits(a.n):
         if only and name not in only:
@@ -63,27 +71,50 @@ def main():
         g = c.gates()
         row = {"circuit": name, "ops": len(c), "variants": {}}
         per = {}
-        for p in pipes:
-            st.set_option(qv.OPT_PIPE, p)
+        ref.init_basis(0)
+        ref.apply_gates(g)
+        for var in variants:
+            st.set_option(qv.OPT_JIT, 0)
+            st.set_option(qv.OPT_PIPE, 0)
+            for kv in var.split(","):
+                k, v = kv.split("=")
+                st.set_option(getattr(qv, "OPT_" + k.strip().upper()), int(v))
             st.init_basis(0)
-            st.apply_gates(g)  # warm-up (and module load)
+            st.apply_gates(g)  # warm-up (module load, JIT compiles in mode 2)
             st.sync()
+            dev = st.max_deviation(ref)
+            qv.jit_info(True)
+            st.reset_stats()
+            stream = torch.cuda.ExternalStream(st.stream())
+            ev_ms = []
+            for _ in range(a.reps):  # whole-circuit device time, CUDA events on the state's stream
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                st.apply_gates(g, sync=False)
+                e1.record(stream)
+                st.sync()
+                ev_ms.append(e0.elapsed_time(e1))
+            st.reset_stats()
             runs = kernel_times(st, g, a.reps)
-            names = [nm for nm, _ in runs[0]]
-            ms = [statistics.median(r[i][1] for r in runs) for i in range(len(names))]
-            per[p] = ms
-            row["variants"][f"pipe{p}"] = {"total_ms": sum(ms), "passes": len(ms), "pass_ms": [round(x, 4) for x in ms],
-                                           "kernels": sorted(set(names))}
+            npass = min(len(r) for r in runs)  # CUPTI can drop records: use the common prefix
+            names = [nm for nm, _ in runs[0][:npass]]
+            ms = [statistics.median(r[i][1] for r in runs) for i in range(npass)]
+            per[var] = ms
+            row["variants"][var] = {"event_ms": statistics.median(ev_ms), "total_ms": sum(ms), "passes": len(ms), "pass_ms": [round(x, 4) for x in ms],
+                                    "kernels": sorted(set(n.split("(")[0] for n in names)),
+                                    "jit_passes": st.stats()["jit_passes"] / a.reps, "max_dev_vs_k_tile": dev}
         if len({len(v) for v in per.values()}) == 1:
             npass = len(next(iter(per.values())))
-            best = [min(per[p][i] for p in pipes) for i in range(npass)]
+            best = [min(per[p][i] for p in variants) for i in range(npass)]
             row["best_of"] = {"total_ms": sum(best),
-                              "pick": [min(pipes, key=lambda p: per[p][i]) for i in range(npass)]}
+                              "pick": [min(variants, key=lambda p: per[p][i]) for i in range(npass)]}
         rows.append(row)
-        print(name, " ".join(f"{k}={v['total_ms']:.2f}ms/{v['passes']}" for k, v in row["variants"].items()),
+        print(name, " ".join(f"{k}={v['event_ms']:.2f}ms(cupti {v['total_ms']:.2f}/{v['passes']}) dev={v['max_dev_vs_k_tile']:.1e}"
+                             for k, v in row["variants"].items()),
               f"best={row.get('best_of', {}).get('total_ms', float('nan')):.2f}", file=sys.stderr, flush=True)
-    print(json.dumps({"n": a.n, "precision": a.precision, "reps": a.reps, "timing": "CUPTI kernel activity "
-                      "(torch.profiler), median over reps", "rows": rows}, indent=1))
+    print(json.dumps({"n": a.n, "precision": a.precision, "reps": a.reps, "timing": "event_ms: CUDA events around the "
+                      "circuit on the state's stream; pass_ms: CUPTI kernel activity (torch.profiler; it can miss "
+                      "launches, so total_ms/passes may undercount); medians over reps", "rows": rows}, indent=1))
 
 
 if __name__ == "__main__":
