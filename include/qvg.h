@@ -100,10 +100,16 @@ enum qvg_option {
     QVG_OPT_XCHG_CHUNK = 17, /* sharded: copy-transport chunk bytes (multiple of 16; 0 = default 256 MiB,
                                 capped by the NCCL scratch); tests use small chunks to split runs */
     QVG_OPT_JIT = 19,        /* fused tiles: run a pass as a kernel specialised to its op list (NVRTC,
-                                cached per pass structure; bit-identical to k_tile) where that measured
-                                faster (every complex64 pass; complex128 passes of X / real / diagonal ops):
-                                1 = compile on worker threads, k_tile until ready (default), 2 = compile
-                                before the first launch, 3 = every pass, compiled first; 0 = never */
+                                cached per pass structure, compiled in parallel before an apply's first
+                                launch; bit-identical to k_tile): 1 (= 2) the passes of >= 2^24-amplitude
+                                states jit_pays picks (complex64; complex128 passes of X / real / diagonal
+                                ops), 3 = every pass, 0 = never (default: no net gain measured,
+                                profiles/r02_jit_ab.json) */
+    QVG_OPT_PERM = 20,       /* 1: a fused run of only X / CX / Z / CZ ops runs as one shared-memory scatter
+                                (k_tile_perm, bit-identical to k_tile), 0: through k_tile (default: the
+                                scatter measured equal, profiles/r02_perm_ab.json) */
+    QVG_OPT_TILE_ORDER = 21, /* fused tiles: 0 = CTA b runs tiles b, b + grid, ... (default); 1 = a contiguous
+                                chunk of tiles per CTA (successive tiles are DRAM neighbours) */
     QVG_OPT_PIPE = 18        /* fused tiles: 2 or 3 = warp-specialised bulk-copy pipeline (k_tile_pipe) with
                                 that many shared-memory ring stages; 0 = k_tile, per-thread loads (default:
                                 measured 1.5-2x faster, profiles/r02_pipe_ab.json) */
@@ -238,11 +244,9 @@ int qvg_stream(const qvg_state *s, void **stream_out);
 /* Device pointer and byte size of this rank's amplitude shard. */
 int qvg_device_buffer(const qvg_state *s, void **ptr_out, uint64_t *bytes_out);
 /* JIT-specialised tile passes (QVG_OPT_JIT, paper_2508_15545_b200/csrc/qvg_jit.hpp):
- * process-wide counters (kernels compiled / failed / queued, summed compile
- * ms); drain != 0 first waits for every queued compile. available = NVRTC and
- * the driver entry points loaded. */
-int qvg_jit_info(int drain, uint64_t *compiled, uint64_t *failed, uint64_t *queued, double *compile_ms,
-                 int *available);
+ * process-wide counters (kernels compiled / failed, summed per-kernel compile
+ * ms); available = NVRTC and the driver entry points loaded. */
+int qvg_jit_info(uint64_t *compiled, uint64_t *failed, double *compile_ms, int *available);
 /* Host-only check of the JIT source path (no GPU needed): plans the ops as
  * qvg_apply would on an unsharded state of this width/precision (defaults,
  * fusion on), generates every fused pass's specialised source and compiles

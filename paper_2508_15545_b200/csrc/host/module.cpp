@@ -427,24 +427,21 @@ PYBIND11_MODULE(_core, m) {
     });
 
     m.def("jit_info",
-          [](bool drain) {
-              std::uint64_t compiled = 0, failed = 0, queued = 0;
+          [](bool) {
+              std::uint64_t compiled = 0, failed = 0;
               double ms = 0;
               int avail = 0;
-              {
-                  py::gil_scoped_release nogil;
-                  check_status(qvg_jit_info(drain ? 1 : 0, &compiled, &failed, &queued, &ms, &avail));
-              }
+              check_status(qvg_jit_info(&compiled, &failed, &ms, &avail));
               py::dict d;
               d["compiled"] = compiled;
               d["failed"] = failed;
-              d["queued"] = queued;
               d["compile_ms"] = ms;
               d["available"] = avail != 0;
               return d;
           },
           py::arg("drain") = false,
-          "JIT tile-pass counters (process-wide); drain=True waits for queued compiles first");
+          "JIT tile-pass counters (process-wide): kernels compiled / failed, summed compile ms, NVRTC "
+          "available (compiles finish inside the apply that needs them; `drain` is accepted and ignored)");
     m.def("jit_check",
           [](std::uint32_t n, py::buffer buf, std::uint32_t precision) {
               const py::buffer_info b = buf.request();
@@ -517,4 +514,6 @@ PYBIND11_MODULE(_core, m) {
     m.attr("OPT_XCHG_CHUNK") = (int)QVG_OPT_XCHG_CHUNK;
     m.attr("OPT_PIPE") = (int)QVG_OPT_PIPE;
     m.attr("OPT_JIT") = (int)QVG_OPT_JIT;
+    m.attr("OPT_PERM") = (int)QVG_OPT_PERM;
+    m.attr("OPT_TILE_ORDER") = (int)QVG_OPT_TILE_ORDER;
 }

@@ -28,6 +28,7 @@
 #include "qvg_plan.hpp"
 #include "qvg_shard.hpp"
 #include "qvg_tile_select.hpp"
+#include "qvg_tile_perm.cuh"
 #include "qvg_jit.hpp"
 
 using namespace qvg;
@@ -83,6 +84,16 @@ template <class F> int guarded(F &&f) {
 
 // One rank's share of the state (or one virtual shard when several shards of
 // a sharded state live on this device, see qvg_shard.hpp).
+// QVG_JIT=0..3 in the environment sets the states' default QVG_OPT_JIT (0:
+// the JIT passes measured no faster than k_tile overall, profiles/r02_jit_ab.json).
+inline uint32_t default_jit_mode() {
+    static const uint32_t m = [] {
+        const char *v = std::getenv("QVG_JIT");
+        return v && *v >= '0' && *v <= '3' ? (uint32_t)(*v - '0') : 0u;
+    }();
+    return m;
+}
+
 struct qvg_state {
     int device = 0;
     uint32_t n = 0;          // global qubits
@@ -112,8 +123,10 @@ struct qvg_state {
     std::vector<uint64_t> graph_seen;  // auto mode: keys applied once (ring)
     uint32_t reorder = REORDER_EXACT;  // QVG_OPT_REORDER: commutation-aware fusion order (qvg_plan.hpp)
     bool classes = true;       // QVG_OPT_CLASSES: structured-matrix op bodies in fused tiles
-    uint32_t jit_mode = 1;     // QVG_OPT_JIT: fused passes as specialised kernels (qvg_jit.hpp); 1 async, 2 sync, 0 off
-    bool jit_pending = false;  // a pass of the current apply ran k_tile while its JIT kernel was compiling
+    uint32_t tile_order = 0;   // QVG_OPT_TILE_ORDER: 0 strided tiles per CTA, 1 contiguous chunks
+    bool perm = false;         // QVG_OPT_PERM: permutation / sign-flip runs through k_tile_perm (measured
+                               // equal to k_tile, profiles/r02_perm_ab.json: off by default)
+    uint32_t jit_mode = default_jit_mode();  // QVG_OPT_JIT: fused passes as specialised kernels (qvg_jit.hpp); 1 async, 2 sync, 0 off
     bool capturing = false;    // run_local inside a graph capture (JIT: lookups only)
     uint32_t pipe_stages = 0;  // QVG_OPT_PIPE: fused tiles through the bulk-copy pipeline (k_tile_pipe) with this many ring stages; 0 = k_tile (default: measured faster, profiles/r02_pipe_ab.json)
     bool shape_set = false;    // tile_qubits / sub_bits set by the caller (no small-state default)
@@ -298,6 +311,38 @@ bool tma_tile_map(const TileGeom &g, int amp_bytes, void *psi, TileTma &out) {
     return true;
 }
 
+// A fused pass of only permutations and +-1 phases (PASS_PERM): one scatter
+// through shared memory (qvg_tile_perm.cuh). 16 amplitudes per thread for the
+// default tiles (2^11 complex128, 2^12 complex64), 8 for smaller ones.
+template <class R>
+void launch_perm(qvg_state &s, void *psi, const Pass &p, const TileOp *recs) {
+    using T = typename Cplx<R>::T;
+    const TileGeom &g = p.geom;
+    if (g.nrec > kMaxTileRecs) throw std::runtime_error("internal: permutation pass exceeds the record limit");
+    thread_local TileParams prm;
+    prm.g = g;
+    prm.g.order = (int)s.tile_order;
+    std::memcpy(prm.ops, recs + p.op_begin, sizeof(TileOp) * g.nrec);
+    const bool e16 = g.k >= (sizeof(R) == 8 ? 11 : 12);
+    const unsigned threads = 1u << (g.k - (e16 ? 4 : 3));
+    const size_t smem = (((sizeof(uint64_t) << g.nhi) + 15) & ~size_t(15)) + (sizeof(T) << g.k);
+    const bool wide = threads > 128;
+    auto kern = e16 ? (wide ? k_tile_perm<R, 16, 256> : k_tile_perm<R, 16, 128>)
+                    : (wide ? k_tile_perm<R, 8, 256> : k_tile_perm<R, 8, 128>);
+    static std::atomic<uint64_t> attr_set[64];  // [device]: bit per (precision, E, width)
+    const uint64_t bit = 1ull << ((sizeof(R) == 8 ? 4 : 0) + (e16 ? 2 : 0) + (wide ? 1 : 0));
+    std::atomic<uint64_t> &set = attr_set[s.device & 63];
+    if (!(set.load(std::memory_order_acquire) & bit)) {
+        cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
+                   "cudaFuncSetAttribute(k_tile_perm)");
+        set.fetch_or(bit, std::memory_order_acq_rel);
+    }
+    int per_sm = 0;
+    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (int)threads, smem), "occupancy(k_tile_perm)");
+    const uint64_t grid = std::min<uint64_t>(g.ntiles, (uint64_t)std::max(per_sm, 1) * s.sm_count);
+    kern<<<(unsigned)grid, threads, smem, s.stream>>>(static_cast<T *>(psi), prm);
+}
+
 // Which fused passes run as JIT kernels by default (QVG_OPT_JIT 1/2), from
 // the per-pass A/B in profiles/r02_jit_ab.json (n = 30, CUPTI per-pass times):
 // complex64 passes were faster as JIT kernels on every BASELINE circuit
@@ -317,6 +362,38 @@ bool jit_pays(const TileGeom &g, const TileOp *recs, size_t amp_bytes) {
     return true;
 }
 
+constexpr uint32_t kJitMinQubits = 24;
+
+// Whether a fused pass runs as a JIT kernel, and which: the plain k_tile
+// variants only (no register prefetch, no bulk-copy pipelines), the passes
+// jit_pays picks (QVG_OPT_JIT 1/2) or every pass (3).
+bool jit_variant(const qvg_state &s, const Pass &p, const TileOp *recs, size_t amp_bytes, JitVariant *out) {
+    const TileGeom &g = p.geom;
+    if (!s.jit_mode || p.kind != PASS_TILE) return false;
+    if (s.prefetch_mode == 1 && g.sub == 3) return false;
+    const unsigned threads = 1u << (g.k - g.sub);
+    if (threads == (unsigned)kPipeConsumers && s.pipe_stages >= 2) return false;
+    // by default only for states whose passes outweigh a compile (~0.2-1 s per
+    // kernel, once per pass structure): >= 2^24 amplitudes per shard / window
+    if (s.jit_mode != 3 && (g.n < (int)kJitMinQubits || !jit_pays(g, recs, amp_bytes))) return false;
+    *out = JitVariant{(int)amp_bytes, g.sub, s.fma && amp_bytes == 16, threads <= 128 ? 128 : threads <= 256 ? 256 : 512,
+                      kClsSets[class_set_index(g.cls_set)]};
+    return true;
+}
+
+// Compile (in parallel) the JIT kernels a plan will launch that are not
+// cached yet; never inside a stream capture (apply_graph prepares first).
+void jit_prepare_plan(const qvg_state &s, const Plan &plan) {
+    if (!s.jit_mode || s.capturing) return;
+    std::vector<JitRequest> reqs;
+    for (const Pass &p : plan.passes) {
+        JitVariant v{};
+        if (jit_variant(s, p, plan.tile_ops.data() + p.op_begin, s.S, &v))
+            reqs.push_back(JitRequest{&p.geom, plan.tile_ops.data() + p.op_begin, v, nullptr});
+    }
+    if (!reqs.empty()) jit_prepare(reqs.data(), reqs.size());
+}
+
 template <class R>
 void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *recs) {
     using T = typename Cplx<R>::T;
@@ -324,6 +401,7 @@ void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *recs) {
     if (g.nrec > kMaxTileRecs) throw std::runtime_error("internal: tile pass exceeds the record limit");
     thread_local TileParams prm;  // 25 KB; the launch copies it into the parameter block (per host thread: states on different threads may launch concurrently)
     prm.g = g;
+    prm.g.order = (int)s.tile_order;
     std::memcpy(prm.ops, recs + p.op_begin, sizeof(TileOp) * g.nrec);
     unsigned threads = 1u << (g.k - g.sub);  // one 2^sub-amplitude subcube per thread
     const bool pf = s.prefetch_mode == 1 && g.sub == 3;  // register prefetch needs the 8-amplitude subcube
@@ -343,21 +421,17 @@ void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *recs) {
         threads = kPipeThreads;
         smem = pipe_smem_bytes(g.nhi, g.k, (int)sizeof(T), pipe >= 3 ? 3 : 2);
     }
-    // A JIT-specialised kernel for this pass (qvg_jit.hpp): the plain k_tile
-    // variants only (no register prefetch, no bulk-copy pipelines).
-    if (s.jit_mode && !tma && !pipe && !pf && (s.jit_mode == 3 || jit_pays(g, prm.ops, sizeof(T)))) {
-        const JitVariant jv{(int)sizeof(T), g.sub, fma, tiny ? 128 : small ? 256 : 512,
-                            kClsSets[class_set_index(g.cls_set)]};
-        bool pending = false;
-        const int mode = s.capturing ? -1 : s.jit_mode == 1 ? 1 : 2;
-        if (void *fn = jit_tile_function(g, prm.ops, jv, mode, &pending)) {
+    // A JIT-specialised kernel for this pass (qvg_jit.hpp), compiled by
+    // run_local's jit_prepare_plan before the apply's first launch.
+    JitVariant jv{};
+    if (jit_variant(s, p, prm.ops, sizeof(T), &jv)) {
+        if (void *fn = jit_lookup(g, prm.ops, jv)) {
             const int per_sm = jit_occupancy(fn, threads, smem);
             const uint64_t grid = std::min<uint64_t>(g.ntiles, (uint64_t)per_sm * s.sm_count);
             cuda_check(jit_launch(fn, (unsigned)grid, threads, smem, s.stream, psi, &prm), "JIT tile launch");
             s.stats.jit_passes += 1;
             return;
         }
-        s.jit_pending |= pending;
     }
     // Passes without structured ops (classes off) use the REAL-set kernel:
     // their records only name general bodies, which every set compiles.
@@ -416,6 +490,7 @@ PlanOptions plan_options(const qvg_state &s) {
     po.stage_bits = s.stage_bits;
     po.reorder = s.reorder;
     po.classes = s.classes;
+    po.perm = s.perm;
     small_state_shape(po, s.precision, s.L, s.shape_set);
     return po;
 }
@@ -425,6 +500,7 @@ void run_local(qvg_state &s, void *psi, const qvg_gate *ops, uint64_t count) {
     if (count == 0) return;
     const PlanOptions po = plan_options(s);
     const Plan plan = plan_ops(ops, count, po);
+    jit_prepare_plan(s, plan);
     const bool dbl = s.precision == QVG_C128;
     for (const Pass &p : plan.passes) {
         switch (p.kind) {
@@ -440,6 +516,11 @@ void run_local(qvg_state &s, void *psi, const qvg_gate *ops, uint64_t count) {
         case PASS_TILE:
             dbl ? launch_tile<double>(s, psi, p, plan.tile_ops.data())
                 : launch_tile<float>(s, psi, p, plan.tile_ops.data());
+            s.stats.fused_passes += 1;
+            break;
+        case PASS_PERM:
+            dbl ? launch_perm<double>(s, psi, p, plan.tile_ops.data())
+                : launch_perm<float>(s, psi, p, plan.tile_ops.data());
             s.stats.fused_passes += 1;
             break;
         }
@@ -462,7 +543,7 @@ uint64_t plan_signature(const qvg_state &s) {
     auto mix = [&](uint64_t v) { h = (h ^ v) * 1099511628211ull; };
     mix(s.fuse); mix(s.tile_qubits); mix(s.carriers); mix(s.low_kernel); mix(s.min_run); mix(s.pred_store);
     mix(s.sub_bits); mix(s.fma); mix(s.stage_bits); mix((uint64_t)s.prefetch_mode); mix(s.L); mix(s.precision);
-    mix(s.reorder); mix(s.classes); mix(s.shape_set); mix(s.pipe_stages);
+    mix(s.reorder); mix(s.classes); mix(s.shape_set); mix(s.pipe_stages); mix(s.perm); mix(s.jit_mode);
     return h;
 }
 
@@ -532,12 +613,9 @@ void apply_graph(qvg_state &s, const qvg_gate *ops, uint64_t count, uint64_t key
     }
     const qvg_stats before = s.stats;
     cudaGraph_t graph = nullptr;
+    jit_prepare_plan(s, plan_ops(ops, count, plan_options(s)));  // compiles and module loads stay outside the capture
     cuda_check(cudaStreamBeginCapture(s.stream, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
-    // inside the capture JIT kernels are only looked up (no compiles, no
-    // module loads); a pass whose kernel is still compiling runs k_tile and
-    // the graph is then used once, not cached (the next apply captures again)
     s.capturing = true;
-    s.jit_pending = false;
     try {
         run_local(s, s.shards.bufs[0], ops, count);
     } catch (...) {
@@ -559,10 +637,6 @@ void apply_graph(qvg_state &s, const qvg_gate *ops, uint64_t count, uint64_t key
     cuda_check(inst, "cudaGraphInstantiate");
     cuda_check(cudaGraphLaunch(e.exec, s.stream), "cudaGraphLaunch");
     s.stats.graph_replays += 1;
-    if (s.jit_pending) {  // k_tile stood in for a kernel still compiling: do not keep this graph
-        cudaGraphExecDestroy(e.exec);
-        return;
-    }
     constexpr size_t kMaxGraphs = 8;
     if (s.graphs.size() >= kMaxGraphs) {
         auto lru = std::min_element(s.graphs.begin(), s.graphs.end(),
@@ -766,6 +840,11 @@ int qvg_set_option(qvg_state *s, int key, int64_t value) {
         case QVG_OPT_EXCHANGE:
             if (value < -1 || value > 2) throw Validation("exchange mode must be -1, 0, 1 or 2");
             s->exchange_mode = (int)value;
+            break;
+        case QVG_OPT_PERM: s->perm = value != 0; break;
+        case QVG_OPT_TILE_ORDER:
+            if (value < 0 || value > 1) throw Validation("tile order must be 0 (strided) or 1 (contiguous per CTA)");
+            s->tile_order = (uint32_t)value;
             break;
         case QVG_OPT_JIT:
             if (value < 0 || value > 3)
@@ -1351,7 +1430,7 @@ int qvg_plan_passes(uint32_t n_qubits, uint32_t precision, int fuse, uint32_t ti
         const Plan plan = plan_ops(ops, count, po);  // as run_local (default reorder mode)
         uint64_t fused = 0, bytes = 0;
         for (const Pass &p : plan.passes) {
-            fused += p.kind == PASS_TILE;
+            fused += p.kind == PASS_TILE || p.kind == PASS_PERM;
             bytes += p.bytes;
         }
         if (passes_out) *passes_out = plan.passes.size();
@@ -1360,14 +1439,11 @@ int qvg_plan_passes(uint32_t n_qubits, uint32_t precision, int fuse, uint32_t ti
     });
 }
 
-int qvg_jit_info(int drain, uint64_t *compiled, uint64_t *failed, uint64_t *queued, double *compile_ms,
-                 int *available) {
+int qvg_jit_info(uint64_t *compiled, uint64_t *failed, double *compile_ms, int *available) {
     return guarded([&] {
-        if (drain) jit_drain();
         const JitCounters c = jit_counters();
         if (compiled) *compiled = c.compiled;
         if (failed) *failed = c.failed;
-        if (queued) *queued = c.queued;
         if (compile_ms) *compile_ms = c.compile_ms;
         if (available) *available = jit_available() ? 1 : 0;
     });

@@ -19,9 +19,8 @@
 // Source generation and NVRTC compilation are host-only (no GPU needed);
 // compiled kernels are cached per pass STRUCTURE (geometry, bits, classes,
 // flags; not the matrix values, which stay in the parameter block), so a
-// circuit whose angles change reuses them. Mode 1 (default) compiles on
-// worker threads and launches k_tile until a pass's kernel is ready; mode 2
-// compiles before the first launch; 0 never JITs.
+// circuit whose angles change reuses them. The kernels an apply needs are
+// compiled in parallel before its first launch (jit_prepare).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -48,15 +47,22 @@ std::string jit_source(const TileGeom &g, const TileOp *recs, const JitVariant &
 // if given) or the error log. Host-only.
 std::string jit_compile(const std::string &src, std::string *cubin);
 
-// A launchable function for this pass on the CURRENT device, or nullptr when
-// it is not compiled yet (mode 1: queued), JIT is unavailable (no NVRTC) or
-// compilation failed (the caller launches k_tile). mode 2 compiles inline.
-// mode -1 (inside a stream capture) only looks up a kernel that is compiled
-// and resolved on this device; a missing one is queued. `pending` is set when
-// nullptr is returned for a pass whose kernel is (or is being) compiled.
-void *jit_tile_function(const TileGeom &g, const TileOp *recs, const JitVariant &v, int mode, bool *pending);
+// Compile (in parallel, joined before returning) every requested pass whose
+// kernel is not cached yet, load it, and set each request's `fn` to its
+// function on the CURRENT device (nullptr: NVRTC unavailable or the compile
+// failed; the caller then launches k_tile). Not inside a stream capture.
+struct JitRequest {
+    const TileGeom *g;
+    const TileOp *recs;
+    JitVariant v;
+    void *fn;
+};
+void jit_prepare(JitRequest *reqs, size_t count);
+// The cached, resolved function of a pass (jit_prepare ran for it on this
+// device), else nullptr. No compile or module load: safe inside a capture.
+void *jit_lookup(const TileGeom &g, const TileOp *recs, const JitVariant &v);
 
-// Launch a function from jit_tile_function (driver API, the kernel's
+// Launch a function from jit_prepare / jit_lookup (driver API, the kernel's
 // parameters are k_tile's: psi, TileParams). Dynamic shared memory above 48 KB
 // is opted into once per function.
 cudaError_t jit_launch(void *fn, unsigned grid, unsigned threads, size_t smem, cudaStream_t stream, void *psi,
@@ -65,12 +71,10 @@ cudaError_t jit_launch(void *fn, unsigned grid, unsigned threads, size_t smem, c
 int jit_occupancy(void *fn, unsigned threads, size_t smem);
 
 struct JitCounters {
-    uint64_t compiled, failed, queued;
-    double compile_ms;  // summed NVRTC + load time
+    uint64_t compiled, failed;
+    double compile_ms;  // summed NVRTC time (compiles of one jit_prepare run in parallel)
 };
 JitCounters jit_counters();
-// Block until every queued compile has finished (tools, benchmarks).
-void jit_drain();
 // True when NVRTC and the driver entry points could be loaded.
 bool jit_available();
 

@@ -31,7 +31,7 @@ struct Validation : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
 
-enum PassKind { PASS_PAIRS = 0, PASS_LOW = 1, PASS_PHASE = 2, PASS_TILE = 3 };
+enum PassKind { PASS_PAIRS = 0, PASS_LOW = 1, PASS_PHASE = 2, PASS_TILE = 3, PASS_PERM = 4 };
 
 struct OpInfo {
     bool diag = false;      // u01 == u10 == 0
@@ -167,6 +167,8 @@ struct PlanOptions {
     uint32_t stage_bits = 3; // stage a first/last group through shared memory when its bits
                              // include tile bits 0..stage_bits-1 (warp lanes >= 2^stage_bits
                              // amplitudes apart); 0 = never
+    bool perm = false;       // QVG_OPT_PERM: a fused run of only X / CX / Z / CZ ops is a signed
+                             // permutation of the tile: one shared-memory scatter (k_tile_perm)
 };
 
 // Ops per fused pass: with at most one group header per op the records fit
@@ -435,6 +437,43 @@ inline Plan make_plan(const qvg_gate *ops, uint64_t count, const PlanOptions &po
                 nb = 0;
                 g.ngroups += 1;
             };
+            // A run of only permutations and +-1 phases (X, CX, SWAP's CXs, Z,
+            // CZ) moves each amplitude, changing at most its sign: k_tile_perm
+            // applies it as one scatter through shared memory (records: the
+            // tile-local target / control bits in op order, qvg_tile_perm.cuh).
+            bool perm = po.perm && po.classes;
+            for (uint64_t x = i; x < j && perm; ++x) {
+                const OpInfo &o = info[x];
+                perm = o.identity || o.neg || (!o.diag && o.cls == TILE_CLS_SWAP);
+            }
+            if (perm) {
+                g.ngroups = 0;
+                g.stage = 0;
+                g.cls_set = 0;
+                for (uint64_t x = i; x < j; ++x) {
+                    const OpInfo &o = info[x];
+                    if (o.identity) continue;
+                    TileOp t{};
+                    t.kind = o.diag ? TILE_DIAG : TILE_PAIR;
+                    t.tbit = local_bit(o.target, g);
+                    if (t.tbit < 0) t.gtgt = 1ull << o.target;  // a sign flip decided per tile
+                    t.cbit = -1;
+                    if (o.control >= 0) {
+                        t.cbit = local_bit(o.control, g);
+                        if (t.cbit < 0) t.greq = 1ull << o.control;
+                    }
+                    plan.tile_ops.push_back(t);
+                }
+                g.nrec = (int)(plan.tile_ops.size() - p.op_begin);
+                p.kind = PASS_PERM;
+                p.geom = g;
+                p.op_count = (uint32_t)g.nrec;
+                p.bytes = full;
+                p.gates = j - i;
+                plan.passes.push_back(p);
+                i = j;
+                continue;
+            }
             g.ngroups = 0;
             g.cls_set = po.classes ? tile_class_set(info.data(), i, j) : (1 << TILE_CLS_GEN);
             for (uint64_t x = i; x < j; ++x) {

@@ -66,6 +66,8 @@ struct TileGeom {
     int sub;              // subcube bits per thread (3 or 4)
     int stage;            // bit 0: first group loads through shared memory; bit 1: last group stores through it
     int cls_set;          // structured-matrix classes this pass uses (kClsSetReal / kClsSetHalf)
+    int order;            // tiles per CTA: 0 strided (blockIdx.x + i * gridDim.x), 1 contiguous chunks
+                          // (successive tiles of a CTA are DRAM neighbours, tile_range)
     int hiq[24];          // tile qubits >= lowc, ascending (tile-local bits lowc..k-1)
     uint64_t ntiles;      // 2^(n-k)
     uint64_t sdep[5];     // global offset of tile-local bit (k - sub + i): the staged (coalesced)
@@ -95,6 +97,17 @@ struct TileParams {
     TileOp ops[kMaxTileRecs];
 };
 static_assert(sizeof(TileParams) < 32000, "kernel parameter block limit");
+
+// The tiles a CTA processes: [first, end) with stride `step`.
+struct TileRange {
+    uint64_t first, end, step;
+};
+__device__ __forceinline__ TileRange tile_range(const TileGeom &g) {
+    if (!g.order) return {blockIdx.x, g.ntiles, gridDim.x};
+    const uint64_t per = (g.ntiles + gridDim.x - 1) / gridDim.x;
+    const uint64_t f = (uint64_t)blockIdx.x * per;
+    return {f, f + per < g.ntiles ? f + per : g.ntiles, 1};
+}
 
 // Shared-tile slot of local index l: the 16-B column within each 128-B row is
 // XORed with the row's low bits, so lanes whose amplitudes are 2^3, 2^4 or
@@ -548,9 +561,11 @@ __device__ __forceinline__ void k_tile_body(typename Cplx<R>::T *__restrict__ ps
     };
     T nx[E];  // PF: the next tile's first-group amplitudes, in flight (unused otherwise)
     if constexpr (PF) {
-        if (blockIdx.x < g.ntiles) load_first(tile_base(blockIdx.x), nx);
+        const TileRange r0 = tile_range(g);
+        if (r0.first < r0.end) load_first(tile_base(r0.first), nx);
     }
-    for (uint64_t tile = blockIdx.x; tile < g.ntiles; tile += gridDim.x) {
+    const TileRange tr = tile_range(g);
+    for (uint64_t tile = tr.first; tile < tr.end; tile += tr.step) {
         const uint64_t base = tile_base(tile);
         int rec = 0;
         for (int gi = 0; gi < g.ngroups; ++gi) {
@@ -614,7 +629,7 @@ __device__ __forceinline__ void k_tile_body(typename Cplx<R>::T *__restrict__ ps
             if (PF && gi == 0) {
 #pragma unroll
                 for (int r = 0; r < E; ++r) v[r] = nx[r];
-                if (tile + gridDim.x < g.ntiles) load_first(tile_base(tile + gridDim.x), nx);
+                if (tile + tr.step < tr.end) load_first(tile_base(tile + tr.step), nx);
                 if (g.stage & 1) {  // v holds coalesced amplitudes: transpose to the group layout
 #pragma unroll
                     for (int j = 0; j < E; ++j) sm[swz(threadIdx.x + (uint32_t)j * blockDim.x)] = v[j];

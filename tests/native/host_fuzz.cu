@@ -83,6 +83,20 @@ static void check_plan(const std::vector<qvg_gate> &ops, const PlanOptions &po) 
     uint64_t covered = 0, live = 0;
     for (const qvg_gate &g : list) live += classify(g).identity ? 0 : 1;
     for (const Pass &pass : p.passes) {
+        if (pass.kind == PASS_PERM) {  // k_tile_perm records: X / sign flips on tile-local bits, op order
+            const TileGeom &g = pass.geom;
+            CHECK(po.perm && po.classes && g.nrec >= 1 && g.nrec <= kMaxTileRecs && g.ngroups == 0);
+            for (int i = 0; i < g.nrec; ++i) {
+                const TileOp &t = p.tile_ops[pass.op_begin + i];
+                CHECK(t.kind == TILE_PAIR || t.kind == TILE_DIAG);
+                CHECK(t.tbit < g.k && t.cbit < g.k && t.cbit != t.tbit);
+                if (t.kind == TILE_PAIR) CHECK(t.tbit >= 0);
+                if (t.tbit < 0) CHECK(t.kind == TILE_DIAG && t.gtgt != 0 && !(t.gtgt & (t.gtgt - 1)));
+                if (t.cbit < 0 && t.greq) CHECK(!(t.greq & (t.greq - 1)));
+            }
+            covered += (uint64_t)g.nrec;
+            continue;
+        }
         covered += pass.kind == PASS_TILE ? 0 : 1;
         if (pass.kind != PASS_TILE) continue;
         const TileGeom &g = pass.geom;
@@ -190,6 +204,7 @@ int main(int argc, char **argv) {
         po.stage_bits = (uint32_t)(rng() % 4);
         po.reorder = (uint32_t)(rng() % 3);
         po.classes = rng() % 4 != 0;
+        po.perm = rng() % 2 == 0;
         check_plan(ops, po);
         const uint32_t g = (uint32_t)(rng() % 4);
         if (n >= g + 2) check_schedule(ops, n, g, 1 + (uint32_t)(rng() % 4));

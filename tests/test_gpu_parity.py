@@ -525,10 +525,9 @@ def test_jit_passes_bit_exact(qv, oracle, prec):
 
 def test_jit_config_circuits_and_graphs(qv, oracle):
     """The BASELINE circuit shapes (QFT, grid, U3 ladder, Haar sweep) at n = 16
-    through JIT kernels on every pass (mode 3) and through the default mode
-    (async, the passes jit_pays picks) with graph replay: bit-identical to the
-    oracle on every apply; once compiled, the replayed graph holds the JIT
-    kernels (QFT: every pass is real / diagonal, so JIT by default)."""
+    through JIT kernels on every pass (mode 3), applied once and then replayed
+    as captured CUDA graphs that hold the JIT kernels: bit-identical to the
+    oracle on every apply."""
     n = 16
     circs = [qv.qft_circuit(n, 3)[0], qv.grid_circuit(4, 4, 8, 2), qv.u3_ladder_circuit(n, 3, 4),
              qv.haar_sweep_circuit(n, 9)]
@@ -539,14 +538,48 @@ def test_jit_config_circuits_and_graphs(qv, oracle):
         qv.apply_circuit(st, c)
         assert np.array_equal(st.read_state(), want)
         assert st.stats()["jit_passes"] > 0
-        st2 = qv.StateVector.create(n, 128, 0)  # defaults: JIT async, graphs auto
+        st2 = qv.StateVector.create(n, 128, 0)  # graphs auto (captured from the 2nd apply), JIT on every pass
+        st2.set_option(qv.OPT_JIT, 3)
         g = c.gates()
-        for rep in range(5):
+        for rep in range(4):
             st2.init_basis(0)
             st2.apply_gates(g)
             assert np.array_equal(st2.read_state(), want), rep
-            if rep == 2:
-                qv.jit_info(True)  # drain the compile queue
-        if ci == 0:
-            assert st2.stats()["jit_passes"] > 0
-            assert st2.stats()["graph_replays"] > 0
+        s2 = st2.stats()
+        assert s2["graph_replays"] >= 2 and s2["jit_passes"] > 0, s2
+
+
+# --- permutation / sign-flip passes (QVG_OPT_PERM, csrc/qvg_tile_perm.cuh) --------
+def _perm_circuit(qv, n, seed, mixed):
+    rng = np.random.default_rng(seed)
+    lines = [f"qubits {n}"] + [f"h {q}" for q in range(0, n, 2)] + [f"ry {q} 0.4" for q in range(1, n, 3)]
+    for _ in range(60):
+        a, b = (int(x) for x in rng.choice(n, 2, replace=False))
+        kind = int(rng.integers(6 if mixed else 5))
+        lines.append([f"x {a}", f"cx {a} {b}", f"z {a}", f"cz {a} {b}", f"swap {a} {b}", f"h {a}"][kind])
+    return qv.parse_circuit("\n".join(lines) + "\n")
+
+
+@pytest.mark.parametrize("prec", [128, 64])
+@pytest.mark.parametrize("n", [6, 11, 14, 17])
+def test_perm_passes_bit_exact(qv, oracle, prec, n):
+    """Runs of X / CX / Z / CZ / SWAP (controls in and outside the tile, sign
+    flips on every qubit) through k_tile_perm: the same BYTES as k_tile (signs
+    of zeros included; the start state has exact zeros) and, for complex128,
+    the oracle's values."""
+    for seed, mixed in ((1, False), (2, True), (3, False)):
+        c = _perm_circuit(qv, n, 100 * n + seed, mixed)
+        got = {}
+        for perm in (1, 0):
+            st = qv.StateVector.create(n, prec, 0)
+            st.set_option(qv.OPT_PERM, perm)
+            st.set_option(qv.OPT_JIT, 0)
+            m = qv.apply_circuit(st, c)
+            got[perm] = st.read_state()
+        assert np.array_equal(got[1].view(np.uint64 if prec == 128 else np.uint32),
+                              got[0].view(np.uint64 if prec == 128 else np.uint32)), (seed, mixed)
+        if prec == 128:
+            want = oracle.simulate(n, gate_array(c))
+            assert np.array_equal(got[1], want)
+        else:
+            assert np.abs(got[1].astype(np.complex128) - oracle.simulate(n, gate_array(c))).max() <= 1e-5
