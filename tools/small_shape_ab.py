@@ -47,8 +47,18 @@ def main():
                 st.sync()
                 ts.append(e0.elapsed_time(e1))
             s = st.stats()
+            # kernel time inside one apply (CUPTI): the rest of device_ms is launch gaps
+            from torch.profiler import ProfilerActivity, profile
+            with profile(activities=[ProfilerActivity.CUDA]) as prof:
+                st.apply_gates(g)
+                st.sync()
+                torch.cuda.synchronize()
+            ks = [(e.time_range.end - e.time_range.start) / 1e3 for e in prof.events()
+                  if e.device_type == torch.autograd.DeviceType.CUDA and ("k_" in e.name or "qvg" in e.name)]
             print(json.dumps({"n": n, "tile_qubits": k, "sub": sub, "passes": s["passes"] / a.reps,
-                              "graph_replays": s["graph_replays"], "device_ms": statistics.median(ts)}), flush=True)
+                              "graph_replays": s["graph_replays"], "device_ms": statistics.median(ts),
+                              "kernel_ms_sum": sum(ks), "kernels_seen": len(ks),
+                              "kernel_ms_max": max(ks) if ks else 0}), flush=True)
             del st
 
 
