@@ -110,6 +110,8 @@ enum qvg_option {
                                 scatter measured equal, profiles/r02_perm_ab.json) */
     QVG_OPT_TILE_ORDER = 21, /* fused tiles: 0 = CTA b runs tiles b, b + grid, ... (default); 1 = a contiguous
                                 chunk of tiles per CTA (successive tiles are DRAM neighbours) */
+    QVG_OPT_TILE_GRID = 22,  /* fused tiles: 0 = one persistent wave of CTAs loops over the tiles, 1 = one
+                                CTA per tile, -1 = auto (default: 1 for complex128, 0 for complex64) */
     QVG_OPT_PIPE = 18        /* fused tiles: 2 or 3 = warp-specialised bulk-copy pipeline (k_tile_pipe) with
                                 that many shared-memory ring stages; 0 = k_tile, per-thread loads (default:
                                 measured 1.5-2x faster, profiles/r02_pipe_ab.json) */

@@ -516,4 +516,5 @@ PYBIND11_MODULE(_core, m) {
     m.attr("OPT_JIT") = (int)QVG_OPT_JIT;
     m.attr("OPT_PERM") = (int)QVG_OPT_PERM;
     m.attr("OPT_TILE_ORDER") = (int)QVG_OPT_TILE_ORDER;
+    m.attr("OPT_TILE_GRID") = (int)QVG_OPT_TILE_GRID;
 }

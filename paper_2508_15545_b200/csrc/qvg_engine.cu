@@ -123,6 +123,7 @@ struct qvg_state {
     std::vector<uint64_t> graph_seen;  // auto mode: keys applied once (ring)
     uint32_t reorder = REORDER_EXACT;  // QVG_OPT_REORDER: commutation-aware fusion order (qvg_plan.hpp)
     bool classes = true;       // QVG_OPT_CLASSES: structured-matrix op bodies in fused tiles
+    int tile_grid = -1;        // QVG_OPT_TILE_GRID: 0 persistent CTAs over tiles, 1 one CTA per tile, -1 auto
     uint32_t tile_order = 0;   // QVG_OPT_TILE_ORDER: 0 strided tiles per CTA, 1 contiguous chunks
     bool perm = false;         // QVG_OPT_PERM: permutation / sign-flip runs through k_tile_perm (measured
                                // equal to k_tile, profiles/r02_perm_ab.json: off by default)
@@ -453,7 +454,15 @@ void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *recs) {
     int per_sm = 0;
     cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (int)threads, smem), "occupancy(k_tile)");
     per_sm = std::max(per_sm, 1);
-    const uint64_t grid = std::min<uint64_t>(g.ntiles, (uint64_t)per_sm * s.sm_count);
+    // persistent (one wave of CTAs looping over tiles) or one CTA per tile
+    // (the hardware scheduler staggers CTAs; QVG_OPT_TILE_GRID 1)
+    // (auto: one CTA per tile for complex128, whose passes vary most in work per
+    // tile, e.g. QFT phases controlled by a qubit outside the tile: C1 -9%,
+    // C0-style -4%, C2/C3 -1.5%; complex64 measured 2-3% slower that way on
+    // three of the four circuits, profiles/r02_tile_grid_ab.json)
+    const bool per_tile = s.tile_grid < 0 ? sizeof(R) == 8 : s.tile_grid == 1;
+    const uint64_t grid = per_tile ? std::min<uint64_t>(g.ntiles, 0x7fffffffull)
+                                   : std::min<uint64_t>(g.ntiles, (uint64_t)per_sm * s.sm_count);
     kern<<<(unsigned)grid, threads, smem, s.stream>>>(static_cast<T *>(psi), prm);
 }
 
@@ -543,7 +552,7 @@ uint64_t plan_signature(const qvg_state &s) {
     auto mix = [&](uint64_t v) { h = (h ^ v) * 1099511628211ull; };
     mix(s.fuse); mix(s.tile_qubits); mix(s.carriers); mix(s.low_kernel); mix(s.min_run); mix(s.pred_store);
     mix(s.sub_bits); mix(s.fma); mix(s.stage_bits); mix((uint64_t)s.prefetch_mode); mix(s.L); mix(s.precision);
-    mix(s.reorder); mix(s.classes); mix(s.shape_set); mix(s.pipe_stages); mix(s.perm); mix(s.jit_mode);
+    mix(s.reorder); mix(s.classes); mix(s.shape_set); mix(s.pipe_stages); mix(s.perm); mix(s.jit_mode); mix(s.tile_grid); mix(s.tile_order);
     return h;
 }
 
@@ -842,6 +851,10 @@ int qvg_set_option(qvg_state *s, int key, int64_t value) {
             s->exchange_mode = (int)value;
             break;
         case QVG_OPT_PERM: s->perm = value != 0; break;
+        case QVG_OPT_TILE_GRID:
+            if (value < -1 || value > 1) throw Validation("tile grid must be -1 (auto), 0 (persistent) or 1 (CTA per tile)");
+            s->tile_grid = (int)value;
+            break;
         case QVG_OPT_TILE_ORDER:
             if (value < 0 || value > 1) throw Validation("tile order must be 0 (strided) or 1 (contiguous per CTA)");
             s->tile_order = (uint32_t)value;
