@@ -537,22 +537,32 @@ def e2e_leg(qv, st, circ, recs, line, args):
     states = [st] + [qv.StateVector.create(n, 128, 0) for _ in range(E2E_STATES - 1)]
     steps = max(2 * E2E_STATES, args.steps)
     per = count // E2E_CHUNKS
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for k in range(steps):
-        s, (_, buf) = states[k % E2E_STATES], bufs[k % E2E_STATES]
-        for c in range(E2E_CHUNKS):
-            s.load_async(buf[c * per:(c + 1) * per], c * per)
-        qv.apply_circuit(s, circ, sync=False)
-        for c in range(E2E_CHUNKS):
-            s.read_async(buf[c * per:(c + 1) * per], c * per)
-    for s in states:
-        s.sync()
-    ms = (time.perf_counter() - t0) * 1e3 / steps
+
+    def stream_of_steps(apply):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for k in range(steps):
+            s, (_, buf) = states[k % E2E_STATES], bufs[k % E2E_STATES]
+            for c in range(E2E_CHUNKS):
+                s.load_async(buf[c * per:(c + 1) * per], c * per)
+            if apply:
+                qv.apply_circuit(s, circ, sync=False)
+            for c in range(E2E_CHUNKS):
+                s.read_async(buf[c * per:(c + 1) * per], c * per)
+        for s in states:
+            s.sync()
+        return (time.perf_counter() - t0) * 1e3 / steps
+
+    ms = stream_of_steps(True)
+    # the same stream of copies with no circuit: the sustained floor of this
+    # H2D + D2H pattern (tools/e2e_streams_ab.py: dedicated copy streams are
+    # no faster, profiles/r02_e2e_streams.json)
+    copy_ms = stream_of_steps(False)
     del states[1:]
     pcie = pcie_bidir_gbs(bufs[0][0], bufs[1][0])
     line["e2e"] = {"value": len(circ) * count / (ms / 1e3), "unit": UNIT, "ms_per_step": ms,
                    "pcie_bidir_gbs": pcie, "pcie_frac": (2 * count * 16 / (ms / 1e3) / 1e9) / pcie,
+                   "copy_only_ms_per_step": copy_ms, "copy_only_frac": copy_ms / ms,
                    # one request alone, synchronous: load -> apply -> read
                    "serial": {"value": len(circ) * count / (latency / 1e3), "unit": UNIT, "ms": latency},
                    "steps": steps, "h2d_bytes_per_step": count * 16, "d2h_bytes_per_step": count * 16,
