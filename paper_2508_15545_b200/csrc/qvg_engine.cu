@@ -261,7 +261,11 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 // of tile / non-tile qubits above it. False when the pass needs more than 5
 // dims (it then runs k_tile).
 bool tma_tile_map(const TileGeom &g, int amp_bytes, void *psi, TileTma &out) {
-    const int rb = amp_bytes == 16 ? 3 : 4;
+    // complex128 only: SWIZZLE_128B permutes 16-B chunks, which is k_tile's
+    // swz() only when one amplitude is one chunk (a complex64 pass through the
+    // TMA kernel measured wrong, round 2; it runs k_tile)
+    if (amp_bytes != 16) return false;
+    const int rb = 3;
     if (g.lowc < rb) return false;
     struct Seg { int start, len, gap; };
     std::vector<Seg> segs;

@@ -88,14 +88,30 @@ def test_repeated_apply_reuses_plan_buffers(qv, oracle):
 
 @pytest.mark.parametrize("opt,val", [("OPT_TILE_QUBITS", 5), ("OPT_TILE_QUBITS", 12), ("OPT_CARRIERS", 0),
                                      ("OPT_CARRIERS", 6), ("OPT_SUB_BITS", 3), ("OPT_LOW_KERNEL", 1),
-                                     ("OPT_MIN_RUN", 128), ("OPT_PRED_STORE", 1)])
-def test_options_keep_bits(qv, oracle, opt, val):
-    c = qv.random_circuit(13, 400, 77)
-    want = oracle.simulate(13, gate_array(c))
-    st = qv.StateVector.create(13, 128, 0)
+                                     ("OPT_MIN_RUN", 128), ("OPT_PRED_STORE", 1), ("OPT_PIPE", 2), ("OPT_PIPE", 3),
+                                     ("OPT_PIPE", 4), ("OPT_TILE_GRID", 0), ("OPT_TILE_GRID", 1),
+                                     ("OPT_TILE_ORDER", 1), ("OPT_PERM", 1), ("OPT_JIT", 3)])
+@pytest.mark.parametrize("prec", [128, 64])
+def test_options_keep_bits(qv, oracle, opt, val, prec):
+    """Every engine option leaves complex128 bit-identical to the oracle and
+    complex64 within 1e-5 (and bit-identical to the default options): the
+    pipelines (bulk-copy ring, tensor-map TMA; complex64 passes fall back to
+    k_tile there), tile grid / order, permutation passes, JIT passes."""
+    n = 15 if opt in ("OPT_PIPE", "OPT_TILE_GRID", "OPT_TILE_ORDER") else 13
+    c = qv.random_circuit(n, 400, 77)
+    want = oracle.simulate(n, gate_array(c))
+    st = qv.StateVector.create(n, prec, 0)
     st.set_option(getattr(qv, opt), val)
     qv.apply_circuit(st, c, tile_qubits=val if opt == "OPT_TILE_QUBITS" else 0)
-    assert np.array_equal(st.read_state(), want)
+    got = st.read_state()
+    if prec == 128:
+        assert np.array_equal(got, want)
+    else:
+        assert np.abs(got.astype(np.complex128) - want).max() <= 1e-5
+        if opt not in ("OPT_TILE_QUBITS", "OPT_SUB_BITS", "OPT_CARRIERS"):  # same tile shapes: same bits
+            ref = qv.StateVector.create(n, prec, 0)
+            qv.apply_circuit(ref, c)
+            assert st.max_deviation(ref) == 0.0
 
 
 def test_bad_options(qv):
