@@ -464,7 +464,7 @@ void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *recs) {
     // tile, e.g. QFT phases controlled by a qubit outside the tile: C1 -9%,
     // C0-style -4%, C2/C3 -1.5%; complex64 measured 2-3% slower that way on
     // three of the four circuits, profiles/r02_tile_grid_ab.json)
-    const bool per_tile = s.tile_grid < 0 ? sizeof(R) == 8 : s.tile_grid == 1;
+    const bool per_tile = !tma && !pipe && (s.tile_grid < 0 ? sizeof(R) == 8 : s.tile_grid == 1);
     const uint64_t grid = per_tile ? std::min<uint64_t>(g.ntiles, 0x7fffffffull)
                                    : std::min<uint64_t>(g.ntiles, (uint64_t)per_sm * s.sm_count);
     kern<<<(unsigned)grid, threads, smem, s.stream>>>(static_cast<T *>(psi), prm);
