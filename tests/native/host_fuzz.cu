@@ -89,7 +89,7 @@ static void check_plan(const std::vector<qvg_gate> &ops, const PlanOptions &po) 
             for (int i = 0; i < g.nrec; ++i) {
                 const TileOp &t = p.tile_ops[pass.op_begin + i];
                 CHECK(t.kind == TILE_PAIR || t.kind == TILE_DIAG);
-                CHECK(t.tbit < g.k && t.cbit < g.k && t.cbit != t.tbit);
+                CHECK(t.tbit < g.k && t.cbit < g.k && (t.cbit < 0 || t.cbit != t.tbit));
                 if (t.kind == TILE_PAIR) CHECK(t.tbit >= 0);
                 if (t.tbit < 0) CHECK(t.kind == TILE_DIAG && t.gtgt != 0 && !(t.gtgt & (t.gtgt - 1)));
                 if (t.cbit < 0 && t.greq) CHECK(!(t.greq & (t.greq - 1)));
