@@ -1246,6 +1246,11 @@ struct OocIo {
                        uint64_t piece) = 0;
     // all chunks of the segment are home (streams synchronized)
     virtual void drain() {}
+    // true: copies are plain stream-ordered cudaMemcpyAsync, so the next
+    // segment may start fetching pieces whose sources are already home
+    // (fetch_piece), without a segment barrier
+    virtual bool overlap_ok() const { return false; }
+    virtual void fetch_piece(qvg_state &, char *, uint64_t, uint64_t, uint64_t) {}
 };
 
 // Host memory: copies go straight between the user's buffer and HBM.
@@ -1266,6 +1271,13 @@ struct HostMemIo : OocIo {
             cuda_check(cudaMemcpyAsync(h + (base_off + offhi[m]) * S, win + m * piece * S, piece * S,
                                        cudaMemcpyDeviceToHost, W.stream),
                        "out-of-core D2H");
+    }
+    bool overlap_ok() const override { return true; }
+    // window slot `slot` <- host amplitudes [host_off, host_off + piece)
+    void fetch_piece(qvg_state &W, char *win, uint64_t slot, uint64_t host_off, uint64_t piece) override {
+        cuda_check(cudaMemcpyAsync(win + slot * piece * S, h + host_off * S, piece * S, cudaMemcpyHostToDevice,
+                                   W.stream),
+                   "out-of-core H2D");
     }
 };
 
@@ -1323,38 +1335,92 @@ struct CallbackIo : OocIo {
 };
 
 // The out-of-core executor shared by qvg_apply_host and qvg_apply_stream.
+// Chunks rotate over `nwin` device windows, each on its own stream, so chunk
+// k+1's H2D and gates overlap chunk k's D2H. Between segments (the qubit
+// grouping changes, so every new chunk gathers pieces of every old one):
+//   * overlap-capable I/O (host memory): no barrier. Each piece of a new chunk
+//     waits only for the D2H event of the LAST old chunk it overlaps, and the
+//     pieces are fetched in the order their sources come home, so the first
+//     chunk of segment s+1 loads while the last chunks of segment s drain;
+//   * caller I/O (file callbacks through staging buffers): a full barrier.
 void ooc_run(OocIo &io, uint32_t n, uint32_t precision, uint32_t w, const qvg_gate *ops, uint64_t count,
-             qvg_state *const win[2], qvg_stats *stats_out) {
+             qvg_state *const *win, int nwin, qvg_stats *stats_out) {
     const uint64_t S = precision == QVG_C128 ? 16 : 8;
     const std::vector<OocSegment> segs = plan_ooc(n, w, ops, count);
     std::vector<qvg_gate> local;
     uint64_t host_bytes = 0;
+    const uint64_t nchunks = 1ull << (n - w);
+    std::vector<cudaEvent_t> done[2];  // D2H-complete event per chunk: previous / current segment
+    for (auto &v : done) {
+        v.assign(nchunks, nullptr);
+        for (auto &e : v) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    }
+    struct EvFree {
+        std::vector<cudaEvent_t> *d;
+        ~EvFree() {
+            for (int i = 0; i < 2; ++i)
+                for (auto e : d[i]) cudaEventDestroy(e);
+        }
+    } ev_free{done};
+    const bool overlap = io.overlap_ok();
+    uint64_t seq = 0;  // chunk sequence number across segments: window = seq % nwin
+    const OocSegment *prev = nullptr;
+    std::vector<uint64_t> order;
+    std::vector<uint64_t> dep;
     for (const OocSegment &sg : segs) {
-        const uint64_t nchunks = 1ull << (n - w);
         const uint64_t piece = 1ull << sg.lowc;
         const uint64_t npieces = 1ull << sg.hiq.size();
         std::vector<uint64_t> offhi(npieces, 0);
         for (uint64_t m = 0; m < npieces; ++m)
             for (size_t b = 0; b < sg.hiq.size(); ++b)
                 if ((m >> b) & 1) offhi[m] |= 1ull << sg.hiq[b];
-        for (uint64_t c = 0; c < nchunks; ++c) {
-            const int wi = (int)(c & 1);
+        for (uint64_t c = 0; c < nchunks; ++c, ++seq) {
+            const int wi = (int)(seq % (uint64_t)nwin);
             qvg_state &W = *win[wi];
             char *buf = static_cast<char *>(W.shards.bufs[0]);
             const uint64_t base_off = pdep_host(c, sg.outmask);
-            io.fetch(W, wi, buf, base_off, offhi, piece);
+            if (overlap && prev) {
+                // piece m overlaps old chunks pext(x, prev->outmask) for x in its range;
+                // the last of them (bits varying inside the piece all 1) gates it
+                const uint64_t lowvar = prev->outmask & (piece - 1);
+                dep.resize(npieces);
+                order.resize(npieces);
+                for (uint64_t m = 0; m < npieces; ++m) {
+                    dep[m] = pext_host(base_off + offhi[m] + lowvar, prev->outmask);
+                    order[m] = m;
+                }
+                std::stable_sort(order.begin(), order.end(), [&](uint64_t a, uint64_t b) { return dep[a] < dep[b]; });
+                uint64_t waited = ~0ull;
+                for (uint64_t m : order) {
+                    if (dep[m] != waited) {
+                        cuda_check(cudaStreamWaitEvent(W.stream, done[0][dep[m]], 0), "cudaStreamWaitEvent");
+                        waited = dep[m];
+                    }
+                    io.fetch_piece(W, buf, m, base_off + offhi[m], piece);
+                }
+            } else {
+                io.fetch(W, wi, buf, base_off, offhi, piece);
+            }
             chunk_ops(sg, ops, base_off, local);
             run_local(W, buf, local.data(), local.size());
             io.store(W, wi, buf, base_off, offhi, piece);
+            if (overlap) cuda_check(cudaEventRecord(done[1][c], W.stream), "cudaEventRecord");
             host_bytes += 2 * (piece * npieces) * S;
         }
-        // the next segment regroups the qubits: every chunk must be home first
-        for (int i = 0; i < 2; ++i) cuda_check(cudaStreamSynchronize(win[i]->stream), "out-of-core sync");
-        io.drain();
+        if (overlap) {
+            std::swap(done[0], done[1]);
+            prev = &sg;
+        } else {
+            // the next segment regroups the qubits: every chunk must be home first
+            for (int i = 0; i < nwin; ++i) cuda_check(cudaStreamSynchronize(win[i]->stream), "out-of-core sync");
+            io.drain();
+        }
     }
+    for (int i = 0; i < nwin; ++i) cuda_check(cudaStreamSynchronize(win[i]->stream), "out-of-core sync");
+    io.drain();
     if (stats_out) {
         *stats_out = qvg_stats{};
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < nwin; ++i) {
             stats_out->passes += win[i]->stats.passes;
             stats_out->fused_passes += win[i]->stats.fused_passes;
             stats_out->kernel_launches += win[i]->stats.kernel_launches;
@@ -1368,7 +1434,7 @@ void ooc_run(OocIo &io, uint32_t n, uint32_t precision, uint32_t w, const qvg_ga
 
 int ooc_entry(uint32_t n, uint32_t precision, int device, uint32_t window_qubits, const qvg_gate *ops,
               uint64_t count, qvg_stats *stats_out, const std::function<std::unique_ptr<OocIo>(uint64_t)> &make_io) {
-    qvg_state *win[2] = {nullptr, nullptr};
+    qvg_state *win[3] = {nullptr, nullptr, nullptr};
     const int rc = guarded([&] {
         if (precision != QVG_C64 && precision != QVG_C128) throw Validation("precision must be 64 or 128");
         if (n < 1 || n > 48) throw Validation("n_qubits must be in [1, 48]");
@@ -1376,13 +1442,21 @@ int ooc_entry(uint32_t n, uint32_t precision, int device, uint32_t window_qubits
         for (uint64_t i = 0; i < count; ++i) validate_op(ops[i], n, i);
         const uint32_t w = std::min(window_qubits, n);
         if (w < 4) throw Validation("window_qubits must be >= 4");
-        // two windows on their own streams: chunk k+1's copies and gates overlap chunk k's
-        for (auto &ws : win) {
-            const int r = create_impl(w, precision, device, 0, 1, nullptr, false, &ws);
+        // windows on their own streams: chunk k+1's copies and gates overlap
+        // chunk k's. Three when they fit in 3/4 of the free HBM (chunk k+2's
+        // H2D then need not wait for chunk k's D2H), else two.
+        const uint64_t wbytes = ((uint64_t)(precision / 8)) << w;
+        size_t free_b = 0, total_b = 0;
+        cuda_check(cudaSetDevice(device), "cudaSetDevice");
+        cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+        const std::unique_ptr<OocIo> io = make_io(wbytes);
+        // (caller I/O keeps two: its staging buffers are per window)
+        const int nwin = (io->overlap_ok() && n - w >= 2 && 4 * 3 * wbytes <= 3 * (uint64_t)free_b) ? 3 : 2;
+        for (int i = 0; i < nwin; ++i) {
+            const int r = create_impl(w, precision, device, 0, 1, nullptr, false, &win[i]);
             if (r != QVG_OK) throw CudaFail(r, g_last_error);
         }
-        const std::unique_ptr<OocIo> io = make_io(((uint64_t)(precision / 8)) << w);
-        ooc_run(*io, n, precision, w, ops, count, win, stats_out);
+        ooc_run(*io, n, precision, w, ops, count, win, nwin, stats_out);
     });
     for (auto *ws : win)
         if (ws) qvg_destroy(ws);

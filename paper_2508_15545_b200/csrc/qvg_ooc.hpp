@@ -79,6 +79,13 @@ inline uint64_t pdep_host(uint64_t v, uint64_t mask) {
     return r;
 }
 
+inline uint64_t pext_host(uint64_t v, uint64_t mask) {
+    uint64_t r = 0, bit = 1;
+    for (uint64_t m = mask; m; m &= m - 1, bit <<= 1)
+        if (v & m & (~m + 1)) r |= bit;
+    return r;
+}
+
 // Window bit of global qubit q, -1 when q is outside the window.
 inline int window_bit(const OocSegment &s, uint32_t q) {
     if ((int)q < s.lowc) return (int)q;

@@ -71,6 +71,15 @@ def main():
         st = qv.apply_circuit_host(amps, c, a.w)
         times.append(time.perf_counter() - t0)
     host_bytes = st["host_bytes"]
+    # the same streaming with (almost) no compute: one segment of one Z gate,
+    # i.e. the sustained H2D + D2H rate of this chunk pattern
+    z = qv.parse_circuit(f"qubits {a.n}\nz 0\n")
+    one = []
+    for _ in range(2):
+        t0 = time.perf_counter()
+        s1 = qv.apply_circuit_host(amps, z, a.w)
+        one.append(time.perf_counter() - t0)
+    seg_gbs = s1["host_bytes"] / min(one) / 1e9
     norm = float(np.sum(np.abs(amps[: 1 << 26]) ** 2))  # a slice; the full check is the tests'
     gbs = bidir_gbs(1 << 30)
     s = min(times)
@@ -79,6 +88,7 @@ def main():
         "host_bytes": host_bytes, "wall_s": s, "wall_all_s": times,
         "host_gbs": host_bytes / s / 1e9, "pcie_bidir_gbs": gbs,
         "pcie_floor_s": host_bytes / (gbs * 1e9), "pcie_frac": host_bytes / s / 1e9 / gbs,
+        "one_segment_copy_gbs": seg_gbs, "copy_stream_frac": host_bytes / s / 1e9 / seg_gbs,
         "first_2^26_probability": norm,
         "what": "qvg_apply_host: state in pinned host memory, two HBM windows; host_bytes = H2D + D2H of every "
                 "segment; floor = host_bytes at the measured pinned bidirectional rate (1 GiB chunks of a "
