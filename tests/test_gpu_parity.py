@@ -352,8 +352,11 @@ from hypothesis import HealthCheck, given, settings, strategies as hs  # noqa: E
 @settings(max_examples=80, deadline=None, suppress_health_check=[HealthCheck.function_scoped_fixture])
 @given(n=hs.integers(2, 14), depth=hs.integers(1, 150), seed=hs.integers(0, 2**32 - 1),
        fuse=hs.booleans(), tile=hs.integers(5, 12), sub=hs.sampled_from([3, 4]), stage=hs.integers(0, 3),
-       g=hs.integers(0, 2), exchange=hs.integers(0, 2), batch=hs.sampled_from([1, 4]), graph=hs.booleans())
-def test_random_options_bit_exact(qv, oracle, n, depth, seed, fuse, tile, sub, stage, g, exchange, batch, graph):
+       g=hs.integers(0, 2), exchange=hs.integers(0, 2), batch=hs.sampled_from([1, 4]), graph=hs.booleans(),
+       grid=hs.integers(-1, 1), perm=hs.booleans(), pipe=hs.sampled_from([0, 0, 2, 4]),
+       jit=hs.sampled_from([0, 0, 0, 3]))
+def test_random_options_bit_exact(qv, oracle, n, depth, seed, fuse, tile, sub, stage, g, exchange, batch, graph,
+                                  grid, perm, pipe, jit):
     if n < 2 * g + 2:
         g = 0
     c = qv.random_circuit(n, depth, seed)
@@ -361,7 +364,8 @@ def test_random_options_bit_exact(qv, oracle, n, depth, seed, fuse, tile, sub, s
     st = (qv.StateVector.create(n, 128, 0) if g == 0
           else qv.StateVector.create_sharded(n, 128, 0, 0, 1 << g, None))
     for key, val in ((qv.OPT_SUB_BITS, sub), (qv.OPT_STAGE, stage), (qv.OPT_EXCHANGE, exchange),
-                     (qv.OPT_BATCH_EXCHANGE, batch), (qv.OPT_GRAPH, int(graph))):
+                     (qv.OPT_BATCH_EXCHANGE, batch), (qv.OPT_GRAPH, int(graph)), (qv.OPT_TILE_GRID, grid),
+                     (qv.OPT_PERM, int(perm)), (qv.OPT_PIPE, pipe), (qv.OPT_JIT, jit)):
         st.set_option(key, val)
     for _ in range(2 if graph else 1):  # a graph replays on the second run
         st.init_basis(0)
