@@ -348,23 +348,21 @@ void launch_perm(qvg_state &s, void *psi, const Pass &p, const TileOp *recs) {
     kern<<<(unsigned)grid, threads, smem, s.stream>>>(static_cast<T *>(psi), prm);
 }
 
-// Which fused passes run as JIT kernels by default (QVG_OPT_JIT 1/2), from
-// the per-pass A/B in profiles/r02_jit_ab.json (n = 30, CUPTI per-pass times):
-// complex64 passes were faster as JIT kernels on every BASELINE circuit
-// (3-11%); complex128 passes were faster only when their pair ops are the
-// cheap classes (X, real: the CX and QFT passes, 6-7%), and slower (up to
-// 20%) with general, U3 (real u00) or +-1/2 / sqrt(W) bodies, whose straight-
-// line code spills and misses the instruction cache where k_tile's shared
-// op bodies do not.
-bool jit_pays(const TileGeom &g, const TileOp *recs, size_t amp_bytes) {
-    if (amp_bytes == 8) return true;
+// Which fused passes run as JIT kernels under QVG_OPT_JIT 1/2: those of at
+// least 32 ops, three quarters of them diagonal (the QFT's controlled-phase
+// passes). Their specialised kernel runs a run of same-shape phases as one
+// loop over the records with no per-op dispatch: ~7% faster per heavy QFT
+// pass at n = 30 (profiles/r02_jit_loop_ab.json). On passes of general,
+// U3 or +-1/2 bodies the JIT kernels measured slower (spills, i-cache), so
+// they keep k_tile.
+bool jit_pays(const TileGeom &g, const TileOp *recs, size_t) {
+    int ops = 0, diag = 0;
     for (int i = 0; i < g.nrec; ++i) {
-        const TileOp &o = recs[i];
-        if (o.kind != TILE_PAIR) continue;
-        const int cls = (o.slot & 0xff) / 30;
-        if (cls != TILE_CLS_REAL && cls != TILE_CLS_SWAP) return false;
+        if (recs[i].kind == TILE_GROUP) continue;
+        ++ops;
+        diag += recs[i].kind == TILE_DIAG;
     }
-    return true;
+    return ops >= 32 && 4 * diag >= 3 * ops;
 }
 
 constexpr uint32_t kJitMinQubits = 24;
