@@ -112,9 +112,12 @@ enum qvg_option {
                                 chunk of tiles per CTA (successive tiles are DRAM neighbours) */
     QVG_OPT_TILE_GRID = 22,  /* fused tiles: 0 = one persistent wave of CTAs loops over the tiles, 1 = one
                                 CTA per tile, -1 = auto (default: 1 for complex128, 0 for complex64) */
-    QVG_OPT_PIPE = 18        /* fused tiles: 2 or 3 = warp-specialised bulk-copy pipeline (k_tile_pipe) with
-                                that many shared-memory ring stages; 0 = k_tile, per-thread loads (default:
-                                measured 1.5-2x faster, profiles/r02_pipe_ab.json) */
+    QVG_OPT_PIPE = 18        /* fused tiles, data movement: 0 = k_tile (per-thread loads); 2 or 3 =
+                                warp-specialised bulk-copy ring with that many stages (k_tile_pipe) and 4 =
+                                tensor-map TMA (both measured slower, profiles/r02_pipe_ab.json); 5 =
+                                k_tile_ahead (the next tile's cp.async load runs under the last register
+                                group, same occupancy) for every pass, 6 = for passes light in FP64 work;
+                                -1 = auto (default: 6 for complex128, 0 for complex64) */
 };
 
 /* Counters (the reference's Metrics, metrics.hpp:14-30, plus the GPU pass

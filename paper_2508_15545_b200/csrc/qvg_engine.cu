@@ -14,6 +14,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -129,7 +130,7 @@ struct qvg_state {
                                // equal to k_tile, profiles/r02_perm_ab.json: off by default)
     uint32_t jit_mode = default_jit_mode();  // QVG_OPT_JIT: fused passes as specialised kernels (qvg_jit.hpp); 1 async, 2 sync, 0 off
     bool capturing = false;    // run_local inside a graph capture (JIT: lookups only)
-    uint32_t pipe_stages = 0;  // QVG_OPT_PIPE: fused tiles through the bulk-copy pipeline (k_tile_pipe) with this many ring stages; 0 = k_tile (default: measured faster, profiles/r02_pipe_ab.json)
+    int pipe_stages = -1;  // -1 auto (pipe_mode): k_tile_ahead for light complex128 passes. QVG_OPT_PIPE: fused tiles through the bulk-copy pipeline (k_tile_pipe) with this many ring stages; 0 = k_tile (default: measured faster, profiles/r02_pipe_ab.json)
     bool shape_set = false;    // tile_qubits / sub_bits set by the caller (no small-state default)
     struct GraphEntry {
         uint64_t key = 0;
@@ -375,7 +376,7 @@ bool jit_variant(const qvg_state &s, const Pass &p, const TileOp *recs, size_t a
     if (!s.jit_mode || p.kind != PASS_TILE) return false;
     if (s.prefetch_mode == 1 && g.sub == 3) return false;
     const unsigned threads = 1u << (g.k - g.sub);
-    if (threads == (unsigned)kPipeConsumers && s.pipe_stages >= 2) return false;
+    if (threads == (unsigned)kPipeConsumers && s.pipe_stages >= 2 && s.pipe_stages <= 5) return false;  // an explicit pipeline
     // by default only for states whose passes outweigh a compile (~0.2-1 s per
     // kernel, once per pass structure): >= 2^24 amplitudes per shard / window
     if (s.jit_mode != 3 && (g.n < (int)kJitMinQubits || !jit_pays(g, recs, amp_bytes))) return false;
@@ -397,6 +398,26 @@ void jit_prepare_plan(const qvg_state &s, const Plan &plan) {
     if (!reqs.empty()) jit_prepare(reqs.data(), reqs.size());
 }
 
+#ifdef QVG_TILE_TRACE
+// Debug builds only (tools/tile_trace.py): phase stamps of the tiles
+// [first, first + count) of every following k_tile launch go to `buf`.
+static unsigned long long *g_trace_buf = nullptr;
+static uint64_t g_trace_first = 0, g_trace_count = 0, g_trace_launches = 0, g_trace_launch = 0;
+#endif
+
+// QVG_OPT_PIPE resolved: auto = 6 (k_tile_ahead for light passes) for complex128, 0 (k_tile) for complex64,
+// where the ahead kernel measured within +-3% per pass.
+inline int pipe_mode(const qvg_state &s) { return s.pipe_stages >= 0 ? s.pipe_stages : (s.S == 16 ? 6 : 0); }
+constexpr double kAheadMaxWeight = 135.0;
+// Tiles per CTA of a "one CTA per tile" grid: up to 16 (a power of two) while at least four waves of CTAs
+// remain, so CTAs still start staggered and balance uneven tiles.
+constexpr uint64_t kTilesPerCta = 16;
+inline uint64_t tiles_per_cta(uint64_t ntiles, uint64_t resident) {
+    uint64_t t = 1;
+    while (t < kTilesPerCta && ntiles / (2 * t) >= 4 * resident) t *= 2;
+    return t;
+}
+
 template <class R>
 void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *recs) {
     using T = typename Cplx<R>::T;
@@ -405,6 +426,12 @@ void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *recs) {
     thread_local TileParams prm;  // 25 KB; the launch copies it into the parameter block (per host thread: states on different threads may launch concurrently)
     prm.g = g;
     prm.g.order = (int)s.tile_order;
+#ifdef QVG_TILE_TRACE
+    prm.g.trace = g_trace_buf && g_trace_launch < g_trace_launches
+                      ? g_trace_buf + 24 * g_trace_count * g_trace_launch++ : nullptr;
+    prm.g.trace_first = g_trace_first;
+    prm.g.trace_count = g_trace_count;
+#endif
     std::memcpy(prm.ops, recs + p.op_begin, sizeof(TileOp) * g.nrec);
     unsigned threads = 1u << (g.k - g.sub);  // one 2^sub-amplitude subcube per thread
     const bool pf = s.prefetch_mode == 1 && g.sub == 3;  // register prefetch needs the 8-amplitude subcube
@@ -415,9 +442,21 @@ void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *recs) {
     const bool tiny = threads <= 128;  // sub 4 at k <= 11: 128-thread CTAs
     // the bulk-copy pipelines serve 128-thread tiles (every default shape)
     const bool pipe_ok = threads == (unsigned)kPipeConsumers && !pf;
-    const bool tma = pipe_ok && s.pipe_stages == 4 && tma_tile_map(g, (int)sizeof(T), psi, prm.tma);
-    const int pipe = (!tma && pipe_ok && (s.pipe_stages == 2 || s.pipe_stages == 3)) ? (int)s.pipe_stages : 0;
-    if (tma) {
+    const int pm = pipe_mode(s);
+    const bool tma = pipe_ok && pm == 4 && tma_tile_map(g, (int)sizeof(T), psi, prm.tma);
+    const int pipe = (!tma && pipe_ok && (pm == 2 || pm == 3)) ? pm : 0;
+    // k_tile_ahead (qvg_tile_ahead.cuh): 128-thread tiles of the default subcubes; always uses the shared tile
+    // QVG_OPT_PIPE 5: every eligible pass; 6: passes whose FP64 work per pair is light enough for the hidden
+    // load to pay (tile_pass_weight <= kAheadMaxWeight; heavier passes are FP64-issue bound and measured
+    // 0-7% slower, profiles/r02_ahead_ab.json)
+    // (and several tiles per CTA, or there is no next tile to load ahead)
+    const uint64_t per_cta = tiles_per_cta(g.ntiles, 5ull * s.sm_count);
+    const bool ahead = pipe_ok && (pm == 5 || pm == 6) && !fma && (g.sub == 4 || (g.sub == 5 && sizeof(R) == 4)) &&
+                       (pm == 5 || (s.tile_grid != 0 && per_cta >= 4 &&
+                                    tile_pass_weight(prm.ops, g.nrec) <= kAheadMaxWeight));
+    if (ahead) {
+        smem = (((sizeof(uint64_t) << g.nhi) + 15) & ~size_t(15)) + (sizeof(T) << g.k);
+    } else if (tma) {
         threads = kPipeThreads;
         smem = tma_smem_bytes(g.k, (int)sizeof(T), 2);
     } else if (pipe) {
@@ -439,13 +478,13 @@ void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *recs) {
     // Passes without structured ops (classes off) use the REAL-set kernel:
     // their records only name general bodies, which every set compiles.
     const int set_idx = class_set_index(g.cls_set);
-    const TileKernel<R> kern = tile_kernel<R>(set_idx, TileVariant{g.sub, tiny, small, fma, pf, pipe, tma});
+    const TileKernel<R> kern = tile_kernel<R>(set_idx, TileVariant{g.sub, tiny, small, fma, pf, pipe, tma, ahead});
     // The shared-memory opt-in is a per-device function attribute: set it once
     // per (device, variant).
-    static std::atomic<uint64_t> attr_set[64][4][8];  // [device][class set][variant / 64]: a bit per variant
+    static std::atomic<uint64_t> attr_set[64][4][16];  // [device][class set][variant / 64]: a bit per variant
     const int variant = (sizeof(R) == 8 ? 1 : 0) | (g.sub == 4 ? 2 : 0) | (fma ? 4 : 0) | (small ? 8 : 0) |
                         (pf ? 16 : 0) | (tiny ? 32 : 0) | (g.sub == 5 ? 64 : 0) | (pipe ? (pipe >= 3 ? 256 : 128) : 0) |
-                        (tma ? 384 : 0);
+                        (tma ? 384 : 0) | (ahead ? 512 : 0);
     std::atomic<uint64_t> &set = attr_set[s.device & 63][set_idx][variant >> 6];
     const uint64_t bit = 1ull << (variant & 63);
     if (!(set.load(std::memory_order_acquire) & bit)) {
@@ -462,9 +501,14 @@ void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *recs) {
     // tile, e.g. QFT phases controlled by a qubit outside the tile: C1 -9%,
     // C0-style -4%, C2/C3 -1.5%; complex64 measured 2-3% slower that way on
     // three of the four circuits, profiles/r02_tile_grid_ab.json)
-    const bool per_tile = !tma && !pipe && (s.tile_grid < 0 ? sizeof(R) == 8 : s.tile_grid == 1);
-    const uint64_t grid = per_tile ? std::min<uint64_t>(g.ntiles, 0x7fffffffull)
-                                   : std::min<uint64_t>(g.ntiles, (uint64_t)per_sm * s.sm_count);
+    const bool per_tile = !tma && !pipe && (s.tile_grid < 0 ? sizeof(R) == 8 || ahead : s.tile_grid == 1);
+    // "One CTA per tile" runs up to kTilesPerCta tiles per CTA (b, b + grid, ...) while that leaves several
+    // waves of CTAs: the CTA preamble (offset table, first barrier) is paid once per 16 tiles and k_tile_ahead
+    // hides 15 of 16 loads, while CTAs still start staggered and balance uneven tiles (a fully persistent
+    // grid measured 9% slower for k_tile_ahead, profiles/r02_ahead_ab.json).
+    const uint64_t resident = (uint64_t)per_sm * s.sm_count;
+    const uint64_t split = g.ntiles / tiles_per_cta(g.ntiles, resident);
+    const uint64_t grid = per_tile ? std::min<uint64_t>(split, 0x7fffffffull) : std::min<uint64_t>(g.ntiles, resident);
     kern<<<(unsigned)grid, threads, smem, s.stream>>>(static_cast<T *>(psi), prm);
 }
 
@@ -795,6 +839,16 @@ int qvg_info(const qvg_state *s, uint32_t *n, uint32_t *precision, uint32_t *ran
     });
 }
 
+#ifdef QVG_TILE_TRACE
+extern "C" void qvg_debug_tile_trace(void *buf, uint64_t first, uint64_t count, uint64_t launches) {
+    g_trace_buf = static_cast<unsigned long long *>(buf);  // 24 * count * launches words
+    g_trace_first = first;
+    g_trace_count = count;
+    g_trace_launches = launches;
+    g_trace_launch = 0;
+}
+#endif
+
 int qvg_set_option(qvg_state *s, int key, int64_t value) {
     return guarded([&] {
         check_state(s);
@@ -867,9 +921,10 @@ int qvg_set_option(qvg_state *s, int key, int64_t value) {
             s->jit_mode = (uint32_t)value;
             break;
         case QVG_OPT_PIPE:
-            if (value < 0 || value > 4 || value == 1)
-                throw Validation("pipe must be 0 (k_tile), 2 or 3 (bulk-copy ring stages) or 4 (tensor-map TMA)");
-            s->pipe_stages = (uint32_t)value;
+            if (value < -1 || value > 6 || value == 1)
+                throw Validation("pipe must be 0 (k_tile), 2 or 3 (bulk-copy ring stages), 4 (tensor-map TMA), 5 (next tile's "
+                                 "load under the last group, every pass) or 6 (the same for light passes)");
+            s->pipe_stages = (int)value;
             break;
         case QVG_OPT_XCHG_CHUNK:
             if (value < 0 || (value % 16) != 0) throw Validation("exchange chunk must be a multiple of 16 bytes (0 = default)");

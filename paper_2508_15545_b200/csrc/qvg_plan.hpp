@@ -211,6 +211,36 @@ inline Pass single_pass(const qvg_gate &g, const OpInfo &o, const PlanOptions &p
     return p;
 }
 
+// FP64 work of a fused pass per amplitude pair, from its records (the op
+// bodies of qvg_tile.cuh): general 28, real-u00 24, +-1/2 entries 16, real 12,
+// sqrt(W) 12, X 4 (moves through DADD), a phase 6 per multiplied amplitude;
+// an op controlled inside its group touches half the pairs. Used to pick the
+// kernel per pass (qvg_engine.cu launch_tile): light passes are bound by
+// exposed HBM latency, heavy ones by FP64 issue.
+inline double tile_pass_weight(const TileOp *recs, int nrec) {
+    static const double cls_w[6] = {28, 12, 4, 16, 12, 24};  // TileCls order: GEN REAL SWAP HALF SQW U00R
+    double w = 0;
+    for (int i = 0; i < nrec; ++i) {
+        const TileOp &o = recs[i];
+        if (o.kind == TILE_GROUP) continue;
+        const int d = o.slot & 0xff;
+        if (d < kDispDiag) {
+            const int cls = d / 30, k = (d % 30) % 6;  // k = K + 1: 0 = no control in the group
+            w += cls_w[cls < 6 ? cls : 0] * (k ? 0.5 : 1.0);
+        } else {
+            const int dd = d - kDispDiag;
+            if (dd >= 36) continue;  // sign flips: no FP64
+            const int j = dd / 6, k = dd % 6;  // j = J + 1 (0: target outside the group), k = K + 1
+            double x = j ? 6.0 : 12.0 * 0.5;   // target in the group: half the amplitudes; else t1 decides (half the threads)
+            if (o.slot & kSlotD0) x *= 2;
+            if (k) x *= 0.5;
+            if (o.slot & kSlotCtlTest) x *= 0.5;
+            w += x;
+        }
+    }
+    return w;
+}
+
 // Global index offset of tile-local bit p: the low carriers map to
 // themselves, bits >= lowc to their high qubits.
 inline uint64_t tile_bit_offset(const TileGeom &g, int p) {

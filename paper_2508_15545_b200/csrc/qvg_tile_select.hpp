@@ -6,6 +6,7 @@
 
 #include "qvg_tile.cuh"
 #include "qvg_tile_pipe.cuh"
+#include "qvg_tile_ahead.cuh"
 
 namespace qvg {
 
@@ -20,6 +21,7 @@ struct TileVariant {
     bool pf;     // next-tile register prefetch (QVG_OPT_PREFETCH)
     int pipe;    // > 0: k_tile_pipe with this many ring stages (QVG_OPT_PIPE; 128-thread tiles only)
     bool tma;    // k_tile_tma: one tensor-map TMA per tile (QVG_OPT_PIPE 4)
+    bool ahead;  // k_tile_ahead: next tile's cp.async load under the last group (QVG_OPT_PIPE 5; 128-thread tiles)
 };
 
 // Class-set index: 0 {gen, real, X}, 1 {gen, +-1/2, X}, 2 {gen, +-1/2, sqrt(W)},
@@ -63,6 +65,12 @@ inline TileKernel<R> tile_kernel(int set_idx, const TileVariant &v) {
 // qvg_tile_inst.cu only.
 template <class R, int CM>
 TileKernel<R> tile_kernel_pick(const TileVariant &v) {
+    if (v.ahead && v.tiny && !v.pf && !v.fma) {  // qvg_tile_ahead.cuh
+        if constexpr (sizeof(R) == 4) {
+            if (v.sub == 5) return k_tile_ahead<R, 5, false, 128, CM>;
+        }
+        if (v.sub == 4) return k_tile_ahead<R, 4, false, 128, CM>;
+    }
     if (v.tma && v.tiny && !v.pf) {  // tensor-map pipeline (qvg_tile_pipe.cuh)
         if constexpr (sizeof(R) == 4) {
             if (v.sub == 5) return k_tile_tma<R, 5, false, CM, 2>;

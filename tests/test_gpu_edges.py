@@ -89,14 +89,16 @@ def test_repeated_apply_reuses_plan_buffers(qv, oracle):
 @pytest.mark.parametrize("opt,val", [("OPT_TILE_QUBITS", 5), ("OPT_TILE_QUBITS", 12), ("OPT_CARRIERS", 0),
                                      ("OPT_CARRIERS", 6), ("OPT_SUB_BITS", 3), ("OPT_LOW_KERNEL", 1),
                                      ("OPT_MIN_RUN", 128), ("OPT_PRED_STORE", 1), ("OPT_PIPE", 2), ("OPT_PIPE", 3),
-                                     ("OPT_PIPE", 4), ("OPT_TILE_GRID", 0), ("OPT_TILE_GRID", 1),
+                                     ("OPT_PIPE", 4), ("OPT_PIPE", 5), ("OPT_PIPE", 6), ("OPT_PIPE", 0),
+                                     ("OPT_TILE_GRID", 0), ("OPT_TILE_GRID", 1),
                                      ("OPT_TILE_ORDER", 1), ("OPT_PERM", 1), ("OPT_JIT", 3)])
 @pytest.mark.parametrize("prec", [128, 64])
 def test_options_keep_bits(qv, oracle, opt, val, prec):
     """Every engine option leaves complex128 bit-identical to the oracle and
     complex64 within 1e-5 (and bit-identical to the default options): the
     pipelines (bulk-copy ring, tensor-map TMA; complex64 passes fall back to
-    k_tile there), tile grid / order, permutation passes, JIT passes."""
+    k_tile there), the load-ahead kernel, tile grid / order, permutation
+    passes, JIT passes."""
     n = 15 if opt in ("OPT_PIPE", "OPT_TILE_GRID", "OPT_TILE_ORDER") else 13
     c = qv.random_circuit(n, 400, 77)
     want = oracle.simulate(n, gate_array(c))
@@ -271,3 +273,28 @@ def test_warp_shuffle_low_kernel_per_gate(qv, oracle, prec, n):
         assert np.array_equal(got, want), np.abs(got - want).max()
     else:
         assert np.abs(got.astype(np.complex128) - want).max() <= 1e-5
+
+
+@pytest.mark.parametrize("prec", [128, 64])
+@pytest.mark.parametrize("grid", [0, -1])
+def test_load_ahead_kernel_several_tiles_per_cta(qv, oracle, prec, grid):
+    """k_tile_ahead (QVG_OPT_PIPE 5: the next tile's cp.async load lands in the
+    shared tile while the last register group runs) with CTAs that run several
+    tiles in a row (n = 22: 2048 tiles on a persistent grid, or the default
+    tiles-per-CTA split): complex128 bit-identical to the oracle, complex64
+    bit-identical to k_tile; staged first / last groups included (random
+    circuits put gates on qubits 0..2)."""
+    n = 22
+    c = qv.random_circuit(n, 120, 4242)
+    st = qv.StateVector.create(n, prec, 0)
+    st.set_option(qv.OPT_PIPE, 5)
+    st.set_option(qv.OPT_TILE_GRID, grid)
+    m = qv.apply_circuit(st, c)
+    assert m["traversals"] < len(c)
+    if prec == 128:
+        want = oracle.simulate(n, gate_array(c))
+        assert np.array_equal(st.read_state(), want)
+    ref = qv.StateVector.create(n, prec, 0)
+    ref.set_option(qv.OPT_PIPE, 0)
+    qv.apply_circuit(ref, c)
+    assert st.max_deviation(ref) == 0.0

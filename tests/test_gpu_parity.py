@@ -353,7 +353,7 @@ from hypothesis import HealthCheck, given, settings, strategies as hs  # noqa: E
 @given(n=hs.integers(2, 14), depth=hs.integers(1, 150), seed=hs.integers(0, 2**32 - 1),
        fuse=hs.booleans(), tile=hs.integers(5, 12), sub=hs.sampled_from([3, 4]), stage=hs.integers(0, 3),
        g=hs.integers(0, 2), exchange=hs.integers(0, 2), batch=hs.sampled_from([1, 4]), graph=hs.booleans(),
-       grid=hs.integers(-1, 1), perm=hs.booleans(), pipe=hs.sampled_from([0, 0, 2, 4]),
+       grid=hs.integers(-1, 1), perm=hs.booleans(), pipe=hs.sampled_from([-1, 0, 2, 4, 5, 5, 6]),
        jit=hs.sampled_from([0, 0, 0, 3]))
 def test_random_options_bit_exact(qv, oracle, n, depth, seed, fuse, tile, sub, stage, g, exchange, batch, graph,
                                   grid, perm, pipe, jit):

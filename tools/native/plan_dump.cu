@@ -48,8 +48,9 @@ int main(int argc, char **argv) {
             continue;
         }
         const TileGeom &gm = p.geom;
-        std::printf("pass %d tile gates %llu groups %d recs %d lowc %d stage %d cls %d hiq", pi++,
-                    (unsigned long long)p.gates, gm.ngroups, gm.nrec, gm.lowc, gm.stage, gm.cls_set);
+        std::printf("pass %d tile gates %llu groups %d recs %d lowc %d stage %d cls %d weight %.0f hiq", pi++,
+                    (unsigned long long)p.gates, gm.ngroups, gm.nrec, gm.lowc, gm.stage, gm.cls_set,
+                    tile_pass_weight(plan.tile_ops.data() + p.op_begin, gm.nrec));
         for (int i = 0; i < gm.nhi; ++i) std::printf(" %d", gm.hiq[i]);
         std::printf("\n");
         int rec = 0;
