@@ -394,7 +394,7 @@ def fused_leg(qv, st, circ, line, args):
     line["fused"] = {"ms_per_step": ms, "value": len(circ) * (1 << circ.n_qubits) / (ms / 1e3),
                      "passes_per_step": s["passes"] / reps, "fused_passes_per_step": s["fused_passes"] / reps,
                      "hbm_gbs": hbm, "hbm_frac": hbm / peaks()[0],
-                     "note": "compute/latency-bound tile passes (profiles/r01_fused_passes.json)"}
+                     "note": "tile passes (k_tile / k_tile_ahead): per-pass DRAM, FP64 and issue figures in profiles/r02_fused_passes.json"}
     st.set_option(qv.OPT_FUSE, 0)
 
 

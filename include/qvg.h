@@ -111,7 +111,7 @@ enum qvg_option {
     QVG_OPT_TILE_ORDER = 21, /* fused tiles: 0 = CTA b runs tiles b, b + grid, ... (default); 1 = a contiguous
                                 chunk of tiles per CTA (successive tiles are DRAM neighbours) */
     QVG_OPT_TILE_GRID = 22,  /* fused tiles: 0 = one persistent wave of CTAs loops over the tiles, 1 = one
-                                CTA per tile, -1 = auto (default: 1 for complex128, 0 for complex64) */
+                                CTA per tile (up to 16 tiles per CTA while several waves of CTAs remain), -1 = auto (default: 1) */
     QVG_OPT_PIPE = 18        /* fused tiles, data movement: 0 = k_tile (per-thread loads); 2 or 3 =
                                 warp-specialised bulk-copy ring with that many stages (k_tile_pipe) and 4 =
                                 tensor-map TMA (both measured slower, profiles/r02_pipe_ab.json); 5 =

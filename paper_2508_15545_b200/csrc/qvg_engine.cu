@@ -408,7 +408,7 @@ static uint64_t g_trace_first = 0, g_trace_count = 0, g_trace_launches = 0, g_tr
 // QVG_OPT_PIPE resolved: auto = 6 (k_tile_ahead for light passes) for complex128, 0 (k_tile) for complex64,
 // where the ahead kernel measured within +-3% per pass.
 inline int pipe_mode(const qvg_state &s) { return s.pipe_stages >= 0 ? s.pipe_stages : (s.S == 16 ? 6 : 0); }
-constexpr double kAheadMaxWeight = 135.0;
+constexpr double kAheadMaxWeight = 300.0;
 // Tiles per CTA of a "one CTA per tile" grid: up to 16 (a power of two) while at least four waves of CTAs
 // remain, so CTAs still start staggered and balance uneven tiles.
 constexpr uint64_t kTilesPerCta = 16;
@@ -451,7 +451,8 @@ void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *recs) {
     // 0-7% slower, profiles/r02_ahead_ab.json)
     // (and several tiles per CTA, or there is no next tile to load ahead)
     const uint64_t per_cta = tiles_per_cta(g.ntiles, 5ull * s.sm_count);
-    const bool ahead = pipe_ok && (pm == 5 || pm == 6) && !fma && (g.sub == 4 || (g.sub == 5 && sizeof(R) == 4)) &&
+    const bool ahead_ok = !pf && g.sub == 4 && (threads == 128 || threads == 256);  // (32-amplitude complex64 subcubes spill there)
+    const bool ahead = ahead_ok && (pm == 5 || pm == 6) && !fma &&
                        (pm == 5 || (s.tile_grid != 0 && per_cta >= 4 &&
                                     tile_pass_weight(prm.ops, g.nrec) <= kAheadMaxWeight));
     if (ahead) {
@@ -495,13 +496,12 @@ void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *recs) {
     int per_sm = 0;
     cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (int)threads, smem), "occupancy(k_tile)");
     per_sm = std::max(per_sm, 1);
-    // persistent (one wave of CTAs looping over tiles) or one CTA per tile
-    // (the hardware scheduler staggers CTAs; QVG_OPT_TILE_GRID 1)
-    // (auto: one CTA per tile for complex128, whose passes vary most in work per
-    // tile, e.g. QFT phases controlled by a qubit outside the tile: C1 -9%,
-    // C0-style -4%, C2/C3 -1.5%; complex64 measured 2-3% slower that way on
-    // three of the four circuits, profiles/r02_tile_grid_ab.json)
-    const bool per_tile = !tma && !pipe && (s.tile_grid < 0 ? sizeof(R) == 8 || ahead : s.tile_grid == 1);
+    // persistent (one wave of CTAs looping over tiles) or a CTA per tile (QVG_OPT_TILE_GRID 1; the hardware
+    // scheduler staggers CTAs, which balances passes whose work per tile varies, e.g. QFT phases controlled by a
+    // qubit outside the tile). Auto = per tile: with up to 16 tiles per CTA (below) it measured faster than the
+    // persistent wave in both precisions (complex128 C1 -9%, complex64 C1 -8%, C2 -5%;
+    // profiles/r02_tile_grid_ab.json, r02_ahead_ab.json).
+    const bool per_tile = !tma && !pipe && (s.tile_grid < 0 || s.tile_grid == 1);
     // "One CTA per tile" runs up to kTilesPerCta tiles per CTA (b, b + grid, ...) while that leaves several
     // waves of CTAs: the CTA preamble (offset table, first barrier) is paid once per 16 tiles and k_tile_ahead
     // hides 15 of 16 loads, while CTAs still start staggered and balance uneven tiles (a fully persistent

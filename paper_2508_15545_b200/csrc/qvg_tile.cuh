@@ -565,6 +565,7 @@ struct TileOpsRuntime {
     }
 };
 
+
 template <class R, int SUB, bool FMA, int MAXT, bool PF, int CM, class Ops>
 __device__ __forceinline__ void k_tile_body(typename Cplx<R>::T *__restrict__ psi, const TileParams &prm) {
     using T = typename Cplx<R>::T;

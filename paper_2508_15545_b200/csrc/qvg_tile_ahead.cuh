@@ -22,7 +22,7 @@
 // the lowest tile bits) issues the copies after its stores instead.
 //
 // Same records, op bodies (TileOpsRuntime) and arithmetic as k_tile:
-// bit-identical results. complex128 and complex64.
+// bit-identical results. complex128 and complex64 (16-amplitude subcubes).
 #pragma once
 
 #include "qvg_tile.cuh"
@@ -40,6 +40,8 @@ __device__ __forceinline__ void cp_async_amp(void *smem_dst, const void *gmem_sr
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
+// (6 CTAs per SM instead of 5, i.e. 80 registers: spills; QFT -7%, ladder +15%, not kept.
+// Requesting the next record's dispatch word before an op's body: C3 +1.5%, not kept.)
 template <class R, int SUB, bool FMA, int MAXT, int CM>
 __global__ void __launch_bounds__(MAXT, (tile_min_blocks<R, SUB, MAXT, false>()))
 k_tile_ahead(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ TileParams prm) {
@@ -96,6 +98,8 @@ k_tile_ahead(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ Tile
         for (int gi = 0; gi < g.ngroups; ++gi) {
             const int nops = ops[rec].tbit;
             const uint64_t packed = ops[rec].gtgt;
+            // global offsets of the group's bits (the planner's group header, as in k_tile)
+            const uint64_t *gdep = reinterpret_cast<const uint64_t *>(ops[rec].u);
             ++rec;
             int b[SUB];
 #pragma unroll
@@ -103,16 +107,26 @@ k_tile_ahead(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ Tile
             uint32_t l0 = threadIdx.x;
 #pragma unroll
             for (int j = 0; j < SUB; ++j) l0 = (uint32_t)ins0(l0, b[j]);
-            auto lidx = [&](int r) {
-                uint32_t l = l0;
+            // Shared slot of subcube amplitude r: swz is XOR-linear and l0 has
+            // zeros at the group's bits, so swz(l0 | bits(r)) = swz(l0) ^ XOR_j
+            // r_j swz(2^b_j): one XOR per slot instead of ORs, a shift and a mask.
+            uint32_t s0, sb[SUB];
+            auto slots = [&]() {
+                s0 = swz(l0);
 #pragma unroll
-                for (int j = 0; j < SUB; ++j) l |= ((r >> j) & 1) ? (1u << b[j]) : 0u;
-                return l;
+                for (int j = 0; j < SUB; ++j) sb[j] = swz(1u << b[j]);
+            };
+            auto sidx = [&](int r) {
+                uint32_t x = s0;
+#pragma unroll
+                for (int j = 0; j < SUB; ++j) x ^= ((r >> j) & 1) ? sb[j] : 0u;
+                return x;
             };
             const bool last = gi == g.ngroups - 1;
             T v[E];
+            slots();
 #pragma unroll
-            for (int r = 0; r < E; ++r) v[r] = sm[swz(lidx(r))];
+            for (int r = 0; r < E; ++r) v[r] = sm[sidx(r)];
             if (last && !(g.stage & 2)) {
                 __syncthreads();  // the buffer has been read by everyone: refill it under this group's ops
                 if (more) fetch(tile_base(tile + tr.step));
@@ -121,32 +135,45 @@ k_tile_ahead(typename Cplx<R>::T *__restrict__ psi, const __grid_constant__ Tile
             TileOpsRuntime::template apply<R, SUB, FMA, CM>(gi, v, base, ops, rec, nops);
             rec += nops;
             trc.mark_after(7 + 3 * gi, v[0].x, v[E - 1].y);
-            // the slot indices are recomputed after the op loop (the asm hides
-            // the equality): kept live across it they spill (16 registers)
+            // the slot indices and addresses are recomputed after the op loop
+            // (the asm hides the equality): kept live across it they spill
             asm volatile("" : "+r"(l0));
+#pragma unroll
+            for (int j = 0; j < SUB; ++j) asm volatile("" : "+r"(b[j]));
             if (!last) {
                 // each thread rewrites exactly the slots it read
+                slots();
 #pragma unroll
-                for (int r = 0; r < E; ++r) sm[swz(lidx(r))] = v[r];
+                for (int r = 0; r < E; ++r) sm[sidx(r)] = v[r];
                 __syncthreads();
             } else if (g.stage & 2) {
+                slots();
 #pragma unroll
-                for (int r = 0; r < E; ++r) sm[swz(lidx(r))] = v[r];
+                for (int r = 0; r < E; ++r) sm[sidx(r)] = v[r];
                 __syncthreads();
 #pragma unroll
-                for (int j = 0; j < E; ++j) v[j] = sm[swz(threadIdx.x + (uint32_t)j * blockDim.x)];
+                for (int j = 0; j < E; ++j) v[j] = sm[st + (uint32_t)j * MAXT];
+                const uint64_t dt = base | offhi[threadIdx.x >> g.lowc] | (threadIdx.x & lowm);
 #pragma unroll
                 for (int j = 0; j < E; ++j) {
-                    const uint32_t l = threadIdx.x + (uint32_t)j * blockDim.x;
-                    st_amp(psi + (base | offhi[l >> g.lowc] | (l & lowm)), v[j]);
+                    uint64_t a = dt;
+#pragma unroll
+                    for (int i = 0; i < SUB; ++i)
+                        if ((j >> i) & 1) a |= g.sdep[i];
+                    st_amp(psi + a, v[j]);
                 }
                 __syncthreads();
                 if (more) fetch(tile_base(tile + tr.step));
             } else {
+                // amplitude r of the subcube sits at base | dep(l0) | OR_j r_j gdep[j]
+                const uint64_t dl0 = base | offhi[l0 >> g.lowc] | (l0 & lowm);
 #pragma unroll
                 for (int r = 0; r < E; ++r) {
-                    const uint32_t lr = lidx(r);
-                    st_amp(psi + (base | offhi[lr >> g.lowc] | (lr & lowm)), v[r]);
+                    uint64_t a = dl0;
+#pragma unroll
+                    for (int j = 0; j < SUB; ++j)
+                        if ((r >> j) & 1) a |= gdep[j];
+                    st_amp(psi + a, v[r]);
                 }
             }
             trc.mark(8 + 3 * gi);

@@ -65,11 +65,8 @@ inline TileKernel<R> tile_kernel(int set_idx, const TileVariant &v) {
 // qvg_tile_inst.cu only.
 template <class R, int CM>
 TileKernel<R> tile_kernel_pick(const TileVariant &v) {
-    if (v.ahead && v.tiny && !v.pf && !v.fma) {  // qvg_tile_ahead.cuh
-        if constexpr (sizeof(R) == 4) {
-            if (v.sub == 5) return k_tile_ahead<R, 5, false, 128, CM>;
-        }
-        if (v.sub == 4) return k_tile_ahead<R, 4, false, 128, CM>;
+    if (v.ahead && v.small && !v.pf && !v.fma) {  // qvg_tile_ahead.cuh
+        if (v.sub == 4) return v.tiny ? k_tile_ahead<R, 4, false, 128, CM> : k_tile_ahead<R, 4, false, 256, CM>;
     }
     if (v.tma && v.tiny && !v.pf) {  // tensor-map pipeline (qvg_tile_pipe.cuh)
         if constexpr (sizeof(R) == 4) {

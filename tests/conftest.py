@@ -73,3 +73,31 @@ def checksums_numpy(amps, chunk_amps, base_index=0):
         out[:, 0] = w0.reshape(-1, chunk_amps).sum(axis=1, dtype=np.uint64)
         out[:, 1] = w1.reshape(-1, chunk_amps).sum(axis=1, dtype=np.uint64)
     return out
+
+
+def algorithmic_bytes(n, amp_bytes, op):
+    """SURVEY §8d's bytes of one gate pass, restated from the table (not from
+    the planner): 2 * touched * S with touched = the amplitudes the gate reads
+    and writes -- all of them for a dense or general-diagonal 1q gate, the
+    control = 1 half for a controlled gate, the target = 1 half for
+    diag(1, d), the |11> quarter for a controlled diag(1, d), nothing for the
+    identity -- charged in whole 32-B sectors when the touched runs are
+    shorter than a sector, and never more than the whole state."""
+    u = [float(x) for x in op["u"]]
+    ctl, tgt = int(op["control"]), int(op["target"])
+    full = 2 * (1 << n) * amp_bytes
+    diag = u[2] == 0 and u[3] == 0 and u[4] == 0 and u[5] == 0
+    phase = diag and u[0] == 1 and u[1] == 0
+    if phase and u[6] == 1 and u[7] == 0:
+        return 0
+    forced = []  # bits that must be 1 in a touched amplitude
+    if ctl >= 0:
+        forced.append(ctl)
+    if phase:
+        forced.append(tgt)
+    b = full >> len(forced)
+    if forced:
+        run = (1 << min(forced)) * amp_bytes
+        if run < 32:
+            b *= 32 // run
+    return min(b, full)

@@ -298,3 +298,35 @@ def test_load_ahead_kernel_several_tiles_per_cta(qv, oracle, prec, grid):
     ref.set_option(qv.OPT_PIPE, 0)
     qv.apply_circuit(ref, c)
     assert st.max_deviation(ref) == 0.0
+
+
+@pytest.mark.parametrize("prec,S", [(128, 16), (64, 8)])
+def test_counter_laws_on_device(qv, oracle, prec, S):
+    """The reference's single-traversal law as exact equalities on the device
+    (proj/tests/test_kernel.cpp:253-277): with
+    fusion off every non-identity gate is exactly one HBM pass and one kernel
+    launch, and `bytes_moved` is SURVEY §8d's per-gate bytes summed from the
+    table; with fusion on the counters equal the planner's (qvg_plan_passes)
+    and a fused pass is charged one traversal of the state."""
+    from conftest import algorithmic_bytes
+    n = 18
+    ops, _ = oracle.random_circuit(n, 300, 99)
+    gates = ops.tobytes()
+    want = [algorithmic_bytes(n, S, op) for op in ops]
+    st = qv.StateVector.create(n, prec, 0)
+    st.set_option(qv.OPT_GRAPH, 0)
+    st.set_option(qv.OPT_FUSE, 0)
+    st.apply_gates(gates)
+    s = st.stats()
+    live = sum(1 for w in want if w)
+    assert s["gates_applied"] == len(ops)
+    assert s["passes"] == live and s["kernel_launches"] == live and s["fused_passes"] == 0
+    assert s["bytes_moved"] == sum(want)
+    st.reset_stats()
+    st.set_option(qv.OPT_FUSE, 1)
+    st.apply_gates(gates)
+    s = st.stats()
+    p, f, b = qv.plan_passes(n, gates, precision=prec)
+    assert (s["passes"], s["fused_passes"], s["bytes_moved"]) == (p, f, b)
+    assert s["kernel_launches"] == p and p < live
+    assert b >= f * 2 * (1 << n) * S

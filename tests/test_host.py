@@ -173,6 +173,62 @@ def test_planner_bit_exact_reorder(qv):
     assert f == p and p == 14
 
 
+@pytest.mark.parametrize("prec,S", [(128, 16), (64, 8)])
+def test_counter_law_per_gate_plan(qv, oracle, prec, S):
+    """The reference's single-traversal law (SPEC.md:393,
+    proj/tests/test_kernel.cpp:253-277: one traversal per gate, an exact
+    equality) for the per-gate plan: passes = non-identity ops, and the
+    planner's bytes equal SURVEY §8d's per-gate bytes summed over the ops,
+    computed here from the table alone."""
+    from conftest import algorithmic_bytes
+    for n, depth, seed in ((6, 200, 1), (12, 300, 2), (20, 300, 3), (30, 200, 4)):
+        ops, _ = oracle.random_circuit(n, depth, seed)
+        want = [algorithmic_bytes(n, S, op) for op in ops]
+        p, f, b = qv.plan_passes(n, ops.tobytes(), precision=prec, fuse=False)
+        assert f == 0 and p == sum(1 for w in want if w) and b == sum(want)
+        for op, w in list(zip(ops, want))[:40]:  # and gate by gate
+            assert qv.plan_passes(n, op.tobytes(), precision=prec, fuse=False) == (1 if w else 0, 0, w)
+
+
+def test_counter_law_fused_plan(qv, oracle):
+    """A fused pass costs one traversal of the state whatever it holds
+    (SURVEY §8d): a plan's bytes are its fused passes * 2 * 2^n * S plus the
+    per-gate bytes of the ops left unfused, and never more than one pass per
+    gate would cost in traversals."""
+    for n, depth, seed in ((14, 400, 5), (24, 600, 6), (30, 800, 7)):
+        ops, _ = oracle.random_circuit(n, depth, seed)
+        full = 2 * (1 << n) * 16
+        p, f, b = qv.plan_passes(n, ops.tobytes())
+        p1, _, b1 = qv.plan_passes(n, ops.tobytes(), fuse=False)
+        assert p <= p1 and f <= p
+        assert b >= f * full and b - f * full <= b1
+        if f == p:
+            assert b == p * full
+
+
+def test_default_tile_kernels_do_not_spill():
+    """The fused tile kernels' default complex128 instantiations (16-amplitude
+    subcubes, 128 threads, every class set) sit on a register cliff: a spill of
+    a few bytes costs 9-17%. The build's ptxas logs must show none
+    for k_tile and k_tile_ahead."""
+    import glob
+    logs = sorted(glob.glob(os.path.join(ROOT, "paper_2508_15545_b200", "build", "tile_double_*.ptxas.log")))
+    if not logs:
+        pytest.skip("no ptxas logs (the library was not built by the in-tree Makefile)")
+    seen = 0
+    for path in logs:
+        lines = open(path).read().splitlines()
+        for i, line in enumerate(lines):
+            m = re.search(r"Compiling entry function '_ZN3qvg(6k_tile|12k_tile_ahead)IdLi4ELb0ELi128E", line)
+            if not m:
+                continue
+            props = " ".join(lines[i + 1:i + 4])
+            assert "0 bytes spill stores, 0 bytes spill loads" in props, (path, m.group(1), props)
+            assert "Used 96 registers" in props or re.search(r"Used (8\d|9[0-5]) registers", props), props
+            seen += 1
+    assert seen == 2 * len(logs)
+
+
 def test_planner_rejects_bad_ops(qv):
     with pytest.raises(qv.ValidationError):
         qv.plan_passes(3, qv.parse_circuit("qubits 4\nh 3\n").gates())

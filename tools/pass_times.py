@@ -18,6 +18,8 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+if os.environ.get("QVG_PKG_ROOT"):  # an alternative build of the package (A/B of compile-time variants)
+    sys.path.insert(0, os.environ["QVG_PKG_ROOT"])
 
 import torch  # noqa: E402
 from torch.profiler import ProfilerActivity, profile  # noqa: E402
