@@ -657,6 +657,22 @@ __device__ __forceinline__ void k_tile_body(typename Cplx<R>::T *__restrict__ ps
                 for (int j = 0; j < SUB; ++j) l |= ((r >> j) & 1) ? (1u << b[j]) : 0u;
                 return l;
             };
+            // Shared slot of subcube amplitude r: swz is XOR-linear and l0 has
+            // zeros at the group's bits, so swz(lidx(r)) = swz(l0) ^ XOR_j r_j
+            // swz(2^b_j): one XOR per slot. s0 / sb are computed right before
+            // each use (slots()), never kept live across the op loop.
+            uint32_t s0, sb[SUB];
+            auto slots = [&]() {
+                s0 = swz(l0);
+#pragma unroll
+                for (int j = 0; j < SUB; ++j) sb[j] = swz(1u << b[j]);
+            };
+            auto sidx = [&](int r) {
+                uint32_t x = s0;
+#pragma unroll
+                for (int j = 0; j < SUB; ++j) x ^= ((r >> j) & 1) ? sb[j] : 0u;
+                return x;
+            };
             // complex128 (FP64-issue bound) takes the offsets; complex64 (ALU-issue
             // bound) measured faster with the per-amplitude lookups (64-bit ORs
             // cost it more than the LDS latency): C3 c64 525 vs 597 ms
@@ -701,8 +717,9 @@ __device__ __forceinline__ void k_tile_body(typename Cplx<R>::T *__restrict__ ps
 #pragma unroll
                     for (int j = 0; j < E; ++j) sm[swz(threadIdx.x + (uint32_t)j * blockDim.x)] = v[j];
                     __syncthreads();
+                    slots();
 #pragma unroll
-                    for (int r = 0; r < E; ++r) v[r] = sm[swz(lidx(r))];
+                    for (int r = 0; r < E; ++r) v[r] = sm[sidx(r)];
                 }
             } else if (gi == 0 && (g.stage & 1)) {
                 // the group's bits include the lowest tile bits, so its lanes
@@ -714,15 +731,17 @@ __device__ __forceinline__ void k_tile_body(typename Cplx<R>::T *__restrict__ ps
 #pragma unroll
                 for (int j = 0; j < E; ++j) sm[swz(threadIdx.x + (uint32_t)j * blockDim.x)] = v[j];
                 __syncthreads();
+                slots();
 #pragma unroll
-                for (int r = 0; r < E; ++r) v[r] = sm[swz(lidx(r))];
+                for (int r = 0; r < E; ++r) v[r] = sm[sidx(r)];
             } else if (gi == 0) {
                 const uint64_t dl0 = dep_l0();
 #pragma unroll
                 for (int r = 0; r < E; ++r) v[r] = ld_amp(psi + gaddr(dl0, r));
             } else {
+                slots();
 #pragma unroll
-                for (int r = 0; r < E; ++r) v[r] = sm[swz(lidx(r))];
+                for (int r = 0; r < E; ++r) v[r] = sm[sidx(r)];
             }
             trc.mark_after(6 + 3 * gi, v[0].x, v[E - 1].y);
             Ops::template apply<R, SUB, FMA, CM>(gi, v, base, ops, rec, nops);
@@ -731,8 +750,10 @@ __device__ __forceinline__ void k_tile_body(typename Cplx<R>::T *__restrict__ ps
             if (gi == g.ngroups - 1 && (g.stage & 2)) {
                 // each thread rewrites only the slots it read, then the tile
                 // leaves coalesced
+                asm volatile("" : "+r"(l0));  // recompute the slots: nothing extra live across the op loop
+                slots();
 #pragma unroll
-                for (int r = 0; r < E; ++r) sm[swz(lidx(r))] = v[r];
+                for (int r = 0; r < E; ++r) sm[sidx(r)] = v[r];
                 __syncthreads();
 #pragma unroll
                 for (int j = 0; j < E; ++j) v[j] = sm[swz(threadIdx.x + (uint32_t)j * blockDim.x)];
@@ -746,8 +767,10 @@ __device__ __forceinline__ void k_tile_body(typename Cplx<R>::T *__restrict__ ps
                     st_amp(psi + (base | offhi[lr >> g.lowc] | (lr & lowm)), v[r]);
                 }
             } else {
+                asm volatile("" : "+r"(l0));
+                slots();
 #pragma unroll
-                for (int r = 0; r < E; ++r) sm[swz(lidx(r))] = v[r];
+                for (int r = 0; r < E; ++r) sm[sidx(r)] = v[r];
                 __syncthreads();
             }
             trc.mark(8 + 3 * gi);
