@@ -454,7 +454,7 @@ void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *recs) {
     const uint64_t per_cta = tiles_per_cta(g.ntiles, 5ull * s.sm_count);
     const bool ahead_ok = !pf && g.sub == 4 && (threads == 128 || threads == 256);  // (32-amplitude complex64 subcubes spill there)
     const bool ahead = ahead_ok && (pm == 5 || pm == 6) && !fma &&
-                       (pm == 5 || (s.tile_grid != 0 && per_cta >= 4 &&
+                       (pm == 5 || (s.tile_grid != 0 && per_cta >= 2 &&
                                     tile_pass_weight(prm.ops, g.nrec) <= kAheadMaxWeight));
     if (ahead) {
         smem = (((sizeof(uint64_t) << g.nhi) + 15) & ~size_t(15)) + (sizeof(T) << g.k);
