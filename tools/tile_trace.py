@@ -66,7 +66,6 @@ def main():
         ck(lib.qvg_set_option(st, int(k), ctypes.c_int64(int(v))))
     ck(lib.qvg_init_basis(st, ctypes.c_uint64(0)))
     gates = np.frombuffer(circuit(a.circuit, a.n).gates().tobytes(), dtype=np.uint8).copy()
-    rec = 96 if gates.size % 96 == 0 else None
     count = len(circuit(a.circuit, a.n))
     gp = gates.ctypes.data_as(ctypes.c_void_p)
     ck(lib.qvg_apply(st, gp, ctypes.c_uint64(count)))  # warm-up, untraced
@@ -76,12 +75,11 @@ def main():
     buf = torch.zeros(24 * a.count * a.launches, dtype=torch.int64, device="cuda")
     lib.qvg_debug_tile_trace(ctypes.c_void_p(buf.data_ptr()), ctypes.c_uint64(first), ctypes.c_uint64(a.count),
                              ctypes.c_uint64(a.launches))
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ck(lib.qvg_apply(st, gp, ctypes.c_uint64(count)))
     ck(lib.qvg_sync(st))
     torch.cuda.synchronize()
     t = buf.cpu().numpy().reshape(a.launches, a.count, 24)
-    out = {"n": a.n, "circuit": a.circuit, "grid": a.grid, "count": a.count, "record_bytes": rec, "launches": []}
+    out = {"n": a.n, "circuit": a.circuit, "grid": a.grid, "count": a.count, "launches": []}
     for li in range(a.launches):
         r = t[li]
         r = r[r[:, 2] != 0]
