@@ -167,6 +167,8 @@ struct PlanOptions {
     uint32_t stage_bits = 3; // stage a first/last group through shared memory when its bits
                              // include tile bits 0..stage_bits-1 (warp lanes >= 2^stage_bits
                              // amplitudes apart); 0 = never
+    bool group_reorder = true;  // ops may join an earlier register group of their pass when the reorder rule
+                                // allows the move, and an X-class op's control may stay a thread-index bit
     bool perm = false;       // QVG_OPT_PERM: a fused run of only X / CX / Z / CZ ops is a signed
                              // permutation of the tile: one shared-memory scatter (k_tile_perm)
 };
@@ -226,7 +228,7 @@ inline double tile_pass_weight(const TileOp *recs, int nrec) {
         const int d = o.slot & 0xff;
         if (d < kDispDiag) {
             const int cls = d / 30, k = (d % 30) % 6;  // k = K + 1: 0 = no control in the group
-            w += cls_w[cls < 6 ? cls : 0] * (k ? 0.5 : 1.0);
+            w += cls_w[cls < 6 ? cls : 0] * (k || (o.slot & kSlotCtlTest) ? 0.5 : 1.0);
         } else {
             const int dd = d - kDispDiag;
             if (dd >= 36) continue;  // sign flips: no FP64
@@ -428,8 +430,17 @@ inline Plan make_plan(const qvg_gate *ops, uint64_t count, const PlanOptions &po
                         if (t.tbit >= 0 && gbits[s] == t.tbit) J = s;
                         if (t.cbit >= 0 && gbits[s] == t.cbit) K = s;
                     }
+                    auto tpos = [&](int p) {  // thread-index bit of a tile bit outside the group
+                        int below = 0;
+                        for (int x = 0; x < g.sub; ++x) below += gbits[x] < p;
+                        return p - below;
+                    };
                     if (t.kind == TILE_PAIR) {
                         t.slot = 30 * t.slot + 6 * J + K + 1;
+                        if (K < 0 && t.cbit >= 0) {  // an X-class op's control left outside the group: tested per thread
+                            t.slot |= kSlotCtlTest;
+                            t.cbit = tpos(t.cbit);
+                        }
                     } else {
                         const bool neg = (t.slot & 2) != 0, d0one = (t.slot & 1) != 0;
                         t.slot = kDispDiag + (neg ? 36 : 0) + 6 * (J + 1) + K + 1;
@@ -440,11 +451,6 @@ inline Plan make_plan(const qvg_gate *ops, uint64_t count, const PlanOptions &po
                         // store that position, so the kernel tests threadIdx.x (which
                         // it can re-read) instead of the subcube base l0 (which it
                         // spilled under the 96-register limit and reloaded per op).
-                        auto tpos = [&](int p) {
-                            int below = 0;
-                            for (int x = 0; x < g.sub; ++x) below += gbits[x] < p;
-                            return p - below;
-                        };
                         if (K < 0 && t.cbit >= 0) t.cbit = tpos(t.cbit);
                         if (J < 0 && t.tbit >= 0) t.tbit = tpos(t.tbit);
                     }
@@ -506,57 +512,97 @@ inline Plan make_plan(const qvg_gate *ops, uint64_t count, const PlanOptions &po
             }
             g.ngroups = 0;
             g.cls_set = po.classes ? tile_class_set(info.data(), i, j) : (1 << TILE_CLS_GEN);
-            for (uint64_t x = i; x < j; ++x) {
-                const OpInfo &o = info[x];
-                if (o.identity) continue;
-                TileOp t{};
-                std::memcpy(t.u, ops[x].u, sizeof(t.u));
-                t.kind = o.diag ? TILE_DIAG : TILE_PAIR;
-                t.tbit = local_bit(o.target, g);
-                if (t.tbit < 0) t.gtgt = 1ull << o.target;
-                t.cbit = -1;
-                if (o.control >= 0) {
-                    t.cbit = local_bit(o.control, g);
-                    if (t.cbit < 0) t.greq = 1ull << o.control;
-                }
-                if (t.kind == TILE_DIAG)  // d0 == 1 / neg flags, coded in close_group
-                    t.slot = (ops[x].u[0] == 1.0 && ops[x].u[1] == 0.0 ? 1 : 0) | (po.classes && o.neg ? 2 : 0);
-                else
-                    t.slot = ((g.cls_set >> o.cls) & 1) ? o.cls : TILE_CLS_GEN;
-                if (t.kind == TILE_PAIR && t.slot == TILE_CLS_HALF) half_record(ops[x].u, t.u);
-                if (t.kind == TILE_PAIR && t.slot == TILE_CLS_SQW) sqw_record(ops[x].u, t.u);
-                if (po.amp_bytes == 8) {  // complex64: the kernel reads 8 floats (no F2F per use)
-                    float f[8];
-                    for (int e = 0; e < 8; ++e) f[e] = (float)t.u[e];
-                    std::memset(t.u, 0, sizeof(t.u));
-                    std::memcpy(t.u, f, sizeof(f));
-                }
-                if (t.kind == TILE_PAIR) {
-                    // The target must be a register bit. An in-tile control is
-                    // made one too: the control test is then the same for every
-                    // thread (no lane divergence) and skips half the pairs.
-                    int need[2] = {t.tbit, t.cbit};
-                    auto missing = [&] {
-                        int m = 0;
-                        for (int x : need) {
-                            if (x < 0) continue;
-                            bool have = false;
-                            for (int b = 0; b < nb; ++b) have |= gbits[b] == x;
-                            m += have ? 0 : 1;
+            // Ops join register groups in circuit order, except that (QVG_OPT_REORDER
+            // on) an op further down the run may join the CURRENT group when it fits
+            // the group's bits and may move ahead of every op skipped so far: disjoint
+            // qubits, and with REORDER_EXACT the moved op is an exact commuter
+            // (permutation or sign flip) unless only such ops were skipped (the rule of
+            // reorder_for_tiles). A U3 layer followed by a CX ladder then needs one
+            // group per 4 qubits instead of one for the layer and one per 3 CX.
+            std::vector<uint64_t> pend;
+            for (uint64_t x = i; x < j; ++x)
+                if (!info[x].identity) pend.push_back(x);
+            std::vector<char> done(pend.size(), 0);
+            std::vector<char> blocked(n, 0);
+            size_t first = 0;
+            while (first < pend.size()) {
+                std::fill(blocked.begin(), blocked.end(), 0);
+                bool general_skipped = false, any_skipped = false;
+                for (size_t q = first; q < pend.size(); ++q) {
+                    if (done[q]) continue;
+                    const uint64_t x = pend[q];
+                    const OpInfo &o = info[x];
+                    bool ok = !(blocked[o.target] || (o.control >= 0 && blocked[o.control]));
+                    if (ok && any_skipped && (po.reorder == REORDER_NONE || !po.group_reorder)) ok = false;
+                    if (ok && po.reorder == REORDER_EXACT && general_skipped && !exact_commuter(o)) ok = false;
+                    TileOp t{};
+                    int need[2] = {-1, -1};
+                    if (ok) {
+                        std::memcpy(t.u, ops[x].u, sizeof(t.u));
+                        t.kind = o.diag ? TILE_DIAG : TILE_PAIR;
+                        t.tbit = local_bit(o.target, g);
+                        if (t.tbit < 0) t.gtgt = 1ull << o.target;
+                        t.cbit = -1;
+                        if (o.control >= 0) {
+                            t.cbit = local_bit(o.control, g);
+                            if (t.cbit < 0) t.greq = 1ull << o.control;
                         }
-                        return m;
-                    };
-                    if (nb + missing() > g.sub) close_group();
-                    for (int x : need) {
-                        if (x < 0) continue;
-                        bool have = false;
-                        for (int b = 0; b < nb; ++b) have |= gbits[b] == x;
-                        if (!have) gbits[nb++] = x;
+                        if (t.kind == TILE_DIAG)  // d0 == 1 / neg flags, coded in close_group
+                            t.slot = (ops[x].u[0] == 1.0 && ops[x].u[1] == 0.0 ? 1 : 0) | (po.classes && o.neg ? 2 : 0);
+                        else
+                            t.slot = ((g.cls_set >> o.cls) & 1) ? o.cls : TILE_CLS_GEN;
+                        if (t.kind == TILE_PAIR) {
+                            // The target must be a register bit. An in-tile control is
+                            // made one too: the control test is then the same for every
+                            // thread (no lane divergence) and skips half the pairs. An
+                            // X-class op (CX: its body only moves amplitudes) whose
+                            // control does not fit the group keeps it as a bit of the
+                            // thread index instead (tested per thread, like a diagonal
+                            // op's control): threads with control 0 skip the op.
+                            need[0] = t.tbit;
+                            need[1] = t.cbit;
+                            auto missing = [&] {
+                                int m = 0;
+                                for (int y : need) {
+                                    if (y < 0) continue;
+                                    bool have = false;
+                                    for (int bb = 0; bb < nb; ++bb) have |= gbits[bb] == y;
+                                    m += have ? 0 : 1;
+                                }
+                                return m;
+                            };
+                            if (nb + missing() > (int)g.sub && t.slot == TILE_CLS_SWAP && t.cbit >= 0 && po.group_reorder)
+                                need[1] = -1;
+                            if (nb + missing() > (int)g.sub) ok = false;  // not this group's (a fresh group always fits)
+                        }
                     }
+                    if (!ok) {
+                        blocked[o.target] = 1;
+                        if (o.control >= 0) blocked[o.control] = 1;
+                        general_skipped = general_skipped || !exact_commuter(o);
+                        any_skipped = true;
+                        continue;
+                    }
+                    if (t.kind == TILE_PAIR && t.slot == TILE_CLS_HALF) half_record(ops[x].u, t.u);
+                    if (t.kind == TILE_PAIR && t.slot == TILE_CLS_SQW) sqw_record(ops[x].u, t.u);
+                    if (po.amp_bytes == 8) {  // complex64: the kernel reads 8 floats (no F2F per use)
+                        float f[8];
+                        for (int e = 0; e < 8; ++e) f[e] = (float)t.u[e];
+                        std::memset(t.u, 0, sizeof(t.u));
+                        std::memcpy(t.u, f, sizeof(f));
+                    }
+                    for (int y : need) {
+                        if (y < 0) continue;
+                        bool have = false;
+                        for (int bb = 0; bb < nb; ++bb) have |= gbits[bb] == y;
+                        if (!have) gbits[nb++] = y;
+                    }
+                    group.push_back(t);
+                    done[q] = 1;
                 }
-                group.push_back(t);
+                close_group();
+                while (first < pend.size() && done[first]) ++first;
             }
-            close_group();
             g.stage = 0;
             if (po.stage_bits > 0) {
                 if (first_low >= po.stage_bits) g.stage |= 1;

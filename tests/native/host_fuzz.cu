@@ -119,9 +119,15 @@ static void check_plan(const std::vector<qvg_gate> &ops, const PlanOptions &po) 
                     uv[e] = po.amp_bytes == 8 ? (double)reinterpret_cast<const float *>(t.u)[e] : t.u[e];
                 CHECK(t.kind == TILE_PAIR || t.kind == TILE_DIAG);
                 if (t.kind == TILE_PAIR) {
-                    // 30*class + 6*J + (K+1) with J >= 0 (target in the group)
-                    CHECK((t.slot & ~0xff) == 0 && t.slot < kDispDiag);
-                    const int cls = t.slot / 30, js = 8 * ((t.slot % 30) / 6);
+                    // 30*class + 6*J + (K+1) with J >= 0 (target in the group); an X-class op may
+                    // keep an in-tile control outside the group as a thread-index bit (kSlotCtlTest)
+                    CHECK((t.slot & ~(0xff | kSlotCtlTest)) == 0 && (t.slot & 0xff) < kDispDiag);
+                    const int pd = t.slot & 0xff;
+                    const int cls = pd / 30, js = 8 * ((pd % 30) / 6), pk = (pd % 30) % 6 - 1;
+                    if (t.slot & kSlotCtlTest)
+                        CHECK(cls == TILE_CLS_SWAP && pk < 0 && t.cbit >= 0 && t.cbit < g.k - g.sub);
+                    else
+                        CHECK(pk >= 0 || t.cbit < 0);
                     CHECK(cls >= TILE_CLS_GEN && cls <= TILE_CLS_U00R && (po.classes || cls == TILE_CLS_GEN));
                     CHECK((g.cls_set >> cls) & 1);
                     if (cls == TILE_CLS_SQW)  // (s0/2, -s0 s1, q, 0) per row

@@ -568,20 +568,25 @@ def _perm_circuit(qv, n, seed, mixed):
 @pytest.mark.parametrize("n", [6, 11, 14, 17])
 def test_perm_passes_bit_exact(qv, oracle, prec, n):
     """Runs of X / CX / Z / CZ / SWAP (controls in and outside the tile, sign
-    flips on every qubit) through k_tile_perm: the same BYTES as k_tile (signs
-    of zeros included; the start state has exact zeros) and, for complex128,
-    the oracle's values."""
+    flips on every qubit) through k_tile_perm: in circuit order (QVG_OPT_REORDER
+    0) the same BYTES as k_tile (signs of zeros included; the start state has
+    exact zeros); with the default reordering (a sign flip and a move may swap,
+    which can change the sign of an exact zero only) the same values; and, for
+    complex128, the oracle's values."""
     for seed, mixed in ((1, False), (2, True), (3, False)):
         c = _perm_circuit(qv, n, 100 * n + seed, mixed)
         got = {}
-        for perm in (1, 0):
+        for perm, reorder in ((1, 0), (0, 0), (1, 2), (0, 2)):
             st = qv.StateVector.create(n, prec, 0)
             st.set_option(qv.OPT_PERM, perm)
             st.set_option(qv.OPT_JIT, 0)
+            st.set_option(qv.OPT_REORDER, reorder)
             m = qv.apply_circuit(st, c)
-            got[perm] = st.read_state()
-        assert np.array_equal(got[1].view(np.uint64 if prec == 128 else np.uint32),
-                              got[0].view(np.uint64 if prec == 128 else np.uint32)), (seed, mixed)
+            got[perm, reorder] = st.read_state()
+        bits = np.uint64 if prec == 128 else np.uint32
+        assert np.array_equal(got[1, 0].view(bits), got[0, 0].view(bits)), (seed, mixed)
+        assert np.array_equal(got[1, 2], got[0, 2]) and np.array_equal(got[1, 2], got[1, 0]), (seed, mixed)
+        got = {1: got[1, 2], 0: got[0, 2]}
         if prec == 128:
             want = oracle.simulate(n, gate_array(c))
             assert np.array_equal(got[1], want)
