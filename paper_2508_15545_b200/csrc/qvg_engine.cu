@@ -131,7 +131,7 @@ struct qvg_state {
                                // equal to k_tile, profiles/r02_perm_ab.json: off by default)
     uint32_t jit_mode = default_jit_mode();  // QVG_OPT_JIT: fused passes as specialised kernels (qvg_jit.hpp); 1 async, 2 sync, 0 off
     bool capturing = false;    // run_local inside a graph capture (JIT: lookups only)
-    int pipe_stages = -1;  // -1 auto (pipe_mode): k_tile_ahead for light complex128 passes. QVG_OPT_PIPE: fused tiles through the bulk-copy pipeline (k_tile_pipe) with this many ring stages; 0 = k_tile (default: measured faster, profiles/r02_pipe_ab.json)
+    int pipe_stages = -1;  // QVG_OPT_PIPE: -1 auto (pipe_mode below), 0 k_tile, 2/3 bulk-copy ring stages (k_tile_pipe), 4 tensor-map TMA, 5/6 k_tile_ahead (every pass / light passes)
     bool shape_set = false;    // tile_qubits / sub_bits set by the caller (no small-state default)
     struct GraphEntry {
         uint64_t key = 0;
@@ -446,11 +446,11 @@ void launch_tile(qvg_state &s, void *psi, const Pass &p, const TileOp *recs) {
     const int pm = pipe_mode(s);
     const bool tma = pipe_ok && pm == 4 && tma_tile_map(g, (int)sizeof(T), psi, prm.tma);
     const int pipe = (!tma && pipe_ok && (pm == 2 || pm == 3)) ? pm : 0;
-    // k_tile_ahead (qvg_tile_ahead.cuh): 128-thread tiles of the default subcubes; always uses the shared tile
-    // QVG_OPT_PIPE 5: every eligible pass; 6: passes whose FP64 work per pair is light enough for the hidden
-    // load to pay (tile_pass_weight <= kAheadMaxWeight; heavier passes are FP64-issue bound and measured
-    // 0-7% slower, profiles/r02_ahead_ab.json)
-    // (and several tiles per CTA, or there is no next tile to load ahead)
+    // k_tile_ahead (qvg_tile_ahead.cuh): 16-amplitude subcubes in 128- or 256-thread CTAs; it always uses the
+    // shared tile. QVG_OPT_PIPE 5: every eligible pass. 6 (auto for complex128): passes whose FP64 work per pair
+    // is light enough for the hidden load to pay (tile_pass_weight <= kAheadMaxWeight; heavier passes are
+    // FP64-issue bound and measured 0-8% slower, profiles/r02_ahead_ab.json) on grids with at least two tiles
+    // per CTA (with one there is no next tile to load ahead).
     const uint64_t per_cta = tiles_per_cta(g.ntiles, 5ull * s.sm_count);
     const bool ahead_ok = !pf && g.sub == 4 && (threads == 128 || threads == 256);  // (32-amplitude complex64 subcubes spill there)
     const bool ahead = ahead_ok && (pm == 5 || pm == 6) && !fma &&
